@@ -1,0 +1,508 @@
+// tgs_oracle.cpp -- TEST INFRASTRUCTURE ONLY (see tgs_oracle.h).
+//
+// Plain single-threaded C++17, compiled with -O2 -ffp-contract=off and no
+// fast-math, default MXCSR (no FTZ/DAZ).  Every step follows the paper in its
+// order and notation; every silent point follows a DESIGN.md reading (R#).
+#include "tgs_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <set>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+constexpr uint32_t D = 59;  // PAPER.md:101-103 "D = 59"
+
+struct Ctx {
+  or_config cfg{};
+  uint64_t K = 0;       // global blocks, K = ceil(N/B)
+  uint32_t Kloc = 0;    // blocks owned by this shard (R17: k % G == rank)
+  uint32_t P = 0;       // slots
+  std::vector<float> bounds;  // Kloc x 4 (c_k, r_k)
+  or_fill_fn fill = nullptr;
+  void* fill_user = nullptr;
+  bool track_all = false;
+  std::vector<char> tracked;
+
+  // per local block state
+  std::vector<int64_t> last_access;  // -1 = never accessed (R4)
+  std::vector<uint32_t> step;        // Adam step counter (R7)
+  std::vector<int32_t> slot_of;      // -1 = not resident
+  std::vector<char> ever_resident, evicted_once;
+  std::vector<int64_t> admit_iter;
+
+  // per slot state
+  std::vector<int64_t> block_of;     // local id or -1
+  std::vector<char> dirty;
+
+  // data (tracked blocks only): host tier record and slot contents
+  std::unordered_map<uint32_t, std::vector<float>> host;  // theta|m|v (persist) or theta
+  std::unordered_map<int32_t, std::vector<float>> slot_data;  // theta|m|v
+
+  // sets, as sorted vectors of local ids
+  std::vector<uint32_t> R;                // R_t
+  std::vector<uint32_t> A_prev;           // R_t n K_t
+  std::vector<std::vector<uint32_t>> percam;
+  std::vector<uint32_t> Kset, Rnew, Splus, Sminus, Omega, A, evicted_dirty;
+
+  int64_t t = 0;          // number of activates so far
+  bool can_step = false;  // one step_adam per activate
+  uint64_t nonfinite = std::numeric_limits<uint64_t>::max();
+  or_stats st{};
+
+  uint64_t gid_block(uint32_t l) const { return (uint64_t)l * cfg.world_size + cfg.rank; }
+  uint32_t rows(uint32_t l) const {
+    uint64_t lo = gid_block(l) * cfg.block_size;
+    if (lo >= cfg.n_gaussians) return 0;
+    uint64_t r = cfg.n_gaussians - lo;
+    return (uint32_t)std::min<uint64_t>(r, cfg.block_size);
+  }
+  size_t rec_floats() const { return (size_t)cfg.block_size * D; }
+  uint32_t n_arr() const { return cfg.moments == OR_PERSIST ? 3u : 1u; }
+  uint64_t rec_bytes() const { return (uint64_t)rec_floats() * 4u; }
+  bool is_tracked(uint32_t l) const { return track_all || tracked[l]; }
+
+  std::vector<float>& host_rec(uint32_t l) {
+    auto it = host.find(l);
+    if (it != host.end()) return it->second;
+    std::vector<float> v((size_t)n_arr() * rec_floats(), 0.0f);  // m = v = 0 initially
+    if (fill) fill(fill_user, gid_block(l), v.data());
+    return host.emplace(l, std::move(v)).first->second;
+  }
+};
+
+// Level-1 test: cull iff d < -r_k for some plane; R2: d is
+// the fmaf chain x -> y -> z with d0 as the first addend.
+bool sphere_visible(const float* b, const float* pl /* 6x4 */) {
+  for (int p = 0; p < 6; ++p) {
+    const float* n = pl + 4 * p;
+    float d = std::fmaf(n[2], b[2], std::fmaf(n[1], b[1], std::fmaf(n[0], b[0], n[3])));
+    if (d < -b[3]) return false;
+  }
+  return true;
+}
+
+std::vector<uint32_t> set_union(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+  std::vector<uint32_t> o;
+  std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+  return o;
+}
+std::vector<uint32_t> set_inter(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+  std::vector<uint32_t> o;
+  std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+  return o;
+}
+std::vector<uint32_t> set_minus(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+  std::vector<uint32_t> o;
+  std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+  return o;
+}
+bool contains(const std::vector<uint32_t>& s, uint32_t x) {
+  return std::binary_search(s.begin(), s.end(), x);
+}
+
+}  // namespace
+
+struct or_ctx {
+  Ctx c;
+};
+
+extern "C" {
+
+int or_create(const or_config* cfg, const float* bounds_global, or_fill_fn fill, void* fill_user,
+              int track_all, or_ctx** out) {
+  if (!cfg || !out || !bounds_global) return OR_EINVAL;
+  const or_config& g = *cfg;
+  if (g.dim != D || g.block_size < 4 || g.block_size % 4 != 0 || g.capacity == 0 ||
+      g.n_gaussians == 0)
+    return OR_EINVAL;
+  if (!(g.lambda >= 0.0 && g.lambda <= 1.0) || !(g.gamma > 0.0 && g.gamma < 1.0)) return OR_EINVAL;
+  if (g.quota_den == 0 || g.quota_num > g.quota_den) return OR_EINVAL;
+  if (g.world_size < 1 || g.rank < 0 || g.rank >= g.world_size) return OR_EINVAL;
+  if (g.moments != OR_PERSIST && g.moments != OR_COLD_RESTART) return OR_EINVAL;
+  uint32_t P = g.pool_slots ? g.pool_slots : 2u * g.capacity;
+  if (P < g.capacity) return OR_EINVAL;
+  or_ctx* o = new or_ctx();
+  Ctx& c = o->c;
+  c.cfg = g;
+  c.P = P;
+  c.K = (g.n_gaussians + g.block_size - 1) / g.block_size;
+  c.Kloc = (uint32_t)((c.K > (uint64_t)g.rank) ? (c.K - g.rank + g.world_size - 1) / g.world_size : 0);
+  c.bounds.resize((size_t)c.Kloc * 4);
+  for (uint32_t l = 0; l < c.Kloc; ++l) {
+    const float* b = bounds_global + 4 * c.gid_block(l);
+    for (int i = 0; i < 4; ++i) {
+      if (!std::isfinite(b[i])) { delete o; return OR_EINVAL; }
+      c.bounds[4 * l + i] = b[i];
+    }
+    if (b[3] < 0.0f) { delete o; return OR_EINVAL; }
+  }
+  c.fill = fill;
+  c.fill_user = fill_user;
+  c.track_all = track_all != 0;
+  c.tracked.assign(c.Kloc, 0);
+  c.last_access.assign(c.Kloc, -1);
+  c.step.assign(c.Kloc, 0);
+  c.slot_of.assign(c.Kloc, -1);
+  c.ever_resident.assign(c.Kloc, 0);
+  c.evicted_once.assign(c.Kloc, 0);
+  c.admit_iter.assign(c.Kloc, 0);
+  c.block_of.assign(P, -1);
+  c.dirty.assign(P, 0);
+  *out = o;
+  return OR_OK;
+}
+
+void or_destroy(or_ctx* o) { delete o; }
+
+int or_track_block(or_ctx* o, uint64_t kg) {
+  Ctx& c = o->c;
+  if (kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;
+  uint64_t l = kg / c.cfg.world_size;
+  if (l >= c.Kloc) return OR_EINVAL;
+  if (c.slot_of[l] >= 0 && !c.tracked[l] && !c.track_all) return OR_ESTATE;  // track before admission
+  c.tracked[l] = 1;
+  return OR_OK;
+}
+
+int or_activate(or_ctx* o, const float* planes, uint32_t J) {
+  Ctx& c = o->c;
+  const or_config& g = c.cfg;
+  if (J > g.max_cameras || (J > 0 && !planes)) return OR_EINVAL;
+  for (uint32_t i = 0; i < J * 24; ++i)
+    if (!std::isfinite(planes[i])) return OR_EINVAL;
+
+  // ---- Alg. 1 l.1 / Eq. Kt_def: K^{(j)} and K = U_j K^{(j)}
+  c.percam.assign(J, {});
+  for (uint32_t j = 0; j < J; ++j)
+    for (uint32_t l = 0; l < c.Kloc; ++l)
+      if (sphere_visible(&c.bounds[4 * l], planes + 24 * j)) c.percam[j].push_back(l);
+  std::vector<uint32_t> Kn;
+  for (uint32_t j = 0; j < J; ++j) Kn = set_union(Kn, c.percam[j]);
+
+  // ---- Alg. 1 l.2: update Recency from R_t n K_t, the blocks
+  //      accessed by the previous iteration (R12): stamp last access = t-1.
+  if (c.t > 0)
+    for (uint32_t l : c.A_prev) c.last_access[l] = c.t - 1;
+
+  // ---- Alg. 1 l.3: candidate pool C_t = R_t u K_{t+1}
+  //      (Tide off, PAPER.md:570-573 / SPEC.md:666: selection from K_{t+1} only)
+  std::vector<uint32_t> cand = g.tide ? set_union(c.R, Kn) : Kn;
+
+  // ---- Alg. 1 l.4-5: s(k) = lam*1[k in K_{t+1}] + (1-lam)*Recency(k)
+  //      Recency(k) = gamma^age, reset on access and aged otherwise;
+  //      R4: age = (t-1) - last_access, saturating at A_max; never accessed -> 0.
+  auto score = [&](uint32_t l) -> double {
+    double rec = 0.0;
+    if (c.last_access[l] >= 0) {
+      int64_t age = (c.t - 1) - c.last_access[l];
+      if (age > (int64_t)g.max_age) age = g.max_age;
+      rec = 1.0;
+      for (int64_t i = 0; i < age; ++i) rec *= g.gamma;
+    }
+    double m = contains(Kn, l) ? 1.0 : 0.0;
+    return g.lambda * m + (1.0 - g.lambda) * rec;
+  };
+  // R11 tie-break: higher score, then already resident (zero traffic), then lower id
+  auto better = [&](uint32_t a, uint32_t b) {
+    double sa = score(a), sb = score(b);
+    if (sa != sb) return sa > sb;
+    bool ra = contains(c.R, a), rb = contains(c.R, b);
+    if (ra != rb) return ra;
+    return a < b;
+  };
+
+  // ---- Alg. 1 l.6: R_{t+1} = CameraBalancedTopC({K^{(j)}}, C_t, s, C)
+  //      (quota reading R10: q_j = min(|K^{(j)}|, floor(beta C / J)),
+  //      union of per-camera top-q_j, then global fill by s over C_t).
+  std::vector<uint32_t> Rn;
+  const uint64_t C = g.capacity;
+  if (cand.size() <= C) {
+    Rn = cand;  // nothing to select
+  } else {
+    std::vector<uint32_t> Q;
+    if (J > 0) {
+      uint64_t q = (C * g.quota_num) / ((uint64_t)g.quota_den * J);
+      for (uint32_t j = 0; j < J; ++j) {
+        std::vector<uint32_t> kj = c.percam[j];
+        std::sort(kj.begin(), kj.end(), better);
+        uint64_t qj = std::min<uint64_t>(kj.size(), q);
+        std::vector<uint32_t> top(kj.begin(), kj.begin() + qj);
+        std::sort(top.begin(), top.end());
+        Q = set_union(Q, top);
+      }
+    }
+    std::vector<uint32_t> rest = set_minus(cand, Q);
+    std::sort(rest.begin(), rest.end(), better);
+    uint64_t fill_n = C - Q.size();
+    std::vector<uint32_t> F(rest.begin(), rest.begin() + std::min<uint64_t>(fill_n, rest.size()));
+    std::sort(F.begin(), F.end());
+    Rn = set_union(Q, F);
+  }
+
+  // ---- Alg. 1 l.7-8: Omega, S+, S-
+  std::vector<uint32_t> Om, Sp, Sm;
+  if (g.tide) {
+    Om = set_inter(c.R, Rn);
+    Sp = set_minus(Rn, c.R);
+    Sm = set_minus(c.R, Rn);
+  } else {  // restage everything
+    Sp = Rn;
+    Sm = c.R;
+  }
+
+  // ---- slots (R13): S+ ascending -> lowest slots not holding R_t, then (if
+  //      short) the slots S- releases, ascending.
+  std::vector<int32_t> freelist;
+  for (uint32_t s = 0; s < c.P; ++s)
+    if (c.block_of[s] < 0) freelist.push_back((int32_t)s);
+  if (freelist.size() < Sp.size()) {
+    std::vector<int32_t> rel;
+    for (uint32_t l : Sm) rel.push_back(c.slot_of[l]);
+    std::sort(rel.begin(), rel.end());
+    freelist.insert(freelist.end(), rel.begin(), rel.end());
+  }
+
+  // ---- stage 4: evict S-, writing back dirty blocks
+  const uint64_t rb = c.rec_bytes() * c.n_arr();
+  c.evicted_dirty.clear();
+  for (uint32_t l : Sm) {
+    int32_t s = c.slot_of[l];
+    if (c.dirty[s]) {
+      if (c.is_tracked(l)) {
+        std::vector<float>& h = c.host_rec(l);
+        std::vector<float>& d = c.slot_data[s];
+        std::memcpy(h.data(), d.data(), sizeof(float) * c.n_arr() * c.rec_floats());
+      }
+      c.st.d2h_bytes += rb;
+      c.st.n_evict_dirty += 1;
+      c.evicted_dirty.push_back(l);
+      c.dirty[s] = 0;
+    }
+    // optimizer state is discarded with the slot in cold mode
+    c.slot_data.erase(s);
+    c.block_of[s] = -1;
+    c.slot_of[l] = -1;
+    c.evicted_once[l] = 1;
+    c.st.resident_streak_sum += (uint64_t)(c.t - c.admit_iter[l]);
+    c.st.streak_count += 1;
+  }
+
+  // ---- stage 2: materialise S+ (PAPER.md:150, 259); cold restart
+  for (size_t i = 0; i < Sp.size(); ++i) {
+    uint32_t l = Sp[i];
+    int32_t s = freelist[i];
+    c.slot_of[l] = s;
+    c.block_of[s] = l;
+    c.dirty[s] = 0;
+    if (c.ever_resident[l]) c.st.readmissions += 1;
+    c.ever_resident[l] = 1;
+    c.admit_iter[l] = c.t;
+    if (g.moments == OR_COLD_RESTART) c.step[l] = 0;
+    if (c.is_tracked(l)) {
+      std::vector<float>& h = c.host_rec(l);
+      std::vector<float> d(3 * c.rec_floats(), 0.0f);
+      std::memcpy(d.data(), h.data(), sizeof(float) * c.n_arr() * c.rec_floats());
+      c.slot_data[s] = std::move(d);
+    }
+  }
+  c.st.h2d_bytes += (uint64_t)Sp.size() * rb;
+
+  // ---- bookkeeping
+  c.Kset = Kn;
+  c.Rnew = Rn;
+  c.Splus = Sp;
+  c.Sminus = Sm;
+  c.Omega = Om;
+  c.R = Rn;
+  c.A = set_inter(Rn, Kn);
+  c.A_prev = c.A;
+  c.st.iter += 1;
+  c.st.n_visible += Kn.size();
+  c.st.n_resident += Rn.size();
+  c.st.n_active_blocks += c.A.size();
+  c.st.n_stage_in += Sp.size();
+  c.st.n_evict += Sm.size();
+  c.t += 1;
+  c.can_step = true;
+  return OR_OK;
+}
+
+int or_step_adam(or_ctx* o, const float* lr, float beta1, float beta2, float eps,
+                 or_grad_fn grad, void* grad_user, or_mask_fn mask, void* mask_user) {
+  Ctx& c = o->c;
+  const or_config& g = c.cfg;
+  if (!c.can_step) return OR_ESTATE;
+  if (!lr) return OR_EINVAL;
+  c.can_step = false;
+  const uint32_t B = g.block_size;
+  const uint32_t nw = (B + 31) / 32;
+  const uint64_t it = (uint64_t)(c.t - 1);  // iteration index of this batch
+  const float omb1 = 1.0f - beta1, omb2 = 1.0f - beta2;
+  std::vector<uint32_t> words(nw);
+  std::vector<float> G((size_t)B * D);
+  for (uint32_t l : c.A) {  // blocks in R n K, ascending
+    const int32_t s = c.slot_of[l];
+    const uint32_t nrows = c.rows(l);
+    const uint64_t kg = c.gid_block(l);
+    if (mask)
+      mask(mask_user, kg, it, words.data());
+    else
+      std::fill(words.begin(), words.end(), 0xFFFFFFFFu);
+    std::vector<char> active(B, 0);
+    uint32_t n_act = 0;
+    for (uint32_t r = 0; r < nrows; ++r)
+      if ((words[r / 32] >> (r % 32)) & 1u) active[r] = 1, ++n_act;
+    if (n_act == 0) continue;  // no row of I_t in this block: untouched, not dirty
+    const uint32_t before = c.step[l];
+    c.step[l] = before + 1;    // R7: per-block step counter
+    c.dirty[s] = 1;            // PAPER.md:293 "marked dirty"
+    c.st.total_updates += 1;
+    c.st.n_active_rows += n_act;
+    if (g.moments == OR_COLD_RESTART && before == 0 && c.evicted_once[l])
+      c.st.cold_restart_updates += 1;
+    if (!c.is_tracked(l)) continue;
+    grad(grad_user, kg, it, G.data());
+    // bias corrections 1 - beta^s, evaluated in double and rounded (R9)
+    const double sd = (double)c.step[l];
+    const float bc1 = (float)(1.0 - std::pow((double)beta1, sd));
+    const float bc2 = (float)(1.0 - std::pow((double)beta2, sd));
+    const float ibs = 1.0f / std::sqrt(bc2);
+    std::vector<float>& d = c.slot_data[s];
+    float* th = d.data();
+    float* m = th + c.rec_floats();
+    float* v = m + c.rec_floats();
+    for (uint32_t r = 0; r < nrows; ++r) {
+      if (!active[r]) continue;  // Eq. masked_update: theta unchanged off I_t
+      bool finite = true;
+      for (uint32_t a = 0; a < D; ++a)
+        if (!std::isfinite(G[(size_t)r * D + a])) {
+          uint64_t idx = (kg * B + r) * D + a;
+          if (idx < c.nonfinite) c.nonfinite = idx;
+          finite = false;
+        }
+      if (!finite) continue;  // R20: the row is skipped and reported
+      for (uint32_t a = 0; a < D; ++a) {
+        const size_t e = (size_t)r * D + a;
+        const float gr = G[e];
+        // Adam (Eq. masked_update u_t with first/second moments)
+        float mt = beta1 * m[e];
+        mt = mt + omb1 * gr;
+        float g2 = gr * gr;
+        float vt = beta2 * v[e];
+        vt = vt + omb2 * g2;
+        m[e] = mt;
+        v[e] = vt;
+        float den = std::sqrt(vt) * ibs;
+        den = den + eps;
+        float ss = lr[a] / bc1;
+        float upd = mt / den;
+        th[e] = th[e] - ss * upd;
+      }
+    }
+  }
+  return c.nonfinite != std::numeric_limits<uint64_t>::max() ? OR_ENONFINITE : OR_OK;
+}
+
+int or_flush(or_ctx* o) {
+  Ctx& c = o->c;
+  const uint64_t rb = c.rec_bytes() * c.n_arr();
+  for (uint32_t l : c.R) {  // consistency barrier: write back dirty residents
+    int32_t s = c.slot_of[l];
+    if (!c.dirty[s]) continue;
+    if (c.is_tracked(l)) {
+      std::vector<float>& h = c.host_rec(l);
+      std::memcpy(h.data(), c.slot_data[s].data(), sizeof(float) * c.n_arr() * c.rec_floats());
+    }
+    c.dirty[s] = 0;
+    c.st.flush_bytes += rb;
+    c.st.n_flush_blocks += 1;
+  }
+  c.can_step = false;
+  return OR_OK;
+}
+
+uint32_t or_get_list(or_ctx* o, int which, uint32_t* blocks, int32_t* slots, uint32_t cap) {
+  Ctx& c = o->c;
+  const std::vector<uint32_t>* v = nullptr;
+  switch (which) {
+    case 0: v = &c.Kset; break;
+    case 1: v = &c.Rnew; break;
+    case 2: v = &c.Splus; break;
+    case 3: v = &c.Sminus; break;
+    case 4: v = &c.Omega; break;
+    case 5: v = &c.A; break;
+    default: return 0;
+  }
+  uint32_t n = (uint32_t)v->size();
+  for (uint32_t i = 0; i < n && i < cap; ++i) {
+    uint32_t l = (*v)[i];
+    if (blocks) blocks[i] = (uint32_t)c.gid_block(l);
+    if (slots) slots[i] = (which == 3) ? -1 : c.slot_of[l];
+  }
+  return n;
+}
+
+uint32_t or_get_percam(or_ctx* o, uint32_t j, uint32_t* blocks, uint32_t cap) {
+  Ctx& c = o->c;
+  if (j >= c.percam.size()) return 0;
+  uint32_t n = (uint32_t)c.percam[j].size();
+  for (uint32_t i = 0; i < n && i < cap; ++i) blocks[i] = (uint32_t)c.gid_block(c.percam[j][i]);
+  return n;
+}
+
+uint32_t or_get_evicted_dirty(or_ctx* o, uint32_t* blocks, uint32_t cap) {
+  Ctx& c = o->c;
+  uint32_t n = (uint32_t)c.evicted_dirty.size();
+  for (uint32_t i = 0; i < n && i < cap; ++i) blocks[i] = (uint32_t)c.gid_block(c.evicted_dirty[i]);
+  return n;
+}
+
+void or_get_slot_map(or_ctx* o, int64_t* out) {
+  Ctx& c = o->c;
+  for (uint32_t s = 0; s < c.P; ++s)
+    out[s] = c.block_of[s] < 0 ? -1 : (int64_t)c.gid_block((uint32_t)c.block_of[s]);
+}
+
+void or_get_stats(or_ctx* o, or_stats* s) { *s = o->c.st; }
+uint64_t or_nonfinite_index(or_ctx* o) { return o->c.nonfinite; }
+uint32_t or_num_local_blocks(or_ctx* o) { return o->c.Kloc; }
+
+uint32_t or_step_count(or_ctx* o, uint64_t kg) {
+  Ctx& c = o->c;
+  uint64_t l = kg / c.cfg.world_size;
+  return l < c.Kloc ? c.step[l] : 0;
+}
+
+int or_read_block(or_ctx* o, uint64_t kg, float* theta, float* m, float* v) {
+  Ctx& c = o->c;
+  if (kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;
+  uint64_t l = kg / c.cfg.world_size;
+  if (l >= c.Kloc || !c.is_tracked((uint32_t)l)) return OR_EINVAL;
+  const size_t n = c.rec_floats();
+  const float* src;
+  std::vector<float> zeros;
+  if (c.slot_of[l] >= 0) {
+    src = c.slot_data[c.slot_of[l]].data();
+  } else {
+    std::vector<float>& h = c.host_rec((uint32_t)l);
+    if (c.n_arr() == 3) {
+      src = h.data();
+    } else {  // cold restart: moments do not exist off-GPU
+      zeros.assign(3 * n, 0.0f);
+      std::memcpy(zeros.data(), h.data(), sizeof(float) * n);
+      src = zeros.data();
+    }
+  }
+  if (theta) std::memcpy(theta, src, sizeof(float) * n);
+  if (m) std::memcpy(m, src + n, sizeof(float) * n);
+  if (v) std::memcpy(v, src + 2 * n, sizeof(float) * n);
+  return OR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+/*
+ * tgs_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU implementation of the TideGS working-set
+ * step (arXiv 2605.20150): Level-1 block culling (Eq.
+ * Kt_def), Tide residency selection and differential streaming (PAPER.md:
+ * 268-322, Alg. 1), eviction/write-back with dirty tracking (PAPER.md:238-251,
+ * 290-293), optimizer-state placement and the masked Adam
+ * update (Eq. masked_update).  Silent points follow the
+ * readings listed in DESIGN.md §3 ("R1".."R22").
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code with the
+ * CUDA path (paper_2605_20150_b200/) and neither side includes the other.
+ *
+ * Parity pins: see tests/test_oracle_*.py.  Functions whose result is fixed
+ * only by an invented reading say "parity unpinned" in DESIGN.md §4.
+ */
+#ifndef TGS_ORACLE_H
+#define TGS_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { OR_OK = 0, OR_EINVAL = 1, OR_ESTATE = 2, OR_ENONFINITE = 6 };
+enum { OR_PERSIST = 0, OR_COLD_RESTART = 1 };
+
+typedef struct {
+  uint64_t n_gaussians;
+  uint32_t dim;          /* 59 */
+  uint32_t block_size;   /* B */
+  uint32_t capacity;     /* C (per shard) */
+  uint32_t pool_slots;   /* P >= C; 0 -> 2C */
+  uint32_t max_cameras;
+  uint32_t max_age;      /* A_max */
+  uint32_t quota_num, quota_den; /* beta */
+  double lambda, gamma;
+  int32_t moments;       /* OR_PERSIST / OR_COLD_RESTART */
+  int32_t tide;          /* 1 = differential, 0 = restage-all ablation */
+  int32_t world_size, rank;
+} or_config;
+
+typedef struct {
+  uint64_t iter, n_visible, n_resident, n_active_blocks, n_stage_in, n_evict, n_evict_dirty,
+      n_active_rows, h2d_bytes, d2h_bytes, flush_bytes, n_flush_blocks, readmissions,
+      cold_restart_updates, total_updates, resident_streak_sum, streak_count;
+} or_stats;
+
+typedef void (*or_fill_fn)(void* user, uint64_t k_global, float* out /* B*59 */);
+typedef void (*or_grad_fn)(void* user, uint64_t k_global, uint64_t t, float* out /* B*59 */);
+typedef void (*or_mask_fn)(void* user, uint64_t k_global, uint64_t t, uint32_t* words);
+
+typedef struct or_ctx or_ctx;
+
+/* bounds_global: K x 4 floats for ALL global blocks; the shard keeps k%G==rank */
+int or_create(const or_config* cfg, const float* bounds_global, or_fill_fn fill, void* fill_user,
+              int track_all, or_ctx** out);
+void or_destroy(or_ctx* c);
+/* data (theta, m, v, Adam values) are kept only for tracked blocks */
+int or_track_block(or_ctx* c, uint64_t k_global);
+
+int or_activate(or_ctx* c, const float* planes /* J x 6 x 4 */, uint32_t J);
+int or_step_adam(or_ctx* c, const float* lr /* 59 */, float beta1, float beta2, float eps,
+                 or_grad_fn grad, void* grad_user, or_mask_fn mask, void* mask_user);
+int or_flush(or_ctx* c);
+
+/* lists of the last activate, ascending global ids:
+ * 0 K_{t+1}, 1 R_{t+1}, 2 S+, 3 S-, 4 Omega, 5 A = R n K; slots where defined */
+uint32_t or_get_list(or_ctx* c, int which, uint32_t* blocks, int32_t* slots, uint32_t cap);
+uint32_t or_get_percam(or_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap);
+/* S- entries that were dirty (written back) in the last activate */
+uint32_t or_get_evicted_dirty(or_ctx* c, uint32_t* blocks, uint32_t cap);
+void or_get_slot_map(or_ctx* c, int64_t* slot_to_block /* P, global ids, -1 free */);
+void or_get_stats(or_ctx* c, or_stats* s);
+/* lowest (gid*59+attr) of a non-finite gradient in an active row, or UINT64_MAX */
+uint64_t or_nonfinite_index(or_ctx* c);
+/* newest version of a tracked block (resident slot, else host tier) */
+int or_read_block(or_ctx* c, uint64_t k_global, float* theta, float* m, float* v);
+uint32_t or_num_local_blocks(or_ctx* c);
+uint32_t or_step_count(or_ctx* c, uint64_t k_global);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,45 @@
+"""Shared test helpers (inputs and bookkeeping only)."""
+import numpy as np
+
+import workload as W
+
+DIM = 59
+
+
+def lr_3dgs():
+    """Per-attribute 3DGS learning rates (R9; xyz, f_dc, f_rest, opacity, scale, rot)."""
+    lr = np.empty(DIM, np.float32)
+    lr[0:3] = 1.6e-4
+    lr[3:6] = 2.5e-3
+    lr[6:51] = 1.25e-4
+    lr[51] = 5e-2
+    lr[52:55] = 5e-3
+    lr[55:59] = 1e-3
+    return lr
+
+
+def tiny():
+    cfg = W.CONFIGS["tiny"]
+    sc = cfg.scene()
+    tr = cfg.trajectory(sc)
+    return cfg, sc, tr
+
+
+def synth_grad(seed, N, B):
+    """python callable k,t -> grads (B,59) from the shared counter generator."""
+    def f(k, t):
+        rows = max(0, min(B, N - k * B))
+        return W.grad_block(seed, k, B, rows, t)
+    return f
+
+
+def synth_mask(seed, N, B, p32):
+    def f(k, t):
+        rows = max(0, min(B, N - k * B))
+        return W.mask_block(seed, k, B, rows, t, p32)
+    return f
+
+
+def mask_rows(words, B):
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:B]
+    return bits.astype(bool)
