@@ -1,0 +1,220 @@
+/*
+ * tidegs.h -- C ABI of the B200-native TideGS working-set step.
+ *
+ * The library implements, for one shard of a block-virtualized Gaussian table,
+ * the per-iteration working-set step of TideGS (arXiv 2605.20150):
+ *
+ *   a1  Level-1 block frustum culling of a camera batch        PAPER.md:196-208 (Eq. Kt_def)
+ *   a2  differential delta  Omega = R_t n R_{t+1},
+ *       S+ = R_{t+1} \ R_t,  S- = R_t \ R_{t+1}                 PAPER.md:280-288, Alg. 1 l.7-8
+ *   a3  residency selection (score s(k), camera-balanced Top-C)
+ *       and cache-slot allocation / eviction                   PAPER.md:268-278, Alg. 1 l.2-6
+ *   a4  gather of S+ block records host tier -> slots and
+ *       write-back of dirty S- records slots -> host tier
+ *   a5  masked (sparse) Adam over the active rows              PAPER.md:717-727 (Eq. masked_update)
+ *
+ * Every silent or ambiguous point follows the readings R1..R22 of DESIGN.md §3
+ * (the same ones the CPU oracle in oracle/ follows).  There is no CPU fallback:
+ * every step of the path runs in CUDA kernels / copy engines of this library.
+ *
+ * Conventions
+ *   - D = 59 fp32 attributes per Gaussian; a block is B rows
+ *     (PAPER.md:180-187); K = ceil(N/B) global blocks, the last truncated.
+ *   - Sharding (R17): global block k is owned by rank k % world_size and has
+ *     local id k / world_size on that rank.  All lists returned below carry
+ *     GLOBAL block ids, ascending.
+ *   - A block "record" is B*59 fp32 (rows >= rows(k) are zero padding, R15).
+ *     Slot layout on the device: [P slots][3][B][59] fp32 (theta | m | v),
+ *     gradients separately [P][B][59].  Host tier: [K_loc][n_arr][B][59]
+ *     with n_arr = 3 (persist: theta|m|v) or 1 (cold restart: theta only).
+ *   - Status codes are returned; nothing throws across the ABI.  A CUDA error
+ *     poisons the context (TGS_EPOISONED afterwards; only tgs_destroy is valid).
+ *   - One host thread per context; one context per (rank, device).
+ */
+#ifndef TIDEGS_H
+#define TIDEGS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGS_DIM 59
+
+typedef struct tgs_ctx tgs_ctx;
+
+typedef enum {
+  TGS_OK = 0,
+  TGS_EINVAL = 1,      /* bad argument / config; context state unchanged            */
+  TGS_ESTATE = 2,      /* call order violated (see tgs_step_adam)                   */
+  TGS_ENOMEM = 3,      /* host pinned or device allocation failed                   */
+  TGS_ECUDA = 4,       /* CUDA runtime error; context poisoned                      */
+  TGS_ENCCL = 5,       /* reserved for collective errors                            */
+  TGS_ENONFINITE = 6,  /* a non-finite gradient was seen in an active row (R20)     */
+  TGS_EPOISONED = 7    /* an earlier CUDA error poisoned this context               */
+} tgs_status;
+
+typedef enum { TGS_MOMENTS_PERSIST = 0, TGS_MOMENTS_COLD_RESTART = 1 } tgs_moments;
+
+typedef struct {
+  uint64_t n_gaussians;  /* N >= 1, global                                          */
+  uint32_t dim;          /* must be 59                               */
+  uint32_t block_size;   /* B >= 4, B % 4 == 0 (4096 in the paper)   */
+  uint32_t capacity;     /* C >= 1 resident blocks on this rank      */
+  uint32_t pool_slots;   /* P >= C device slots; 0 -> 2C (R13)                      */
+  uint32_t max_cameras;  /* J_max in [1, 256]                                       */
+  uint32_t max_age;      /* A_max in [0, 1023]: Recency age saturation (R4)         */
+  uint32_t quota_num, quota_den; /* beta = num/den in [0,1] (R10)                   */
+  double lambda;         /* [0,1]                                */
+  double gamma;          /* (0,1): Recency = gamma^age (R4)                         */
+  int32_t moments;       /* tgs_moments (R6)                      */
+  int32_t tide;          /* 1 = differential streaming; 0 = restage-all ablation    */
+  int32_t world_size, rank; /* block k owned by rank k % world_size (R17)           */
+  int32_t device;        /* CUDA device ordinal                                     */
+  int32_t init_threads;  /* host threads used to build the host tier (0 -> auto)    */
+} tgs_config;
+
+/* Optional device allocator hooks (PyTorch's caching allocator from Python).
+ * NULL -> cudaMalloc / cudaFree. */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* user);
+  void (*free)(void* ptr, void* stream, void* user);
+  void* user;
+} tgs_allocator;
+
+/* Host-tier filler: writes the B x 59 fp32 record of GLOBAL block k (padding
+ * rows zero).  Called from several threads at once: must be thread-safe. */
+typedef void (*tgs_fill_fn)(void* user, uint64_t k_global, float* out);
+
+/* One camera = 6 frustum planes (nx, ny, nz, d0), unit normals, a point p is
+ * inside iff n.p + d0 >= 0 (R1). */
+typedef struct { float plane[6][4]; } tgs_camera;
+
+typedef struct {
+  /* host values, final on return (plan-synchronous, R14) */
+  uint32_t n_visible;        /* |K_{t+1}|                                       */
+  uint32_t n_resident;       /* |R_{t+1}|                                       */
+  uint32_t n_active_blocks;  /* |R_{t+1} n K_{t+1}|                             */
+  uint32_t n_stage_in;       /* |S+|                                            */
+  uint32_t n_evict;          /* |S-|                                            */
+  uint32_t n_evict_dirty;    /* |dirty S-| (0 until known, see tgs_get_stats)   */
+  uint64_t h2d_bytes;        /* |S+| * record bytes * n_arr                     */
+  /* device pointers, library-owned, valid until the next activate/flush/destroy */
+  const uint32_t* d_active_blocks; /* [n_active_blocks] global ids, ascending   */
+  const uint32_t* d_active_slots;  /* [n_active_blocks] slot of each            */
+  float* d_params;           /* slot pool base: slot s at d_params + s*slot_stride */
+  float* d_grads;            /* grad pool base: slot s at d_grads + s*grad_stride   */
+  uint64_t slot_stride;      /* floats per slot in d_params (3*B*59)            */
+  uint64_t grad_stride;      /* floats per slot in d_grads (B*59)               */
+  void* ready;               /* cudaEvent_t: wait on it before touching slots   */
+} tgs_activation;
+
+typedef struct {
+  const float* lr;  /* [59] per-attribute learning rate (host, copied)         */
+  float beta1, beta2, eps;
+} tgs_adam;
+
+typedef struct {
+  uint64_t iter, n_visible, n_resident, n_active_blocks, n_stage_in, n_evict, n_evict_dirty,
+      n_active_rows, h2d_bytes, d2h_bytes, flush_bytes, n_flush_blocks, readmissions,
+      cold_restart_updates, total_updates, resident_streak_sum, streak_count;
+} tgs_stats; /* cumulative */
+
+typedef struct {
+  /* device time of the library's kernels / copies, CUDA events on the stream
+   * each is launched on; accumulated while profiling is enabled */
+  double adam_ms, adam_prologue_ms, plan_ms, h2d_ms, d2h_ms, evict_ms;
+  uint64_t adam_launches, plan_launches, h2d_batches, d2h_batches;
+  uint64_t adam_rows;        /* active rows processed by the timed Adam launches */
+  uint64_t adam_elems_quads; /* 4-row quads visited by the timed Adam launches   */
+  uint64_t h2d_bytes, d2h_bytes; /* bytes moved by the timed copy batches        */
+  uint64_t kernel_launches;  /* every kernel this library launched              */
+  uint64_t copy_calls;       /* cudaMemcpyAsync calls issued (after run merging) */
+} tgs_timing;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Create the context for shard cfg->rank: validates cfg (EINVAL: dim != 59,
+ * B % 4 != 0, C == 0, P < C, lambda/gamma/beta out of range, J_max outside
+ * [1,256], max_age > 1023, non-finite or negative-radius bounds), allocates the
+ * pinned host tier and copies this shard's blocks into it from EITHER
+ * theta_rows (host, N x 59 fp32, global row order; may be freed afterwards) OR
+ * fill (called per owned block; theta_rows must then be NULL), zeroes the host
+ * moments, uploads bounds (host, K x 4 fp32 (cx,cy,cz,r) for ALL global
+ * blocks) and allocates the device slot pool.
+ * compute_stream (cudaStream_t, may be NULL = legacy default) is the stream
+ * tgs_step_adam runs on and the stream callers order their gradient writes on. */
+tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fill_fn fill,
+                          void* fill_user, const float* bounds, const tgs_allocator* alloc,
+                          void* compute_stream, tgs_ctx** out);
+
+tgs_status tgs_destroy(tgs_ctx* ctx);
+
+/* ------------------------------------------------------------ the hot path */
+
+/* Activate the next camera batch (J = n_cams <= J_max; 0 is valid: K = {}).
+ * Runs a1-a3 on the device, reads back the plan (one small host<->device
+ * synchronisation that does NOT wait for the previous tgs_step_adam), issues
+ * the H2D gather of S+ on a copy-engine stream (overlapping the previous
+ * Adam), and the write-back of the dirty S- records after the previous Adam.
+ * EINVAL: J > J_max, cams NULL with J > 0, non-finite plane.  Allowed after
+ * init, after step_adam, after flush, and after another activate (R19). */
+tgs_status tgs_activate(tgs_ctx* ctx, const tgs_camera* cams, uint32_t n_cams,
+                        tgs_activation* out);
+
+/* Masked Adam (a5) over the rows of R n K of the last activate, on the compute
+ * stream, after the activation's ready event.  d_row_mask: device
+ * [P][ceil(B/32)] u32, bit r of slot s = row r active (I_t), or NULL = every
+ * logical row active (R8).  Gradients are read from the grad pool (written by
+ * the caller on the compute stream).  ESTATE unless the previous call was
+ * tgs_activate.  Non-finite gradients: the row is skipped and the lowest
+ * (gid*59 + attr) is reported by tgs_nonfinite_index (R20). */
+tgs_status tgs_step_adam(tgs_ctx* ctx, const tgs_adam* hp, const uint32_t* d_row_mask);
+
+/* Consistency barrier: write every dirty resident record
+ * back to the host tier, wait for all work, clear dirty bits.  Blocks stay
+ * resident. */
+tgs_status tgs_flush(tgs_ctx* ctx);
+
+/* ------------------------------------------------------------- inspection
+ * (synchronising; for tests, metrics and checkpoint export) */
+tgs_status tgs_get_stats(tgs_ctx* ctx, tgs_stats* out);
+tgs_status tgs_get_timing(tgs_ctx* ctx, tgs_timing* out);
+tgs_status tgs_set_profiling(tgs_ctx* ctx, int enabled); /* also resets tgs_timing */
+
+/* Lists of the last activate, GLOBAL ids ascending: which = 0 K_{t+1},
+ * 1 R_{t+1}, 2 S+, 3 S-, 4 Omega, 5 A = R n K.  slots[i] = slot of blocks[i]
+ * after the activate (-1 for S-).  Returns the list length (writes at most cap
+ * entries; blocks/slots may be NULL). */
+uint32_t tgs_get_list(tgs_ctx* ctx, int which, uint32_t* blocks, int32_t* slots, uint32_t cap);
+/* K_{t+1}^{(j)} of the last activate */
+uint32_t tgs_get_percam(tgs_ctx* ctx, uint32_t j, uint32_t* blocks, uint32_t cap);
+/* dirty members of S- written back by the last activate */
+uint32_t tgs_get_evicted_dirty(tgs_ctx* ctx, uint32_t* blocks, uint32_t cap);
+/* slot -> global block id (-1 free), P entries */
+tgs_status tgs_get_slot_map(tgs_ctx* ctx, int64_t* slot_to_block);
+/* lowest gid*59+attr of a non-finite active gradient so far, UINT64_MAX if none */
+uint64_t tgs_nonfinite_index(tgs_ctx* ctx);
+/* newest version of global block k: resident slot if resident, else host tier
+ * (cold restart: m = v = 0 off the device).  Host buffers of B*59 fp32 each,
+ * any may be NULL. */
+tgs_status tgs_read_block(tgs_ctx* ctx, uint64_t k_global, float* theta, float* m, float* v);
+uint32_t tgs_step_count(tgs_ctx* ctx, uint64_t k_global);
+uint32_t tgs_num_local_blocks(const tgs_ctx* ctx);
+uint32_t tgs_pool_slots(const tgs_ctx* ctx);
+
+/* Frustum planes of a pinhole camera (R1): w2c row-major 4x4 world->camera
+ * (camera +z forward, +x right, +y down), intrinsics fx, fy, cx, cy, image
+ * width x height, near/far.  Computed in double, rounded to fp32. */
+tgs_status tgs_frustum_planes(const double w2c[16], double fx, double fy, double cx, double cy,
+                              uint32_t width, uint32_t height, double znear, double zfar,
+                              tgs_camera* out);
+
+const char* tgs_status_string(tgs_status s);
+const char* tgs_last_error(const tgs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIDEGS_H */

@@ -1,0 +1,103 @@
+// tidegs_internal.h -- device-state layout and kernel launchers shared by
+// tidegs_kernels.cu (sm_100a kernels) and tidegs_runtime.cu (host runtime).
+// Nothing here is shared with oracle/ (the two sides share no code).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tgs {
+
+constexpr uint32_t kDim = 59;
+constexpr uint32_t kMaxCams = 256;
+constexpr uint32_t kMaxAge = 1023;
+constexpr uint32_t kMaxBuckets = 2 * 2 * (kMaxAge + 2);  // rank x (in R_t ? 0 : 1)
+
+
+// cumulative counters, same order as tgs_stats
+enum Stat : int {
+  ST_ITER = 0, ST_VISIBLE, ST_RESIDENT, ST_ACTIVE_BLOCKS, ST_STAGE_IN, ST_EVICT, ST_EVICT_DIRTY,
+  ST_ACTIVE_ROWS, ST_H2D, ST_D2H, ST_FLUSH_BYTES, ST_FLUSH_BLOCKS, ST_READMIT, ST_COLD_UPD,
+  ST_TOTAL_UPD, ST_STREAK_SUM, ST_STREAK_CNT, ST_N
+};
+
+// per-activate counters written by the cull kernel (zeroed before it)
+enum Cnt : int { CNT_CAND = 0, CNT_K = 1, CNT_N = 4 };
+
+// plan header: written by k_plan into host-mapped pinned memory (and a device copy)
+struct PlanHdr {
+  uint32_t nK, nR, nSp, nSm, nA, nOm, nfree, fallback;
+  uint32_t n_dirty;   // written by k_evict
+  uint32_t pad[7];
+};
+
+// per active (R n K) entry, written by k_adam_prologue
+struct AdamEnt {
+  uint32_t step;   // new step count, 0 = no active row (block untouched)
+  uint32_t rows;   // logical rows of the block
+  float bc1;       // 1 - beta1^step   (R9)
+  float ibs;       // 1 / sqrt(1 - beta2^step)
+};
+
+struct Dev {
+  // sizes
+  uint64_t N;
+  uint32_t B, Kloc, W, P, PW, C, J_max, n_arr, G, rank, max_age, n_lut_cols;
+  uint32_t quota_num, quota_den;
+  int32_t tide, cold;
+  uint64_t rec_floats;   // B*59
+  // per local block
+  float4* bounds;        // [Kloc] (cx,cy,cz,r)
+  int32_t* last_access;  // [Kloc] -1 = never (R4)
+  uint32_t* step;        // [Kloc] Adam step count (R7)
+  int32_t* b2s;          // [Kloc] slot or -1
+  uint8_t* ever;         // [Kloc] admitted at least once (k_plan only; readmissions)
+  uint8_t* evicted;      // [Kloc] evicted at least once (k_evict only; cold-restart count)
+  int32_t* admit;        // [Kloc] activate index of last admission
+  // bitsets over local blocks, [W] words each
+  uint32_t* percam;      // [J_max][W]
+  uint32_t *Kb, *cand, *Q, *Sp, *Sm, *Om, *Ab;
+  uint32_t* R[2];        // R_t by parity
+  // per slot
+  int32_t* s2b;          // [P] local block or -1
+  uint32_t *occ, *dirty, *rel;  // [PW]
+  // plan outputs
+  uint32_t *sp_blk[2], *sp_slot[2];    // [C] S+ ascending and its slots (parity)
+  uint32_t *sm_blk[2], *sm_slot[2];    // [C] S- ascending and its slots (parity)
+  uint32_t *a_blk[2], *a_slot[2], *a_gid[2];  // [C] A = R n K (parity)
+  PlanHdr* hdr_dev;      // device copy of the header
+  PlanHdr* hdr_map;      // device alias of the mapped host header
+  uint32_t* sp_map;      // mapped host [C][2] (local id, slot) of S+
+  uint32_t* dirty_map;   // mapped host [C][2] (local id, slot) of dirty S-
+  // selection
+  uint16_t* rank_lut;    // [2][max_age+2]
+  uint32_t n_buckets;    // 2 * (number of distinct ranks)
+  uint32_t* cnt;         // [CNT_N]
+  unsigned long long* stats;      // [ST_N]
+  unsigned long long* nonfinite;  // lowest gid*59+attr
+  // Adam
+  AdamEnt* ent;          // [C]
+  float *lut_bc1, *lut_ibs;  // [lut_cap]
+  // pools
+  float* params;         // [P][3][B][59]
+  float* grads;          // [P][B][59]
+};
+
+struct AdamHyper {
+  float lr[kDim];
+  float b1, b2, omb1, omb2, eps;
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_cull(const Dev& d, const float* planes, uint32_t J, int32_t T, int parity,
+                        cudaStream_t s);
+cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s);
+cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s);
+cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
+cudaError_t launch_cold_init(const Dev& d, uint32_t nSp, int parity, cudaStream_t s);
+cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
+                                 cudaStream_t s);
+cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
+                        const AdamHyper& hp, int grid_ctas, cudaStream_t s);
+int adam_grid(int device);
+
+}  // namespace tgs

@@ -1,0 +1,713 @@
+// tidegs_kernels.cu -- sm_100a kernels of the TideGS working-set step.
+//
+//   k_cull           a1  Level-1 sphere-vs-6-plane cull, per-camera bitsets by
+//                        warp ballot, union K_{t+1}, candidate pool, recency stamp
+//                        (PAPER.md:196-208 Eq. Kt_def; Alg. 1 l.1-3)
+//   k_quota          a3  camera-balanced quota: top-q_j of K^{(j)} in score order
+//                        (R10), one CTA per camera
+//   k_plan           a2+a3  global Top-C fill, set differences S+/S-/Omega
+//                        (Alg. 1 l.6-8), slot allocation /
+//                        eviction (R13), active list A = R n K
+//   k_evict          a4  dirty S- records -> write-back list
+//   k_cold_init      a4  cold restart: zero moments of admitted slots
+//   k_adam_prologue  a5  per-block active-row count, step, dirty bit
+//   k_adam           a5  fused masked Adam, 128-bit coalesced (Eq. masked_update)
+//
+// Determinism: every choice (list order, Top-C, slot assignment) comes from
+// prefix sums over id-ordered bitsets, never from atomic arrival order; atomics
+// only carry commutative effects (or/and on bitmaps, integer adds, min).
+// Floating point: IEEE RN intrinsics in the exact order DESIGN.md §3 (R2, R9)
+// fixes; compiled without fast-math, FTZ off.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tidegs_internal.h"
+
+namespace tgs {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t block_rows(const Dev& d, uint32_t l) {
+  const uint64_t lo = ((uint64_t)l * d.G + d.rank) * d.B;
+  if (lo >= d.N) return 0u;
+  const uint64_t r = d.N - lo;
+  return r < d.B ? (uint32_t)r : d.B;
+}
+
+// Exclusive block-wide scan of one u32 per thread.  NT threads; scratch >= 33 words.
+template <int NT>
+__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t& total, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t y = lane < NT / 32 ? sh[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t z = __shfl_up_sync(kFull, y, o);
+      if (lane >= o) y += z;
+    }
+    sh[lane] = y;
+  }
+  __syncthreads();
+  const uint32_t pre = wid ? sh[wid - 1] : 0u;
+  total = sh[NT / 32 - 1];
+  __syncthreads();
+  return pre + x - v;
+}
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* sh) {
+  uint32_t t;
+  block_scan<NT>(v, t, sh);
+  return t;
+}
+
+// Selection key bucket of local block l (R4, R11): rank of (m, b) in descending
+// score s(k) = lam*1[k in K_{t+1}] + (1-lam)*gamma^age (host LUT, exact double
+// ties kept), then resident-first.  Ascending bucket, then ascending id, is the
+// total key order of the oracle's comparator.
+__device__ __forceinline__ uint32_t bucket_of(const Dev& d, uint32_t l, bool inK, bool inR,
+                                              int32_t T) {
+  const int32_t la = d.last_access[l];
+  uint32_t b;
+  if (la < 0) {
+    b = d.max_age + 1;  // never accessed: Recency 0
+  } else {
+    const int32_t age = (T - 1) - la;
+    b = (uint32_t)age > d.max_age ? d.max_age : (uint32_t)age;
+  }
+  const uint32_t r = d.rank_lut[(inK ? d.n_lut_cols : 0u) + b];
+  return 2u * r + (inR ? 0u : 1u);
+}
+
+// CTA-wide Top-n over the candidate bits word(w), w in [0, nw), in key order
+// (bucket asc, id asc).  emit(w, bits) is called once per word with a non-empty
+// selection.  smem: hist[kMaxBuckets], sh[40].
+template <int NT, class WordFn, class EmitFn>
+__device__ void select_top(const Dev& d, uint32_t n, uint32_t nw, int32_t T, uint32_t* hist,
+                           uint32_t* sh, const WordFn& word, const uint32_t* Rcur,
+                           bool allK, const EmitFn& emit) {
+  if (n == 0) return;
+  const uint32_t NB = d.n_buckets;
+  for (uint32_t i = threadIdx.x; i < NB; i += NT) hist[i] = 0;
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w < nw; w += NT) {
+    uint32_t bits = word(w);
+    const uint32_t rw = Rcur[w];
+    const uint32_t kw = allK ? kFull : d.Kb[w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t l = 32u * w + b;
+      atomicAdd(&hist[bucket_of(d, l, (kw >> b) & 1u, (rw >> b) & 1u, T)], 1u);
+    }
+  }
+  __syncthreads();
+  // threshold bucket: first bucket whose inclusive prefix reaches n
+  const uint32_t per = (NB + NT - 1) / NT;
+  const uint32_t b0 = threadIdx.x * per;
+  uint32_t mine = 0;
+  for (uint32_t i = 0; i < per; ++i)
+    if (b0 + i < NB) mine += hist[b0 + i];
+  uint32_t total;
+  uint32_t pre = block_scan<NT>(mine, total, sh);
+  if (threadIdx.x == 0) {
+    sh[34] = NB;  // threshold: all buckets < thr selected entirely
+    sh[35] = 0;   // how many of bucket thr (lowest ids first)
+  }
+  __syncthreads();
+  if (total > n) {
+    for (uint32_t i = 0; i < per && b0 + i < NB; ++i) {
+      const uint32_t h = hist[b0 + i];
+      if (pre < n && n <= pre + h) {
+        sh[34] = b0 + i;
+        sh[35] = n - pre;
+      }
+      pre += h;
+    }
+  }
+  __syncthreads();
+  const uint32_t thr = sh[34], need = sh[35];
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nw; base += NT) {
+    const uint32_t w = base + threadIdx.x;
+    uint32_t sel = 0, tie = 0;
+    if (w < nw) {
+      uint32_t bits = word(w);
+      const uint32_t rw = Rcur[w];
+      const uint32_t kw = allK ? kFull : d.Kb[w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t bk = bucket_of(d, 32u * w + b, (kw >> b) & 1u, (rw >> b) & 1u, T);
+        if (bk < thr) sel |= 1u << b;
+        else if (bk == thr) tie |= 1u << b;
+      }
+    }
+    uint32_t tot;
+    const uint32_t off = block_scan<NT>(__popc(tie), tot, sh);
+    uint32_t start = carry + off;
+    while (tie && start < need) {  // lowest ids of the threshold bucket
+      const uint32_t bit = tie & (0u - tie);
+      sel |= bit;
+      tie ^= bit;
+      ++start;
+    }
+    if (sel) emit(w, sel);
+    carry += tot;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------- a1 cull
+__global__ void __launch_bounds__(256) k_cull(Dev d, const float4* __restrict__ planes,
+                                              uint32_t J, int32_t T, int parity) {
+  __shared__ float4 pl[kMaxCams * 6];
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = planes[i];
+  __syncthreads();
+  const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t w = l >> 5, lane = l & 31;
+  const bool in = l < d.Kloc;
+  float4 c = in ? d.bounds[l] : make_float4(0.f, 0.f, 0.f, 0.f);
+  // Alg. 1 l.2 (R12): blocks accessed by the previous batch (R_t n K_t) get age 0
+  if (in && T > 0 && ((d.Ab[w] >> lane) & 1u)) d.last_access[l] = T - 1;
+  const float nr = -c.w;
+  uint32_t uni = 0;
+  for (uint32_t j = 0; j < J; ++j) {
+    bool vis = in;
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const float4 n = pl[j * 6 + p];
+      // R2: d = n.c + d0 as the fmaf chain x -> y -> z with d0 the first addend
+      const float dist = __fmaf_rn(n.z, c.z, __fmaf_rn(n.y, c.y, __fmaf_rn(n.x, c.x, n.w)));
+      if (dist < nr) vis = false;  // cull iff d < -r_k (NaN stays visible)
+    }
+    const uint32_t bits = __ballot_sync(kFull, vis);
+    if (lane == 0) d.percam[(size_t)j * d.W + w] = bits;
+    uni |= bits;
+  }
+  if (lane == 0 && w < d.W) {
+    d.Kb[w] = uni;  // Eq. Kt_def: K_{t+1} = U_j K^{(j)}
+    const uint32_t cw = d.tide ? (d.R[parity][w] | uni) : uni;  // C_t = R_t u K_{t+1}
+    d.cand[w] = cw;
+    d.Q[w] = 0u;
+    atomicAdd(&d.cnt[CNT_CAND], (uint32_t)__popc(cw));
+    atomicAdd(&d.cnt[CNT_K], (uint32_t)__popc(uni));
+  }
+}
+
+// ------------------------------------------------------ a3 camera quota (R10)
+constexpr int kQuotaNT = 512;
+__global__ void __launch_bounds__(kQuotaNT) k_quota(Dev d, uint32_t J, int32_t T, int parity) {
+  __shared__ uint32_t hist[kMaxBuckets];
+  __shared__ uint32_t sh[40];
+  if (d.cnt[CNT_CAND] <= d.C) return;  // #C_t <= C: nothing to select
+  const uint32_t j = blockIdx.x;
+  const uint32_t* pc = d.percam + (size_t)j * d.W;
+  uint32_t mine = 0;
+  for (uint32_t w = threadIdx.x; w < d.W; w += kQuotaNT) mine += __popc(pc[w]);
+  const uint32_t nj = block_sum<kQuotaNT>(mine, sh);
+  const uint64_t q = ((uint64_t)d.C * d.quota_num) / ((uint64_t)d.quota_den * J);
+  const uint32_t qj = (uint32_t)(nj < q ? nj : q);
+  select_top<kQuotaNT>(
+      d, qj, d.W, T, hist, sh, [&](uint32_t w) { return pc[w]; }, d.R[parity], true,
+      [&](uint32_t w, uint32_t bits) { atomicOr(&d.Q[w], bits); });
+}
+
+// ------------------------------------- a2 + a3 fill, delta, slots, A list
+constexpr int kPlanNT = 1024;
+__global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) {
+  __shared__ uint32_t hist[kMaxBuckets];
+  __shared__ uint32_t sh[40];
+  __shared__ unsigned long long acc[4];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t W = d.W;
+  const uint32_t* R = d.R[parity];
+  uint32_t* Rn = d.R[parity ^ 1];
+  const uint32_t n_cand = d.cnt[CNT_CAND];
+  if (tid < 4) acc[tid] = 0;
+
+  // ---- Alg. 1 l.6: R_{t+1} = CameraBalancedTopC(...)
+  if (n_cand <= d.C) {
+    for (uint32_t w = tid; w < W; w += kPlanNT) Rn[w] = d.cand[w];
+  } else {
+    uint32_t mine = 0;
+    for (uint32_t w = tid; w < W; w += kPlanNT) {
+      const uint32_t q = d.Q[w];
+      Rn[w] = q;
+      mine += __popc(q);
+    }
+    const uint32_t nQ = block_sum<kPlanNT>(mine, sh);
+    const uint32_t nfill = d.C - nQ;
+    select_top<kPlanNT>(
+        d, nfill, W, T, hist, sh, [&](uint32_t w) { return d.cand[w] & ~d.Q[w]; }, R, false,
+        [&](uint32_t w, uint32_t bits) { Rn[w] |= bits; });
+  }
+  __syncthreads();
+
+  // ---- Alg. 1 l.7-8: Omega, S+, S-; A = R_{t+1} n K_{t+1}
+  uint32_t nR_mine = 0, nOm_mine = 0;
+  for (uint32_t w = tid; w < W; w += kPlanNT) {
+    const uint32_t r = R[w], rn = Rn[w];
+    const uint32_t sp = d.tide ? (rn & ~r) : rn;
+    const uint32_t sm = d.tide ? (r & ~rn) : r;
+    const uint32_t om = d.tide ? (r & rn) : 0u;
+    d.Sp[w] = sp;
+    d.Sm[w] = sm;
+    d.Om[w] = om;
+    d.Ab[w] = rn & d.Kb[w];
+    nR_mine += __popc(rn);
+    nOm_mine += __popc(om);
+  }
+  const uint32_t nR = block_sum<kPlanNT>(nR_mine, sh);
+  const uint32_t nOm = block_sum<kPlanNT>(nOm_mine, sh);
+
+  // ---- compaction of S+ and S- (ascending ids) by prefix sums
+  uint32_t* smb = d.sm_blk[parity];
+  uint32_t* sms = d.sm_slot[parity];
+  uint32_t* spb = d.sp_blk[parity];
+  uint32_t* sps = d.sp_slot[parity];
+  uint32_t cSp = 0, cSm = 0;
+  for (uint32_t base = 0; base < W; base += kPlanNT) {
+    const uint32_t w = base + tid;
+    uint32_t sp = w < W ? d.Sp[w] : 0u, sm = w < W ? d.Sm[w] : 0u;
+    uint32_t tp, tm;
+    uint32_t op = cSp + block_scan<kPlanNT>(__popc(sp), tp, sh);
+    uint32_t om = cSm + block_scan<kPlanNT>(__popc(sm), tm, sh);
+    while (sp) {
+      const int b = __ffs(sp) - 1;
+      sp &= sp - 1;
+      spb[op++] = 32u * w + b;
+    }
+    while (sm) {
+      const int b = __ffs(sm) - 1;
+      sm &= sm - 1;
+      const uint32_t l = 32u * w + b;
+      smb[om] = l;
+      sms[om] = (uint32_t)d.b2s[l];
+      ++om;
+    }
+    cSp += tp;
+    cSm += tm;
+  }
+  const uint32_t nSp = cSp, nSm = cSm;
+  __syncthreads();
+
+  // ---- slot allocation (R13): the i-th S+ block takes the i-th lowest slot not
+  //      held by R_t; if short, the slots S- releases, ascending.
+  uint32_t nfree = 0;
+  for (uint32_t base = 0; base < d.PW; base += kPlanNT) {
+    const uint32_t w = base + tid;
+    uint32_t fr = 0;
+    if (w < d.PW) {
+      const uint32_t valid = (32u * (w + 1) <= d.P) ? kFull : ((1u << (d.P - 32u * w)) - 1u);
+      fr = ~d.occ[w] & valid;
+    }
+    uint32_t tot;
+    uint32_t r = nfree + block_scan<kPlanNT>(__popc(fr), tot, sh);
+    while (fr && r < nSp) {
+      const int b = __ffs(fr) - 1;
+      fr &= fr - 1;
+      sps[r++] = 32u * w + b;
+    }
+    nfree += tot;
+  }
+  const uint32_t fallback = nfree < nSp ? 1u : 0u;
+  if (fallback) {
+    for (uint32_t w = tid; w < d.PW; w += kPlanNT) d.rel[w] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < nSm; i += kPlanNT) atomicOr(&d.rel[sms[i] >> 5], 1u << (sms[i] & 31));
+    __syncthreads();
+    uint32_t c = 0;
+    for (uint32_t base = 0; base < d.PW; base += kPlanNT) {
+      const uint32_t w = base + tid;
+      uint32_t fr = w < d.PW ? d.rel[w] : 0u;
+      uint32_t tot;
+      uint32_t r = nfree + c + block_scan<kPlanNT>(__popc(fr), tot, sh);
+      while (fr && r < nSp) {
+        const int b = __ffs(fr) - 1;
+        fr &= fr - 1;
+        sps[r++] = 32u * w + b;
+      }
+      c += tot;
+    }
+  }
+  __syncthreads();
+
+  // ---- eviction bookkeeping (stage 4; dirty write-back decided after Adam(t))
+  unsigned long long streak = 0;
+  for (uint32_t i = tid; i < nSm; i += kPlanNT) {
+    const uint32_t l = smb[i], s = sms[i];
+    d.b2s[l] = -1;
+    d.s2b[s] = -1;
+    atomicAnd(&d.occ[s >> 5], ~(1u << (s & 31)));
+    streak += (unsigned long long)(T - d.admit[l]);
+  }
+  __syncthreads();
+  // ---- admission bookkeeping (stage 2); cold restart resets the step
+  unsigned long long readmit = 0;
+  for (uint32_t i = tid; i < nSp; i += kPlanNT) {
+    const uint32_t l = spb[i], s = sps[i];
+    d.b2s[l] = (int32_t)s;
+    d.s2b[s] = (int32_t)l;
+    atomicOr(&d.occ[s >> 5], 1u << (s & 31));
+    if (d.ever[l]) ++readmit;
+    d.ever[l] = 1;
+    d.admit[l] = T;
+    if (d.cold) d.step[l] = 0u;
+    d.sp_map[2 * i] = l;
+    d.sp_map[2 * i + 1] = s;
+  }
+  if (streak) atomicAdd(&acc[0], streak);
+  if (readmit) atomicAdd(&acc[1], readmit);
+  __syncthreads();
+
+  // ---- A = R_{t+1} n K_{t+1} with slots, ascending (what Adam and C1 consume)
+  uint32_t* ab = d.a_blk[parity];
+  uint32_t* as = d.a_slot[parity];
+  uint32_t* ag = d.a_gid[parity];
+  uint32_t cA = 0;
+  for (uint32_t base = 0; base < W; base += kPlanNT) {
+    const uint32_t w = base + tid;
+    uint32_t a = w < W ? d.Ab[w] : 0u;
+    uint32_t tot;
+    uint32_t o = cA + block_scan<kPlanNT>(__popc(a), tot, sh);
+    while (a) {
+      const int b = __ffs(a) - 1;
+      a &= a - 1;
+      const uint32_t l = 32u * w + b;
+      ab[o] = l;
+      as[o] = (uint32_t)d.b2s[l];
+      ag[o] = l * d.G + d.rank;
+      ++o;
+    }
+    cA += tot;
+  }
+  if (tid == 0) {
+    PlanHdr h{};
+    h.nK = d.cnt[CNT_K];
+    h.nR = nR;
+    h.nSp = nSp;
+    h.nSm = nSm;
+    h.nA = cA;
+    h.nOm = nOm;
+    h.nfree = nfree;
+    h.fallback = fallback;
+    h.n_dirty = 0;
+    *d.hdr_dev = h;
+    *d.hdr_map = h;
+    unsigned long long* st = d.stats;
+    atomicAdd(&st[ST_ITER], 1ull);
+    atomicAdd(&st[ST_VISIBLE], (unsigned long long)h.nK);
+    atomicAdd(&st[ST_RESIDENT], (unsigned long long)nR);
+    atomicAdd(&st[ST_ACTIVE_BLOCKS], (unsigned long long)cA);
+    atomicAdd(&st[ST_STAGE_IN], (unsigned long long)nSp);
+    atomicAdd(&st[ST_EVICT], (unsigned long long)nSm);
+    atomicAdd(&st[ST_H2D], (unsigned long long)nSp * d.rec_floats * 4ull * d.n_arr);
+    atomicAdd(&st[ST_STREAK_SUM], acc[0]);
+    atomicAdd(&st[ST_STREAK_CNT], (unsigned long long)nSm);
+    atomicAdd(&st[ST_READMIT], acc[1]);
+  }
+}
+
+// ---------------------------------------- a4 dirty S- -> write-back list
+constexpr int kEvictNT = 1024;
+__global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int parity) {
+  __shared__ uint32_t sh[40];
+  const uint32_t* smb = d.sm_blk[parity];
+  const uint32_t* sms = d.sm_slot[parity];
+  uint32_t c = 0;
+  for (uint32_t base = 0; base < nSm; base += kEvictNT) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t dirty = 0, l = 0, s = 0;
+    if (i < nSm) {
+      l = smb[i];
+      s = sms[i];
+      d.evicted[l] = 1;  // after Adam(t): the cold-restart counter of Adam(t) saw the old value
+      dirty = (d.dirty[s >> 5] >> (s & 31)) & 1u;  // dirty only if updated
+    }
+    uint32_t tot;
+    const uint32_t o = c + block_scan<kEvictNT>(dirty, tot, sh);
+    if (dirty) {
+      d.dirty_map[2 * o] = l;
+      d.dirty_map[2 * o + 1] = s;
+      atomicAnd(&d.dirty[s >> 5], ~(1u << (s & 31)));
+    }
+    c += tot;
+  }
+  if (threadIdx.x == 0) {
+    d.hdr_map->n_dirty = c;
+    d.hdr_dev->n_dirty = c;
+    atomicAdd(&d.stats[ST_EVICT_DIRTY], (unsigned long long)c);
+    atomicAdd(&d.stats[ST_D2H], (unsigned long long)c * d.rec_floats * 4ull * d.n_arr);
+  }
+}
+
+// ---------------------------------- a4 cold restart: m = v = 0 in new slots
+__global__ void __launch_bounds__(256) k_cold_init(Dev d, int parity) {
+  const uint32_t i = blockIdx.y;
+  const uint32_t s = d.sp_slot[parity][i];
+  float4* mv = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * d.rec_floats + d.rec_floats);
+  const uint32_t n4 = (uint32_t)(2 * d.rec_floats / 4);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += gridDim.x * blockDim.x)
+    __stcs(mv + e, z);
+}
+
+// ------------------------------------------------ a5 prologue (per block)
+__global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int parity,
+                                                       const uint32_t* __restrict__ mask) {
+  __shared__ unsigned long long acc[3];
+  if (threadIdx.x < 3) acc[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (i < nA) {
+    const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+    const uint32_t rows = block_rows(d, l);
+    const uint32_t nw = (d.B + 31) / 32;
+    uint32_t n = 0;
+    for (uint32_t w = lane; w < nw; w += 32) {
+      if (32u * w >= rows) break;
+      const uint32_t valid = (32u * (w + 1) <= rows) ? kFull : ((1u << (rows - 32u * w)) - 1u);
+      const uint32_t word = mask ? mask[(size_t)s * nw + w] : kFull;
+      n += __popc(word & valid);
+    }
+    n = __reduce_add_sync(kFull, n);
+    if (lane == 0) {
+      AdamEnt e{};
+      e.rows = rows;
+      if (n > 0) {  // block holds rows of I_t: update, count, mark dirty
+        const uint32_t before = d.step[l];
+        const uint32_t ns = before + 1u;  // R7: per-block step counter
+        d.step[l] = ns;
+        atomicOr(&d.dirty[s >> 5], 1u << (s & 31));
+        e.step = ns;
+        e.bc1 = d.lut_bc1[ns];
+        e.ibs = d.lut_ibs[ns];
+        atomicAdd(&acc[0], 1ull);
+        atomicAdd(&acc[1], (unsigned long long)n);
+        if (d.cold && before == 0u && d.evicted[l]) atomicAdd(&acc[2], 1ull);
+      }
+      d.ent[i] = e;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (acc[0]) atomicAdd(&d.stats[ST_TOTAL_UPD], acc[0]);
+    if (acc[1]) atomicAdd(&d.stats[ST_ACTIVE_ROWS], acc[1]);
+    if (acc[2]) atomicAdd(&d.stats[ST_COLD_UPD], acc[2]);
+  }
+}
+
+// ------------------------------------------------------- a5 masked Adam
+// A warp owns a contiguous range of 4-row quads (4 rows = 944 B = 59 float4
+// per array); lane f and f+32 load float4 #f of theta, m, v, g (128-bit,
+// coalesced, streaming).  Element e = 4f+q of the quad belongs to row e/59 and
+// attribute e%59, so per-lane row/attribute maps are loop-invariant.
+constexpr int kAdamNT = 256;
+__global__ void __launch_bounds__(kAdamNT) k_adam(Dev d, uint32_t nA, int parity,
+                                                  const uint32_t* __restrict__ mask,
+                                                  AdamHyper hp) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t QB = d.B / 4;
+  const uint64_t total = (uint64_t)nA * QB;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kAdamNT / 32);
+  const uint64_t wid = (uint64_t)blockIdx.x * (kAdamNT / 32) + (threadIdx.x >> 5);
+  const uint64_t chunk = (total + nwarps - 1) / nwarps;
+  uint64_t q0 = wid * chunk;
+  const uint64_t q1 = q0 + chunk < total ? q0 + chunk : total;
+  if (q0 >= q1) return;
+
+  // loop-invariant per-lane element maps (f0 = lane, f1 = lane + 32 < 59)
+  const bool has1 = lane + 32 < 59;
+  uint32_t row0 = 0, row1 = 0;  // 2 bits per component: row of element q
+  float lr0[4], lr1[4];
+  uint32_t a0[4], a1[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
+    const uint32_t r0 = e0 / 59, r1 = has1 ? e1 / 59 : 3u;
+    a0[q] = e0 - 59 * r0;
+    a1[q] = has1 ? e1 - 59 * r1 : 0u;
+    row0 |= r0 << (2 * q);
+    row1 |= r1 << (2 * q);
+    lr0[q] = hp.lr[a0[q]];
+    lr1[q] = hp.lr[a1[q]];
+  }
+  const uint32_t nw = (d.B + 31) / 32;
+  const size_t rf = d.rec_floats;
+
+  int64_t cur = -1;
+  AdamEnt ent{};
+  float ss0[4], ss1[4];
+  const float4 *pg = nullptr;
+  float4 *pt = nullptr, *pm = nullptr, *pv = nullptr;
+  const uint32_t* pmask = nullptr;
+  uint64_t gid0 = 0;
+
+  for (uint64_t qi = q0; qi < q1; ++qi) {
+    const uint64_t i = qi / QB;
+    const uint32_t quad = (uint32_t)(qi - i * QB);
+    if ((int64_t)i != cur) {
+      cur = (int64_t)i;
+      ent = d.ent[i];
+      const uint32_t s = d.a_slot[parity][i];
+      pt = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf);
+      pm = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf + rf);
+      pv = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf + 2 * rf);
+      pg = reinterpret_cast<const float4*>(d.grads + (size_t)s * rf);
+      pmask = mask ? mask + (size_t)s * nw : nullptr;
+      gid0 = (uint64_t)d.a_gid[parity][i] * d.B;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // ss_a = lr[a] / (1 - beta1^s)  (R9)
+        ss0[q] = __fdiv_rn(lr0[q], ent.bc1);
+        ss1[q] = __fdiv_rn(lr1[q], ent.bc1);
+      }
+    }
+    if (ent.step == 0u) continue;  // no active row in this block: untouched
+    const uint32_t r0 = 4u * quad;
+    if (r0 >= ent.rows) continue;
+    uint32_t act = (ent.rows - r0) >= 4u ? 0xFu : ((1u << (ent.rows - r0)) - 1u);
+    if (pmask) act &= (pmask[r0 >> 5] >> (r0 & 31)) & 0xFu;
+    if (act == 0u) continue;  // warp-uniform
+    const size_t f0 = (size_t)quad * 59 + lane, f1 = f0 + 32;
+    const float4 g0 = __ldcs(pg + f0);
+    const float4 g1 = has1 ? __ldcs(pg + f1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 t0 = __ldcs(pt + f0), m0 = __ldcs(pm + f0), v0 = __ldcs(pv + f0);
+    float4 t1 = make_float4(0.f, 0.f, 0.f, 0.f), m1 = t1, v1 = t1;
+    if (has1) {
+      t1 = __ldcs(pt + f1);
+      m1 = __ldcs(pm + f1);
+      v1 = __ldcs(pv + f1);
+    }
+    // R20: a row with any non-finite gradient is skipped (and reported)
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    uint32_t bad = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!isfinite(gg[q])) bad |= 1u << ((row0 >> (2 * q)) & 3u);
+      if (has1 && !isfinite(gg[4 + q])) bad |= 1u << ((row1 >> (2 * q)) & 3u);
+    }
+    bad = __reduce_or_sync(kFull, bad);
+    if (bad & act) {  // rare path: lowest gid*59+attr over active rows
+      unsigned long long best = ~0ull;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t ra = (row0 >> (2 * q)) & 3u, rb = (row1 >> (2 * q)) & 3u;
+        if (((act >> ra) & 1u) && !isfinite(gg[q])) {
+          const unsigned long long idx = (gid0 + r0 + ra) * 59ull + a0[q];
+          best = idx < best ? idx : best;
+        }
+        if (has1 && ((act >> rb) & 1u) && !isfinite(gg[4 + q])) {
+          const unsigned long long idx = (gid0 + r0 + rb) * 59ull + a1[q];
+          best = idx < best ? idx : best;
+        }
+      }
+      if (best != ~0ull) atomicMin(d.nonfinite, best);
+    }
+    const uint32_t upd = act & ~bad;
+    if (upd == 0u) continue;
+    float th[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+    float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t rr = k < 4 ? (row0 >> (2 * k)) & 3u : (row1 >> (2 * (k - 4))) & 3u;
+      if (!((upd >> rr) & 1u)) continue;  // Eq. masked_update: unchanged off I_t
+      const float g = gg[k];
+      // R9 prescribed order, IEEE RN, no contraction
+      float mt = __fmul_rn(hp.b1, mm[k]);
+      mt = __fadd_rn(mt, __fmul_rn(hp.omb1, g));
+      const float g2 = __fmul_rn(g, g);
+      float vt = __fmul_rn(hp.b2, vv[k]);
+      vt = __fadd_rn(vt, __fmul_rn(hp.omb2, g2));
+      mm[k] = mt;
+      vv[k] = vt;
+      float den = __fmul_rn(__fsqrt_rn(vt), ent.ibs);
+      den = __fadd_rn(den, hp.eps);
+      const float u = __fdiv_rn(mt, den);
+      const float ss = k < 4 ? ss0[k] : ss1[k - 4];
+      th[k] = __fsub_rn(th[k], __fmul_rn(ss, u));
+    }
+    __stcs(pt + f0, make_float4(th[0], th[1], th[2], th[3]));
+    __stcs(pm + f0, make_float4(mm[0], mm[1], mm[2], mm[3]));
+    __stcs(pv + f0, make_float4(vv[0], vv[1], vv[2], vv[3]));
+    if (has1) {
+      __stcs(pt + f1, make_float4(th[4], th[5], th[6], th[7]));
+      __stcs(pm + f1, make_float4(mm[4], mm[5], mm[6], mm[7]));
+      __stcs(pv + f1, make_float4(vv[4], vv[5], vv[6], vv[7]));
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers
+cudaError_t launch_cull(const Dev& d, const float* planes, uint32_t J, int32_t T, int parity,
+                        cudaStream_t s) {
+  if (d.Kloc == 0) return cudaSuccess;
+  const uint32_t grid = (d.Kloc + 255) / 256;
+  k_cull<<<grid, 256, 0, s>>>(d, reinterpret_cast<const float4*>(planes), J, T, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s) {
+  if (J == 0 || d.Kloc == 0) return cudaSuccess;
+  k_quota<<<J, kQuotaNT, 0, s>>>(d, J, T, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s) {
+  k_plan<<<1, kPlanNT, 0, s>>>(d, T, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) {
+  k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cold_init(const Dev& d, uint32_t nSp, int parity, cudaStream_t s) {
+  if (nSp == 0) return cudaSuccess;
+  dim3 grid(16, nSp);
+  k_cold_init<<<grid, 256, 0, s>>>(d, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
+                                 cudaStream_t s) {
+  if (nA == 0) return cudaSuccess;
+  const uint32_t grid = (nA + 7) / 8;
+  k_adam_prologue<<<grid, 256, 0, s>>>(d, nA, parity, mask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
+                        const AdamHyper& hp, int grid_ctas, cudaStream_t s) {
+  if (nA == 0) return cudaSuccess;
+  const uint64_t quads = (uint64_t)nA * (d.B / 4);
+  const uint64_t need = (quads + (kAdamNT / 32) - 1) / (kAdamNT / 32);
+  const int grid = (int)(need < (uint64_t)grid_ctas ? need : (uint64_t)grid_ctas);
+  k_adam<<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp);
+  return cudaGetLastError();
+}
+
+int adam_grid(int device) {
+  int sms = 148, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adam, kAdamNT, 0);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+}  // namespace tgs

@@ -1,0 +1,901 @@
+// tidegs_runtime.cu -- host runtime behind the C ABI of include/tidegs.h.
+//
+// Owns the pinned host tier (one shard of Theta, M, V as block records), the
+// device slot pool, the streams/events of the pipeline and the host side of
+// the plan readback.  Per activate:
+//
+//   plan stream    : H2D planes -> k_cull -> k_quota -> k_plan      (a1-a3)
+//   host           : wait for the plan only (not for the previous Adam)
+//   h2d stream     : wait(previous write-back) -> record copies S+  (a4 gather,
+//                    copy engines, pinned host tier -> slots) -> ready
+//   compute stream : [after Adam(t)] k_evict (dirty S- list)        (a4)
+//   host           : wait for k_evict only if |S-| > 0
+//   d2h stream     : dirty S- records slots -> host tier            (a4 scatter)
+//   step_adam      : compute waits ready; k_adam_prologue; k_adam   (a5)
+//
+// S+ always lands in slots that R_t does not hold (R13), so the gather of
+// batch t+1 overlaps Adam of batch t without a hazard; the only orderings are
+// write-back(t) -> gather(t+1) (slot reuse, re-admitted records) and
+// Adam(t) -> write-back(t+1) (dirty decision).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tidegs.h"
+#include "tidegs_internal.h"
+
+using namespace tgs;
+
+namespace {
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool armed = false;
+};
+
+}  // namespace
+
+struct tgs_ctx {
+  tgs_config cfg{};
+  Dev d{};
+  uint64_t K = 0;                 // global blocks
+  uint64_t rec_bytes = 0;         // B*59*4
+  int device = 0;
+  // allocator
+  tgs_allocator alloc{};
+  bool has_alloc = false;
+  std::vector<void*> dev_allocs;
+  // host tier: [Kloc][n_arr][B][59]
+  float* host = nullptr;
+  size_t host_bytes = 0;
+  // mapped pinned
+  PlanHdr* hdr = nullptr;         // host view
+  uint32_t* sp_map = nullptr;     // host view
+  uint32_t* dirty_map = nullptr;  // host view
+  float* planes_pinned = nullptr; // [2][kMaxCams*24]
+  float* planes_dev = nullptr;
+  // streams / events
+  cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
+  bool own_compute = false;
+  cudaEvent_t ev_plan = nullptr, ev_evict = nullptr, ev_d2h = nullptr, ev_ready = nullptr;
+  bool d2h_recorded = false;
+  // Adam LUT (bias corrections, R9)
+  std::vector<float> lut_bc1_h, lut_ibs_h;
+  float* lut_pinned = nullptr;     // [2][lut_cap]
+  uint32_t lut_cap = 0, lut_n = 0;
+  float lut_b1 = NAN, lut_b2 = NAN;
+  int adam_grid = 0;
+  // state
+  int32_t T = 0;                  // activates so far
+  int parity = 0;                 // parity of R_t (current)
+  int last_parity = 0;            // parity the last activate wrote lists into
+  bool can_step = false;
+  bool poisoned = false;
+  PlanHdr last{};                 // header of the last activate
+  uint64_t n_steps = 0;
+  uint64_t host_flush_bytes = 0, host_flush_blocks = 0;
+  std::string err;
+  // profiling
+  bool prof = false;
+  tgs_timing tm{};
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { cudaEvent_t a, b; int kind; uint64_t bytes; };
+  std::vector<Pending> pending;
+};
+
+namespace {
+
+void set_err(tgs_ctx* c, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  c->err = buf;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      c->poisoned = true;                                                             \
+      set_err(c, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+      return TGS_ECUDA;                                                               \
+    }                                                                                 \
+  } while (0)
+
+void* dalloc(tgs_ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~(size_t)255;
+  void* p = nullptr;
+  if (c->has_alloc) {
+    p = c->alloc.alloc(bytes, (void*)c->compute, c->alloc.user);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    p = nullptr;
+  }
+  if (p) c->dev_allocs.push_back(p);
+  return p;
+}
+
+template <class T>
+T* dalloc_t(tgs_ctx* c, size_t n, bool& ok) {
+  T* p = static_cast<T*>(dalloc(c, n * sizeof(T)));
+  if (!p) ok = false;
+  return p;
+}
+
+cudaEvent_t prof_event(tgs_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// kinds: 0 adam, 1 prologue, 2 plan, 3 h2d, 4 d2h, 5 evict
+void prof_begin(tgs_ctx* c, cudaStream_t s, Timer& t) {
+  if (!c->prof) return;
+  t.a = prof_event(c);
+  t.b = prof_event(c);
+  cudaEventRecord(t.a, s);
+  t.armed = true;
+}
+void prof_end(tgs_ctx* c, cudaStream_t s, Timer& t, int kind, uint64_t bytes = 0) {
+  if (!t.armed) return;
+  cudaEventRecord(t.b, s);
+  c->pending.push_back({t.a, t.b, kind, bytes});
+}
+void prof_collect(tgs_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) != cudaSuccess) ms = 0.f;
+    switch (p.kind) {
+      case 0: c->tm.adam_ms += ms; c->tm.adam_launches++; break;
+      case 1: c->tm.adam_prologue_ms += ms; break;
+      case 2: c->tm.plan_ms += ms; c->tm.plan_launches++; break;
+      case 3: c->tm.h2d_ms += ms; c->tm.h2d_batches++; c->tm.h2d_bytes += p.bytes; break;
+      case 4: c->tm.d2h_ms += ms; c->tm.d2h_batches++; c->tm.d2h_bytes += p.bytes; break;
+      case 5: c->tm.evict_ms += ms; break;
+    }
+    c->ev_pool.push_back(p.a);
+    c->ev_pool.push_back(p.b);
+  }
+  c->pending.clear();
+  cudaGetLastError();
+}
+
+// Host LUT of the selection key (R4, R5, R11): rank of every (m, b) pair by
+// descending score s = lam*m + (1-lam)*gamma^b, evaluated in double with
+// gamma^b by repeated multiplication; b = max_age+1 means never accessed
+// (Recency 0).  Pairs with equal doubles share a rank.
+void build_rank_lut(const tgs_config& g, std::vector<uint16_t>& lut, uint32_t& n_ranks) {
+  const uint32_t cols = g.max_age + 2;
+  std::vector<double> score(2 * cols);
+  for (uint32_t m = 0; m < 2; ++m) {
+    double rec = 1.0;
+    for (uint32_t b = 0; b < cols; ++b) {
+      const double recency = (b == cols - 1) ? 0.0 : rec;
+      score[m * cols + b] = g.lambda * (double)m + (1.0 - g.lambda) * recency;
+      rec *= g.gamma;
+    }
+  }
+  std::vector<double> uniq(score);
+  std::sort(uniq.begin(), uniq.end(), [](double a, double b) { return a > b; });
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  lut.resize(2 * cols);
+  for (uint32_t i = 0; i < 2 * cols; ++i)
+    lut[i] = (uint16_t)(std::lower_bound(uniq.begin(), uniq.end(), score[i],
+                                         [](double a, double b) { return a > b; }) -
+                        uniq.begin());
+  n_ranks = (uint32_t)uniq.size();
+}
+
+// bias-correction LUT entry s (R9): 1 - beta^s evaluated in double, rounded to fp32
+void lut_entry(float b1, float b2, uint32_t s, float& bc1, float& ibs) {
+  bc1 = (float)(1.0 - std::pow((double)b1, (double)s));
+  const float bc2 = (float)(1.0 - std::pow((double)b2, (double)s));
+  ibs = 1.0f / std::sqrt(bc2);
+}
+
+tgs_status ensure_lut(tgs_ctx* c, float b1, float b2, uint32_t need) {
+  // need: entries [0, need) must be valid
+  if (need > c->lut_cap) {
+    uint32_t cap = std::max<uint32_t>(c->lut_cap * 2, 1u << 16);
+    while (cap < need) cap *= 2;
+    CK(cudaStreamSynchronize(c->compute));
+    float *bc = nullptr, *ib = nullptr;
+    bool ok = true;
+    bc = dalloc_t<float>(c, cap, ok);
+    ib = dalloc_t<float>(c, cap, ok);
+    if (!ok) return TGS_ENOMEM;
+    if (c->lut_pinned) cudaFreeHost(c->lut_pinned);
+    CK(cudaHostAlloc((void**)&c->lut_pinned, sizeof(float) * 2 * cap, cudaHostAllocDefault));
+    c->d.lut_bc1 = bc;
+    c->d.lut_ibs = ib;
+    c->lut_cap = cap;
+    c->lut_n = 0;  // re-upload
+  }
+  if (!(b1 == c->lut_b1) || !(b2 == c->lut_b2)) {
+    CK(cudaStreamSynchronize(c->compute));  // pending uploads read the pinned mirror
+    c->lut_n = 0;
+    c->lut_b1 = b1;
+    c->lut_b2 = b2;
+  }
+  if (need > c->lut_n) {
+    for (uint32_t s = c->lut_n; s < need; ++s)
+      lut_entry(b1, b2, s, c->lut_pinned[s], c->lut_pinned[c->lut_cap + s]);
+    const size_t n = need - c->lut_n;
+    CK(cudaMemcpyAsync(c->d.lut_bc1 + c->lut_n, c->lut_pinned + c->lut_n, n * sizeof(float),
+                       cudaMemcpyHostToDevice, c->compute));
+    CK(cudaMemcpyAsync(c->d.lut_ibs + c->lut_n, c->lut_pinned + c->lut_cap + c->lut_n,
+                       n * sizeof(float), cudaMemcpyHostToDevice, c->compute));
+    c->lut_n = need;
+  }
+  return TGS_OK;
+}
+
+inline float* host_rec(tgs_ctx* c, uint32_t l) {
+  return c->host + (size_t)l * c->d.n_arr * c->d.rec_floats;
+}
+inline float* slot_rec(tgs_ctx* c, uint32_t s) {
+  return c->d.params + (size_t)s * 3 * c->d.rec_floats;
+}
+
+// Copy runs of (local id, slot) pairs, merging consecutive ids with
+// consecutive slots into one 2-D copy (host pitch n_arr*rec, slot pitch 3*rec).
+tgs_status issue_copies(tgs_ctx* c, const uint32_t* pairs, uint32_t n, bool to_device,
+                        cudaStream_t s) {
+  const size_t w = (size_t)c->d.n_arr * c->rec_bytes;  // bytes per record moved
+  const size_t hp = w, dp = 3 * c->rec_bytes;
+  uint32_t i = 0;
+  while (i < n) {
+    uint32_t j = i + 1;
+    while (j < n && pairs[2 * j] == pairs[2 * (j - 1)] + 1 && pairs[2 * j + 1] == pairs[2 * (j - 1) + 1] + 1)
+      ++j;
+    const uint32_t l = pairs[2 * i], sl = pairs[2 * i + 1], run = j - i;
+    if (hp == dp) {
+      if (to_device)
+        CK(cudaMemcpyAsync(slot_rec(c, sl), host_rec(c, l), w * run, cudaMemcpyHostToDevice, s));
+      else
+        CK(cudaMemcpyAsync(host_rec(c, l), slot_rec(c, sl), w * run, cudaMemcpyDeviceToHost, s));
+    } else {
+      if (to_device)
+        CK(cudaMemcpy2DAsync(slot_rec(c, sl), dp, host_rec(c, l), hp, w, run,
+                             cudaMemcpyHostToDevice, s));
+      else
+        CK(cudaMemcpy2DAsync(host_rec(c, l), hp, slot_rec(c, sl), dp, w, run,
+                             cudaMemcpyDeviceToHost, s));
+    }
+    c->tm.copy_calls++;
+    i = j;
+  }
+  return TGS_OK;
+}
+
+void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user, int nthreads) {
+  const uint32_t Kloc = c->d.Kloc;
+  const size_t rf = c->d.rec_floats;
+  const uint32_t B = c->d.B;
+  std::atomic<uint32_t> next{0};
+  auto work = [&]() {
+    for (;;) {
+      const uint32_t l0 = next.fetch_add(16);
+      if (l0 >= Kloc) break;
+      for (uint32_t l = l0; l < std::min<uint32_t>(l0 + 16, Kloc); ++l) {
+        float* dst = host_rec(c, l);
+        const uint64_t k = (uint64_t)l * c->cfg.world_size + c->cfg.rank;
+        if (rows) {
+          const uint64_t lo = k * B;
+          const uint64_t nr = std::min<uint64_t>(B, c->cfg.n_gaussians - lo);
+          std::memcpy(dst, rows + lo * kDim, nr * kDim * sizeof(float));
+          std::memset(dst + nr * kDim, 0, (rf - nr * kDim) * sizeof(float));
+        } else {
+          fill(user, k, dst);
+        }
+        if (c->d.n_arr == 3) std::memset(dst + rf, 0, 2 * rf * sizeof(float));  // m = v = 0
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < nthreads; ++i) th.emplace_back(work);
+  work();
+  for (auto& t : th) t.join();
+}
+
+tgs_status check(tgs_ctx* c) {
+  if (!c) return TGS_EINVAL;
+  if (c->poisoned) return TGS_EPOISONED;
+  return TGS_OK;
+}
+
+tgs_status sync_all(tgs_ctx* c) {
+  CK(cudaStreamSynchronize(c->plan));
+  CK(cudaStreamSynchronize(c->h2d));
+  CK(cudaStreamSynchronize(c->compute));
+  CK(cudaStreamSynchronize(c->d2h));
+  prof_collect(c);
+  return TGS_OK;
+}
+
+void destroy_impl(tgs_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* p : c->dev_allocs) {
+    if (c->has_alloc)
+      c->alloc.free(p, (void*)c->compute, c->alloc.user);
+    else
+      cudaFree(p);
+  }
+  if (c->host) cudaFreeHost(c->host);
+  if (c->hdr) cudaFreeHost(c->hdr);
+  if (c->sp_map) cudaFreeHost(c->sp_map);
+  if (c->dirty_map) cudaFreeHost(c->dirty_map);
+  if (c->planes_pinned) cudaFreeHost(c->planes_pinned);
+  if (c->lut_pinned) cudaFreeHost(c->lut_pinned);
+  for (cudaEvent_t e : {c->ev_plan, c->ev_evict, c->ev_d2h, c->ev_ready})
+    if (e) cudaEventDestroy(e);
+  for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaStream_t s : {c->plan, c->h2d, c->d2h}) if (s) cudaStreamDestroy(s);
+  cudaGetLastError();
+  delete c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tgs_status_string(tgs_status s) {
+  switch (s) {
+    case TGS_OK: return "ok";
+    case TGS_EINVAL: return "invalid argument";
+    case TGS_ESTATE: return "invalid call order";
+    case TGS_ENOMEM: return "out of memory";
+    case TGS_ECUDA: return "CUDA error";
+    case TGS_ENCCL: return "NCCL error";
+    case TGS_ENONFINITE: return "non-finite gradient";
+    case TGS_EPOISONED: return "context poisoned by an earlier CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* tgs_last_error(const tgs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fill_fn fill,
+                          void* fill_user, const float* bounds, const tgs_allocator* alloc,
+                          void* compute_stream, tgs_ctx** out) {
+  if (!cfg || !out || !bounds) return TGS_EINVAL;
+  const tgs_config& g = *cfg;
+  if (g.dim != kDim || g.block_size < 4 || g.block_size % 4 != 0 || g.capacity == 0 ||
+      g.n_gaussians == 0)
+    return TGS_EINVAL;
+  if (!(g.lambda >= 0.0 && g.lambda <= 1.0) || !(g.gamma > 0.0 && g.gamma < 1.0))
+    return TGS_EINVAL;
+  if (g.quota_den == 0 || g.quota_num > g.quota_den) return TGS_EINVAL;
+  if (g.world_size < 1 || g.rank < 0 || g.rank >= g.world_size) return TGS_EINVAL;
+  if (g.moments != TGS_MOMENTS_PERSIST && g.moments != TGS_MOMENTS_COLD_RESTART) return TGS_EINVAL;
+  if (g.max_cameras < 1 || g.max_cameras > kMaxCams || g.max_age > kMaxAge) return TGS_EINVAL;
+  if ((theta_rows == nullptr) == (fill == nullptr)) return TGS_EINVAL;
+  const uint32_t P = g.pool_slots ? g.pool_slots : 2u * g.capacity;
+  if (P < g.capacity) return TGS_EINVAL;
+  const uint64_t K = (g.n_gaussians + g.block_size - 1) / g.block_size;
+  const uint64_t Kloc64 = K > (uint64_t)g.rank ? (K - g.rank + g.world_size - 1) / g.world_size : 0;
+  if (Kloc64 > (1ull << 31) / 32) return TGS_EINVAL;
+  for (uint64_t k = 0; k < K; ++k) {
+    if (k % g.world_size != (uint64_t)g.rank) continue;
+    for (int i = 0; i < 4; ++i)
+      if (!std::isfinite(bounds[4 * k + i])) return TGS_EINVAL;
+    if (bounds[4 * k + 3] < 0.0f) return TGS_EINVAL;
+  }
+
+  tgs_ctx* c = new tgs_ctx();
+  c->cfg = g;
+  c->device = g.device;
+  c->K = K;
+  if (alloc && alloc->alloc && alloc->free) {
+    c->alloc = *alloc;
+    c->has_alloc = true;
+  }
+  Dev& d = c->d;
+  d.N = g.n_gaussians;
+  d.B = g.block_size;
+  d.Kloc = (uint32_t)Kloc64;
+  d.W = (d.Kloc + 31) / 32;
+  d.P = P;
+  d.PW = (P + 31) / 32;
+  d.C = g.capacity;
+  d.J_max = g.max_cameras;
+  d.n_arr = g.moments == TGS_MOMENTS_PERSIST ? 3u : 1u;
+  d.G = (uint32_t)g.world_size;
+  d.rank = (uint32_t)g.rank;
+  d.max_age = g.max_age;
+  d.n_lut_cols = g.max_age + 2;
+  d.quota_num = g.quota_num;
+  d.quota_den = g.quota_den;
+  d.tide = g.tide ? 1 : 0;
+  d.cold = g.moments == TGS_MOMENTS_COLD_RESTART ? 1 : 0;
+  d.rec_floats = (uint64_t)d.B * kDim;
+  c->rec_bytes = d.rec_floats * sizeof(float);
+
+  auto fail = [&](tgs_status st) {
+    destroy_impl(c);
+    return st;
+  };
+  if (cudaSetDevice(g.device) != cudaSuccess) return fail(TGS_ECUDA);
+  c->compute = (cudaStream_t)compute_stream;
+  if (cudaStreamCreateWithFlags(&c->plan, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(TGS_ECUDA);
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_evict, &c->ev_d2h, &c->ev_ready})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
+
+  // ---- host tier (pinned, block records)
+  c->host_bytes = (size_t)d.Kloc * d.n_arr * c->rec_bytes;
+  if (c->host_bytes &&
+      cudaHostAlloc((void**)&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess) {
+    c->host = nullptr;
+    cudaGetLastError();
+    return fail(TGS_ENOMEM);
+  }
+  int nth = g.init_threads > 0 ? g.init_threads : (int)std::thread::hardware_concurrency();
+  nth = std::max(1, std::min(nth, 128));
+  fill_host_tier(c, theta_rows, fill, fill_user, nth);
+
+  // ---- mapped pinned plan readback
+  if (cudaHostAlloc((void**)&c->hdr, sizeof(PlanHdr), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->sp_map, sizeof(uint32_t) * 2 * (size_t)std::max(d.C, 1u),
+                    cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->dirty_map, sizeof(uint32_t) * 2 * (size_t)std::max(d.C, 1u),
+                    cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 2 * kMaxCams * 24,
+                    cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TGS_ENOMEM);
+  }
+  std::memset(c->hdr, 0, sizeof(PlanHdr));
+  cudaHostGetDevicePointer((void**)&d.hdr_map, c->hdr, 0);
+  cudaHostGetDevicePointer((void**)&d.sp_map, c->sp_map, 0);
+  cudaHostGetDevicePointer((void**)&d.dirty_map, c->dirty_map, 0);
+
+  // ---- device state
+  bool ok = true;
+  const uint32_t Kl = std::max(d.Kloc, 1u), Wd = std::max(d.W, 1u), Cc = std::max(d.C, 1u);
+  d.bounds = dalloc_t<float4>(c, Kl, ok);
+  d.last_access = dalloc_t<int32_t>(c, Kl, ok);
+  d.step = dalloc_t<uint32_t>(c, Kl, ok);
+  d.b2s = dalloc_t<int32_t>(c, Kl, ok);
+  d.ever = dalloc_t<uint8_t>(c, Kl, ok);
+  d.evicted = dalloc_t<uint8_t>(c, Kl, ok);
+  d.admit = dalloc_t<int32_t>(c, Kl, ok);
+  d.percam = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
+  for (uint32_t** p : {&d.Kb, &d.cand, &d.Q, &d.Sp, &d.Sm, &d.Om, &d.Ab, &d.R[0], &d.R[1]})
+    *p = dalloc_t<uint32_t>(c, Wd, ok);
+  d.s2b = dalloc_t<int32_t>(c, P, ok);
+  d.occ = dalloc_t<uint32_t>(c, d.PW, ok);
+  d.dirty = dalloc_t<uint32_t>(c, d.PW, ok);
+  d.rel = dalloc_t<uint32_t>(c, d.PW, ok);
+  for (int p = 0; p < 2; ++p) {
+    d.sp_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.sp_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.sm_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.sm_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.a_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.a_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.a_gid[p] = dalloc_t<uint32_t>(c, Cc, ok);
+  }
+  d.hdr_dev = dalloc_t<PlanHdr>(c, 1, ok);
+  d.cnt = dalloc_t<uint32_t>(c, CNT_N, ok);
+  d.stats = dalloc_t<unsigned long long>(c, ST_N, ok);
+  d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
+  d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
+  c->planes_dev = dalloc_t<float>(c, kMaxCams * 24, ok);
+  std::vector<uint16_t> lut;
+  uint32_t n_ranks = 0;
+  build_rank_lut(g, lut, n_ranks);
+  d.n_buckets = 2 * n_ranks;
+  d.rank_lut = dalloc_t<uint16_t>(c, lut.size(), ok);
+  const size_t pool_floats = (size_t)P * 3 * d.rec_floats, grad_floats = (size_t)P * d.rec_floats;
+  d.params = dalloc_t<float>(c, pool_floats, ok);
+  d.grads = dalloc_t<float>(c, grad_floats, ok);
+  if (!ok) return fail(TGS_ENOMEM);
+
+  // ---- initial contents
+  std::vector<float4> bl(Kl);
+  for (uint32_t l = 0; l < d.Kloc; ++l) {
+    const float* b = bounds + 4 * ((uint64_t)l * g.world_size + g.rank);
+    bl[l] = make_float4(b[0], b[1], b[2], b[3]);
+  }
+  cudaStream_t s0 = c->plan;
+#define CKI(x) do { if ((x) != cudaSuccess) { set_err(c, "%s", #x); return fail(TGS_ECUDA); } } while (0)
+  CKI(cudaMemcpyAsync(d.bounds, bl.data(), sizeof(float4) * Kl, cudaMemcpyHostToDevice, s0));
+  CKI(cudaMemcpyAsync(d.rank_lut, lut.data(), sizeof(uint16_t) * lut.size(), cudaMemcpyHostToDevice, s0));
+  CKI(cudaMemsetAsync(d.last_access, 0xff, sizeof(int32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.step, 0, sizeof(uint32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.b2s, 0xff, sizeof(int32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.ever, 0, Kl, s0));
+  CKI(cudaMemsetAsync(d.evicted, 0, Kl, s0));
+  CKI(cudaMemsetAsync(d.admit, 0, sizeof(int32_t) * Kl, s0));
+  for (uint32_t* p : {d.Kb, d.cand, d.Q, d.Sp, d.Sm, d.Om, d.Ab, d.R[0], d.R[1]})
+    CKI(cudaMemsetAsync(p, 0, sizeof(uint32_t) * Wd, s0));
+  CKI(cudaMemsetAsync(d.percam, 0, sizeof(uint32_t) * (size_t)d.J_max * Wd, s0));
+  CKI(cudaMemsetAsync(d.s2b, 0xff, sizeof(int32_t) * P, s0));
+  CKI(cudaMemsetAsync(d.occ, 0, sizeof(uint32_t) * d.PW, s0));
+  CKI(cudaMemsetAsync(d.dirty, 0, sizeof(uint32_t) * d.PW, s0));
+  CKI(cudaMemsetAsync(d.stats, 0, sizeof(unsigned long long) * ST_N, s0));
+  CKI(cudaMemsetAsync(d.nonfinite, 0xff, sizeof(unsigned long long), s0));
+  CKI(cudaMemsetAsync(d.hdr_dev, 0, sizeof(PlanHdr), s0));
+  CKI(cudaMemsetAsync(d.params, 0, sizeof(float) * pool_floats, s0));
+  CKI(cudaMemsetAsync(d.grads, 0, sizeof(float) * grad_floats, s0));
+  CKI(cudaStreamSynchronize(s0));
+#undef CKI
+  int dev = g.device;
+  c->adam_grid = adam_grid(dev);
+  *out = c;
+  return TGS_OK;
+}
+
+tgs_status tgs_destroy(tgs_ctx* c) {
+  if (!c) return TGS_EINVAL;
+  destroy_impl(c);
+  return TGS_OK;
+}
+
+tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_activation* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (J > c->d.J_max || (J > 0 && !cams)) return TGS_EINVAL;
+  for (uint32_t j = 0; j < J; ++j)
+    for (int p = 0; p < 6; ++p)
+      for (int i = 0; i < 4; ++i)
+        if (!std::isfinite(cams[j].plane[p][i])) return TGS_EINVAL;
+  Dev& d = c->d;
+  const int p = c->parity;  // parity of R_t; lists of this activate go to slot p
+  const int32_t T = c->T;
+
+  // ---- plan stream: a1 cull, a3 quota + fill, a2 delta, slots, A list
+  Timer tp;
+  float* pin = c->planes_pinned + (size_t)(T & 1) * kMaxCams * 24;
+  if (J) std::memcpy(pin, cams, sizeof(float) * 24 * J);
+  prof_begin(c, c->plan, tp);
+  CK(cudaMemsetAsync(d.cnt, 0, sizeof(uint32_t) * CNT_N, c->plan));
+  if (J) CK(cudaMemcpyAsync(c->planes_dev, pin, sizeof(float) * 24 * J, cudaMemcpyHostToDevice, c->plan));
+  CK(launch_cull(d, c->planes_dev, J, T, p, c->plan));
+  CK(launch_quota(d, J, T, p, c->plan));
+  CK(launch_plan(d, T, p, c->plan));
+  prof_end(c, c->plan, tp, 2);
+  c->tm.kernel_launches += (d.Kloc ? 1 : 0) + ((J && d.Kloc) ? 1 : 0) + 1;
+  CK(cudaEventRecord(c->ev_plan, c->plan));
+  CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
+  const PlanHdr h = *c->hdr;
+  c->last = h;
+
+  // ---- a4 write-back decision for S- (after Adam(t) on the compute stream)
+  const bool overlap = !d.tide || h.fallback;  // S+ reuses S- records or slots
+  auto writeback = [&]() -> tgs_status {
+    if (h.nSm == 0) return TGS_OK;
+    Timer te;
+    CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
+    prof_begin(c, c->compute, te);
+    CK(launch_evict(d, h.nSm, p, c->compute));
+    prof_end(c, c->compute, te, 5);
+    c->tm.kernel_launches++;
+    CK(cudaEventRecord(c->ev_evict, c->compute));
+    CK(cudaEventSynchronize(c->ev_evict));
+    const uint32_t nd = c->hdr->n_dirty;
+    c->last.n_dirty = nd;
+    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict, 0));
+    Timer td;
+    prof_begin(c, c->d2h, td);
+    tgs_status s2 = issue_copies(c, c->dirty_map, nd, false, c->d2h);
+    if (s2 != TGS_OK) return s2;
+    prof_end(c, c->d2h, td, 4, (uint64_t)nd * d.n_arr * c->rec_bytes);
+    CK(cudaEventRecord(c->ev_d2h, c->d2h));
+    c->d2h_recorded = true;
+    return TGS_OK;
+  };
+  if (overlap) {
+    st = writeback();
+    if (st != TGS_OK) return st;
+  }
+
+  // ---- a4 gather of S+ into free slots on the copy engines
+  if (c->d2h_recorded) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h, 0));
+  if (h.nSp) {
+    Timer th;
+    prof_begin(c, c->h2d, th);
+    st = issue_copies(c, c->sp_map, h.nSp, true, c->h2d);
+    if (st != TGS_OK) return st;
+    if (d.cold) {
+      CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
+      CK(launch_cold_init(d, h.nSp, p, c->h2d));
+      c->tm.kernel_launches++;
+    }
+    prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
+  }
+  CK(cudaEventRecord(c->ev_ready, c->h2d));
+
+  if (!overlap) {
+    st = writeback();
+    if (st != TGS_OK) return st;
+  }
+
+  c->last_parity = p;
+  c->parity = p ^ 1;
+  c->T = T + 1;
+  c->can_step = true;
+  if (out) {
+    out->n_visible = h.nK;
+    out->n_resident = h.nR;
+    out->n_active_blocks = h.nA;
+    out->n_stage_in = h.nSp;
+    out->n_evict = h.nSm;
+    out->n_evict_dirty = c->last.n_dirty;
+    out->h2d_bytes = (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
+    out->d_active_blocks = d.a_gid[p];
+    out->d_active_slots = d.a_slot[p];
+    out->d_params = d.params;
+    out->d_grads = d.grads;
+    out->slot_stride = 3 * d.rec_floats;
+    out->grad_stride = d.rec_floats;
+    out->ready = (void*)c->ev_ready;
+  }
+  return TGS_OK;
+}
+
+tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_mask) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!c->can_step) return TGS_ESTATE;
+  if (!hp || !hp->lr) return TGS_EINVAL;
+  c->can_step = false;
+  const int p = c->last_parity;
+  const uint32_t nA = c->last.nA;
+  st = ensure_lut(c, hp->beta1, hp->beta2, (uint32_t)std::min<uint64_t>(c->n_steps + 2, 0xffffffffu));
+  if (st != TGS_OK) return st;
+  c->n_steps++;
+  AdamHyper h{};
+  for (uint32_t a = 0; a < kDim; ++a) h.lr[a] = hp->lr[a];
+  h.b1 = hp->beta1;
+  h.b2 = hp->beta2;
+  h.omb1 = 1.0f - hp->beta1;
+  h.omb2 = 1.0f - hp->beta2;
+  h.eps = hp->eps;
+  CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
+  CK(cudaStreamWaitEvent(c->compute, c->ev_ready, 0));
+  if (nA == 0) return TGS_OK;
+  Timer t1, t2;
+  prof_begin(c, c->compute, t1);
+  CK(launch_adam_prologue(c->d, nA, p, d_row_mask, c->compute));
+  prof_end(c, c->compute, t1, 1);
+  prof_begin(c, c->compute, t2);
+  CK(launch_adam(c->d, nA, p, d_row_mask, h, c->adam_grid, c->compute));
+  prof_end(c, c->compute, t2, 0);
+  c->tm.kernel_launches += 2;
+  return TGS_OK;
+}
+
+tgs_status tgs_flush(tgs_ctx* c) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  Dev& d = c->d;
+  std::vector<uint32_t> dirty(d.PW);
+  std::vector<int32_t> s2b(d.P);
+  CK(cudaMemcpy(dirty.data(), d.dirty, sizeof(uint32_t) * d.PW, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(s2b.data(), d.s2b, sizeof(int32_t) * d.P, cudaMemcpyDeviceToHost));
+  std::vector<std::pair<uint32_t, uint32_t>> list;  // (local id, slot), ascending id
+  for (uint32_t s = 0; s < d.P; ++s)
+    if (((dirty[s >> 5] >> (s & 31)) & 1u) && s2b[s] >= 0) list.push_back({(uint32_t)s2b[s], s});
+  std::sort(list.begin(), list.end());
+  std::vector<uint32_t> pairs;
+  for (auto& e : list) pairs.push_back(e.first), pairs.push_back(e.second);
+  st = issue_copies(c, pairs.data(), (uint32_t)list.size(), false, c->d2h);
+  if (st != TGS_OK) return st;
+  CK(cudaStreamSynchronize(c->d2h));
+  CK(cudaMemset(d.dirty, 0, sizeof(uint32_t) * d.PW));
+  CK(cudaDeviceSynchronize());
+  c->host_flush_blocks += list.size();
+  c->host_flush_bytes += (uint64_t)list.size() * d.n_arr * c->rec_bytes;
+  c->can_step = false;
+  return TGS_OK;
+}
+
+tgs_status tgs_get_stats(tgs_ctx* c, tgs_stats* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out) return TGS_EINVAL;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  unsigned long long v[ST_N];
+  CK(cudaMemcpy(v, c->d.stats, sizeof v, cudaMemcpyDeviceToHost));
+  v[ST_FLUSH_BYTES] += c->host_flush_bytes;
+  v[ST_FLUSH_BLOCKS] += c->host_flush_blocks;
+  static_assert(sizeof(tgs_stats) == sizeof(uint64_t) * ST_N, "tgs_stats layout");
+  std::memcpy(out, v, sizeof v);
+  return TGS_OK;
+}
+
+tgs_status tgs_set_profiling(tgs_ctx* c, int enabled) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  c->prof = enabled != 0;
+  c->tm = tgs_timing{};
+  return TGS_OK;
+}
+
+tgs_status tgs_get_timing(tgs_ctx* c, tgs_timing* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out) return TGS_EINVAL;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  *out = c->tm;
+  return TGS_OK;
+}
+
+uint32_t tgs_get_list(tgs_ctx* c, int which, uint32_t* blocks, int32_t* slots, uint32_t cap) {
+  if (check(c) != TGS_OK || which < 0 || which > 5) return 0;
+  if (sync_all(c) != TGS_OK) return 0;
+  Dev& d = c->d;
+  const uint32_t Wd = std::max(d.W, 1u);
+  std::vector<uint32_t> bits(Wd, 0u);
+  uint32_t* src = nullptr;
+  switch (which) {
+    case 0: src = d.Kb; break;
+    case 1: src = d.R[c->parity]; break;  // R_{t+1} (parity flipped after activate)
+    case 2: src = d.Sp; break;
+    case 3: src = d.Sm; break;
+    case 4: src = d.Om; break;
+    case 5: src = d.Ab; break;
+  }
+  if (c->T == 0) return 0;
+  if (cudaMemcpy(bits.data(), src, sizeof(uint32_t) * Wd, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  std::vector<int32_t> b2s(std::max(d.Kloc, 1u));
+  if (slots && cudaMemcpy(b2s.data(), d.b2s, sizeof(int32_t) * b2s.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  uint32_t n = 0;
+  for (uint32_t w = 0; w < d.W; ++w) {
+    uint32_t x = bits[w];
+    while (x) {
+      const int b = __builtin_ctz(x);
+      x &= x - 1;
+      const uint32_t l = 32 * w + b;
+      if (n < cap) {
+        if (blocks) blocks[n] = l * c->cfg.world_size + c->cfg.rank;
+        if (slots) slots[n] = which == 3 ? -1 : b2s[l];
+      }
+      ++n;
+    }
+  }
+  return n;
+}
+
+uint32_t tgs_get_percam(tgs_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap) {
+  if (check(c) != TGS_OK || j >= c->d.J_max || c->T == 0) return 0;
+  if (sync_all(c) != TGS_OK) return 0;
+  Dev& d = c->d;
+  std::vector<uint32_t> bits(std::max(d.W, 1u));
+  if (cudaMemcpy(bits.data(), d.percam + (size_t)j * d.W, sizeof(uint32_t) * d.W,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  uint32_t n = 0;
+  for (uint32_t w = 0; w < d.W; ++w)
+    for (uint32_t x = bits[w]; x; x &= x - 1) {
+      if (n < cap && blocks) blocks[n] = (32 * w + __builtin_ctz(x)) * c->cfg.world_size + c->cfg.rank;
+      ++n;
+    }
+  return n;
+}
+
+uint32_t tgs_get_evicted_dirty(tgs_ctx* c, uint32_t* blocks, uint32_t cap) {
+  if (check(c) != TGS_OK) return 0;
+  if (sync_all(c) != TGS_OK) return 0;
+  const uint32_t n = c->last.nSm ? c->last.n_dirty : 0;
+  for (uint32_t i = 0; i < n && i < cap; ++i)
+    if (blocks) blocks[i] = c->dirty_map[2 * i] * c->cfg.world_size + c->cfg.rank;
+  return n;
+}
+
+tgs_status tgs_get_slot_map(tgs_ctx* c, int64_t* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out) return TGS_EINVAL;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  std::vector<int32_t> s2b(c->d.P);
+  CK(cudaMemcpy(s2b.data(), c->d.s2b, sizeof(int32_t) * c->d.P, cudaMemcpyDeviceToHost));
+  for (uint32_t s = 0; s < c->d.P; ++s)
+    out[s] = s2b[s] < 0 ? -1 : (int64_t)s2b[s] * c->cfg.world_size + c->cfg.rank;
+  return TGS_OK;
+}
+
+uint64_t tgs_nonfinite_index(tgs_ctx* c) {
+  if (check(c) != TGS_OK || sync_all(c) != TGS_OK) return ~0ull;
+  unsigned long long v = ~0ull;
+  if (cudaMemcpy(&v, c->d.nonfinite, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return ~0ull;
+  return v;
+}
+
+tgs_status tgs_read_block(tgs_ctx* c, uint64_t kg, float* theta, float* m, float* v) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (kg % c->cfg.world_size != (uint64_t)c->cfg.rank) return TGS_EINVAL;
+  const uint64_t l = kg / c->cfg.world_size;
+  if (l >= c->d.Kloc) return TGS_EINVAL;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  int32_t s = -1;
+  CK(cudaMemcpy(&s, c->d.b2s + l, sizeof s, cudaMemcpyDeviceToHost));
+  const size_t rb = c->rec_bytes, rf = c->d.rec_floats;
+  float* outs[3] = {theta, m, v};
+  for (int a = 0; a < 3; ++a) {
+    if (!outs[a]) continue;
+    if (s >= 0) {
+      CK(cudaMemcpy(outs[a], slot_rec(c, (uint32_t)s) + a * rf, rb, cudaMemcpyDeviceToHost));
+    } else if (a < (int)c->d.n_arr) {
+      std::memcpy(outs[a], host_rec(c, (uint32_t)l) + a * rf, rb);
+    } else {
+      std::memset(outs[a], 0, rb);  // cold restart: moments do not exist off the device
+    }
+  }
+  return TGS_OK;
+}
+
+uint32_t tgs_step_count(tgs_ctx* c, uint64_t kg) {
+  if (check(c) != TGS_OK || kg % c->cfg.world_size != (uint64_t)c->cfg.rank) return 0;
+  const uint64_t l = kg / c->cfg.world_size;
+  if (l >= c->d.Kloc || sync_all(c) != TGS_OK) return 0;
+  uint32_t s = 0;
+  cudaMemcpy(&s, c->d.step + l, sizeof s, cudaMemcpyDeviceToHost);
+  return s;
+}
+
+uint32_t tgs_num_local_blocks(const tgs_ctx* c) { return c ? c->d.Kloc : 0; }
+uint32_t tgs_pool_slots(const tgs_ctx* c) { return c ? c->d.P : 0; }
+
+tgs_status tgs_frustum_planes(const double w2c[16], double fx, double fy, double cx, double cy,
+                              uint32_t width, uint32_t height, double znear, double zfar,
+                              tgs_camera* out) {
+  if (!w2c || !out || !(fx > 0) || !(fy > 0) || width == 0 || height == 0 || !(znear > 0) ||
+      !(zfar > znear))
+    return TGS_EINVAL;
+  // camera-space planes (inside iff n.pc + d >= 0): x >= -cx z/fx, x <= (w-cx) z/fx, ...
+  const double pc[6][4] = {
+      {fx, 0.0, cx, 0.0},  {-fx, 0.0, (double)width - cx, 0.0},
+      {0.0, fy, cy, 0.0},  {0.0, -fy, (double)height - cy, 0.0},
+      {0.0, 0.0, 1.0, -znear}, {0.0, 0.0, -1.0, zfar},
+  };
+  // world plane: n_w = R^T n_c, d_w = n_c . t + d_c   (pc = R p + t)
+  for (int p = 0; p < 6; ++p) {
+    const double nn = std::sqrt(pc[p][0] * pc[p][0] + pc[p][1] * pc[p][1] + pc[p][2] * pc[p][2]);
+    double n[3] = {pc[p][0] / nn, pc[p][1] / nn, pc[p][2] / nn};
+    double dc = pc[p][3] / nn;
+    double nw[3];
+    for (int i = 0; i < 3; ++i) nw[i] = n[0] * w2c[0 * 4 + i] + n[1] * w2c[1 * 4 + i] + n[2] * w2c[2 * 4 + i];
+    const double dw = n[0] * w2c[3] + n[1] * w2c[7] + n[2] * w2c[11] + dc;
+    const double len = std::sqrt(nw[0] * nw[0] + nw[1] * nw[1] + nw[2] * nw[2]);
+    for (int i = 0; i < 3; ++i) out->plane[p][i] = (float)(nw[i] / len);
+    out->plane[p][3] = (float)(dw / len);
+  }
+  return TGS_OK;
+}
+
+}  // extern "C"

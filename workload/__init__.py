@@ -263,3 +263,45 @@ CONFIGS = {
     "300m_random": Workload("300m_random", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
                             _AERIAL, True),
 }
+
+
+# ------------------------------------------------------ CUDA twin (harness)
+_cuda_lib = None
+
+
+def cuda_lib():
+    """libtgsworkload_cuda.so: bit-identical device twin of grad_block / mask_block
+    (stands in for the renderer's backward pass; not part of the product)."""
+    global _cuda_lib
+    if _cuda_lib is None:
+        path = os.path.join(_HERE, "libtgsworkload_cuda.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make`")
+        L = C.CDLL(path)
+        vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+        L.wl_cuda_synth_grads.argtypes = [vp, u64, vp, vp, u32, u32, u64, u64, u64, vp]
+        L.wl_cuda_synth_mask.argtypes = [vp, u32, vp, vp, u32, u32, u64, u64, u64, u32, vp]
+        _cuda_lib = L
+    return _cuda_lib
+
+
+def synth_grads_cuda(act, B, N, seed, t, stream):
+    """Write counter-hash gradients of the active blocks of a tgs_activation into
+    its grad pool (on `stream`, after the activation's ready event)."""
+    if act.n_active_blocks == 0:
+        return
+    rc = cuda_lib().wl_cuda_synth_grads(act.d_grads, act.grad_stride, act.d_active_blocks,
+                                        act.d_active_slots, act.n_active_blocks, B, N, seed, t,
+                                        stream)
+    if rc != 0:
+        raise RuntimeError(f"wl_cuda_synth_grads: cuda error {rc}")
+
+
+def synth_mask_cuda(d_mask, act, B, N, seed, t, p32, stream):
+    if act.n_active_blocks == 0:
+        return
+    rc = cuda_lib().wl_cuda_synth_mask(d_mask, (B + 31) // 32, act.d_active_blocks,
+                                       act.d_active_slots, act.n_active_blocks, B, N, seed, t,
+                                       p32, stream)
+    if rc != 0:
+        raise RuntimeError(f"wl_cuda_synth_mask: cuda error {rc}")
