@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the TideGS working-set step (a1-a5) on B200.
+
+One step = tgs_activate(camera batch t) + tgs_step_adam over R n K, i.e. the
+whole hot path: cull, residency selection, delta, slot allocation/eviction,
+gather of S+ from the pinned host tier, write-back of dirty S-, masked Adam.
+Prints ONE JSON line (rank 0).  See DESIGN.md §6 for every field.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config 300m] [--moments cold]
+  python bench.py --impl reference ...      # the CPU oracle as the reference arm
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload as W  # noqa: E402
+
+METRIC = "active Gaussians materialised+updated/sec"
+ROW_BYTES_ADAM = 1652  # read g, m, v, theta (4 x 236 B) + write theta, m, v (3 x 236 B)
+
+
+def lr_3dgs():
+    lr = np.empty(59, np.float32)
+    lr[0:3], lr[3:6], lr[6:51], lr[51], lr[52:55], lr[55:59] = 1.6e-4, 2.5e-3, 1.25e-4, 5e-2, 5e-3, 1e-3
+    return lr
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="300m", choices=sorted(W.CONFIGS))
+    ap.add_argument("--moments", default="cold", choices=["cold", "persist"])
+    ap.add_argument("--start", type=int, default=0, help="first batch index of the trajectory")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def link_peak(torch, dev):
+    """Measured pinned host<->device copy bandwidth (GB/s) on this box, 1 GiB."""
+    n = 1 << 30
+    x = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    best = {"h2d": 0.0, "d2h": 0.0}
+    for _ in range(3):
+        for k, f in (("h2d", lambda: d.copy_(x, non_blocking=True)),
+                     ("d2h", lambda: x.copy_(d, non_blocking=True))):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            f()
+            torch.cuda.synchronize()
+            best[k] = max(best[k], n / (time.perf_counter() - t) / 1e9)
+    del x, d
+    return best
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return ws, rank, local
+
+
+def run_reference(args, ws, rank):
+    """Reference arm = the CPU oracle as it stands, on the host cores, same
+    config / metric; each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    import oracle as O
+    wl = W.CONFIGS[args.config]
+    sc = wl.scene()
+    tr = wl.trajectory(sc)
+    moments = O.COLD_RESTART if args.moments == "cold" else O.PERSIST
+    o = O.Oracle(O.make_config(sc.N, sc.B, wl.capacity, moments=moments), sc.bounds(),
+                 fill=None, track_all=True)
+    syn = _synth_struct(sc)
+    gfn = C.cast(W.lib().wl_grad_cb, C.c_void_p).value
+    lr = lr_3dgs()
+    times, rows = [], []
+    total = args.warmup + args.steps
+    budget = 150.0  # seconds of oracle work for the whole run
+    t_all = time.perf_counter()
+    timed = 0
+    for i in range(total):
+        t0 = time.perf_counter()
+        before = o.stats()["n_active_rows"]
+        o.activate(tr.batch_planes(args.start + i, wl.J))
+        o.step_adam(lr, grad=(gfn, C.addressof(syn)))
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            rows.append(o.stats()["n_active_rows"] - before)
+            timed += 1
+        if time.perf_counter() - t_all > budget and timed >= 1:
+            break
+    o.close()
+    value = sum(rows) / sum(times)
+    cores = 1
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gaussians/s",
+            "n_gpus": 0, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _config_dict(args, wl, ws),
+            "cpu_baseline": {"value": value, "unit": "Gaussians/s", "cores": cores,
+                             "kind": "oracle",
+                             "sample": f"oracle (single-thread C++17) from batch {args.start}, "
+                                       f"{len(times)} timed of {total} requested steps "
+                                       f"(capped at {budget:.0f}s), rows zero-filled"},
+            "e2e": {"value": value, "unit": "Gaussians/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _synth_struct(sc):
+    class Synth(C.Structure):
+        _fields_ = [("seed", C.c_uint64), ("n_gaussians", C.c_uint64),
+                    ("block_size", C.c_uint32), ("p32", C.c_uint32)]
+    return Synth(W.SEEDS["grads"], sc.N, sc.B, 0)
+
+
+def _config_dict(args, wl, ws):
+    return {"workload": f"{wl.name}: {wl.n_gaussians:,} Gaussians, {wl.traj} trajectory "
+                        f"({'random' if wl.shuffled else 'smooth'} order), J={wl.J} cameras/batch",
+            "n_gaussians": wl.n_gaussians, "block_size": wl.block_size, "J": wl.J,
+            "capacity_blocks_per_gpu": -(-wl.capacity // ws), "moments": args.moments,
+            "policy": "tide", "world_size": ws,
+            "l2": "inputs larger than L2 (Adam touches GBs per step)",
+            "grads": "synthetic counter-hash gradients resident in the grad pool (renderer out of scope)",
+            "seeds": W.SEEDS}
+
+
+def cpu_baseline(args, wl, sc, tr, budget_s):
+    """The oracle as it stands, single thread, on a bounded sample of the same
+    workload (the first batches from --start), rows zero-filled."""
+    import oracle as O
+    moments = O.COLD_RESTART if args.moments == "cold" else O.PERSIST
+    o = O.Oracle(O.make_config(sc.N, sc.B, wl.capacity, moments=moments), sc.bounds(),
+                 fill=None, track_all=True)
+    syn = _synth_struct(sc)
+    gfn = C.cast(W.lib().wl_grad_cb, C.c_void_p).value
+    lr = lr_3dgs()
+    t0 = time.perf_counter()
+    n = 0
+    rows = 0
+    while True:
+        before = o.stats()["n_active_rows"]
+        o.activate(tr.batch_planes(args.start + n, wl.J))
+        o.step_adam(lr, grad=(gfn, C.addressof(syn)))
+        rows += o.stats()["n_active_rows"] - before
+        n += 1
+        if time.perf_counter() - t0 > budget_s or n >= 64:
+            break
+    dt = time.perf_counter() - t0
+    o.close()
+    return {"value": rows / dt, "unit": "Gaussians/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {n} batches from {args.start} of the same workload "
+                      f"({dt:.1f}s single-thread, rows zero-filled, cold start)"}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    import paper_2605_20150_b200 as P
+    from paper_2605_20150_b200 import tidegs as T
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = W.CONFIGS[args.config]
+    sc = wl.scene()
+    tr = wl.trajectory(sc)
+    cap = -(-wl.capacity // ws)
+    moments = T.COLD_RESTART if args.moments == "cold" else T.PERSIST
+    t_setup = time.perf_counter()
+    cfg = T.make_config(sc.N, sc.B, cap, moments=moments, world_size=ws, rank=rank,
+                        device=local)
+    stream = torch.cuda.Stream(device=dev)
+    table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream)
+    setup_s = time.perf_counter() - t_setup
+    # synthetic gradients for every slot, written once (renderer out of scope)
+    P_ = table.P
+    ids = torch.arange(P_, dtype=torch.int32, device=dev) % max(1, table.num_local_blocks)
+    ids = ids * ws + rank
+    slots = torch.arange(P_, dtype=torch.int32, device=dev)
+    act0 = table.activate(np.zeros((0, 6, 4), np.float32))
+    W.cuda_lib().wl_cuda_synth_grads(act0.d_grads, act0.grad_stride, ids.data_ptr(),
+                                     slots.data_ptr(), P_, sc.B, sc.N, W.SEEDS["grads"], 0,
+                                     stream.cuda_stream)
+    torch.cuda.synchronize()
+    lr = lr_3dgs()
+    J = wl.J
+    total = args.warmup + args.steps
+    planes = [tr.batch_planes(args.start + i, J) for i in range(total + args.steps)]
+
+    def step(i):
+        table.activate(planes[i])
+        table.step_adam(lr)
+
+    for i in range(args.warmup):
+        step(i)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    table.set_profiling(True)
+    st0 = table.stats()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for i in range(args.warmup, total):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1)
+    st1 = table.stats()
+    tm = table.timing()
+    rows = st1["n_active_rows"] - st0["n_active_rows"]
+    h2d = st1["h2d_bytes"] - st0["h2d_bytes"]
+    d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
+    stage_in = st1["n_stage_in"] - st0["n_stage_in"]
+    visible = st1["n_visible"] - st0["n_visible"]
+    if ws > 1:
+        t = torch.tensor([rows, ms, h2d, d2h, stage_in, visible, tm["adam_ms"]],
+                         dtype=torch.float64, device=dev)
+        mx = t.clone()
+        torch.distributed.all_reduce(t)
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        rows, h2d, d2h, stage_in, visible = (float(x) for x in (t[0], t[2], t[3], t[4], t[5]))
+        ms = float(mx[1])
+    value = rows / (ms / 1e3)
+
+    # ---- e2e: same metric through the public API with host buffers and a
+    #      per-step device->host read of the result (stats), wall clock
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rows_e = 0
+        h2d_e = d2h_e = 0
+        n_e = max(1, min(args.steps, 20))
+        prev = table.stats()
+        for i in range(total, total + n_e):
+            step(i)
+            cur = table.stats()  # synchronises + reads the step's counters
+            rows_e += cur["n_active_rows"] - prev["n_active_rows"]
+            h2d_e += cur["h2d_bytes"] - prev["h2d_bytes"] + J * 96
+            d2h_e += cur["d2h_bytes"] - prev["d2h_bytes"] + 17 * 8
+            prev = cur
+        dt = time.perf_counter() - t0
+        e2e = {"value": rows_e / dt, "unit": "Gaussians/s",
+               "h2d_bytes_per_step": int(h2d_e / n_e), "d2h_bytes_per_step": int(d2h_e / n_e),
+               "ms_per_step": 1e3 * dt / n_e}
+
+    hbm_peak, peak_kind = peaks()
+    adam_rows = rows if ws == 1 else rows / ws
+    adam_ms = tm["adam_ms"] / max(1, tm["adam_launches"])
+    achieved = (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM / (adam_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "k_adam", "achieved": achieved, "peak": hbm_peak,
+            "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+            "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM,
+            "avg_launch_ms": adam_ms}
+    lp = link_peak(torch, dev) if rank == 0 else None
+    link = None
+    if rank == 0:
+        h2d_rate = tm["h2d_bytes"] / (tm["h2d_ms"] / 1e3) / 1e9 if tm["h2d_ms"] else None
+        d2h_rate = tm["d2h_bytes"] / (tm["d2h_ms"] / 1e3) / 1e9 if tm["d2h_ms"] else None
+        link = {"bound": "host-link", "h2d_achieved": h2d_rate, "d2h_achieved": d2h_rate,
+                "h2d_peak": lp["h2d"], "d2h_peak": lp["d2h"], "unit": "GB/s",
+                "h2d_frac": (h2d_rate / lp["h2d"]) if h2d_rate else None,
+                "d2h_frac": (d2h_rate / lp["d2h"]) if d2h_rate else None,
+                "peak_kind": "measured in this run: pinned 1 GiB cudaMemcpy",
+                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, wl, sc, tr, args.cpu_sample_s)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Gaussians/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": _config_dict(args, wl, ws),
+                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": tm["kernel_launches"],
+                "roofline": roof, "link_roofline": link, "cpu_baseline": cpu,
+                "detail": {"active_blocks_per_step": None if not args.steps else
+                           (st1["n_active_blocks"] - st0["n_active_blocks"]) / args.steps,
+                           "visible_blocks_per_step": visible / args.steps,
+                           "stage_in_blocks_per_step": stage_in / args.steps,
+                           "h2d_GB_per_step": h2d / args.steps / 1e9,
+                           "d2h_GB_per_step": d2h / args.steps / 1e9,
+                           "plan_ms_per_step": tm["plan_ms"] / args.steps,
+                           "adam_prologue_ms_per_step": tm["adam_prologue_ms"] / args.steps,
+                           "h2d_ms_per_step": tm["h2d_ms"] / args.steps,
+                           "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
+                           "copy_calls_per_step": tm["copy_calls"] / args.steps,
+                           "setup_s": setup_s}}
+        print(json.dumps(line), flush=True)
+    table.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

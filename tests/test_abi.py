@@ -1,0 +1,102 @@
+"""The C-ABI library loads, exports every entry point include/tidegs.h declares,
+and validates configs before touching the device (no GPU needed)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2605_20150_b200 import tidegs as T
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_and_binding_declare_the_same_symbols():
+    hdr = open(os.path.join(ROOT, "include", "tidegs.h")).read()
+    declared = set(re.findall(r"^(?:tgs_status|uint32_t|uint64_t|const char\*)\s+(tgs_\w+)\s*\(",
+                              hdr, re.M))
+    assert declared == set(T.SYMBOLS)
+
+
+def test_library_exports_every_symbol():
+    L = T.lib()
+    for s in T.SYMBOLS:
+        assert hasattr(L, s), s
+    assert L.tgs_status_string(T.EINVAL) == b"invalid argument"
+
+
+def test_elf_has_sm100a_code():
+    """The product .so carries sm_100a SASS (no PTX-only JIT path)."""
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", T.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _init(cfg, bounds, rows=None):
+    h = C.c_void_p()
+    rp = rows.ctypes.data if rows is not None else None
+    fill = None if rows is not None else C.cast(T.FILL_FN(lambda *a: None), C.c_void_p).value
+    return T.lib().tgs_init_table(C.byref(cfg), rp, fill, None,
+                                  bounds.ctypes.data_as(C.POINTER(C.c_float)), None, None,
+                                  C.byref(h))
+
+
+@pytest.mark.parametrize("field,value", [("dim", 58), ("block_size", 6), ("block_size", 0),
+                                         ("capacity", 0), ("n_gaussians", 0),
+                                         ("lambda_", 1.5), ("lambda_", -0.1), ("gamma", 1.0),
+                                         ("gamma", 0.0), ("quota_den", 0), ("quota_num", 3),
+                                         ("world_size", 0), ("rank", 2), ("moments", 7),
+                                         ("max_cameras", 0), ("max_cameras", 300),
+                                         ("max_age", 5000), ("pool_slots", 3)])
+def test_invalid_config_is_einval(field, value):
+    cfg = T.make_config(1000, 16, 4)
+    setattr(cfg, field, value)
+    bounds = np.zeros((63, 4), np.float32)
+    assert _init(cfg, bounds) == T.EINVAL
+
+
+def test_invalid_bounds_and_sources_are_einval():
+    cfg = T.make_config(64, 16, 2)
+    b = np.zeros((4, 4), np.float32)
+    b[2, 0] = np.nan
+    assert _init(cfg, b) == T.EINVAL
+    b = np.zeros((4, 4), np.float32)
+    b[1, 3] = -1.0
+    assert _init(cfg, b) == T.EINVAL
+    # exactly one of theta_rows / fill
+    h = C.c_void_p()
+    ok_b = np.zeros((4, 4), np.float32)
+    assert T.lib().tgs_init_table(C.byref(cfg), None, None, None,
+                                  ok_b.ctypes.data_as(C.POINTER(C.c_float)), None, None,
+                                  C.byref(h)) == T.EINVAL
+
+
+def test_frustum_planes_helper_matches_pinhole_geometry():
+    """R1 helper: a point projecting inside the image at near<=z<=far is inside
+    all six planes; one outside the image or depth range is outside one."""
+    rng = np.random.default_rng(3)
+    ang = 0.3
+    Rm = np.array([[np.cos(ang), 0, np.sin(ang)], [0, 1, 0], [-np.sin(ang), 0, np.cos(ang)]])
+    t = np.array([0.5, -0.2, 2.0])
+    w2c = np.eye(4)
+    w2c[:3, :3] = Rm
+    w2c[:3, 3] = t
+    fx = fy = 400.0
+    W_, H = 640, 480
+    planes = T.frustum_planes(w2c, fx, fy, 320.0, 240.0, W_, H, 0.5, 50.0).astype(np.float64)
+    for _ in range(2000):
+        p = rng.uniform(-40, 40, 3)
+        pc = Rm @ p + t
+        inside_img = False
+        if 0.5 <= pc[2] <= 50.0:
+            u, v = fx * pc[0] / pc[2] + 320.0, fy * pc[1] / pc[2] + 240.0
+            inside_img = 0 <= u <= W_ and 0 <= v <= H
+        d = planes[:, :3] @ p + planes[:, 3]
+        margin = 1e-4 * (1 + np.abs(p).sum())
+        if inside_img:
+            assert (d >= -margin).all()
+        elif (d > margin).all():
+            raise AssertionError(f"point {p} outside the frustum is inside all planes")
+    assert T.lib().tgs_frustum_planes(None, 1, 1, 0, 0, 1, 1, 0.1, 1.0, None) == T.EINVAL

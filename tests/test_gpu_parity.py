@@ -1,0 +1,199 @@
+"""CUDA path vs CPU oracle, element by element, on the same seeded inputs
+(north star: bit-exact indexing, Adam within 1e-6 relative)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workload as W
+from helpers import tiny
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(sc, **kw):
+    from gpu_harness import Pair
+    return Pair(sc, **kw)
+
+
+def _drive(pr, tr, J, iters, *, check_blocks_every=0, adam=True):
+    worst = 0
+    for t in range(iters):
+        act = pr.activate(tr.batch_planes(t, J))
+        pr.t = t
+        pr.compare_plan(J)
+        pr.compare_evicted_dirty()
+        assert act.n_stage_in == pr.orc.list("S+").size
+        assert act.n_active_blocks == pr.orc.list("A").size
+        if adam:
+            rc = pr.step(act, t)
+            assert rc == O.OK
+        if check_blocks_every and t % check_blocks_every == 0:
+            worst = max(worst, pr.compare_blocks(pr.orc.list("R")))
+    pr.compare_stats()
+    return worst
+
+
+@pytest.mark.parametrize("moments", [O.PERSIST, O.COLD_RESTART])
+@pytest.mark.parametrize("lam,quota", [(0.7, (1, 2)), (0.0, (1, 2)), (1.0, (0, 1)),
+                                       (0.5, (1, 2))])
+def test_tiny_trajectory_parity(moments, lam, quota):
+    """configs[0]: 100k Gaussians / 64 blocks, 16-pose orbit, C=24 < K (forces
+    eviction, quota and re-admission): every list, slot map, dirty set and
+    counter bit-exact; theta/m/v of every block after flush within 1e-6."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, lam=lam, quota=quota, moments=moments)
+    worst = _drive(pr, tr, cfg.J, 40, check_blocks_every=7)
+    pr.gpu.flush()
+    pr.orc.flush()
+    pr.compare_stats()
+    worst = max(worst, pr.compare_blocks(range(sc.K)))
+    assert worst == 0, f"max ULP {worst} (prescribed op order should give 0)"
+    pr.close()
+
+
+@pytest.mark.parametrize("J", [1, 2, 4, 7])
+def test_tiny_batch_sizes_and_quota(J):
+    """Several cameras per batch; capacity small enough that the camera quota binds."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=16, lam=0.3, quota=(1, 2))
+    _drive(pr, tr, J, 24, check_blocks_every=11)
+    pr.close()
+
+
+def test_tide_off_restage_all():
+    """Ablation: every batch restages R_{t+1}, dirty R_t is
+    written back first; bytes and contents still match the oracle."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, tide=0)
+    worst = _drive(pr, tr, cfg.J, 20, check_blocks_every=5)
+    assert worst == 0
+    pr.close()
+
+
+def test_small_pool_uses_released_slots():
+    """P = C: S+ must reuse the slots S- releases (R13 fallback path)."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, pool_slots=cfg.capacity)
+    worst = _drive(pr, tr, cfg.J, 30, check_blocks_every=6)
+    assert worst == 0
+    pr.close()
+
+
+def test_masked_rows_parity():
+    """Sparse I_t (p = 0.25 row mask): masked rows bitwise unchanged, steps and
+    dirty bits only for blocks with an active row."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, mask_p=0.25)
+    worst = _drive(pr, tr, cfg.J, 24, check_blocks_every=5)
+    assert worst == 0
+    pr.close()
+
+
+def test_empty_mask_leaves_everything_clean():
+    """Empty I_t: nothing updated, nothing dirty, no step."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, mask_p=0.0)
+    _drive(pr, tr, cfg.J, 12)
+    st = pr.gpu.stats()
+    assert st["total_updates"] == 0 and st["d2h_bytes"] == 0
+    pr.gpu.flush()
+    assert pr.gpu.stats()["flush_bytes"] == 0
+    pr.close()
+
+
+def test_static_batch_zero_traffic_and_empty_batch():
+    """Static view with capacity: S+ = S- = {} after the first batch;
+    J = 0 keeps R (R19)."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=40)
+    pl = tr.batch_planes(3, cfg.J)
+    for t in range(5):
+        act = pr.activate(pl)
+        pr.t = t
+        pr.compare_plan(cfg.J)
+        if t:
+            assert act.n_stage_in == 0 and act.n_evict == 0
+        pr.step(act, t)
+    act = pr.activate(np.zeros((0, 6, 4), np.float32))
+    pr.compare_plan(0)
+    assert act.n_visible == 0 and act.n_stage_in == 0
+    pr.compare_stats()
+    pr.close()
+
+
+def test_nonfinite_gradient_reported_and_row_skipped():
+    """R20: a NaN gradient skips its row, the lowest (gid*59+attr) is reported."""
+    import torch
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity)
+    act = pr.activate(tr.batch_planes(0, cfg.J))
+    blocks = pr.orc.list("A", with_slots=True)
+    k, s = int(blocks[0][1]), int(blocks[1][1])
+    r, a = 5, 17
+
+    def hook(act_):
+        ptr = act_.d_grads + 4 * (s * act_.grad_stride + r * 59 + a)
+        assert W.cuda_lib().wl_cuda_poke(ptr, float("nan"), pr.stream) == 0
+
+    def ograd(_u, kk, t, out):
+        W.lib().wl_grad_block(42, kk, sc.B, sc.rows(kk), t, out)
+        if kk == k:
+            out[r * 59 + a] = float("nan")
+
+    import ctypes as C
+    gfn = O.GRAD_FN(ograd)
+    rc = pr.step(act, 0, grad_hook=hook, oracle_grad=(C.cast(gfn, C.c_void_p).value, None))
+    assert rc == O.ENONFINITE
+    assert pr.gpu.nonfinite_index() == pr.orc.nonfinite_index() == (k * sc.B + r) * 59 + a
+    pr.compare_blocks([k])
+    pr.close()
+
+
+def test_conservation_without_updates():
+    """With every mask empty, after any activate sequence + flush the host tier
+    is byte-identical to the initial table (SURVEY §8c conservation)."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, mask_p=0.0)
+    _drive(pr, tr, cfg.J, 30)
+    pr.gpu.flush()
+    for k in range(sc.K):
+        th, m, v = pr.gpu.read_block(k)
+        np.testing.assert_array_equal(th, sc.block_theta(k))
+        assert not m.any() and not v.any()
+    pr.close()
+
+
+@pytest.mark.parametrize("name", ["11m", "100m"])
+def test_full_size_index_parity_and_sampled_rows(name):
+    """BASELINE.json configs at full size, the launch configuration bench.py
+    times: indexing bit-exact every iteration; theta/m/v on sampled blocks."""
+    wl = W.CONFIGS[name]
+    sc = wl.scene()
+    tr = wl.trajectory(sc)
+    pr = _pair(sc, capacity=wl.capacity, track_all=False)
+    assert wl.n_gaussians == sc.N
+    rng = np.random.default_rng(5)
+    sample = sorted(set(rng.integers(0, sc.K, 48).tolist()))
+    iters = 6
+    probe = O.Oracle(O.make_config(sc.N, sc.B, wl.capacity), sc.bounds(), fill=None,
+                     track_all=False)
+    for t in range(iters):
+        probe.activate(tr.batch_planes(t, wl.J))
+    touched = probe.list("R")
+    probe.close()
+    tracked = sorted(set(sample) | set(touched[:: max(1, len(touched) // 48)].tolist()))
+    for k in tracked:
+        assert pr.orc.track(k) == O.OK
+    for t in range(iters):
+        act = pr.activate(tr.batch_planes(t, wl.J))
+        pr.t = t
+        for which in ("K", "R", "S+", "S-", "A"):
+            gb, gs = pr.gpu.list(which, with_slots=True)
+            ob, os_ = pr.orc.list(which, with_slots=True)
+            np.testing.assert_array_equal(gb, ob)
+            np.testing.assert_array_equal(gs, os_)
+        pr.step(act, t)
+    pr.compare_stats()
+    worst = pr.compare_blocks(tracked)
+    assert worst == 0
+    pr.close()

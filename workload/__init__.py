@@ -281,6 +281,7 @@ def cuda_lib():
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         L.wl_cuda_synth_grads.argtypes = [vp, u64, vp, vp, u32, u32, u64, u64, u64, vp]
         L.wl_cuda_synth_mask.argtypes = [vp, u32, vp, vp, u32, u32, u64, u64, u64, u32, vp]
+        L.wl_cuda_poke.argtypes = [vp, C.c_float, vp]
         _cuda_lib = L
     return _cuda_lib
 

@@ -90,3 +90,11 @@ extern "C" int wl_cuda_synth_mask(uint32_t* d_mask, uint32_t words_per_slot,
                                                          B, N, seed, t, p32);
   return (int)cudaGetLastError();
 }
+
+// test hook: overwrite one device float in stream order (fault injection)
+__global__ void wl_poke_kernel(float* p, float v) { *p = v; }
+
+extern "C" int wl_cuda_poke(float* p, float v, void* stream) {
+  wl_poke_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(p, v);
+  return (int)cudaGetLastError();
+}
