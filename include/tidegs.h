@@ -73,6 +73,9 @@ typedef struct {
   int32_t world_size, rank; /* block k owned by rank k % world_size (R17)           */
   int32_t device;        /* CUDA device ordinal                                     */
   int32_t init_threads;  /* host threads used to build the host tier (0 -> auto)    */
+  uint32_t staging_blocks; /* write-back staging ring, records per parity (0 -> C/4);
+                              an activate evicting more dirty records than this
+                              writes them back straight from the slots instead  */
 } tgs_config;
 
 /* Optional device allocator hooks (PyTorch's caching allocator from Python).

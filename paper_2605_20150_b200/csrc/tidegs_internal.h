@@ -68,6 +68,9 @@ struct Dev {
   PlanHdr* hdr_map;      // device alias of the mapped host header
   uint32_t* sp_map;      // mapped host [C][2] (local id, slot) of S+
   uint32_t* dirty_map;   // mapped host [C][2] (local id, slot) of dirty S-
+  uint32_t* dl_slot;     // [C] device copy of the dirty S- slots (pack source)
+  float* staging[2];     // [S_max][n_arr][B][59] write-back staging ring (parity)
+  uint32_t S_max;        // staging capacity in records
   // selection
   uint16_t* rank_lut;    // [2][max_age+2]
   uint32_t n_buckets;    // 2 * (number of distinct ranks)
@@ -82,17 +85,24 @@ struct Dev {
   float* grads;          // [P][B][59]
 };
 
+// camera batch passed by value as a kernel parameter (24 KB < 32 KB limit),
+// so the plan never queues behind the gather on the copy engine
+struct PlanesArg {
+  float4 p[kMaxCams * 6];
+};
+
 struct AdamHyper {
   float lr[kDim];
   float b1, b2, omb1, omb2, eps;
 };
 
 // launchers (return cudaGetLastError())
-cudaError_t launch_cull(const Dev& d, const float* planes, uint32_t J, int32_t T, int parity,
-                        cudaStream_t s);
+cudaError_t launch_cull(const Dev& d, const PlanesArg& planes, uint32_t J, int32_t T,
+                        int parity, cudaStream_t s);
 cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
+cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
 cudaError_t launch_cold_init(const Dev& d, uint32_t nSp, int parity, cudaStream_t s);
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s);

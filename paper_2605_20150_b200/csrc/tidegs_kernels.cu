@@ -169,10 +169,10 @@ __device__ void select_top(const Dev& d, uint32_t n, uint32_t nw, int32_t T, uin
 }
 
 // ------------------------------------------------------------------- a1 cull
-__global__ void __launch_bounds__(256) k_cull(Dev d, const float4* __restrict__ planes,
+__global__ void __launch_bounds__(256) k_cull(Dev d, const __grid_constant__ PlanesArg planes,
                                               uint32_t J, int32_t T, int parity) {
   __shared__ float4 pl[kMaxCams * 6];
-  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = planes[i];
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = planes.p[i];
   __syncthreads();
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t w = l >> 5, lane = l & 31;
@@ -405,6 +405,8 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
     h.n_dirty = 0;
     *d.hdr_dev = h;
     *d.hdr_map = h;
+    d.cnt[CNT_CAND] = 0u;  // ready for the next activate's cull
+    d.cnt[CNT_K] = 0u;
     unsigned long long* st = d.stats;
     atomicAdd(&st[ST_ITER], 1ull);
     atomicAdd(&st[ST_VISIBLE], (unsigned long long)h.nK);
@@ -440,6 +442,7 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
     if (dirty) {
       d.dirty_map[2 * o] = l;
       d.dirty_map[2 * o + 1] = s;
+      d.dl_slot[o] = s;
       atomicAnd(&d.dirty[s >> 5], ~(1u << (s & 31)));
     }
     c += tot;
@@ -450,6 +453,31 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
     atomicAdd(&d.stats[ST_EVICT_DIRTY], (unsigned long long)c);
     atomicAdd(&d.stats[ST_D2H], (unsigned long long)c * d.rec_floats * 4ull * d.n_arr);
   }
+}
+
+// ------------------- a4 pack: dirty S- records -> write-back staging ring
+// grid (chunks, nSm); entry i < n_dirty copies its slot's theta (| m | v when
+// moments persist) into staging[parity][i] with 128-bit streaming loads and
+// stores, so the slot is free for the next gather as soon as this kernel ends
+// and the copy engine drains the staging ring to the host tier meanwhile.
+__global__ void __launch_bounds__(256) k_pack(Dev d, int parity) {
+  const uint32_t i = blockIdx.y;
+  if (i >= d.hdr_dev->n_dirty) return;
+  const uint32_t s = d.dl_slot[i];
+  const size_t n4 = (size_t)d.n_arr * d.rec_floats / 4;
+  const float4* src = reinterpret_cast<const float4*>(d.params + (size_t)s * 3 * d.rec_floats);
+  float4* dst = reinterpret_cast<float4*>(d.staging[parity] + (size_t)i * d.n_arr * d.rec_floats);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; e + 3 * stride < n4; e += 4 * stride) {  // 4 independent 16 B loads in flight
+    const float4 a = __ldcs(src + e), b = __ldcs(src + e + stride);
+    const float4 c = __ldcs(src + e + 2 * stride), f = __ldcs(src + e + 3 * stride);
+    __stcs(dst + e, a);
+    __stcs(dst + e + stride, b);
+    __stcs(dst + e + 2 * stride, c);
+    __stcs(dst + e + 3 * stride, f);
+  }
+  for (; e < n4; e += stride) __stcs(dst + e, __ldcs(src + e));
 }
 
 // ---------------------------------- a4 cold restart: m = v = 0 in new slots
@@ -653,11 +681,11 @@ __global__ void __launch_bounds__(kAdamNT) k_adam(Dev d, uint32_t nA, int parity
 }  // namespace
 
 // ------------------------------------------------------------- launchers
-cudaError_t launch_cull(const Dev& d, const float* planes, uint32_t J, int32_t T, int parity,
-                        cudaStream_t s) {
+cudaError_t launch_cull(const Dev& d, const PlanesArg& planes, uint32_t J, int32_t T,
+                        int parity, cudaStream_t s) {
   if (d.Kloc == 0) return cudaSuccess;
   const uint32_t grid = (d.Kloc + 255) / 256;
-  k_cull<<<grid, 256, 0, s>>>(d, reinterpret_cast<const float4*>(planes), J, T, parity);
+  k_cull<<<grid, 256, 0, s>>>(d, planes, J, T, parity);
   return cudaGetLastError();
 }
 
@@ -674,6 +702,13 @@ cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s) {
 
 cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) {
   k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) {
+  if (nSm == 0) return cudaSuccess;
+  dim3 grid(16, nSm);
+  k_pack<<<grid, 256, 0, s>>>(d, parity);
   return cudaGetLastError();
 }
 

@@ -61,13 +61,17 @@ struct tgs_ctx {
   PlanHdr* hdr = nullptr;         // host view
   uint32_t* sp_map = nullptr;     // host view
   uint32_t* dirty_map = nullptr;  // host view
-  float* planes_pinned = nullptr; // [2][kMaxCams*24]
-  float* planes_dev = nullptr;
+  float* planes_pinned = nullptr; // [kMaxCams*24] staging of the kernel parameter
   // streams / events
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
   bool own_compute = false;
-  cudaEvent_t ev_plan = nullptr, ev_evict = nullptr, ev_d2h = nullptr, ev_ready = nullptr;
-  bool d2h_recorded = false;
+  cudaEvent_t ev_plan = nullptr, ev_ready = nullptr;
+  cudaEvent_t ev_evict[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  bool evict_rec[2] = {false, false}, d2h_rec[2] = {false, false};
+  bool prev_direct = false;        // previous activate wrote back straight from slots
+  // dirty records the previous activate packed: local id -> staging index
+  std::vector<std::pair<uint32_t, uint32_t>> prev_packed;
+  int prev_pack_parity = 0;
   // Adam LUT (bias corrections, R9)
   std::vector<float> lut_bc1_h, lut_ibs_h;
   float* lut_pinned = nullptr;     // [2][lut_cap]
@@ -345,7 +349,8 @@ void destroy_impl(tgs_ctx* c) {
   if (c->dirty_map) cudaFreeHost(c->dirty_map);
   if (c->planes_pinned) cudaFreeHost(c->planes_pinned);
   if (c->lut_pinned) cudaFreeHost(c->lut_pinned);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_evict, c->ev_d2h, c->ev_ready})
+  for (cudaEvent_t e : {c->ev_plan, c->ev_ready, c->ev_evict[0], c->ev_evict[1], c->ev_d2h[0],
+                        c->ev_d2h[1]})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -440,7 +445,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
-  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_evict, &c->ev_d2h, &c->ev_ready})
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready, &c->ev_evict[0], &c->ev_evict[1],
+                         &c->ev_d2h[0], &c->ev_d2h[1]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
 
   // ---- host tier (pinned, block records)
@@ -502,7 +508,10 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   d.stats = dalloc_t<unsigned long long>(c, ST_N, ok);
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
-  c->planes_dev = dalloc_t<float>(c, kMaxCams * 24, ok);
+  d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
+  d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C / 4);
+  for (int p = 0; p < 2; ++p)
+    d.staging[p] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
   std::vector<uint16_t> lut;
   uint32_t n_ranks = 0;
   build_rank_lut(g, lut, n_ranks);
@@ -564,16 +573,17 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
         if (!std::isfinite(cams[j].plane[p][i])) return TGS_EINVAL;
   Dev& d = c->d;
   const int p = c->parity;  // parity of R_t; lists of this activate go to slot p
+  const int q = p ^ 1;      // parity of the previous activate
   const int32_t T = c->T;
 
-  // ---- plan stream: a1 cull, a3 quota + fill, a2 delta, slots, A list
+  // ---- plan stream: a1 cull, a3 quota + fill, a2 delta, slots, A list.
+  //      Planes travel as a kernel parameter: nothing here queues on a copy engine.
   Timer tp;
-  float* pin = c->planes_pinned + (size_t)(T & 1) * kMaxCams * 24;
-  if (J) std::memcpy(pin, cams, sizeof(float) * 24 * J);
+  static_assert(sizeof(PlanesArg) == sizeof(float) * kMaxCams * 24, "planes layout");
+  PlanesArg* pa = reinterpret_cast<PlanesArg*>(c->planes_pinned);
+  if (J) std::memcpy(pa, cams, sizeof(float) * 24 * J);
   prof_begin(c, c->plan, tp);
-  CK(cudaMemsetAsync(d.cnt, 0, sizeof(uint32_t) * CNT_N, c->plan));
-  if (J) CK(cudaMemcpyAsync(c->planes_dev, pin, sizeof(float) * 24 * J, cudaMemcpyHostToDevice, c->plan));
-  CK(launch_cull(d, c->planes_dev, J, T, p, c->plan));
+  CK(launch_cull(d, *pa, J, T, p, c->plan));
   CK(launch_quota(d, J, T, p, c->plan));
   CK(launch_plan(d, T, p, c->plan));
   prof_end(c, c->plan, tp, 2);
@@ -582,42 +592,94 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
   const PlanHdr h = *c->hdr;
   c->last = h;
+  c->last.n_dirty = 0;
 
-  // ---- a4 write-back decision for S- (after Adam(t) on the compute stream)
-  const bool overlap = !d.tide || h.fallback;  // S+ reuses S- records or slots
+  // ---- a4 write-back of dirty S-.  Runs on the compute stream after Adam(t-1)
+  //      (the dirty decision, R14).  Normal path: k_evict compacts the dirty
+  //      list, k_pack copies those records into the staging ring, the slots
+  //      are free at once and the copy engine drains the ring to the host
+  //      tier.  Direct path (S+ may reuse S- slots or records in this very
+  //      activate, or the ring is too small): copy straight from the slots.
+  const bool reuse_now = !d.tide || h.fallback;
+  const bool direct = reuse_now || h.nSm > d.S_max;
+  std::vector<std::pair<uint32_t, uint32_t>> packed;
   auto writeback = [&]() -> tgs_status {
     if (h.nSm == 0) return TGS_OK;
     Timer te;
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
+    if (!direct && c->d2h_rec[p]) CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[p], 0));
     prof_begin(c, c->compute, te);
     CK(launch_evict(d, h.nSm, p, c->compute));
+    if (!direct) CK(launch_pack(d, h.nSm, p, c->compute));
     prof_end(c, c->compute, te, 5);
-    c->tm.kernel_launches++;
-    CK(cudaEventRecord(c->ev_evict, c->compute));
-    CK(cudaEventSynchronize(c->ev_evict));
+    c->tm.kernel_launches += direct ? 1 : 2;
+    CK(cudaEventRecord(c->ev_evict[p], c->compute));
+    c->evict_rec[p] = true;
+    CK(cudaEventSynchronize(c->ev_evict[p]));
     const uint32_t nd = c->hdr->n_dirty;
     c->last.n_dirty = nd;
-    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict, 0));
+    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[p], 0));
     Timer td;
     prof_begin(c, c->d2h, td);
-    tgs_status s2 = issue_copies(c, c->dirty_map, nd, false, c->d2h);
-    if (s2 != TGS_OK) return s2;
+    if (direct) {
+      st = issue_copies(c, c->dirty_map, nd, false, c->d2h);
+      if (st != TGS_OK) return st;
+    } else {
+      // staging record i -> host record of dirty_map[i]; runs of consecutive ids merge
+      const size_t w = (size_t)d.n_arr * c->rec_bytes;
+      uint32_t i = 0;
+      while (i < nd) {
+        uint32_t j = i + 1;
+        while (j < nd && c->dirty_map[2 * j] == c->dirty_map[2 * (j - 1)] + 1) ++j;
+        CK(cudaMemcpyAsync(host_rec(c, c->dirty_map[2 * i]),
+                           d.staging[p] + (size_t)i * d.n_arr * d.rec_floats, w * (j - i),
+                           cudaMemcpyDeviceToHost, c->d2h));
+        c->tm.copy_calls++;
+        i = j;
+      }
+      packed.reserve(nd);
+      for (uint32_t k = 0; k < nd; ++k) packed.push_back({c->dirty_map[2 * k], k});
+    }
     prof_end(c, c->d2h, td, 4, (uint64_t)nd * d.n_arr * c->rec_bytes);
-    CK(cudaEventRecord(c->ev_d2h, c->d2h));
-    c->d2h_recorded = true;
+    CK(cudaEventRecord(c->ev_d2h[p], c->d2h));
+    c->d2h_rec[p] = true;
     return TGS_OK;
   };
-  if (overlap) {
+  if (reuse_now) {
     st = writeback();
     if (st != TGS_OK) return st;
+    if (h.nSm) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
   }
 
-  // ---- a4 gather of S+ into free slots on the copy engines
-  if (c->d2h_recorded) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h, 0));
+  // ---- a4 gather of S+ into free slots on the copy engine.  Hazards: the
+  //      slots the previous activate released (pack done, or its direct D2H
+  //      done) and host records written back two activates ago.  Blocks the
+  //      previous activate packed and this one re-admits come from the ring.
+  if (c->evict_rec[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[q], 0));
+  if (c->prev_direct && c->d2h_rec[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[q], 0));
+  if (c->d2h_rec[p]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
   if (h.nSp) {
     Timer th;
     prof_begin(c, c->h2d, th);
-    st = issue_copies(c, c->sp_map, h.nSp, true, c->h2d);
+    std::vector<uint32_t> from_host;
+    from_host.reserve(2 * h.nSp);
+    size_t pi = 0;  // prev_packed is ascending by id, like S+
+    const size_t w = (size_t)d.n_arr * c->rec_bytes, dp = 3 * c->rec_bytes;
+    for (uint32_t i = 0; i < h.nSp; ++i) {
+      const uint32_t l = c->sp_map[2 * i], sl = c->sp_map[2 * i + 1];
+      while (pi < c->prev_packed.size() && c->prev_packed[pi].first < l) ++pi;
+      if (pi < c->prev_packed.size() && c->prev_packed[pi].first == l) {
+        const float* src = d.staging[c->prev_pack_parity] +
+                           (size_t)c->prev_packed[pi].second * d.n_arr * d.rec_floats;
+        CK(cudaMemcpy2DAsync(slot_rec(c, sl), dp, src, w, w, 1, cudaMemcpyDeviceToDevice,
+                             c->h2d));
+        c->tm.copy_calls++;
+      } else {
+        from_host.push_back(l);
+        from_host.push_back(sl);
+      }
+    }
+    st = issue_copies(c, from_host.data(), (uint32_t)(from_host.size() / 2), true, c->h2d);
     if (st != TGS_OK) return st;
     if (d.cold) {
       CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
@@ -628,13 +690,16 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   }
   CK(cudaEventRecord(c->ev_ready, c->h2d));
 
-  if (!overlap) {
+  if (!reuse_now) {
     st = writeback();
     if (st != TGS_OK) return st;
   }
+  c->prev_packed.swap(packed);
+  c->prev_pack_parity = p;
+  c->prev_direct = direct && h.nSm > 0;
 
   c->last_parity = p;
-  c->parity = p ^ 1;
+  c->parity = q;
   c->T = T + 1;
   c->can_step = true;
   if (out) {
