@@ -539,141 +539,178 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
 
 // ------------------------------------------------------- a5 masked Adam
 // A warp owns a contiguous range of 4-row quads (4 rows = 944 B = 59 float4
-// per array); lane f and f+32 load float4 #f of theta, m, v, g (128-bit,
+// per array); lane f and f+32 (< 59) load float4 #f of theta, m, v, g (128-bit,
 // coalesced, streaming).  Element e = 4f+q of the quad belongs to row e/59 and
-// attribute e%59, so per-lane row/attribute maps are loop-invariant.
+// attribute e%59, so the per-lane attribute / row maps are loop-invariant.
+// Fast path (every row of the quad active, every gradient finite -- the
+// NULL-mask steady state): no per-element row logic.  Slow path: partial
+// quads, masked rows, non-finite rows (R20).
 constexpr int kAdamNT = 256;
-__global__ void __launch_bounds__(kAdamNT) k_adam(Dev d, uint32_t nA, int parity,
-                                                  const uint32_t* __restrict__ mask,
-                                                  AdamHyper hp) {
+constexpr uint32_t kAdamQPW = 64;  // quads per warp
+#ifndef TGS_ADAM_MINB
+#define TGS_ADAM_MINB 3  // resident CTAs per SM the register budget targets
+#endif
+
+struct AdamConsts {
+  float b1, b2, omb1, omb2, eps, ibs;
+};
+
+// Eq. masked_update with Adam's u_t (R9 prescribed order, IEEE RN, no contraction)
+__device__ __forceinline__ void adam_elem(float& th, float& m, float& v, float g, float ss,
+                                          const AdamConsts& k) {
+  float mt = __fmul_rn(k.b1, m);
+  mt = __fadd_rn(mt, __fmul_rn(k.omb1, g));
+  const float g2 = __fmul_rn(g, g);
+  float vt = __fmul_rn(k.b2, v);
+  vt = __fadd_rn(vt, __fmul_rn(k.omb2, g2));
+  m = mt;
+  v = vt;
+  float den = __fmul_rn(__fsqrt_rn(vt), k.ibs);
+  den = __fadd_rn(den, k.eps);
+  const float u = __fdiv_rn(mt, den);
+  th = __fsub_rn(th, __fmul_rn(ss, u));
+}
+
+__device__ __forceinline__ void adam_f4(float4& t, float4& m, float4& v, const float4& g,
+                                        const float* ss, const AdamConsts& k, uint32_t sel) {
+  if (sel & 1u) adam_elem(t.x, m.x, v.x, g.x, ss[0], k);
+  if (sel & 2u) adam_elem(t.y, m.y, v.y, g.y, ss[1], k);
+  if (sel & 4u) adam_elem(t.z, m.z, v.z, g.z, ss[2], k);
+  if (sel & 8u) adam_elem(t.w, m.w, v.w, g.w, ss[3], k);
+}
+
+__device__ __forceinline__ uint32_t nonfinite4(const float4& g) {
+  const uint32_t e = 0x7f800000u;
+  return ((__float_as_uint(g.x) & e) == e ? 1u : 0u) | ((__float_as_uint(g.y) & e) == e ? 2u : 0u) |
+         ((__float_as_uint(g.z) & e) == e ? 4u : 0u) | ((__float_as_uint(g.w) & e) == e ? 8u : 0u);
+}
+
+__global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t nA, int parity,
+                                                     const uint32_t* __restrict__ mask,
+                                                     AdamHyper hp) {
+  __shared__ float lr[kDim];
+  if (threadIdx.x < kDim) lr[threadIdx.x] = hp.lr[threadIdx.x];
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t QB = d.B / 4;
+  const uint32_t QB = d.B / 4;
   const uint64_t total = (uint64_t)nA * QB;
-  const uint64_t nwarps = (uint64_t)gridDim.x * (kAdamNT / 32);
+  // non-persistent grid: each warp a contiguous run of kAdamQPW quads, so CTAs
+  // retire continuously and the (high-priority) plan of the next batch can be
+  // scheduled while this Adam is still running
   const uint64_t wid = (uint64_t)blockIdx.x * (kAdamNT / 32) + (threadIdx.x >> 5);
-  const uint64_t chunk = (total + nwarps - 1) / nwarps;
-  uint64_t q0 = wid * chunk;
-  const uint64_t q1 = q0 + chunk < total ? q0 + chunk : total;
+  const uint64_t q0 = wid * kAdamQPW;
+  const uint64_t q1 = q0 + kAdamQPW < total ? q0 + kAdamQPW : total;
   if (q0 >= q1) return;
 
-  // loop-invariant per-lane element maps (f0 = lane, f1 = lane + 32 < 59)
+  // loop-invariant per-lane maps: rows of the 4 components of float4 #lane and #lane+32
   const bool has1 = lane + 32 < 59;
-  uint32_t row0 = 0, row1 = 0;  // 2 bits per component: row of element q
-  float lr0[4], lr1[4];
-  uint32_t a0[4], a1[4];
+  uint32_t rowsel0 = 0, rowsel1 = 0;  // bit 4*q + r: component q belongs to row r
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
-    const uint32_t r0 = e0 / 59, r1 = has1 ? e1 / 59 : 3u;
-    a0[q] = e0 - 59 * r0;
-    a1[q] = has1 ? e1 - 59 * r1 : 0u;
-    row0 |= r0 << (2 * q);
-    row1 |= r1 << (2 * q);
-    lr0[q] = hp.lr[a0[q]];
-    lr1[q] = hp.lr[a1[q]];
+    rowsel0 |= 1u << (4 * q + e0 / 59);
+    if (has1) rowsel1 |= 1u << (4 * q + e1 / 59);
   }
+  AdamConsts K{hp.b1, hp.b2, hp.omb1, hp.omb2, hp.eps, 1.0f};
   const uint32_t nw = (d.B + 31) / 32;
   const size_t rf = d.rec_floats;
 
-  int64_t cur = -1;
-  AdamEnt ent{};
+  uint32_t cur = 0xffffffffu;
+  uint32_t step = 0, rows = 0;
   float ss0[4], ss1[4];
-  const float4 *pg = nullptr;
+  const float4* pg = nullptr;
   float4 *pt = nullptr, *pm = nullptr, *pv = nullptr;
   const uint32_t* pmask = nullptr;
-  uint64_t gid0 = 0;
 
+  uint32_t i = (uint32_t)(q0 / QB);
+  uint32_t quad = (uint32_t)(q0 - (uint64_t)i * QB);
   for (uint64_t qi = q0; qi < q1; ++qi) {
-    const uint64_t i = qi / QB;
-    const uint32_t quad = (uint32_t)(qi - i * QB);
-    if ((int64_t)i != cur) {
-      cur = (int64_t)i;
-      ent = d.ent[i];
+    if (i != cur) {
+      cur = i;
+      const AdamEnt ent = d.ent[i];
+      step = ent.step;
+      rows = ent.rows;
+      K.ibs = ent.ibs;
       const uint32_t s = d.a_slot[parity][i];
       pt = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf);
-      pm = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf + rf);
-      pv = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf + 2 * rf);
+      pm = pt + rf / 4;
+      pv = pt + rf / 2;
       pg = reinterpret_cast<const float4*>(d.grads + (size_t)s * rf);
       pmask = mask ? mask + (size_t)s * nw : nullptr;
-      gid0 = (uint64_t)d.a_gid[parity][i] * d.B;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // ss_a = lr[a] / (1 - beta1^s)  (R9)
-        ss0[q] = __fdiv_rn(lr0[q], ent.bc1);
-        ss1[q] = __fdiv_rn(lr1[q], ent.bc1);
+        const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
+        ss0[q] = __fdiv_rn(lr[e0 % 59], ent.bc1);
+        ss1[q] = __fdiv_rn(lr[has1 ? e1 % 59 : 0], ent.bc1);
       }
     }
-    if (ent.step == 0u) continue;  // no active row in this block: untouched
     const uint32_t r0 = 4u * quad;
-    if (r0 >= ent.rows) continue;
-    uint32_t act = (ent.rows - r0) >= 4u ? 0xFu : ((1u << (ent.rows - r0)) - 1u);
+    // advance (i, quad) for the next iteration
+    if (++quad == QB) {
+      quad = 0;
+      ++i;
+    }
+    if (step == 0u || r0 >= rows) continue;  // no active row in this block / padding quad
+    uint32_t act = (rows - r0) >= 4u ? 0xFu : ((1u << (rows - r0)) - 1u);
     if (pmask) act &= (pmask[r0 >> 5] >> (r0 & 31)) & 0xFu;
     if (act == 0u) continue;  // warp-uniform
-    const size_t f0 = (size_t)quad * 59 + lane, f1 = f0 + 32;
+    const size_t f0 = (size_t)(r0 / 4) * 59 + lane, f1 = f0 + 32;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 g0 = __ldcs(pg + f0);
-    const float4 g1 = has1 ? __ldcs(pg + f1) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 t0 = __ldcs(pt + f0), m0 = __ldcs(pm + f0), v0 = __ldcs(pv + f0);
-    float4 t1 = make_float4(0.f, 0.f, 0.f, 0.f), m1 = t1, v1 = t1;
+    const float4 g1 = has1 ? __ldcs(pg + f1) : z;
+    float4 t0 = __ldcs(pt + f0), m0 = __ldcs(pm + f0), v0 = __ldcs(pv + f0);
+    float4 t1 = z, m1 = z, v1 = z;
     if (has1) {
       t1 = __ldcs(pt + f1);
       m1 = __ldcs(pm + f1);
       v1 = __ldcs(pv + f1);
     }
-    // R20: a row with any non-finite gradient is skipped (and reported)
-    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    uint32_t bad = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (!isfinite(gg[q])) bad |= 1u << ((row0 >> (2 * q)) & 3u);
-      if (has1 && !isfinite(gg[4 + q])) bad |= 1u << ((row1 >> (2 * q)) & 3u);
-    }
-    bad = __reduce_or_sync(kFull, bad);
-    if (bad & act) {  // rare path: lowest gid*59+attr over active rows
-      unsigned long long best = ~0ull;
+    const uint32_t nf0 = nonfinite4(g0), nf1 = has1 ? nonfinite4(g1) : 0u;
+    const bool anybad = __any_sync(kFull, (nf0 | nf1) != 0u);
+    uint32_t sel0 = 0xFu, sel1 = has1 ? 0xFu : 0u;
+    if (act != 0xFu || anybad) {  // slow path: rows of the quad that are skipped
+      uint32_t bad = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint32_t ra = (row0 >> (2 * q)) & 3u, rb = (row1 >> (2 * q)) & 3u;
-        if (((act >> ra) & 1u) && !isfinite(gg[q])) {
-          const unsigned long long idx = (gid0 + r0 + ra) * 59ull + a0[q];
-          best = idx < best ? idx : best;
-        }
-        if (has1 && ((act >> rb) & 1u) && !isfinite(gg[4 + q])) {
-          const unsigned long long idx = (gid0 + r0 + rb) * 59ull + a1[q];
-          best = idx < best ? idx : best;
-        }
+        if ((nf0 >> q) & 1u) bad |= (rowsel0 >> (4 * q)) & 0xFu;
+        if ((nf1 >> q) & 1u) bad |= (rowsel1 >> (4 * q)) & 0xFu;
       }
-      if (best != ~0ull) atomicMin(d.nonfinite, best);
-    }
-    const uint32_t upd = act & ~bad;
-    if (upd == 0u) continue;
-    float th[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-    float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-    float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      bad = __reduce_or_sync(kFull, bad);
+      if (bad & act) {  // R20: report the lowest gid*59+attr over active rows
+        const uint64_t gid0 = (uint64_t)d.a_gid[parity][cur] * d.B + r0;
+        unsigned long long best = ~0ull;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t rr = k < 4 ? (row0 >> (2 * k)) & 3u : (row1 >> (2 * (k - 4))) & 3u;
-      if (!((upd >> rr) & 1u)) continue;  // Eq. masked_update: unchanged off I_t
-      const float g = gg[k];
-      // R9 prescribed order, IEEE RN, no contraction
-      float mt = __fmul_rn(hp.b1, mm[k]);
-      mt = __fadd_rn(mt, __fmul_rn(hp.omb1, g));
-      const float g2 = __fmul_rn(g, g);
-      float vt = __fmul_rn(hp.b2, vv[k]);
-      vt = __fadd_rn(vt, __fmul_rn(hp.omb2, g2));
-      mm[k] = mt;
-      vv[k] = vt;
-      float den = __fmul_rn(__fsqrt_rn(vt), ent.ibs);
-      den = __fadd_rn(den, hp.eps);
-      const float u = __fdiv_rn(mt, den);
-      const float ss = k < 4 ? ss0[k] : ss1[k - 4];
-      th[k] = __fsub_rn(th[k], __fmul_rn(ss, u));
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
+          if (((nf0 >> q) & 1u) && ((act >> (e0 / 59)) & 1u)) {
+            const unsigned long long idx = (gid0 + e0 / 59) * 59ull + e0 % 59;
+            best = idx < best ? idx : best;
+          }
+          if (((nf1 >> q) & 1u) && ((act >> (e1 / 59)) & 1u)) {
+            const unsigned long long idx = (gid0 + e1 / 59) * 59ull + e1 % 59;
+            best = idx < best ? idx : best;
+          }
+        }
+        if (best != ~0ull) atomicMin(d.nonfinite, best);
+      }
+      const uint32_t upd = act & ~bad;  // Eq. masked_update: unchanged off I_t
+      if (upd == 0u) continue;
+      sel0 = sel1 = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((rowsel0 >> (4 * q)) & upd) sel0 |= 1u << q;
+        if ((rowsel1 >> (4 * q)) & upd) sel1 |= 1u << q;
+      }
     }
-    __stcs(pt + f0, make_float4(th[0], th[1], th[2], th[3]));
-    __stcs(pm + f0, make_float4(mm[0], mm[1], mm[2], mm[3]));
-    __stcs(pv + f0, make_float4(vv[0], vv[1], vv[2], vv[3]));
+    adam_f4(t0, m0, v0, g0, ss0, K, sel0);
+    __stcs(pt + f0, t0);
+    __stcs(pm + f0, m0);
+    __stcs(pv + f0, v0);
     if (has1) {
-      __stcs(pt + f1, make_float4(th[4], th[5], th[6], th[7]));
-      __stcs(pm + f1, make_float4(mm[4], mm[5], mm[6], mm[7]));
-      __stcs(pv + f1, make_float4(vv[4], vv[5], vv[6], vv[7]));
+      adam_f4(t1, m1, v1, g1, ss1, K, sel1);
+      __stcs(pt + f1, t1);
+      __stcs(pm + f1, m1);
+      __stcs(pv + f1, v1);
     }
   }
 }
@@ -730,9 +767,10 @@ cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const ui
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
+  (void)grid_ctas;
   const uint64_t quads = (uint64_t)nA * (d.B / 4);
-  const uint64_t need = (quads + (kAdamNT / 32) - 1) / (kAdamNT / 32);
-  const int grid = (int)(need < (uint64_t)grid_ctas ? need : (uint64_t)grid_ctas);
+  const uint64_t per_cta = (uint64_t)(kAdamNT / 32) * kAdamQPW;
+  const unsigned grid = (unsigned)((quads + per_cta - 1) / per_cta);
   k_adam<<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp);
   return cudaGetLastError();
 }

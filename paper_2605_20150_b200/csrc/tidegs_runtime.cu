@@ -257,35 +257,64 @@ inline float* slot_rec(tgs_ctx* c, uint32_t s) {
   return c->d.params + (size_t)s * 3 * c->d.rec_floats;
 }
 
-// Copy runs of (local id, slot) pairs, merging consecutive ids with
-// consecutive slots into one 2-D copy (host pitch n_arr*rec, slot pitch 3*rec).
+// A batch of 1-D copies submitted with one cudaMemcpyBatchAsync: the copy
+// engines then keep both PCIe directions busy at once (measured on this box:
+// ~49 + 49 GB/s for 370 single-record copies per direction, against ~31 + 30
+// GB/s for the same copies issued one cudaMemcpyAsync at a time;
+// profiles/linkbench_r01.txt).  Adjacent copies merge when both sides are
+// contiguous.
+struct CopyBatch {
+  std::vector<void*> dst;
+  std::vector<void*> src;
+  std::vector<size_t> size;
+  uint64_t bytes = 0;
+  void add(void* d, const void* s, size_t n) {
+    bytes += n;
+    if (!dst.empty() && (char*)dst.back() + size.back() == (char*)d &&
+        (char*)src.back() + size.back() == (const char*)s) {
+      size.back() += n;
+      return;
+    }
+    dst.push_back(d);
+    src.push_back(const_cast<void*>(s));
+    size.push_back(n);
+  }
+};
+
+tgs_status submit(tgs_ctx* c, CopyBatch& b, cudaStream_t s) {
+  if (b.dst.empty()) return TGS_OK;
+  if (b.dst.size() == 1) {
+    CK(cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, s));
+  } else {
+    cudaMemcpyAttributes at{};
+    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t aidx = 0, fail = 0;
+    CK(cudaMemcpyBatchAsync(b.dst.data(), b.src.data(), b.size.data(), b.dst.size(), &at, &aidx,
+                            1, &fail, s));
+  }
+  c->tm.copy_calls += b.dst.size();
+  return TGS_OK;
+}
+
+// Records of (local id, slot) pairs between the host tier and the slots
+// (theta only when moments cold-restart: the slot keeps m, v behind theta).
+void add_records(tgs_ctx* c, CopyBatch& b, const uint32_t* pairs, uint32_t n, bool to_device) {
+  const size_t w = (size_t)c->d.n_arr * c->rec_bytes;
+  for (uint32_t i = 0; i < n; ++i) {
+    float* h = host_rec(c, pairs[2 * i]);
+    float* d = slot_rec(c, pairs[2 * i + 1]);
+    if (to_device)
+      b.add(d, h, w);
+    else
+      b.add(h, d, w);
+  }
+}
+
 tgs_status issue_copies(tgs_ctx* c, const uint32_t* pairs, uint32_t n, bool to_device,
                         cudaStream_t s) {
-  const size_t w = (size_t)c->d.n_arr * c->rec_bytes;  // bytes per record moved
-  const size_t hp = w, dp = 3 * c->rec_bytes;
-  uint32_t i = 0;
-  while (i < n) {
-    uint32_t j = i + 1;
-    while (j < n && pairs[2 * j] == pairs[2 * (j - 1)] + 1 && pairs[2 * j + 1] == pairs[2 * (j - 1) + 1] + 1)
-      ++j;
-    const uint32_t l = pairs[2 * i], sl = pairs[2 * i + 1], run = j - i;
-    if (hp == dp) {
-      if (to_device)
-        CK(cudaMemcpyAsync(slot_rec(c, sl), host_rec(c, l), w * run, cudaMemcpyHostToDevice, s));
-      else
-        CK(cudaMemcpyAsync(host_rec(c, l), slot_rec(c, sl), w * run, cudaMemcpyDeviceToHost, s));
-    } else {
-      if (to_device)
-        CK(cudaMemcpy2DAsync(slot_rec(c, sl), dp, host_rec(c, l), hp, w, run,
-                             cudaMemcpyHostToDevice, s));
-      else
-        CK(cudaMemcpy2DAsync(host_rec(c, l), hp, slot_rec(c, sl), dp, w, run,
-                             cudaMemcpyDeviceToHost, s));
-    }
-    c->tm.copy_calls++;
-    i = j;
-  }
-  return TGS_OK;
+  CopyBatch b;
+  add_records(c, b, pairs, n, to_device);
+  return submit(c, b, s);
 }
 
 void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user, int nthreads) {
@@ -441,7 +470,10 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   };
   if (cudaSetDevice(g.device) != cudaSuccess) return fail(TGS_ECUDA);
   c->compute = (cudaStream_t)compute_stream;
-  if (cudaStreamCreateWithFlags(&c->plan, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  // the plan is latency-critical (the host waits for it): highest priority
+  if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
@@ -625,18 +657,13 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
       st = issue_copies(c, c->dirty_map, nd, false, c->d2h);
       if (st != TGS_OK) return st;
     } else {
-      // staging record i -> host record of dirty_map[i]; runs of consecutive ids merge
+      // staging record i -> host record of dirty_map[i] (runs of consecutive ids merge)
       const size_t w = (size_t)d.n_arr * c->rec_bytes;
-      uint32_t i = 0;
-      while (i < nd) {
-        uint32_t j = i + 1;
-        while (j < nd && c->dirty_map[2 * j] == c->dirty_map[2 * (j - 1)] + 1) ++j;
-        CK(cudaMemcpyAsync(host_rec(c, c->dirty_map[2 * i]),
-                           d.staging[p] + (size_t)i * d.n_arr * d.rec_floats, w * (j - i),
-                           cudaMemcpyDeviceToHost, c->d2h));
-        c->tm.copy_calls++;
-        i = j;
-      }
+      CopyBatch b;
+      for (uint32_t k = 0; k < nd; ++k)
+        b.add(host_rec(c, c->dirty_map[2 * k]), d.staging[p] + (size_t)k * d.n_arr * d.rec_floats, w);
+      st = submit(c, b, c->d2h);
+      if (st != TGS_OK) return st;
       packed.reserve(nd);
       for (uint32_t k = 0; k < nd; ++k) packed.push_back({c->dirty_map[2 * k], k});
     }
@@ -661,25 +688,21 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   if (h.nSp) {
     Timer th;
     prof_begin(c, c->h2d, th);
-    std::vector<uint32_t> from_host;
-    from_host.reserve(2 * h.nSp);
+    CopyBatch b;
     size_t pi = 0;  // prev_packed is ascending by id, like S+
-    const size_t w = (size_t)d.n_arr * c->rec_bytes, dp = 3 * c->rec_bytes;
+    const size_t w = (size_t)d.n_arr * c->rec_bytes;
     for (uint32_t i = 0; i < h.nSp; ++i) {
       const uint32_t l = c->sp_map[2 * i], sl = c->sp_map[2 * i + 1];
       while (pi < c->prev_packed.size() && c->prev_packed[pi].first < l) ++pi;
       if (pi < c->prev_packed.size() && c->prev_packed[pi].first == l) {
-        const float* src = d.staging[c->prev_pack_parity] +
-                           (size_t)c->prev_packed[pi].second * d.n_arr * d.rec_floats;
-        CK(cudaMemcpy2DAsync(slot_rec(c, sl), dp, src, w, w, 1, cudaMemcpyDeviceToDevice,
-                             c->h2d));
-        c->tm.copy_calls++;
+        // re-admitted right after its write-back: newest copy is in the ring
+        b.add(slot_rec(c, sl), d.staging[c->prev_pack_parity] +
+                                   (size_t)c->prev_packed[pi].second * d.n_arr * d.rec_floats, w);
       } else {
-        from_host.push_back(l);
-        from_host.push_back(sl);
+        b.add(slot_rec(c, sl), host_rec(c, l), w);
       }
     }
-    st = issue_copies(c, from_host.data(), (uint32_t)(from_host.size() / 2), true, c->h2d);
+    st = submit(c, b, c->h2d);
     if (st != TGS_OK) return st;
     if (d.cold) {
       CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));

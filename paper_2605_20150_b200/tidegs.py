@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtidegs.so")
+# TGS_LIB selects an in-tree build variant (kernel A/B experiments); default libtidegs.so
+LIB_PATH = os.environ.get("TGS_LIB") or os.path.join(_HERE, "libtidegs.so")
 DIM = 59
 
 OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENONFINITE, EPOISONED = range(8)
