@@ -67,8 +67,12 @@ struct Dev {
   PlanHdr* hdr_dev;      // device copy of the header
   PlanHdr* hdr_map;      // device alias of the mapped host header
   uint32_t* sp_map;      // mapped host [C][2] (local id, slot) of S+
-  uint32_t* dirty_map;   // mapped host [C][2] (local id, slot) of dirty S-
+  uint32_t* dirty_map[2];  // mapped host [C][2] (local id, slot) of dirty S- (parity)
+  uint32_t* ndirty_map;    // mapped host [2] |dirty S-| (parity)
+  uint32_t* ndirty_dev;    // [2] |dirty S-| (parity), read by k_pack
   uint32_t* dl_slot;     // [C] device copy of the dirty S- slots (pack source)
+  int32_t* wb_tag;       // [Kloc] activate index at which the block was packed (-1 never)
+  uint32_t* wb_idx;      // [Kloc] its staging-ring index then
   float* staging[2];     // [S_max][n_arr][B][59] write-back staging ring (parity)
   uint32_t S_max;        // staging capacity in records
   // selection
@@ -103,6 +107,9 @@ cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaSt
 cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
 cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
+cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t T, bool tag,
+                                cudaStream_t s);
+cudaError_t launch_readmit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s);
 cudaError_t launch_cold_init(const Dev& d, uint32_t nSp, int parity, cudaStream_t s);
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s);

@@ -423,7 +423,8 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
 
 // ---------------------------------------- a4 dirty S- -> write-back list
 constexpr int kEvictNT = 1024;
-__global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int parity) {
+__global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int parity, int32_t T,
+                                                    int tag) {
   __shared__ uint32_t sh[40];
   const uint32_t* smb = d.sm_blk[parity];
   const uint32_t* sms = d.sm_slot[parity];
@@ -440,16 +441,20 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
     uint32_t tot;
     const uint32_t o = c + block_scan<kEvictNT>(dirty, tot, sh);
     if (dirty) {
-      d.dirty_map[2 * o] = l;
-      d.dirty_map[2 * o + 1] = s;
+      d.dirty_map[parity][2 * o] = l;
+      d.dirty_map[parity][2 * o + 1] = s;
       d.dl_slot[o] = s;
+      if (tag) {  // packed into staging[parity][o]: a re-admission next batch reads it there
+        d.wb_tag[l] = T;
+        d.wb_idx[l] = o;
+      }
       atomicAnd(&d.dirty[s >> 5], ~(1u << (s & 31)));
     }
     c += tot;
   }
   if (threadIdx.x == 0) {
-    d.hdr_map->n_dirty = c;
-    d.hdr_dev->n_dirty = c;
+    d.ndirty_map[parity] = c;
+    d.ndirty_dev[parity] = c;
     atomicAdd(&d.stats[ST_EVICT_DIRTY], (unsigned long long)c);
     atomicAdd(&d.stats[ST_D2H], (unsigned long long)c * d.rec_floats * 4ull * d.n_arr);
   }
@@ -462,7 +467,7 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
 // and the copy engine drains the staging ring to the host tier meanwhile.
 __global__ void __launch_bounds__(256) k_pack(Dev d, int parity) {
   const uint32_t i = blockIdx.y;
-  if (i >= d.hdr_dev->n_dirty) return;
+  if (i >= d.ndirty_dev[parity]) return;
   const uint32_t s = d.dl_slot[i];
   const size_t n4 = (size_t)d.n_arr * d.rec_floats / 4;
   const float4* src = reinterpret_cast<const float4*>(d.params + (size_t)s * 3 * d.rec_floats);
@@ -478,6 +483,24 @@ __global__ void __launch_bounds__(256) k_pack(Dev d, int parity) {
     __stcs(dst + e + 3 * stride, f);
   }
   for (; e < n4; e += stride) __stcs(dst + e, __ldcs(src + e));
+}
+
+// ------------- a4 re-admission fixup: S+ blocks packed by the previous batch
+// Their newest record sits in the previous staging ring (its write-back to the
+// host tier may still be in flight), so it is copied ring -> slot over the
+// copy-engine value the gather brought.  grid (chunks, nSp).
+__global__ void __launch_bounds__(256) k_readmit(Dev d, int parity, int32_t T) {
+  const uint32_t i = blockIdx.y;
+  const uint32_t l = d.sp_blk[parity][i];
+  if (d.wb_tag[l] != T - 1) return;
+  const uint32_t s = d.sp_slot[parity][i];
+  const size_t n4 = (size_t)d.n_arr * d.rec_floats / 4;
+  const float4* src = reinterpret_cast<const float4*>(
+      d.staging[parity ^ 1] + (size_t)d.wb_idx[l] * d.n_arr * d.rec_floats);
+  float4* dst = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * d.rec_floats);
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
+       e += (size_t)gridDim.x * blockDim.x)
+    __stcs(dst + e, __ldcs(src + e));
 }
 
 // ---------------------------------- a4 cold restart: m = v = 0 in new slots
@@ -546,7 +569,7 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
 // NULL-mask steady state): no per-element row logic.  Slow path: partial
 // quads, masked rows, non-finite rows (R20).
 constexpr int kAdamNT = 256;
-constexpr uint32_t kAdamQPW = 64;  // quads per warp
+constexpr uint32_t kAdamQPW = 16;  // quads per warp (short CTA lifetime: the plan gets SMs)
 #ifndef TGS_ADAM_MINB
 #define TGS_ADAM_MINB 3  // resident CTAs per SM the register budget targets
 #endif
@@ -738,7 +761,20 @@ cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s) {
 }
 
 cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) {
-  k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity);
+  k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity, 0, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t T, bool tag,
+                                cudaStream_t s) {
+  k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity, T, tag ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_readmit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s) {
+  if (nSp == 0 || T == 0) return cudaSuccess;
+  dim3 grid(8, nSp);
+  k_readmit<<<grid, 256, 0, s>>>(d, parity, T);
   return cudaGetLastError();
 }
 

@@ -1,29 +1,38 @@
 // tidegs_runtime.cu -- host runtime behind the C ABI of include/tidegs.h.
 //
 // Owns the pinned host tier (one shard of Theta, M, V as block records), the
-// device slot pool, the streams/events of the pipeline and the host side of
-// the plan readback.  Per activate:
+// device slot pool, the streams/events of the pipeline, the plan readback and
+// an I/O thread for the write-back.  Per activate t (parity p = t & 1;
+// DESIGN.md §2):
 //
-//   plan stream    : H2D planes -> k_cull -> k_quota -> k_plan      (a1-a3)
-//   host           : wait for the plan only (not for the previous Adam)
-//   h2d stream     : wait(previous write-back) -> record copies S+  (a4 gather,
-//                    copy engines, pinned host tier -> slots) -> ready
-//   compute stream : [after Adam(t)] k_evict (dirty S- list)        (a4)
-//   host           : wait for k_evict only if |S-| > 0
-//   d2h stream     : dirty S- records slots -> host tier            (a4 scatter)
-//   step_adam      : compute waits ready; k_adam_prologue; k_adam   (a5)
+//   plan stream    : [lists of p free: Adam/evict/gather of t-2 done]
+//                    k_cull -> k_quota -> k_plan                       (a1-a3)
+//   host           : wait for the plan only (never for an Adam)
+//   h2d stream     : [slots freed by t-1, host records written by t-2]
+//                    one cudaMemcpyBatchAsync of S+ host tier -> slots (a4 gather)
+//                    -> k_readmit (S+ packed by t-1: newest copy in the ring)
+//                    -> k_cold_init -> ready[p]
+//   compute stream : [after Adam(t-1)] k_evict (dirty S-) -> k_pack (slots ->
+//                    staging ring p) -> evict[p]                        (a4)
+//   I/O thread     : waits evict[p], reads the dirty list, one batch of
+//                    staging ring p -> host tier on the d2h stream -> d2h[p]
+//   step_adam      : compute waits ready[p]; k_adam_prologue; k_adam   (a5)
 //
 // S+ always lands in slots that R_t does not hold (R13), so the gather of
-// batch t+1 overlaps Adam of batch t without a hazard; the only orderings are
-// write-back(t) -> gather(t+1) (slot reuse, re-admitted records) and
-// Adam(t) -> write-back(t+1) (dirty decision).
+// batch t overlaps Adam of batch t-1; the write-back of t is decided after
+// Adam(t-1) (R14) without blocking the caller.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <climits>
+#include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -60,18 +69,29 @@ struct tgs_ctx {
   // mapped pinned
   PlanHdr* hdr = nullptr;         // host view
   uint32_t* sp_map = nullptr;     // host view
-  uint32_t* dirty_map = nullptr;  // host view
+  uint32_t* dirty_map[2] = {nullptr, nullptr};  // host views (parity)
+  uint32_t* ndirty = nullptr;     // host view [2]
   float* planes_pinned = nullptr; // [kMaxCams*24] staging of the kernel parameter
-  // streams / events
+  // streams / events (ev_*[p]: last record by an activate of parity p)
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
-  bool own_compute = false;
-  cudaEvent_t ev_plan = nullptr, ev_ready = nullptr;
-  cudaEvent_t ev_evict[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
-  bool evict_rec[2] = {false, false}, d2h_rec[2] = {false, false};
-  bool prev_direct = false;        // previous activate wrote back straight from slots
-  // dirty records the previous activate packed: local id -> staging index
-  std::vector<std::pair<uint32_t, uint32_t>> prev_packed;
-  int prev_pack_parity = 0;
+  cudaEvent_t ev_plan = nullptr;
+  cudaEvent_t ev_ready[2] = {}, ev_evict[2] = {}, ev_d2h[2] = {}, ev_lists[2] = {};
+  bool rec_ready[2] = {}, rec_evict[2] = {}, rec_lists[2] = {};
+  int32_t d2h_job[2] = {-1, -1};   // activate index of the last write-back job of parity p
+  bool prev_direct = false;        // previous activate wrote back straight from its slots
+  bool prev_packed = false;        // previous activate packed dirty records into its ring
+  // I/O thread (write-back issue)
+  struct Job { int32_t T; int parity; bool direct; };
+  std::thread io;
+  std::mutex mu;
+  std::condition_variable cv_job, cv_done;
+  std::deque<Job> jobs;
+  int32_t inflight = -1;
+  bool stop = false;
+  std::atomic<bool> io_failed{false};
+  std::string io_err;
+  uint32_t last_ndirty = 0;
+  std::mutex prof_mu;
   // Adam LUT (bias corrections, R9)
   std::vector<float> lut_bc1_h, lut_ibs_h;
   float* lut_pinned = nullptr;     // [2][lut_cap]
@@ -92,8 +112,10 @@ struct tgs_ctx {
   bool prof = false;
   tgs_timing tm{};
   std::vector<cudaEvent_t> ev_pool;
-  struct Pending { cudaEvent_t a, b; int kind; uint64_t bytes; };
+  struct Pending { cudaEvent_t a, b; int kind; uint64_t bytes; int32_t iter; };
   std::vector<Pending> pending;
+  bool trace = false;             // TGS_TRACE=1: print every timed span (stderr)
+  cudaEvent_t trace_base = nullptr;
 };
 
 namespace {
@@ -151,6 +173,7 @@ cudaEvent_t prof_event(tgs_ctx* c) {
 // kinds: 0 adam, 1 prologue, 2 plan, 3 h2d, 4 d2h, 5 evict
 void prof_begin(tgs_ctx* c, cudaStream_t s, Timer& t) {
   if (!c->prof) return;
+  std::lock_guard<std::mutex> g(c->prof_mu);
   t.a = prof_event(c);
   t.b = prof_event(c);
   cudaEventRecord(t.a, s);
@@ -158,13 +181,22 @@ void prof_begin(tgs_ctx* c, cudaStream_t s, Timer& t) {
 }
 void prof_end(tgs_ctx* c, cudaStream_t s, Timer& t, int kind, uint64_t bytes = 0) {
   if (!t.armed) return;
+  std::lock_guard<std::mutex> g(c->prof_mu);
   cudaEventRecord(t.b, s);
-  c->pending.push_back({t.a, t.b, kind, bytes});
+  c->pending.push_back({t.a, t.b, kind, bytes, c->T});
 }
 void prof_collect(tgs_ctx* c) {
+  std::lock_guard<std::mutex> g(c->prof_mu);
+  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "cold_init", "readmit"};
   for (auto& p : c->pending) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.a, p.b) != cudaSuccess) ms = 0.f;
+    if (c->trace && c->trace_base) {
+      float t0 = 0.f;
+      cudaEventElapsedTime(&t0, c->trace_base, p.a);
+      fprintf(stderr, "[tgs trace] it %d %-10s %9.3f .. %9.3f ms (%7.3f) %llu B\n", p.iter,
+              names[p.kind], t0, t0 + ms, ms, (unsigned long long)p.bytes);
+    }
     switch (p.kind) {
       case 0: c->tm.adam_ms += ms; c->tm.adam_launches++; break;
       case 1: c->tm.adam_prologue_ms += ms; break;
@@ -172,6 +204,7 @@ void prof_collect(tgs_ctx* c) {
       case 3: c->tm.h2d_ms += ms; c->tm.h2d_batches++; c->tm.h2d_bytes += p.bytes; break;
       case 4: c->tm.d2h_ms += ms; c->tm.d2h_batches++; c->tm.d2h_bytes += p.bytes; break;
       case 5: c->tm.evict_ms += ms; break;
+      case 6: case 7: break;
     }
     c->ev_pool.push_back(p.a);
     c->ev_pool.push_back(p.b);
@@ -347,13 +380,107 @@ void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user,
   for (auto& t : th) t.join();
 }
 
+// ---------------------------------------------------------------- I/O thread
+// Issues the write-back of each activate once its k_evict/k_pack finished:
+// the dirty decision depends on Adam(t-1) (R14), so the caller's thread never
+// waits for it.  Jobs run in activate order.
+void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
+  Dev& d = c->d;
+  const int p = j.parity;
+  auto fail = [&](const char* what, cudaError_t e) {
+    std::lock_guard<std::mutex> g(c->mu);
+    c->io_err = std::string(what) + ": " + cudaGetErrorString(e);
+    c->io_failed = true;
+  };
+  cudaError_t e = cudaEventSynchronize(c->ev_evict[p]);
+  if (e != cudaSuccess) return fail("io: cudaEventSynchronize(evict)", e);
+  const uint32_t nd = c->ndirty[p];
+  const uint32_t* dl = c->dirty_map[p];
+  const size_t w = (size_t)d.n_arr * c->rec_bytes;
+  CopyBatch b;
+  for (uint32_t k = 0; k < nd; ++k) {
+    float* h = host_rec(c, dl[2 * k]);
+    const float* src = j.direct ? slot_rec(c, dl[2 * k + 1])
+                                : d.staging[p] + (size_t)k * d.n_arr * d.rec_floats;
+    b.add(h, src, w);
+  }
+  Timer td;
+  prof_begin(c, c->d2h, td);
+  if (!b.dst.empty()) {
+    if (b.dst.size() == 1) {
+      e = cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, c->d2h);
+    } else {
+      cudaMemcpyAttributes at{};
+      at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      size_t aidx = 0, failidx = 0;
+      e = cudaMemcpyBatchAsync(b.dst.data(), b.src.data(), b.size.data(), b.dst.size(), &at,
+                               &aidx, 1, &failidx, c->d2h);
+    }
+    if (e != cudaSuccess) return fail("io: write-back batch", e);
+  }
+  prof_end(c, c->d2h, td, 4, (uint64_t)nd * w);
+  e = cudaEventRecord(c->ev_d2h[p], c->d2h);
+  if (e != cudaSuccess) return fail("io: cudaEventRecord(d2h)", e);
+  std::lock_guard<std::mutex> g(c->mu);
+  c->tm.copy_calls += b.dst.size();
+  c->last_ndirty = nd;
+}
+
+void io_main(tgs_ctx* c) {
+  cudaSetDevice(c->device);
+  for (;;) {
+    tgs_ctx::Job j;
+    {
+      std::unique_lock<std::mutex> g(c->mu);
+      c->cv_job.wait(g, [&] { return c->stop || !c->jobs.empty(); });
+      if (c->jobs.empty()) return;  // stop requested and drained
+      j = c->jobs.front();
+      c->jobs.pop_front();
+      c->inflight = j.T;
+    }
+    if (!c->io_failed) io_process(c, j);
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      c->inflight = -1;
+    }
+    c->cv_done.notify_all();
+  }
+}
+
+void io_submit(tgs_ctx* c, const tgs_ctx::Job& j) {
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    c->jobs.push_back(j);
+  }
+  c->cv_job.notify_one();
+}
+
+// Wait until every write-back job of an activate <= T has been issued (its
+// d2h event recorded), so a cudaStreamWaitEvent on it refers to that record.
+void io_join(tgs_ctx* c, int32_t T) {
+  std::unique_lock<std::mutex> g(c->mu);
+  c->cv_done.wait(g, [&] {
+    return (c->jobs.empty() || c->jobs.front().T > T) && (c->inflight < 0 || c->inflight > T);
+  });
+}
+
 tgs_status check(tgs_ctx* c) {
   if (!c) return TGS_EINVAL;
+  if (c->io_failed && !c->poisoned) {
+    std::lock_guard<std::mutex> g(c->mu);
+    c->poisoned = true;
+    c->err = c->io_err;
+  }
   if (c->poisoned) return TGS_EPOISONED;
   return TGS_OK;
 }
 
 tgs_status sync_all(tgs_ctx* c) {
+  io_join(c, INT32_MAX);
+  if (c->io_failed) {
+    check(c);
+    return TGS_ECUDA;
+  }
   CK(cudaStreamSynchronize(c->plan));
   CK(cudaStreamSynchronize(c->h2d));
   CK(cudaStreamSynchronize(c->compute));
@@ -364,6 +491,14 @@ tgs_status sync_all(tgs_ctx* c) {
 
 void destroy_impl(tgs_ctx* c) {
   if (!c) return;
+  if (c->io.joinable()) {
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      c->stop = true;
+    }
+    c->cv_job.notify_all();
+    c->io.join();
+  }
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (void* p : c->dev_allocs) {
@@ -373,13 +508,12 @@ void destroy_impl(tgs_ctx* c) {
       cudaFree(p);
   }
   if (c->host) cudaFreeHost(c->host);
-  if (c->hdr) cudaFreeHost(c->hdr);
-  if (c->sp_map) cudaFreeHost(c->sp_map);
-  if (c->dirty_map) cudaFreeHost(c->dirty_map);
-  if (c->planes_pinned) cudaFreeHost(c->planes_pinned);
-  if (c->lut_pinned) cudaFreeHost(c->lut_pinned);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_ready, c->ev_evict[0], c->ev_evict[1], c->ev_d2h[0],
-                        c->ev_d2h[1]})
+  for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
+                  (void*)c->ndirty, (void*)c->planes_pinned, (void*)c->lut_pinned})
+    if (h) cudaFreeHost(h);
+  for (cudaEvent_t e : {c->ev_plan, c->ev_ready[0], c->ev_ready[1], c->ev_evict[0],
+                        c->ev_evict[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_lists[0],
+                        c->ev_lists[1], c->trace_base})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -477,8 +611,9 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
-  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready, &c->ev_evict[0], &c->ev_evict[1],
-                         &c->ev_d2h[0], &c->ev_d2h[1]})
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready[0], &c->ev_ready[1], &c->ev_evict[0],
+                         &c->ev_evict[1], &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_lists[0],
+                         &c->ev_lists[1]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
 
   // ---- host tier (pinned, block records)
@@ -494,20 +629,24 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   fill_host_tier(c, theta_rows, fill, fill_user, nth);
 
   // ---- mapped pinned plan readback
+  const size_t list_bytes = sizeof(uint32_t) * 2 * (size_t)std::max(d.C, 1u);
   if (cudaHostAlloc((void**)&c->hdr, sizeof(PlanHdr), cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->sp_map, sizeof(uint32_t) * 2 * (size_t)std::max(d.C, 1u),
-                    cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->dirty_map, sizeof(uint32_t) * 2 * (size_t)std::max(d.C, 1u),
-                    cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 2 * kMaxCams * 24,
+      cudaHostAlloc((void**)&c->sp_map, list_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->dirty_map[0], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->dirty_map[1], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * 2, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * kMaxCams * 24,
                     cudaHostAllocDefault) != cudaSuccess) {
     cudaGetLastError();
     return fail(TGS_ENOMEM);
   }
   std::memset(c->hdr, 0, sizeof(PlanHdr));
+  std::memset(c->ndirty, 0, sizeof(uint32_t) * 2);
   cudaHostGetDevicePointer((void**)&d.hdr_map, c->hdr, 0);
   cudaHostGetDevicePointer((void**)&d.sp_map, c->sp_map, 0);
-  cudaHostGetDevicePointer((void**)&d.dirty_map, c->dirty_map, 0);
+  cudaHostGetDevicePointer((void**)&d.dirty_map[0], c->dirty_map[0], 0);
+  cudaHostGetDevicePointer((void**)&d.dirty_map[1], c->dirty_map[1], 0);
+  cudaHostGetDevicePointer((void**)&d.ndirty_map, c->ndirty, 0);
 
   // ---- device state
   bool ok = true;
@@ -541,6 +680,9 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
   d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
+  d.ndirty_dev = dalloc_t<uint32_t>(c, 2, ok);
+  d.wb_tag = dalloc_t<int32_t>(c, Kl, ok);
+  d.wb_idx = dalloc_t<uint32_t>(c, Kl, ok);
   d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C / 4);
   for (int p = 0; p < 2; ++p)
     d.staging[p] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
@@ -570,6 +712,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   CKI(cudaMemsetAsync(d.ever, 0, Kl, s0));
   CKI(cudaMemsetAsync(d.evicted, 0, Kl, s0));
   CKI(cudaMemsetAsync(d.admit, 0, sizeof(int32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.wb_tag, 0xff, sizeof(int32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * 2, s0));
   for (uint32_t* p : {d.Kb, d.cand, d.Q, d.Sp, d.Sm, d.Om, d.Ab, d.R[0], d.R[1]})
     CKI(cudaMemsetAsync(p, 0, sizeof(uint32_t) * Wd, s0));
   CKI(cudaMemsetAsync(d.percam, 0, sizeof(uint32_t) * (size_t)d.J_max * Wd, s0));
@@ -585,6 +729,7 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
 #undef CKI
   int dev = g.device;
   c->adam_grid = adam_grid(dev);
+  c->io = std::thread(io_main, c);
   *out = c;
   return TGS_OK;
 }
@@ -609,7 +754,11 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   const int32_t T = c->T;
 
   // ---- plan stream: a1 cull, a3 quota + fill, a2 delta, slots, A list.
-  //      Planes travel as a kernel parameter: nothing here queues on a copy engine.
+  //      The lists of parity p are free once activate t-2's Adam, write-back
+  //      kernels and gather are done (GPU-side waits only).  Planes travel as
+  //      a kernel parameter: nothing here queues behind a copy engine.
+  if (c->rec_lists[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_lists[p], 0));
+  if (c->rec_ready[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_ready[p], 0));
   Timer tp;
   static_assert(sizeof(PlanesArg) == sizeof(float) * kMaxCams * 24, "planes layout");
   PlanesArg* pa = reinterpret_cast<PlanesArg*>(c->planes_pinned);
@@ -624,102 +773,91 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
   const PlanHdr h = *c->hdr;
   c->last = h;
-  c->last.n_dirty = 0;
 
-  // ---- a4 write-back of dirty S-.  Runs on the compute stream after Adam(t-1)
-  //      (the dirty decision, R14).  Normal path: k_evict compacts the dirty
-  //      list, k_pack copies those records into the staging ring, the slots
-  //      are free at once and the copy engine drains the ring to the host
-  //      tier.  Direct path (S+ may reuse S- slots or records in this very
-  //      activate, or the ring is too small): copy straight from the slots.
+  // ---- a4 write-back of dirty S-, enqueued on the compute stream after
+  //      Adam(t-1) (the dirty decision).  Normal path: k_evict compacts the
+  //      dirty list and k_pack copies those records into staging ring p, so
+  //      their slots are free at once; the I/O thread then drains the ring to
+  //      the host tier.  Direct path (this activate's S+ may reuse S- slots or
+  //      records, or the ring is too small): the copies read the slots.
   const bool reuse_now = !d.tide || h.fallback;
   const bool direct = reuse_now || h.nSm > d.S_max;
-  std::vector<std::pair<uint32_t, uint32_t>> packed;
   auto writeback = [&]() -> tgs_status {
-    if (h.nSm == 0) return TGS_OK;
     Timer te;
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-    if (!direct && c->d2h_rec[p]) CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[p], 0));
+    if (!direct && c->d2h_job[p] >= 0) {  // ring p is still drained by job t-2
+      io_join(c, c->d2h_job[p]);
+      CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[p], 0));
+    }
     prof_begin(c, c->compute, te);
-    CK(launch_evict(d, h.nSm, p, c->compute));
+    CK(launch_evict_tagged(d, h.nSm, p, T, !direct, c->compute));
     if (!direct) CK(launch_pack(d, h.nSm, p, c->compute));
     prof_end(c, c->compute, te, 5);
     c->tm.kernel_launches += direct ? 1 : 2;
     CK(cudaEventRecord(c->ev_evict[p], c->compute));
-    c->evict_rec[p] = true;
-    CK(cudaEventSynchronize(c->ev_evict[p]));
-    const uint32_t nd = c->hdr->n_dirty;
-    c->last.n_dirty = nd;
-    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[p], 0));
-    Timer td;
-    prof_begin(c, c->d2h, td);
-    if (direct) {
-      st = issue_copies(c, c->dirty_map, nd, false, c->d2h);
-      if (st != TGS_OK) return st;
-    } else {
-      // staging record i -> host record of dirty_map[i] (runs of consecutive ids merge)
-      const size_t w = (size_t)d.n_arr * c->rec_bytes;
-      CopyBatch b;
-      for (uint32_t k = 0; k < nd; ++k)
-        b.add(host_rec(c, c->dirty_map[2 * k]), d.staging[p] + (size_t)k * d.n_arr * d.rec_floats, w);
-      st = submit(c, b, c->d2h);
-      if (st != TGS_OK) return st;
-      packed.reserve(nd);
-      for (uint32_t k = 0; k < nd; ++k) packed.push_back({c->dirty_map[2 * k], k});
-    }
-    prof_end(c, c->d2h, td, 4, (uint64_t)nd * d.n_arr * c->rec_bytes);
-    CK(cudaEventRecord(c->ev_d2h[p], c->d2h));
-    c->d2h_rec[p] = true;
+    c->rec_evict[p] = true;
+    io_submit(c, {T, p, direct});
+    c->d2h_job[p] = T;
     return TGS_OK;
   };
-  if (reuse_now) {
+  if (reuse_now && h.nSm) {
     st = writeback();
     if (st != TGS_OK) return st;
-    if (h.nSm) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
+    io_join(c, T);
+    if (c->io_failed) return check(c);
+    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
   }
 
-  // ---- a4 gather of S+ into free slots on the copy engine.  Hazards: the
-  //      slots the previous activate released (pack done, or its direct D2H
-  //      done) and host records written back two activates ago.  Blocks the
-  //      previous activate packed and this one re-admits come from the ring.
-  if (c->evict_rec[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[q], 0));
-  if (c->prev_direct && c->d2h_rec[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[q], 0));
-  if (c->d2h_rec[p]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
+  // ---- a4 gather of S+ into free slots: one batch on the copy engine.
+  //      Hazards: slots freed by t-1 (pack done, or its direct write-back
+  //      done) and host records written back by t-2.
+  if (c->rec_evict[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[q], 0));
+  if (c->prev_direct) {
+    io_join(c, T - 1);
+    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[q], 0));
+  }
+  if (c->d2h_job[p] >= 0 && c->d2h_job[p] < T) {
+    io_join(c, c->d2h_job[p]);
+    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
+  }
+  if (c->io_failed) return check(c);
   if (h.nSp) {
     Timer th;
     prof_begin(c, c->h2d, th);
     CopyBatch b;
-    size_t pi = 0;  // prev_packed is ascending by id, like S+
-    const size_t w = (size_t)d.n_arr * c->rec_bytes;
-    for (uint32_t i = 0; i < h.nSp; ++i) {
-      const uint32_t l = c->sp_map[2 * i], sl = c->sp_map[2 * i + 1];
-      while (pi < c->prev_packed.size() && c->prev_packed[pi].first < l) ++pi;
-      if (pi < c->prev_packed.size() && c->prev_packed[pi].first == l) {
-        // re-admitted right after its write-back: newest copy is in the ring
-        b.add(slot_rec(c, sl), d.staging[c->prev_pack_parity] +
-                                   (size_t)c->prev_packed[pi].second * d.n_arr * d.rec_floats, w);
-      } else {
-        b.add(slot_rec(c, sl), host_rec(c, l), w);
-      }
-    }
+    add_records(c, b, c->sp_map, h.nSp, true);
     st = submit(c, b, c->h2d);
     if (st != TGS_OK) return st;
-    if (d.cold) {
-      CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
-      CK(launch_cold_init(d, h.nSp, p, c->h2d));
+    prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
+    if (c->prev_packed) {  // S+ blocks the previous batch packed: newest copy is in its ring
+      Timer tr;
+      prof_begin(c, c->h2d, tr);
+      CK(launch_readmit(d, h.nSp, p, T, c->h2d));
+      prof_end(c, c->h2d, tr, 7);
       c->tm.kernel_launches++;
     }
-    prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
+    if (d.cold) {
+      Timer tc;
+      CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
+      prof_begin(c, c->h2d, tc);
+      CK(launch_cold_init(d, h.nSp, p, c->h2d));
+      prof_end(c, c->h2d, tc, 6);
+      c->tm.kernel_launches++;
+    }
   }
-  CK(cudaEventRecord(c->ev_ready, c->h2d));
+  CK(cudaEventRecord(c->ev_ready[p], c->h2d));
+  c->rec_ready[p] = true;
 
-  if (!reuse_now) {
+  if (!reuse_now && h.nSm) {
     st = writeback();
     if (st != TGS_OK) return st;
   }
-  c->prev_packed.swap(packed);
-  c->prev_pack_parity = p;
+  // lists of parity p stay in use until this batch's write-back kernels (and
+  // its Adam, which re-records this event) are done
+  CK(cudaEventRecord(c->ev_lists[p], c->compute));
+  c->rec_lists[p] = true;
   c->prev_direct = direct && h.nSm > 0;
+  c->prev_packed = !direct && h.nSm > 0;
 
   c->last_parity = p;
   c->parity = q;
@@ -731,7 +869,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     out->n_active_blocks = h.nA;
     out->n_stage_in = h.nSp;
     out->n_evict = h.nSm;
-    out->n_evict_dirty = c->last.n_dirty;
+    out->n_evict_dirty = 0;  // decided after the previous Adam; see tgs_get_stats
     out->h2d_bytes = (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
     out->d_active_blocks = d.a_gid[p];
     out->d_active_slots = d.a_slot[p];
@@ -739,7 +877,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     out->d_grads = d.grads;
     out->slot_stride = 3 * d.rec_floats;
     out->grad_stride = d.rec_floats;
-    out->ready = (void*)c->ev_ready;
+    out->ready = (void*)c->ev_ready[p];
   }
   return TGS_OK;
 }
@@ -763,7 +901,7 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   h.omb2 = 1.0f - hp->beta2;
   h.eps = hp->eps;
   CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-  CK(cudaStreamWaitEvent(c->compute, c->ev_ready, 0));
+  CK(cudaStreamWaitEvent(c->compute, c->ev_ready[p], 0));
   if (nA == 0) return TGS_OK;
   Timer t1, t2;
   prof_begin(c, c->compute, t1);
@@ -773,6 +911,7 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   CK(launch_adam(c->d, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
   c->tm.kernel_launches += 2;
+  CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }
 
@@ -825,6 +964,12 @@ tgs_status tgs_set_profiling(tgs_ctx* c, int enabled) {
   if (st != TGS_OK) return st;
   c->prof = enabled != 0;
   c->tm = tgs_timing{};
+  const char* tr = getenv("TGS_TRACE");
+  c->trace = c->prof && tr && tr[0] == '1';
+  if (c->trace) {
+    if (!c->trace_base) cudaEventCreate(&c->trace_base);
+    cudaEventRecord(c->trace_base, c->compute);
+  }
   return TGS_OK;
 }
 
@@ -896,9 +1041,10 @@ uint32_t tgs_get_percam(tgs_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap) 
 uint32_t tgs_get_evicted_dirty(tgs_ctx* c, uint32_t* blocks, uint32_t cap) {
   if (check(c) != TGS_OK) return 0;
   if (sync_all(c) != TGS_OK) return 0;
-  const uint32_t n = c->last.nSm ? c->last.n_dirty : 0;
+  const int p = c->last_parity;
+  const uint32_t n = (c->T > 0 && c->last.nSm) ? c->ndirty[p] : 0;
   for (uint32_t i = 0; i < n && i < cap; ++i)
-    if (blocks) blocks[i] = c->dirty_map[2 * i] * c->cfg.world_size + c->cfg.rank;
+    if (blocks) blocks[i] = c->dirty_map[p][2 * i] * c->cfg.world_size + c->cfg.rank;
   return n;
 }
 

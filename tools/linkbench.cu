@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <cstdint>
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
@@ -115,5 +117,60 @@ int main() {
   at.flags = 0;
   one("batch(noflag) h2d 370", b_h2d);
   two("batch(noflag) h2d || d2h", b_h2d, b_d2h);
+
+  // (1) the same batches while an HBM-saturating kernel runs on a third stream
+  const size_t hb = (size_t)8 << 30;
+  char *x, *y;
+  CK(cudaMalloc(&x, hb));
+  CK(cudaMalloc(&y, hb));
+  auto hbm = [&](cudaStream_t s) { for (int r = 0; r < 6; ++r) zc_copy<<<148 * 4, 512, 0, s>>>((float4*)y, (const float4*)x, hb / 16); };
+  {
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e[0], s3);
+    hbm(s3);
+    cudaEventRecord(e[1], s3);
+    CK(cudaDeviceSynchronize());
+    printf("%-34s %7.1f GB/s (r+w)\n", "HBM copy kernel alone", 6 * 2.0 * hb / (ms_between(e[0], e[1]) * 1e6));
+    for (int rep = 0; rep < 2; ++rep) {
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(e[0], s3);
+      cudaStreamWaitEvent(s1, e[0], 0);
+      cudaStreamWaitEvent(s2, e[0], 0);
+      hbm(s3);
+      b_h2d(s1);
+      b_d2h(s2);
+      cudaEventRecord(e[1], s1);
+      cudaEventRecord(e[2], s2);
+      cudaEventRecord(e[3], s3);
+      CK(cudaDeviceSynchronize());
+      if (rep) printf("%-34s h2d %6.2f d2h %6.2f GB/s, HBM kernel %.2f ms\n", "batch || batch || HBM kernel",
+                      bytes / (ms_between(e[0], e[1]) * 1e6), bytes / (ms_between(e[0], e[2]) * 1e6), ms_between(e[0], e[3]));
+    }
+  }
+  CK(cudaFree(x));
+  CK(cudaFree(y));
+  // (2) records scattered over a large pinned host region (host-tier-like)
+  const size_t big = (size_t)64 << 30;
+  char* hbig;
+  if (cudaHostAlloc((void**)&hbig, big, cudaHostAllocDefault) == cudaSuccess) {
+    for (size_t i = 0; i < big; i += 4096) hbig[i] = 0;
+    const size_t nrec = big / rec;
+    std::vector<void*> bs(n), bd(n);
+    uint64_t st = 88172645463325252ull;
+    for (int i = 0; i < n; ++i) {
+      st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+      char* r = hbig + (st % nrec) * rec;
+      bs[i] = r;
+      bd[i] = r;
+    }
+    auto s_h2d = [&](cudaStream_t s) { CK(cudaMemcpyBatchAsync(hd.data(), bs.data(), sz.data(), n, &at, &aidx, 1, &fail, s)); };
+    auto s_d2h = [&](cudaStream_t s) { CK(cudaMemcpyBatchAsync(bd.data(), ds.data(), sz.data(), n, &at, &aidx, 1, &fail, s)); };
+    one("scattered-64GB batch h2d", s_h2d);
+    one("scattered-64GB batch d2h", s_d2h);
+    two("scattered-64GB batch h2d || d2h", s_h2d, s_d2h);
+    cudaFreeHost(hbig);
+  } else {
+    printf("64 GB pinned alloc failed\n");
+  }
   return 0;
 }
