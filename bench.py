@@ -251,6 +251,7 @@ def main():
     cfg = T.make_config(sc.N, sc.B, cap, moments=moments, world_size=ws, rank=rank,
                         device=local)
     stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
     table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream)
     setup_s = time.perf_counter() - t_setup
     # synthetic gradients for every slot, written once (renderer out of scope)
@@ -268,8 +269,22 @@ def main():
     total = args.warmup + args.steps
     planes = [tr.batch_planes(args.start + i, J) for i in range(total + args.steps)]
 
+    from paper_2605_20150_b200 import shard
+
+    class _CudaView:  # zero-copy torch view of a library-owned device list
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4",
+                                             "data": (ptr or 0, False), "version": 3}
+
     def step(i):
-        table.activate(planes[i])
+        act = table.activate(planes[i])
+        if ws > 1:  # C1 active-set exchange + C2 count reduction (NCCL over NVLink)
+            n = act.n_active_blocks
+            A = torch.as_tensor(_CudaView(act.d_active_blocks, n), device=dev) if n else \
+                torch.empty(0, dtype=torch.int32, device=dev)
+            shard.exchange_active(A, cap)
+            shard.reduce_counts(torch.tensor([act.n_visible, act.n_resident, act.n_stage_in,
+                                              act.n_evict, n], dtype=torch.int64, device=dev))
         table.step_adam(lr)
 
     for i in range(args.warmup):

@@ -77,6 +77,9 @@ def lib():
         L.or_num_local_blocks.argtypes = [vp]
         L.or_step_count.restype = C.c_uint32
         L.or_step_count.argtypes = [vp, C.c_uint64]
+        L.or_fine_filter.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint32)]
+        L.or_exp_det.restype = C.c_float
+        L.or_exp_det.argtypes = [C.c_float]
         _lib = L
     return _lib
 
@@ -209,6 +212,23 @@ class Oracle:
 
     def step_count(self, k) -> int:
         return int(lib().or_step_count(self.h, k))
+
+    def fine_filter(self, k) -> np.ndarray:
+        """I_t bits of block k (Level-2 filter, NEXT f1)."""
+        w = np.zeros((self.B + 31) // 32, np.uint32)
+        rc = lib().or_fine_filter(self.h, k, w.ctypes.data_as(C.POINTER(C.c_uint32)))
+        if rc != OK:
+            raise OracleError(rc, "or_fine_filter")
+        return w
+
+    @property
+    def fine_filter_mask(self):
+        """(C fn, user) mask callback: step_adam with I_t from the fine filter."""
+        return C.cast(lib().or_fine_filter_cb, C.c_void_p).value, self.h.value
+
+
+def exp_det(x: float) -> float:
+    return float(lib().or_exp_det(x))
 
     @property
     def num_local_blocks(self) -> int:

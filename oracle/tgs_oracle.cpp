@@ -45,6 +45,7 @@ struct Ctx {
   std::unordered_map<int32_t, std::vector<float>> slot_data;  // theta|m|v
 
   // sets, as sorted vectors of local ids
+  std::vector<float> planes;              // camera batch of the last activate (J x 6 x 4)
   std::vector<uint32_t> R;                // R_t
   std::vector<uint32_t> A_prev;           // R_t n K_t
   std::vector<std::vector<uint32_t>> percam;
@@ -85,6 +86,49 @@ bool sphere_visible(const float* b, const float* pl /* 6x4 */) {
     if (d < -b[3]) return false;
   }
   return true;
+}
+
+// R24: deterministic exp for the Level-2 extent, written out so that any
+// IEEE machine with a correctly rounded fma gives the same bits: k = rint(x
+// log2 e) by the 1.5*2^23 trick, Cody-Waite reduction r = x - k ln2 (two fma
+// steps), degree-7 Taylor polynomial in Horner form (fma), exact scaling 2^k.
+// Valid for x in [-80, 80] (the generator's log-scales are in [-12, 5]).
+float exp_det(float x) {
+  if (x > 80.0f) x = 80.0f;
+  if (x < -80.0f) x = -80.0f;
+  const float t = std::fmaf(x, 1.44269504088896341f, 12582912.0f);
+  const float kf = t - 12582912.0f;
+  float r = std::fmaf(kf, -0.693145751953125f, x);
+  r = std::fmaf(kf, -1.428606765330187045e-06f, r);
+  float p = 1.98412698412698413e-04f;                 // 1/5040
+  p = std::fmaf(p, r, 1.38888888888888889e-03f);      // 1/720
+  p = std::fmaf(p, r, 8.33333333333333333e-03f);      // 1/120
+  p = std::fmaf(p, r, 4.16666666666666667e-02f);      // 1/24
+  p = std::fmaf(p, r, 1.66666666666666667e-01f);      // 1/6
+  p = std::fmaf(p, r, 0.5f);
+  p = std::fmaf(p, r, 1.0f);
+  p = std::fmaf(p, r, 1.0f);
+  const int k = (int)kf;
+  uint32_t bits = (uint32_t)(k + 127) << 23;
+  float two_k;
+  std::memcpy(&two_k, &bits, 4);
+  return p * two_k;
+}
+
+// Level-2 test of one Gaussian: the
+// sphere (mu_i, 3 * exp(max log-scale)) against each camera of the batch with
+// the Level-1 rule (cull iff d < -r on some plane, R2), visible if any camera
+// keeps it.
+bool gaussian_visible(const float* row, const std::vector<float>& planes) {
+  float s = row[52];
+  if (row[53] > s) s = row[53];
+  if (row[54] > s) s = row[54];
+  const float ext = 3.0f * exp_det(s);
+  const float b[4] = {row[0], row[1], row[2], ext};
+  const size_t J = planes.size() / 24;
+  for (size_t j = 0; j < J; ++j)
+    if (sphere_visible(b, planes.data() + 24 * j)) return true;
+  return false;
 }
 
 std::vector<uint32_t> set_union(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
@@ -178,6 +222,7 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
     if (!std::isfinite(planes[i])) return OR_EINVAL;
 
   // ---- Alg. 1 l.1 / Eq. Kt_def: K^{(j)} and K = U_j K^{(j)}
+  c.planes.assign(planes, planes + (size_t)J * 24);
   c.percam.assign(J, {});
   for (uint32_t j = 0; j < J; ++j)
     for (uint32_t l = 0; l < c.Kloc; ++l)
@@ -472,6 +517,27 @@ void or_get_slot_map(or_ctx* o, int64_t* out) {
 void or_get_stats(or_ctx* o, or_stats* s) { *s = o->c.st; }
 uint64_t or_nonfinite_index(or_ctx* o) { return o->c.nonfinite; }
 uint32_t or_num_local_blocks(or_ctx* o) { return o->c.Kloc; }
+
+float or_exp_det(float x) { return exp_det(x); }
+
+int or_fine_filter(or_ctx* o, uint64_t kg, uint32_t* words) {
+  Ctx& c = o->c;
+  if (kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;
+  const uint64_t l = kg / c.cfg.world_size;
+  const uint32_t nw = (c.cfg.block_size + 31) / 32;
+  std::fill(words, words + nw, 0u);
+  if (l >= c.Kloc || !contains(c.A, (uint32_t)l)) return OR_OK;  // I_t lies inside R n K
+  if (!c.is_tracked((uint32_t)l)) return OR_EINVAL;
+  const float* th = c.slot_data[c.slot_of[l]].data();
+  const uint32_t nrows = c.rows((uint32_t)l);
+  for (uint32_t r = 0; r < nrows; ++r)
+    if (gaussian_visible(th + (size_t)r * D, c.planes)) words[r / 32] |= 1u << (r % 32);
+  return OR_OK;
+}
+
+void or_fine_filter_cb(void* ctx, uint64_t kg, uint64_t /*t*/, uint32_t* words) {
+  or_fine_filter((or_ctx*)ctx, kg, words);
+}
 
 uint32_t or_step_count(or_ctx* o, uint64_t kg) {
   Ctx& c = o->c;

@@ -80,6 +80,15 @@ int or_read_block(or_ctx* c, uint64_t k_global, float* theta, float* m, float* v
 uint32_t or_num_local_blocks(or_ctx* c);
 uint32_t or_step_count(or_ctx* c, uint64_t k_global);
 
+/* Level-2 fine filter (NEXT f1): I_t bits of a block of
+ * A = R n K from its current slot theta and the last camera batch (R24).
+ * words: ceil(B/32); blocks outside A give all-zero words. */
+int or_fine_filter(or_ctx* c, uint64_t k_global, uint32_t* words);
+/* the same as an or_mask_fn, user = the or_ctx itself */
+void or_fine_filter_cb(void* ctx, uint64_t k_global, uint64_t t, uint32_t* words);
+/* the deterministic exp of R24 (exported for its pins) */
+float or_exp_det(float x);
+
 #ifdef __cplusplus
 }
 #endif

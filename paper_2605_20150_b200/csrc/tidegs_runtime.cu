@@ -73,8 +73,8 @@ struct tgs_ctx {
   uint32_t* ndirty = nullptr;     // host view [2]
   float* planes_pinned = nullptr; // [kMaxCams*24] staging of the kernel parameter
   // streams / events (ev_*[p]: last record by an activate of parity p)
-  cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_plan = nullptr;
+  cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr, fix = nullptr;
+  cudaEvent_t ev_plan = nullptr, ev_gstart = nullptr, ev_gdone = nullptr;
   cudaEvent_t ev_ready[2] = {}, ev_evict[2] = {}, ev_d2h[2] = {}, ev_lists[2] = {};
   bool rec_ready[2] = {}, rec_evict[2] = {}, rec_lists[2] = {};
   int32_t d2h_job[2] = {-1, -1};   // activate index of the last write-back job of parity p
@@ -485,6 +485,7 @@ tgs_status sync_all(tgs_ctx* c) {
   CK(cudaStreamSynchronize(c->h2d));
   CK(cudaStreamSynchronize(c->compute));
   CK(cudaStreamSynchronize(c->d2h));
+  CK(cudaStreamSynchronize(c->fix));
   prof_collect(c);
   return TGS_OK;
 }
@@ -511,13 +512,14 @@ void destroy_impl(tgs_ctx* c) {
   for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
                   (void*)c->ndirty, (void*)c->planes_pinned, (void*)c->lut_pinned})
     if (h) cudaFreeHost(h);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_ready[0], c->ev_ready[1], c->ev_evict[0],
+  for (cudaEvent_t e : {c->ev_plan, c->ev_gstart, c->ev_gdone, c->ev_ready[0], c->ev_ready[1],
+                        c->ev_evict[0],
                         c->ev_evict[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_lists[0],
                         c->ev_lists[1], c->trace_base})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  for (cudaStream_t s : {c->plan, c->h2d, c->d2h}) if (s) cudaStreamDestroy(s);
+  for (cudaStream_t s : {c->plan, c->h2d, c->d2h, c->fix}) if (s) cudaStreamDestroy(s);
   cudaGetLastError();
   delete c;
 }
@@ -609,9 +611,11 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   // the plan is latency-critical (the host waits for it): highest priority
   if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
+      cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->fix, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
-  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready[0], &c->ev_ready[1], &c->ev_evict[0],
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_gstart, &c->ev_gdone, &c->ev_ready[0],
+                         &c->ev_ready[1], &c->ev_evict[0],
                          &c->ev_evict[1], &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_lists[0],
                          &c->ev_lists[1]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
@@ -821,7 +825,24 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
   }
   if (c->io_failed) return check(c);
+  // the fix-up stream zeroes moments (cold restart) while the batch streams in
+  // and patches re-admissions after it; the next gather does not wait for it
+  cudaStream_t ready_on = c->h2d;
   if (h.nSp) {
+    const bool fixups = d.cold || c->prev_packed;
+    if (fixups) {
+      CK(cudaEventRecord(c->ev_gstart, c->h2d));
+      CK(cudaStreamWaitEvent(c->fix, c->ev_gstart, 0));
+      CK(cudaStreamWaitEvent(c->fix, c->ev_plan, 0));
+      ready_on = c->fix;
+    }
+    if (d.cold) {
+      Timer tc;
+      prof_begin(c, c->fix, tc);
+      CK(launch_cold_init(d, h.nSp, p, c->fix));
+      prof_end(c, c->fix, tc, 6);
+      c->tm.kernel_launches++;
+    }
     Timer th;
     prof_begin(c, c->h2d, th);
     CopyBatch b;
@@ -830,22 +851,19 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     if (st != TGS_OK) return st;
     prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
     if (c->prev_packed) {  // S+ blocks the previous batch packed: newest copy is in its ring
+      CK(cudaEventRecord(c->ev_gdone, c->h2d));
+      CK(cudaStreamWaitEvent(c->fix, c->ev_gdone, 0));
       Timer tr;
-      prof_begin(c, c->h2d, tr);
-      CK(launch_readmit(d, h.nSp, p, T, c->h2d));
-      prof_end(c, c->h2d, tr, 7);
+      prof_begin(c, c->fix, tr);
+      CK(launch_readmit(d, h.nSp, p, T, c->fix));
+      prof_end(c, c->fix, tr, 7);
       c->tm.kernel_launches++;
-    }
-    if (d.cold) {
-      Timer tc;
-      CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
-      prof_begin(c, c->h2d, tc);
-      CK(launch_cold_init(d, h.nSp, p, c->h2d));
-      prof_end(c, c->h2d, tc, 6);
-      c->tm.kernel_launches++;
+    } else if (fixups) {
+      CK(cudaEventRecord(c->ev_gdone, c->h2d));
+      CK(cudaStreamWaitEvent(c->fix, c->ev_gdone, 0));
     }
   }
-  CK(cudaEventRecord(c->ev_ready[p], c->h2d));
+  CK(cudaEventRecord(c->ev_ready[p], ready_on));
   c->rec_ready[p] = true;
 
   if (!reuse_now && h.nSm) {

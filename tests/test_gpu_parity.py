@@ -51,6 +51,42 @@ def test_tiny_trajectory_parity(moments, lam, quota):
     pr.close()
 
 
+@pytest.mark.parametrize("staging", [1, 64])
+@pytest.mark.parametrize("moments", [O.PERSIST, O.COLD_RESTART])
+def test_writeback_paths(staging, moments):
+    """Write-back through the staging ring (k_pack, I/O thread, re-admission
+    from the ring by k_readmit) and straight from the slots (ring too small):
+    same lists, bytes and contents as the oracle."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, moments=moments, staging_blocks=staging)
+    worst = _drive(pr, tr, cfg.J, 48, check_blocks_every=5)
+    pr.gpu.flush()
+    pr.orc.flush()
+    pr.compare_stats()
+    worst = max(worst, pr.compare_blocks(range(sc.K)))
+    assert worst == 0
+    pr.close()
+
+
+def test_readmission_right_after_writeback():
+    """Alternate two disjoint views with C = one view: every block is evicted
+    dirty and re-admitted the next batch, so the gather must take the record
+    from the staging ring (its host write-back may still be in flight)."""
+    cfg, sc, tr = tiny()
+    a, b = tr.batch_planes(0, 1), tr.batch_planes(8, 1)
+    pr = _pair(sc, capacity=14, staging_blocks=64, lam=1.0, quota=(0, 1))
+    for t in range(16):
+        act = pr.activate(a if t % 2 == 0 else b)
+        pr.t = t
+        pr.compare_plan(1)
+        pr.step(act, t)
+    pr.compare_stats()
+    st = pr.gpu.stats()
+    assert st["readmissions"] > 0 and st["n_evict_dirty"] > 0
+    assert pr.compare_blocks(range(sc.K)) == 0
+    pr.close()
+
+
 @pytest.mark.parametrize("J", [1, 2, 4, 7])
 def test_tiny_batch_sizes_and_quota(J):
     """Several cameras per batch; capacity small enough that the camera quota binds."""
