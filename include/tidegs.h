@@ -127,7 +127,7 @@ typedef struct {
 typedef struct {
   /* device time of the library's kernels / copies, CUDA events on the stream
    * each is launched on; accumulated while profiling is enabled */
-  double adam_ms, adam_prologue_ms, plan_ms, h2d_ms, d2h_ms, evict_ms;
+  double adam_ms, adam_prologue_ms, plan_ms, h2d_ms, d2h_ms, evict_ms, fine_ms;
   uint64_t adam_launches, plan_launches, h2d_batches, d2h_batches;
   uint64_t adam_rows;        /* active rows processed by the timed Adam launches */
   uint64_t adam_elems_quads; /* 4-row quads visited by the timed Adam launches   */
@@ -174,6 +174,15 @@ tgs_status tgs_activate(tgs_ctx* ctx, const tgs_camera* cams, uint32_t n_cams,
  * tgs_activate.  Non-finite gradients: the row is skipped and the lowest
  * (gid*59 + attr) is reported by tgs_nonfinite_index (R20). */
 tgs_status tgs_step_adam(tgs_ctx* ctx, const tgs_adam* hp, const uint32_t* d_row_mask);
+
+/* Level-2 fine filter (NEXT f1): writes
+ * the I_t row mask of every slot of R n K of the last activate into
+ * d_row_mask (device [P][ceil(B/32)] u32, the layout tgs_step_adam reads):
+ * bit r = row r's sphere (mu, 3*exp(max log-scale), R24 deterministic exp) is
+ * kept by the Level-1 rule for at least one camera of the batch.  Runs on the
+ * compute stream after the gather; call between tgs_activate and
+ * tgs_step_adam (ESTATE otherwise), then pass the same mask to step_adam. */
+tgs_status tgs_fine_filter(tgs_ctx* ctx, uint32_t* d_row_mask);
 
 /* Consistency barrier: write every dirty resident record
  * back to the host tier, wait for all work, clear dirty bits.  Blocks stay

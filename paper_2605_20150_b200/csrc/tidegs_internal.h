@@ -75,6 +75,7 @@ struct Dev {
   uint32_t* wb_idx;      // [Kloc] its staging-ring index then
   float* staging[2];     // [S_max][n_arr][B][59] write-back staging ring (parity)
   uint32_t S_max;        // staging capacity in records
+  float4* last_planes[2];  // [kMaxCams*6] camera batch of the activate of that parity
   // selection
   uint16_t* rank_lut;    // [2][max_age+2]
   uint32_t n_buckets;    // 2 * (number of distinct ranks)
@@ -115,6 +116,8 @@ cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const ui
                                  cudaStream_t s);
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s);
+cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
+                        cudaStream_t s);
 int adam_grid(int device);
 
 }  // namespace tgs

@@ -172,7 +172,10 @@ __device__ void select_top(const Dev& d, uint32_t n, uint32_t nw, int32_t T, uin
 __global__ void __launch_bounds__(256) k_cull(Dev d, const __grid_constant__ PlanesArg planes,
                                               uint32_t J, int32_t T, int parity) {
   __shared__ float4 pl[kMaxCams * 6];
-  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = planes.p[i];
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) {
+    pl[i] = planes.p[i];
+    if (blockIdx.x == 0) d.last_planes[parity][i] = planes.p[i];  // for the Level-2 filter
+  }
   __syncthreads();
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t w = l >> 5, lane = l & 31;
@@ -560,6 +563,65 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
   }
 }
 
+// ------------------------------------------- f1 Level-2 fine filter -> I_t
+// R24 deterministic exp: k = rint(x log2 e) by the 1.5*2^23 trick, two-step
+// Cody-Waite reduction, degree-7 Taylor polynomial by fma Horner, exact 2^k.
+__device__ __forceinline__ float exp_det(float x) {
+  if (x > 80.0f) x = 80.0f;
+  if (x < -80.0f) x = -80.0f;
+  const float t = __fmaf_rn(x, 1.44269504088896341f, 12582912.0f);
+  const float kf = __fsub_rn(t, 12582912.0f);
+  float r = __fmaf_rn(kf, -0.693145751953125f, x);
+  r = __fmaf_rn(kf, -1.428606765330187045e-06f, r);
+  float p = 1.98412698412698413e-04f;
+  p = __fmaf_rn(p, r, 1.38888888888888889e-03f);
+  p = __fmaf_rn(p, r, 8.33333333333333333e-03f);
+  p = __fmaf_rn(p, r, 4.16666666666666667e-02f);
+  p = __fmaf_rn(p, r, 1.66666666666666667e-01f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  const int k = (int)kf;
+  return __fmul_rn(p, __int_as_float((k + 127) << 23));
+}
+
+// grid (ceil(B/256), nA): one thread per row of an A block.  The row's
+// extent sphere (mu, 3 exp(max log-scale)) against every camera of the batch
+// with the Level-1 rule; a ballot per 32
+// rows writes the I_t mask word of the slot.
+__global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t J, int parity,
+                                              uint32_t* __restrict__ mask) {
+  __shared__ float4 pl[kMaxCams * 6];
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = d.last_planes[parity][i];
+  __syncthreads();
+  const uint32_t i = blockIdx.y;
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nw = (d.B + 31) / 32;
+  if (r >= nw * 32) return;  // whole warps only
+  const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+  bool vis = false;
+  if (r < block_rows(d, l)) {
+    const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
+    const float x = row[0], y = row[1], z = row[2];
+    float sc = row[52];
+    if (row[53] > sc) sc = row[53];
+    if (row[54] > sc) sc = row[54];
+    const float nr = -__fmul_rn(3.0f, exp_det(sc));
+    for (uint32_t j = 0; j < J && !vis; ++j) {
+      bool in = true;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const float4 n = pl[j * 6 + p];
+        const float dist = __fmaf_rn(n.z, z, __fmaf_rn(n.y, y, __fmaf_rn(n.x, x, n.w)));
+        if (dist < nr) in = false;
+      }
+      vis = in;
+    }
+  }
+  const uint32_t bits = __ballot_sync(kFull, vis);
+  if ((threadIdx.x & 31) == 0) mask[(size_t)s * nw + (r >> 5)] = bits;
+}
+
 // ------------------------------------------------------- a5 masked Adam
 // A warp owns a contiguous range of 4-row quads (4 rows = 944 B = 59 float4
 // per array); lane f and f+32 (< 59) load float4 #f of theta, m, v, g (128-bit,
@@ -808,6 +870,14 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
   const uint64_t per_cta = (uint64_t)(kAdamNT / 32) * kAdamQPW;
   const unsigned grid = (unsigned)((quads + per_cta - 1) / per_cta);
   k_adam<<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
+                        cudaStream_t s) {
+  if (nA == 0) return cudaSuccess;
+  dim3 grid(((d.B + 31) / 32 * 32 + 255) / 256, nA);
+  k_fine<<<grid, 256, 0, s>>>(d, J, parity, mask);
   return cudaGetLastError();
 }
 

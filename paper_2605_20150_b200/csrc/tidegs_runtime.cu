@@ -105,6 +105,7 @@ struct tgs_ctx {
   bool can_step = false;
   bool poisoned = false;
   PlanHdr last{};                 // header of the last activate
+  uint32_t last_J = 0;            // batch size of the last activate
   uint64_t n_steps = 0;
   uint64_t host_flush_bytes = 0, host_flush_blocks = 0;
   std::string err;
@@ -187,7 +188,7 @@ void prof_end(tgs_ctx* c, cudaStream_t s, Timer& t, int kind, uint64_t bytes = 0
 }
 void prof_collect(tgs_ctx* c) {
   std::lock_guard<std::mutex> g(c->prof_mu);
-  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "cold_init", "readmit"};
+  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "cold_init", "readmit", "fine"};
   for (auto& p : c->pending) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.a, p.b) != cudaSuccess) ms = 0.f;
@@ -205,6 +206,7 @@ void prof_collect(tgs_ctx* c) {
       case 4: c->tm.d2h_ms += ms; c->tm.d2h_batches++; c->tm.d2h_bytes += p.bytes; break;
       case 5: c->tm.evict_ms += ms; break;
       case 6: case 7: break;
+      case 8: c->tm.fine_ms += ms; break;
     }
     c->ev_pool.push_back(p.a);
     c->ev_pool.push_back(p.b);
@@ -684,6 +686,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
   d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
+  d.last_planes[0] = dalloc_t<float4>(c, kMaxCams * 6, ok);
+  d.last_planes[1] = dalloc_t<float4>(c, kMaxCams * 6, ok);
   d.ndirty_dev = dalloc_t<uint32_t>(c, 2, ok);
   d.wb_tag = dalloc_t<int32_t>(c, Kl, ok);
   d.wb_idx = dalloc_t<uint32_t>(c, Kl, ok);
@@ -777,6 +781,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
   const PlanHdr h = *c->hdr;
   c->last = h;
+  c->last_J = J;
 
   // ---- a4 write-back of dirty S-, enqueued on the compute stream after
   //      Adam(t-1) (the dirty decision).  Normal path: k_evict compacts the
@@ -930,6 +935,24 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   prof_end(c, c->compute, t2, 0);
   c->tm.kernel_launches += 2;
   CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
+  return TGS_OK;
+}
+
+tgs_status tgs_fine_filter(tgs_ctx* c, uint32_t* d_row_mask) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!c->can_step) return TGS_ESTATE;
+  if (!d_row_mask) return TGS_EINVAL;
+  const int p = c->last_parity;
+  // reads theta of every A slot: after the plan and the gather of this batch
+  CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
+  CK(cudaStreamWaitEvent(c->compute, c->ev_ready[p], 0));
+  if (c->last.nA == 0 || c->d.Kloc == 0) return TGS_OK;
+  Timer tf;
+  prof_begin(c, c->compute, tf);
+  CK(launch_fine(c->d, c->last.nA, c->last_J, p, d_row_mask, c->compute));
+  prof_end(c, c->compute, tf, 8);
+  c->tm.kernel_launches++;
   return TGS_OK;
 }
 

@@ -24,6 +24,7 @@ LISTS = {"K": 0, "R": 1, "S+": 2, "S-": 3, "Omega": 4, "A": 5}
 
 # every entry point include/tidegs.h declares (tests check the exports)
 SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tgs_flush",
+           "tgs_fine_filter",
            "tgs_get_stats", "tgs_get_timing", "tgs_set_profiling", "tgs_get_list",
            "tgs_get_percam", "tgs_get_evicted_dirty", "tgs_get_slot_map",
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
@@ -79,7 +80,7 @@ class Stats(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = ([(n, C.c_double) for n in ("adam_ms", "adam_prologue_ms", "plan_ms", "h2d_ms",
-                                             "d2h_ms", "evict_ms")] +
+                                             "d2h_ms", "evict_ms", "fine_ms")] +
                 [(n, C.c_uint64) for n in ("adam_launches", "plan_launches", "h2d_batches",
                                            "d2h_batches", "adam_rows", "adam_elems_quads",
                                            "h2d_bytes", "d2h_bytes", "kernel_launches",
@@ -113,6 +114,7 @@ def lib():
         L.tgs_activate.argtypes = [vp, C.c_void_p, u32, C.POINTER(Activation)]
         L.tgs_step_adam.argtypes = [vp, C.POINTER(Adam), vp]
         L.tgs_flush.argtypes = [vp]
+        L.tgs_fine_filter.argtypes = [vp, vp]
         L.tgs_get_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.tgs_set_profiling.argtypes = [vp, C.c_int]
@@ -251,6 +253,10 @@ class Table:
         if check:
             self._err(rc, "tgs_step_adam")
         return rc
+
+    def fine_filter(self, mask_ptr):
+        """Level-2 filter: I_t row mask of the last activate's A slots -> mask_ptr."""
+        self._err(lib().tgs_fine_filter(self.h, mask_ptr), "tgs_fine_filter")
 
     def flush(self):
         self._err(lib().tgs_flush(self.h), "tgs_flush")

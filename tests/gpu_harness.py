@@ -82,6 +82,31 @@ class Pair:
         m = (_cfn("wl_mask_cb"), C.addressof(self.msyn)) if self.msyn is not None else None
         return self.orc.step_adam(self.lr, beta1, beta2, eps, grad=g, mask=m)
 
+    def step_fine(self, act, t):
+        """Level-2 filter (f1) -> I_t mask on both sides, compared bit-exact per
+        A block, then masked Adam with it."""
+        torch = self.torch
+        if self.d_mask is None:
+            self.d_mask = torch.zeros((self.gpu.P, (self.B + 31) // 32), dtype=torch.int32,
+                                      device="cuda")
+        self.gpu.fine_filter(self.d_mask.data_ptr())
+        torch.cuda.synchronize()
+        host = self.d_mask.cpu().numpy().view(np.uint32)
+        blocks, slots = self.orc.list("A", with_slots=True)
+        n_rows = 0
+        for k, s in zip(blocks.tolist(), slots.tolist()):
+            ref = self.orc.fine_filter(k)
+            np.testing.assert_array_equal(host[s], ref, err_msg=f"I_t of block {k}, t={t}")
+            n_rows += int(np.unpackbits(ref.view(np.uint8)).sum())
+        self.grads_gpu_only(act, t)
+        self.gpu.step_adam(self.lr, mask_ptr=self.d_mask.data_ptr())
+        g = (_cfn("wl_grad_cb"), C.addressof(self.gsyn))
+        rc = self.orc.step_adam(self.lr, grad=g, mask=self.orc.fine_filter_mask)
+        return rc, n_rows
+
+    def grads_gpu_only(self, act, t):
+        W.synth_grads_cuda(act, self.B, self.N, GRAD_SEED, t, self.stream)
+
     # ---- comparisons
     def compare_plan(self, J):
         for which in ("K", "R", "S+", "S-", "Omega", "A"):

@@ -233,3 +233,23 @@ def test_full_size_index_parity_and_sampled_rows(name):
     worst = pr.compare_blocks(tracked)
     assert worst == 0
     pr.close()
+
+
+@pytest.mark.parametrize("J", [2, 5])
+def test_fine_filter_parity(J):
+    """NEXT f1: the Level-2 I_t mask is bit-exact with the oracle on every A
+    block of every batch, and masked Adam driven by it matches (0 ULP)."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity)
+    total = 0
+    for t in range(16):
+        act = pr.activate(tr.batch_planes(t, J))
+        pr.t = t
+        pr.compare_plan(J)
+        rc, n = pr.step_fine(act, t)
+        assert rc == O.OK
+        total += n
+    pr.compare_stats()
+    assert pr.gpu.stats()["n_active_rows"] == total > 0
+    assert pr.compare_blocks(range(sc.K)) == 0
+    pr.close()
