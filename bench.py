@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--fine-filter", action="store_true",
+                    help="NEXT f1: Level-2 filter -> I_t mask -> masked Adam in every step")
     return ap.parse_args()
 
 
@@ -197,6 +199,7 @@ def _config_dict(args, wl, ws):
             "n_gaussians": wl.n_gaussians, "block_size": wl.block_size, "J": wl.J,
             "capacity_blocks_per_gpu": -(-wl.capacity // ws), "moments": args.moments,
             "policy": "tide", "world_size": ws,
+            "I_t": "Level-2 fine filter (f1)" if getattr(args, "fine_filter", False) else "all rows of R n K (mask NULL)",
             "l2": "inputs larger than L2 (Adam touches GBs per step)",
             "grads": "synthetic counter-hash gradients resident in the grad pool (renderer out of scope)",
             "seeds": W.SEEDS}
@@ -276,8 +279,13 @@ def main():
             self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4",
                                              "data": (ptr or 0, False), "version": 3}
 
+    fmask = torch.zeros((table.P, (sc.B + 31) // 32), dtype=torch.int32, device=dev) \
+        if args.fine_filter else None
+
     def step(i):
         act = table.activate(planes[i])
+        if fmask is not None:
+            table.fine_filter(fmask.data_ptr())
         if ws > 1:  # C1 active-set exchange + C2 count reduction (NCCL over NVLink)
             n = act.n_active_blocks
             A = torch.as_tensor(_CudaView(act.d_active_blocks, n), device=dev) if n else \
@@ -285,7 +293,7 @@ def main():
             shard.exchange_active(A, cap)
             shard.reduce_counts(torch.tensor([act.n_visible, act.n_resident, act.n_stage_in,
                                               act.n_evict, n], dtype=torch.int64, device=dev))
-        table.step_adam(lr)
+        table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
 
     for i in range(args.warmup):
         step(i)
@@ -348,8 +356,15 @@ def main():
     adam_rows = rows if ws == 1 else rows / ws
     adam_ms = tm["adam_ms"] / max(1, tm["adam_launches"])
     achieved = (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM / (adam_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_adam_r01.json")
+    if os.path.exists(tp):  # ncu --set full capture of a k_adam launch of this workload
+        tj = json.load(open(tp))
+        traffic = {"dram_bytes_per_launch": tj["traffic_bytes"],
+                   "algorithmic_bytes_same_launch": tj["algorithmic_bytes"],
+                   "ratio": tj["traffic_over_algorithmic"], "source": tj["source"]}
     roof = {"bound": "hbm", "kernel": "k_adam", "achieved": achieved, "peak": hbm_peak,
-            "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+            "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
             "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM,
             "avg_launch_ms": adam_ms}
@@ -382,6 +397,7 @@ def main():
                            "h2d_GB_per_step": h2d / args.steps / 1e9,
                            "d2h_GB_per_step": d2h / args.steps / 1e9,
                            "plan_ms_per_step": tm["plan_ms"] / args.steps,
+                           "fine_ms_per_step": tm["fine_ms"] / args.steps,
                            "adam_prologue_ms_per_step": tm["adam_prologue_ms"] / args.steps,
                            "h2d_ms_per_step": tm["h2d_ms"] / args.steps,
                            "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
