@@ -24,7 +24,7 @@ class Config(C.Structure):
                 ("max_cameras", C.c_uint32), ("max_age", C.c_uint32),
                 ("quota_num", C.c_uint32), ("quota_den", C.c_uint32), ("lambda_", C.c_double),
                 ("gamma", C.c_double), ("moments", C.c_int32), ("tide", C.c_int32),
-                ("world_size", C.c_int32), ("rank", C.c_int32)]
+                ("world_size", C.c_int32), ("rank", C.c_int32), ("refresh_bounds", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -78,6 +78,7 @@ def lib():
         L.or_step_count.restype = C.c_uint32
         L.or_step_count.argtypes = [vp, C.c_uint64]
         L.or_fine_filter.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint32)]
+        L.or_get_bound.argtypes = [vp, C.c_uint64, C.POINTER(C.c_float)]
         L.or_exp_det.restype = C.c_float
         L.or_exp_det.argtypes = [C.c_float]
         _lib = L
@@ -96,9 +97,10 @@ class OracleError(RuntimeError):
 
 def make_config(n_gaussians, block_size, capacity, *, pool_slots=0, max_cameras=256,
                 max_age=255, quota=(1, 2), lam=0.7, gamma=0.9, moments=PERSIST, tide=1,
-                world_size=1, rank=0) -> Config:
+                world_size=1, rank=0, refresh_bounds=0) -> Config:
     return Config(n_gaussians, DIM, block_size, capacity, pool_slots, max_cameras, max_age,
-                  quota[0], quota[1], lam, gamma, moments, tide, world_size, rank)
+                  quota[0], quota[1], lam, gamma, moments, tide, world_size, rank,
+                  refresh_bounds)
 
 
 class Oracle:
@@ -220,6 +222,13 @@ class Oracle:
         if rc != OK:
             raise OracleError(rc, "or_fine_filter")
         return w
+
+    def bound(self, k) -> np.ndarray:
+        out = np.empty(4, np.float32)
+        rc = lib().or_get_bound(self.h, k, _f(out))
+        if rc != OK:
+            raise OracleError(rc, "or_get_bound")
+        return out
 
     @property
     def fine_filter_mask(self):

@@ -131,6 +131,27 @@ bool gaussian_visible(const float* row, const std::vector<float>& planes) {
   return false;
 }
 
+uint32_t fbits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return u;
+}
+
+// R25 (NEXT f2, "we conservatively refresh each affected block
+// bound as centers move"): radius that holds Gaussian row i around the fixed
+// centre c_k: (|mu_i - c_k| + 3 exp(max log-scale_i)) inflated by 2^-19
+// relative so fp32 rounding cannot make it smaller than the real value.
+float refresh_radius(const float* row, const float* c) {
+  const float dx = row[0] - c[0], dy = row[1] - c[1], dz = row[2] - c[2];
+  const float d2 = std::fmaf(dz, dz, std::fmaf(dy, dy, dx * dx));
+  const float dist = std::sqrt(d2);
+  float s = row[52];
+  if (row[53] > s) s = row[53];
+  if (row[54] > s) s = row[54];
+  const float ext = 3.0f * exp_det(s);
+  return (dist + ext) * 1.0000019073486328f;
+}
+
 std::vector<uint32_t> set_union(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
   std::vector<uint32_t> o;
   std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
@@ -169,6 +190,7 @@ int or_create(const or_config* cfg, const float* bounds_global, or_fill_fn fill,
   if (g.quota_den == 0 || g.quota_num > g.quota_den) return OR_EINVAL;
   if (g.world_size < 1 || g.rank < 0 || g.rank >= g.world_size) return OR_EINVAL;
   if (g.moments != OR_PERSIST && g.moments != OR_COLD_RESTART) return OR_EINVAL;
+  if (g.refresh_bounds && !track_all) return OR_EINVAL;  // needs every block's rows
   uint32_t P = g.pool_slots ? g.pool_slots : 2u * g.capacity;
   if (P < g.capacity) return OR_EINVAL;
   or_ctx* o = new or_ctx();
@@ -450,6 +472,13 @@ int or_step_adam(or_ctx* o, const float* lr, float beta1, float beta2, float eps
         th[e] = th[e] - ss * upd;
       }
     }
+    if (g.refresh_bounds) {  // R25: grow r_k to hold every row after the update
+      float* bd = &c.bounds[4 * l];
+      for (uint32_t r = 0; r < nrows; ++r) {
+        const float rad = refresh_radius(th + (size_t)r * D, bd);
+        if (fbits(rad) > fbits(bd[3])) bd[3] = rad;  // max on the bit pattern (R25)
+      }
+    }
   }
   return c.nonfinite != std::numeric_limits<uint64_t>::max() ? OR_ENONFINITE : OR_OK;
 }
@@ -519,6 +548,15 @@ uint64_t or_nonfinite_index(or_ctx* o) { return o->c.nonfinite; }
 uint32_t or_num_local_blocks(or_ctx* o) { return o->c.Kloc; }
 
 float or_exp_det(float x) { return exp_det(x); }
+
+int or_get_bound(or_ctx* o, uint64_t kg, float* out4) {
+  Ctx& c = o->c;
+  if (kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;
+  const uint64_t l = kg / c.cfg.world_size;
+  if (l >= c.Kloc) return OR_EINVAL;
+  for (int i = 0; i < 4; ++i) out4[i] = c.bounds[4 * l + i];
+  return OR_OK;
+}
 
 int or_fine_filter(or_ctx* o, uint64_t kg, uint32_t* words) {
   Ctx& c = o->c;

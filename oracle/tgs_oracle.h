@@ -39,6 +39,7 @@ typedef struct {
   int32_t moments;       /* OR_PERSIST / OR_COLD_RESTART */
   int32_t tide;          /* 1 = differential, 0 = restage-all ablation */
   int32_t world_size, rank;
+  int32_t refresh_bounds; /* NEXT f2 (R25): grow r_k after each update; needs track_all */
 } or_config;
 
 typedef struct {
@@ -86,6 +87,8 @@ uint32_t or_step_count(or_ctx* c, uint64_t k_global);
 int or_fine_filter(or_ctx* c, uint64_t k_global, uint32_t* words);
 /* the same as an or_mask_fn, user = the or_ctx itself */
 void or_fine_filter_cb(void* ctx, uint64_t k_global, uint64_t t, uint32_t* words);
+/* current bound (cx, cy, cz, r) of a global block of this shard */
+int or_get_bound(or_ctx* c, uint64_t k_global, float* out4);
 /* the deterministic exp of R24 (exported for its pins) */
 float or_exp_det(float x);
 
