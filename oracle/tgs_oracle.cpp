@@ -46,6 +46,7 @@ struct Ctx {
 
   // sets, as sorted vectors of local ids
   std::vector<float> planes;              // camera batch of the last activate (J x 6 x 4)
+  std::vector<float> pend[2];             // R25: refreshed radii of the step of that parity
   std::vector<uint32_t> R;                // R_t
   std::vector<uint32_t> A_prev;           // R_t n K_t
   std::vector<std::vector<uint32_t>> percam;
@@ -244,6 +245,13 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
     if (!std::isfinite(planes[i])) return OR_EINVAL;
 
   // ---- Alg. 1 l.1 / Eq. Kt_def: K^{(j)} and K = U_j K^{(j)}
+  // R25: the refresh of the step two batches back enters the Level-1 test now
+  if (g.refresh_bounds) {
+    std::vector<float>& pd = c.pend[c.t & 1];
+    for (uint32_t l = 0; l < c.Kloc && !pd.empty(); ++l)
+      if (fbits(pd[l]) > fbits(c.bounds[4 * l + 3])) c.bounds[4 * l + 3] = pd[l];
+    pd.assign(pd.size(), 0.0f);
+  }
   c.planes.assign(planes, planes + (size_t)J * 24);
   c.percam.assign(J, {});
   for (uint32_t j = 0; j < J; ++j)
@@ -472,11 +480,13 @@ int or_step_adam(or_ctx* o, const float* lr, float beta1, float beta2, float eps
         th[e] = th[e] - ss * upd;
       }
     }
-    if (g.refresh_bounds) {  // R25: grow r_k to hold every row after the update
-      float* bd = &c.bounds[4 * l];
+    if (g.refresh_bounds) {  // R25: radius holding every row after the update
+      std::vector<float>& pd = c.pend[it & 1];
+      if (pd.empty()) pd.assign(c.Kloc, 0.0f);
+      const float* bd = &c.bounds[4 * l];
       for (uint32_t r = 0; r < nrows; ++r) {
         const float rad = refresh_radius(th + (size_t)r * D, bd);
-        if (fbits(rad) > fbits(bd[3])) bd[3] = rad;  // max on the bit pattern (R25)
+        if (fbits(rad) > fbits(pd[l])) pd[l] = rad;  // max on the bit pattern (R25)
       }
     }
   }

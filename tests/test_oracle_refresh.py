@@ -1,7 +1,7 @@
 """Pins for the oracle's conservative bound refresh (NEXT f2, PAPER.md:192-194,
-R25): after each update every Gaussian of the block lies inside the refreshed
-sphere (checked in double), radii only grow, untouched blocks keep their
-bounds, and the Level-1/Level-2 conservativeness chain survives training that
+R25): once a step's refresh has entered the Level-1 test (two batches later)
+every Gaussian of the block lies inside the refreshed sphere (checked in
+double), radii only grow, untouched blocks keep their bounds, and the Level-1/Level-2 conservativeness chain survives training that
 moves the centres."""
 import ctypes as C
 
@@ -32,6 +32,11 @@ def _train(refresh, iters=12, lr_xyz=0.3, mask_p=None):
     for t in range(iters):
         o.activate(tr.batch_planes(t, 2))
         o.step_adam(lr, grad=gfn, mask=mfn)
+        r_hist.append(np.array([o.bound(k)[3] for k in range(sc.K)]))
+    # R25: a step's refresh enters the Level-1 test two batches later; two empty
+    # batches apply the last two steps' refreshes
+    for _ in range(2):
+        o.activate(np.zeros((0, 6, 4), np.float32))
         r_hist.append(np.array([o.bound(k)[3] for k in range(sc.K)]))
     return sc, tr, o, r_hist
 
