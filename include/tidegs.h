@@ -76,6 +76,8 @@ typedef struct {
   uint32_t staging_blocks; /* write-back staging ring, records per parity (0 -> C/4);
                               an activate evicting more dirty records than this
                               writes them back straight from the slots instead  */
+  int32_t refresh_bounds; /* NEXT f2 (R25): after each update grow r_k to hold every
+                             Gaussian of the block; the cull of batch t+2 sees it  */
 } tgs_config;
 
 /* Optional device allocator hooks (PyTorch's caching allocator from Python).
@@ -213,6 +215,8 @@ uint64_t tgs_nonfinite_index(tgs_ctx* ctx);
  * any may be NULL. */
 tgs_status tgs_read_block(tgs_ctx* ctx, uint64_t k_global, float* theta, float* m, float* v);
 uint32_t tgs_step_count(tgs_ctx* ctx, uint64_t k_global);
+/* current Level-1 bound (cx, cy, cz, r) of global block k (host float[4]) */
+tgs_status tgs_read_bound(tgs_ctx* ctx, uint64_t k_global, float* out4);
 uint32_t tgs_num_local_blocks(const tgs_ctx* ctx);
 uint32_t tgs_pool_slots(const tgs_ctx* ctx);
 

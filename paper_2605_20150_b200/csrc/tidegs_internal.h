@@ -43,10 +43,11 @@ struct Dev {
   uint64_t N;
   uint32_t B, Kloc, W, P, PW, C, J_max, n_arr, G, rank, max_age, n_lut_cols;
   uint32_t quota_num, quota_den;
-  int32_t tide, cold;
+  int32_t tide, cold, refresh;
   uint64_t rec_floats;   // B*59
   // per local block
   float4* bounds;        // [Kloc] (cx,cy,cz,r)
+  uint32_t* pend[2];     // [Kloc] R25 refreshed radius bits of the step of that parity (0 none)
   int32_t* last_access;  // [Kloc] -1 = never (R4)
   uint32_t* step;        // [Kloc] Adam step count (R7)
   int32_t* b2s;          // [Kloc] slot or -1
@@ -118,6 +119,7 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s);
 cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
                         cudaStream_t s);
+cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s);
 int adam_grid(int device);
 
 }  // namespace tgs

@@ -181,6 +181,16 @@ __global__ void __launch_bounds__(256) k_cull(Dev d, const __grid_constant__ Pla
   const uint32_t w = l >> 5, lane = l & 31;
   const bool in = l < d.Kloc;
   float4 c = in ? d.bounds[l] : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (in && d.refresh) {  // R25: the refresh of the step two batches back enters now
+    const uint32_t pv = d.pend[parity][l];
+    if (pv) {
+      if (pv > __float_as_uint(c.w)) {
+        c.w = __uint_as_float(pv);
+        d.bounds[l].w = c.w;
+      }
+      d.pend[parity][l] = 0u;
+    }
+  }
   // Alg. 1 l.2 (R12): blocks accessed by the previous batch (R_t n K_t) get age 0
   if (in && T > 0 && ((d.Ab[w] >> lane) & 1u)) d.last_access[l] = T - 1;
   const float nr = -c.w;
@@ -622,6 +632,34 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t J, int parity,
   if ((threadIdx.x & 31) == 0) mask[(size_t)s * nw + (r >> 5)] = bits;
 }
 
+// -------------------------------- f2 conservative bound refresh (R25)
+// grid (ceil(B/256), nA), after k_adam: every row of an updated block gives
+// (|mu - c_k| + 3 exp(max log-scale)) * (1 + 2^-19) in fp32 RN; the block max
+// (on the bit pattern: radii are >= 0) goes to pend[parity][l], which the cull
+// of batch t+2 merges into r_k.
+__global__ void __launch_bounds__(256) k_refresh(Dev d, int parity) {
+  const uint32_t i = blockIdx.y;
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d.ent[i].step == 0u) return;  // block not updated this step (uniform per CTA)
+  const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+  uint32_t bits = 0u;
+  if (r < block_rows(d, l)) {
+    const float4 c = d.bounds[l];
+    const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
+    const float dx = __fsub_rn(row[0], c.x), dy = __fsub_rn(row[1], c.y);
+    const float dz = __fsub_rn(row[2], c.z);
+    const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    const float dist = __fsqrt_rn(d2);
+    float sc = row[52];
+    if (row[53] > sc) sc = row[53];
+    if (row[54] > sc) sc = row[54];
+    const float ext = __fmul_rn(3.0f, exp_det(sc));
+    bits = __float_as_uint(__fmul_rn(__fadd_rn(dist, ext), 1.0000019073486328f));
+  }
+  bits = __reduce_max_sync(kFull, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicMax(&d.pend[parity][l], bits);
+}
+
 // ------------------------------------------------------- a5 masked Adam
 // A warp owns a contiguous range of 4-row quads (4 rows = 944 B = 59 float4
 // per array); lane f and f+32 (< 59) load float4 #f of theta, m, v, g (128-bit,
@@ -878,6 +916,13 @@ cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint3
   if (nA == 0) return cudaSuccess;
   dim3 grid(((d.B + 31) / 32 * 32 + 255) / 256, nA);
   k_fine<<<grid, 256, 0, s>>>(d, J, parity, mask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s) {
+  if (nA == 0) return cudaSuccess;
+  dim3 grid((d.B + 255) / 256, nA);
+  k_refresh<<<grid, 256, 0, s>>>(d, parity);
   return cudaGetLastError();
 }
 

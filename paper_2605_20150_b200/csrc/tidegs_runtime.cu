@@ -599,6 +599,7 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   d.quota_den = g.quota_den;
   d.tide = g.tide ? 1 : 0;
   d.cold = g.moments == TGS_MOMENTS_COLD_RESTART ? 1 : 0;
+  d.refresh = g.refresh_bounds ? 1 : 0;
   d.rec_floats = (uint64_t)d.B * kDim;
   c->rec_bytes = d.rec_floats * sizeof(float);
 
@@ -686,6 +687,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
   d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
+  d.pend[0] = dalloc_t<uint32_t>(c, Kl, ok);
+  d.pend[1] = dalloc_t<uint32_t>(c, Kl, ok);
   d.last_planes[0] = dalloc_t<float4>(c, kMaxCams * 6, ok);
   d.last_planes[1] = dalloc_t<float4>(c, kMaxCams * 6, ok);
   d.ndirty_dev = dalloc_t<uint32_t>(c, 2, ok);
@@ -721,6 +724,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   CKI(cudaMemsetAsync(d.evicted, 0, Kl, s0));
   CKI(cudaMemsetAsync(d.admit, 0, sizeof(int32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.wb_tag, 0xff, sizeof(int32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.pend[0], 0, sizeof(uint32_t) * Kl, s0));
+  CKI(cudaMemsetAsync(d.pend[1], 0, sizeof(uint32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * 2, s0));
   for (uint32_t* p : {d.Kb, d.cand, d.Q, d.Sp, d.Sm, d.Om, d.Ab, d.R[0], d.R[1]})
     CKI(cudaMemsetAsync(p, 0, sizeof(uint32_t) * Wd, s0));
@@ -934,6 +939,10 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   CK(launch_adam(c->d, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
   c->tm.kernel_launches += 2;
+  if (c->d.refresh) {
+    CK(launch_refresh(c->d, nA, p, c->compute));
+    c->tm.kernel_launches++;
+  }
   CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }
@@ -1141,6 +1150,18 @@ uint32_t tgs_step_count(tgs_ctx* c, uint64_t kg) {
   uint32_t s = 0;
   cudaMemcpy(&s, c->d.step + l, sizeof s, cudaMemcpyDeviceToHost);
   return s;
+}
+
+tgs_status tgs_read_bound(tgs_ctx* c, uint64_t kg, float* out4) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out4 || kg % c->cfg.world_size != (uint64_t)c->cfg.rank) return TGS_EINVAL;
+  const uint64_t l = kg / c->cfg.world_size;
+  if (l >= c->d.Kloc) return TGS_EINVAL;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  CK(cudaMemcpy(out4, c->d.bounds + l, sizeof(float4), cudaMemcpyDeviceToHost));
+  return TGS_OK;
 }
 
 uint32_t tgs_num_local_blocks(const tgs_ctx* c) { return c ? c->d.Kloc : 0; }

@@ -28,7 +28,7 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_get_stats", "tgs_get_timing", "tgs_set_profiling", "tgs_get_list",
            "tgs_get_percam", "tgs_get_evicted_dirty", "tgs_get_slot_map",
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
-           "tgs_pool_slots", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error")
+           "tgs_pool_slots", "tgs_read_bound", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error")
 
 
 class Config(C.Structure):
@@ -38,7 +38,8 @@ class Config(C.Structure):
                 ("quota_num", C.c_uint32), ("quota_den", C.c_uint32), ("lambda_", C.c_double),
                 ("gamma", C.c_double), ("moments", C.c_int32), ("tide", C.c_int32),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32),
-                ("init_threads", C.c_int32), ("staging_blocks", C.c_uint32)]
+                ("init_threads", C.c_int32), ("staging_blocks", C.c_uint32),
+                ("refresh_bounds", C.c_int32)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -128,6 +129,7 @@ def lib():
         L.tgs_nonfinite_index.restype = u64
         L.tgs_nonfinite_index.argtypes = [vp]
         L.tgs_read_block.argtypes = [vp, u64] + [C.POINTER(C.c_float)] * 3
+        L.tgs_read_bound.argtypes = [vp, u64, C.POINTER(C.c_float)]
         L.tgs_step_count.restype = u32
         L.tgs_step_count.argtypes = [vp, u64]
         L.tgs_num_local_blocks.restype = u32
@@ -159,10 +161,11 @@ def _fp(a):
 
 def make_config(n_gaussians, block_size, capacity, *, pool_slots=0, max_cameras=256,
                 max_age=255, quota=(1, 2), lam=0.7, gamma=0.9, moments=PERSIST, tide=1,
-                world_size=1, rank=0, device=0, init_threads=0, staging_blocks=0) -> Config:
+                world_size=1, rank=0, device=0, init_threads=0, staging_blocks=0,
+                refresh_bounds=0) -> Config:
     return Config(n_gaussians, DIM, block_size, capacity, pool_slots, max_cameras, max_age,
                   quota[0], quota[1], lam, gamma, moments, tide, world_size, rank, device,
-                  init_threads, staging_blocks)
+                  init_threads, staging_blocks, refresh_bounds)
 
 
 def torch_allocator(device=0):
@@ -313,6 +316,11 @@ class Table:
 
     def step_count(self, k) -> int:
         return int(lib().tgs_step_count(self.h, k))
+
+    def bound(self, k) -> np.ndarray:
+        out = np.empty(4, np.float32)
+        self._err(lib().tgs_read_bound(self.h, k, _fp(out)), "tgs_read_bound")
+        return out
 
     @property
     def num_local_blocks(self) -> int:

@@ -253,3 +253,28 @@ def test_fine_filter_parity(J):
     assert pr.gpu.stats()["n_active_rows"] == total > 0
     assert pr.compare_blocks(range(sc.K)) == 0
     pr.close()
+
+
+def test_bound_refresh_parity():
+    """NEXT f2: with centres moving ~1 m per step, the refreshed bounds (R25)
+    are bit-exact with the oracle after every batch, and so are K, R, slots
+    and theta/m/v."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, refresh_bounds=1)
+    pr.lr[0:3] = 1.0
+    pr.lr[52:55] = 0.05
+    grew = 0
+    b0 = np.stack([pr.orc.bound(k) for k in range(sc.K)])
+    for t in range(20):
+        act = pr.activate(tr.batch_planes(t, cfg.J))
+        pr.t = t
+        pr.compare_plan(cfg.J)
+        assert pr.step(act, t) == O.OK
+        gb = np.stack([pr.gpu.bound(k) for k in range(sc.K)])
+        ob = np.stack([pr.orc.bound(k) for k in range(sc.K)])
+        np.testing.assert_array_equal(gb.view(np.uint32), ob.view(np.uint32), err_msg=f"t={t}")
+        grew = int((ob[:, 3] > b0[:, 3]).sum())
+    assert grew > 0
+    pr.compare_stats()
+    assert pr.compare_blocks(range(sc.K)) == 0
+    pr.close()
