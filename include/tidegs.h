@@ -195,6 +195,12 @@ tgs_status tgs_flush(tgs_ctx* ctx);
  * (synchronising; for tests, metrics and checkpoint export) */
 tgs_status tgs_get_stats(tgs_ctx* ctx, tgs_stats* out);
 tgs_status tgs_get_timing(tgs_ctx* ctx, tgs_timing* out);
+/* Non-synchronising stats read: enqueues a device->host copy of the device
+ * counters into out (must be pinned host memory, e.g. cudaHostAlloc) on the
+ * compute stream, in stream order after the last tgs_step_adam; valid once
+ * that stream is synchronised.  flush_bytes / n_flush_blocks are not included
+ * (host-side; see tgs_get_stats). */
+tgs_status tgs_get_stats_async(tgs_ctx* ctx, tgs_stats* out);
 tgs_status tgs_set_profiling(tgs_ctx* ctx, int enabled); /* also resets tgs_timing */
 
 /* Lists of the last activate, GLOBAL ids ascending: which = 0 K_{t+1},

@@ -778,20 +778,30 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
     if (pmask) act &= (pmask[r0 >> 5] >> (r0 & 31)) & 0xFu;
     if (act == 0u) continue;  // warp-uniform
     const size_t f0 = (size_t)(r0 / 4) * 59 + lane, f1 = f0 + 32;
+    // components of float4 #lane / #lane+32 whose row is active: lanes whose
+    // float4s hold only inactive rows skip their loads and stores (masked I_t)
+    uint32_t sel0 = 0, sel1 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if ((rowsel0 >> (4 * q)) & act) sel0 |= 1u << q;
+      if ((rowsel1 >> (4 * q)) & act) sel1 |= 1u << q;
+    }
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 g0 = __ldcs(pg + f0);
-    const float4 g1 = has1 ? __ldcs(pg + f1) : z;
-    float4 t0 = __ldcs(pt + f0), m0 = __ldcs(pm + f0), v0 = __ldcs(pv + f0);
-    float4 t1 = z, m1 = z, v1 = z;
-    if (has1) {
+    float4 g0 = z, t0 = z, m0 = z, v0 = z, g1 = z, t1 = z, m1 = z, v1 = z;
+    if (sel0) {
+      g0 = __ldcs(pg + f0);
+      t0 = __ldcs(pt + f0);
+      m0 = __ldcs(pm + f0);
+      v0 = __ldcs(pv + f0);
+    }
+    if (sel1) {
+      g1 = __ldcs(pg + f1);
       t1 = __ldcs(pt + f1);
       m1 = __ldcs(pm + f1);
       v1 = __ldcs(pv + f1);
     }
-    const uint32_t nf0 = nonfinite4(g0), nf1 = has1 ? nonfinite4(g1) : 0u;
-    const bool anybad = __any_sync(kFull, (nf0 | nf1) != 0u);
-    uint32_t sel0 = 0xFu, sel1 = has1 ? 0xFu : 0u;
-    if (act != 0xFu || anybad) {  // slow path: rows of the quad that are skipped
+    const uint32_t nf0 = nonfinite4(g0) & sel0, nf1 = nonfinite4(g1) & sel1;
+    if (__any_sync(kFull, (nf0 | nf1) != 0u)) {  // R20: rows with a non-finite g are skipped
       uint32_t bad = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -799,25 +809,23 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
         if ((nf1 >> q) & 1u) bad |= (rowsel1 >> (4 * q)) & 0xFu;
       }
       bad = __reduce_or_sync(kFull, bad);
-      if (bad & act) {  // R20: report the lowest gid*59+attr over active rows
-        const uint64_t gid0 = (uint64_t)d.a_gid[parity][cur] * d.B + r0;
-        unsigned long long best = ~0ull;
+      // report the lowest gid*59+attr over the active rows
+      const uint64_t gid0 = (uint64_t)d.a_gid[parity][cur] * d.B + r0;
+      unsigned long long best = ~0ull;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
-          if (((nf0 >> q) & 1u) && ((act >> (e0 / 59)) & 1u)) {
-            const unsigned long long idx = (gid0 + e0 / 59) * 59ull + e0 % 59;
-            best = idx < best ? idx : best;
-          }
-          if (((nf1 >> q) & 1u) && ((act >> (e1 / 59)) & 1u)) {
-            const unsigned long long idx = (gid0 + e1 / 59) * 59ull + e1 % 59;
-            best = idx < best ? idx : best;
-          }
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
+        if ((nf0 >> q) & 1u) {
+          const unsigned long long idx = (gid0 + e0 / 59) * 59ull + e0 % 59;
+          best = idx < best ? idx : best;
         }
-        if (best != ~0ull) atomicMin(d.nonfinite, best);
+        if ((nf1 >> q) & 1u) {
+          const unsigned long long idx = (gid0 + e1 / 59) * 59ull + e1 % 59;
+          best = idx < best ? idx : best;
+        }
       }
+      if (best != ~0ull) atomicMin(d.nonfinite, best);
       const uint32_t upd = act & ~bad;  // Eq. masked_update: unchanged off I_t
-      if (upd == 0u) continue;
       sel0 = sel1 = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -825,11 +833,13 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
         if ((rowsel1 >> (4 * q)) & upd) sel1 |= 1u << q;
       }
     }
-    adam_f4(t0, m0, v0, g0, ss0, K, sel0);
-    __stcs(pt + f0, t0);
-    __stcs(pm + f0, m0);
-    __stcs(pv + f0, v0);
-    if (has1) {
+    if (sel0) {
+      adam_f4(t0, m0, v0, g0, ss0, K, sel0);
+      __stcs(pt + f0, t0);
+      __stcs(pm + f0, m0);
+      __stcs(pv + f0, v0);
+    }
+    if (sel1) {
       adam_f4(t1, m1, v1, g1, ss1, K, sel1);
       __stcs(pt + f1, t1);
       __stcs(pm + f1, m1);

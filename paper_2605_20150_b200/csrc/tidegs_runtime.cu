@@ -1007,6 +1007,15 @@ tgs_status tgs_get_stats(tgs_ctx* c, tgs_stats* out) {
   return TGS_OK;
 }
 
+tgs_status tgs_get_stats_async(tgs_ctx* c, tgs_stats* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out) return TGS_EINVAL;
+  CK(cudaMemcpyAsync(out, c->d.stats, sizeof(unsigned long long) * ST_N, cudaMemcpyDeviceToHost,
+                     c->compute));
+  return TGS_OK;
+}
+
 tgs_status tgs_set_profiling(tgs_ctx* c, int enabled) {
   tgs_status st = check(c);
   if (st != TGS_OK) return st;

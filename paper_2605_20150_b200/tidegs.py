@@ -25,7 +25,7 @@ LISTS = {"K": 0, "R": 1, "S+": 2, "S-": 3, "Omega": 4, "A": 5}
 # every entry point include/tidegs.h declares (tests check the exports)
 SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tgs_flush",
            "tgs_fine_filter",
-           "tgs_get_stats", "tgs_get_timing", "tgs_set_profiling", "tgs_get_list",
+           "tgs_get_stats", "tgs_get_stats_async", "tgs_get_timing", "tgs_set_profiling", "tgs_get_list",
            "tgs_get_percam", "tgs_get_evicted_dirty", "tgs_get_slot_map",
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
            "tgs_pool_slots", "tgs_read_bound", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error")
@@ -118,6 +118,7 @@ def lib():
         L.tgs_fine_filter.argtypes = [vp, vp]
         L.tgs_get_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_get_timing.argtypes = [vp, C.POINTER(Timing)]
+        L.tgs_get_stats_async.argtypes = [vp, vp]
         L.tgs_set_profiling.argtypes = [vp, C.c_int]
         L.tgs_get_list.restype = u32
         L.tgs_get_list.argtypes = [vp, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_int32), u32]
@@ -296,6 +297,10 @@ class Table:
         s = Stats()
         self._err(lib().tgs_get_stats(self.h, C.byref(s)), "tgs_get_stats")
         return s.as_dict()
+
+    def stats_async(self, pinned_ptr):
+        """Enqueue a D2H read of the counters into pinned host memory (no sync)."""
+        self._err(lib().tgs_get_stats_async(self.h, pinned_ptr), "tgs_get_stats_async")
 
     def timing(self) -> dict:
         t = Timing()
