@@ -734,6 +734,7 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   CKI(cudaMemsetAsync(d.occ, 0, sizeof(uint32_t) * d.PW, s0));
   CKI(cudaMemsetAsync(d.dirty, 0, sizeof(uint32_t) * d.PW, s0));
   CKI(cudaMemsetAsync(d.stats, 0, sizeof(unsigned long long) * ST_N, s0));
+  CKI(cudaMemsetAsync(d.cnt, 0, sizeof(uint32_t) * CNT_N, s0));  // k_plan re-zeroes it after use
   CKI(cudaMemsetAsync(d.nonfinite, 0xff, sizeof(unsigned long long), s0));
   CKI(cudaMemsetAsync(d.hdr_dev, 0, sizeof(PlanHdr), s0));
   CKI(cudaMemsetAsync(d.params, 0, sizeof(float) * pool_floats, s0));

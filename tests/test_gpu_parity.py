@@ -278,3 +278,18 @@ def test_bound_refresh_parity():
     pr.compare_stats()
     assert pr.compare_blocks(range(sc.K)) == 0
     pr.close()
+
+
+def test_garbage_in_recycled_device_memory():
+    """Every device buffer the library relies on is initialised: poison the
+    caching allocator's free blocks with 0xFF bytes first (regression: the
+    per-activate counters once came uninitialised from a recycled block)."""
+    import torch
+    junk = [torch.full((n,), -1, dtype=torch.int32, device="cuda")
+            for n in [256] * 400 + [4096] * 200 + [131072] * 50 + [1 << 28]]
+    torch.cuda.synchronize()
+    del junk
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity)
+    _drive(pr, tr, cfg.J, 12, check_blocks_every=5)
+    pr.close()
