@@ -273,14 +273,15 @@ tgs_status ensure_lut(tgs_ctx* c, float b1, float b2, uint32_t need) {
     c->lut_b2 = b2;
   }
   if (need > c->lut_n) {
-    for (uint32_t s = c->lut_n; s < need; ++s)
+    // fill the whole capacity at once: one upload per (re)build, none per step
+    for (uint32_t s = c->lut_n; s < c->lut_cap; ++s)
       lut_entry(b1, b2, s, c->lut_pinned[s], c->lut_pinned[c->lut_cap + s]);
-    const size_t n = need - c->lut_n;
+    const size_t n = c->lut_cap - c->lut_n;
     CK(cudaMemcpyAsync(c->d.lut_bc1 + c->lut_n, c->lut_pinned + c->lut_n, n * sizeof(float),
                        cudaMemcpyHostToDevice, c->compute));
     CK(cudaMemcpyAsync(c->d.lut_ibs + c->lut_n, c->lut_pinned + c->lut_cap + c->lut_n,
                        n * sizeof(float), cudaMemcpyHostToDevice, c->compute));
-    c->lut_n = need;
+    c->lut_n = c->lut_cap;
   }
   return TGS_OK;
 }
