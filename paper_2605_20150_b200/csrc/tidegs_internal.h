@@ -77,6 +77,7 @@ struct Dev {
   float* staging[2];     // [S_max][n_arr][B][59] write-back staging ring (parity)
   uint32_t S_max;        // staging capacity in records
   float4* last_planes[2];  // [kMaxCams*6] camera batch of the activate of that parity
+  const float4* planes_map[2];  // mapped pinned host staging of the camera batch (parity)
   // selection
   uint16_t* rank_lut;    // [2][max_age+2]
   uint32_t n_buckets;    // 2 * (number of distinct ranks)
@@ -91,20 +92,13 @@ struct Dev {
   float* grads;          // [P][B][59]
 };
 
-// camera batch passed by value as a kernel parameter (24 KB < 32 KB limit),
-// so the plan never queues behind the gather on the copy engine
-struct PlanesArg {
-  float4 p[kMaxCams * 6];
-};
-
 struct AdamHyper {
   float lr[kDim];
   float b1, b2, omb1, omb2, eps;
 };
 
 // launchers (return cudaGetLastError())
-cudaError_t launch_cull(const Dev& d, const PlanesArg& planes, uint32_t J, int32_t T,
-                        int parity, cudaStream_t s);
+cudaError_t launch_cull(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);

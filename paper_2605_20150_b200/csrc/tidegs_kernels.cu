@@ -169,13 +169,16 @@ __device__ void select_top(const Dev& d, uint32_t n, uint32_t nw, int32_t T, uin
 }
 
 // ------------------------------------------------------------------- a1 cull
-__global__ void __launch_bounds__(256) k_cull(Dev d, const __grid_constant__ PlanesArg planes,
-                                              uint32_t J, int32_t T, int parity) {
+// one CTA: the camera batch from mapped pinned host memory (6 KB at J = 64)
+// into device memory, so the plan never queues behind the gather on a copy engine
+__global__ void __launch_bounds__(256) k_planes(Dev d, uint32_t J, int parity) {
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x)
+    d.last_planes[parity][i] = d.planes_map[parity][i];
+}
+
+__global__ void __launch_bounds__(256) k_cull(Dev d, uint32_t J, int32_t T, int parity) {
   __shared__ float4 pl[kMaxCams * 6];
-  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) {
-    pl[i] = planes.p[i];
-    if (blockIdx.x == 0) d.last_planes[parity][i] = planes.p[i];  // for the Level-2 filter
-  }
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = d.last_planes[parity][i];
   __syncthreads();
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t w = l >> 5, lane = l & 31;
@@ -851,11 +854,11 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
 }  // namespace
 
 // ------------------------------------------------------------- launchers
-cudaError_t launch_cull(const Dev& d, const PlanesArg& planes, uint32_t J, int32_t T,
-                        int parity, cudaStream_t s) {
+cudaError_t launch_cull(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s) {
   if (d.Kloc == 0) return cudaSuccess;
+  if (J) k_planes<<<1, 256, 0, s>>>(d, J, parity);
   const uint32_t grid = (d.Kloc + 255) / 256;
-  k_cull<<<grid, 256, 0, s>>>(d, planes, J, T, parity);
+  k_cull<<<grid, 256, 0, s>>>(d, J, T, parity);
   return cudaGetLastError();
 }
 

@@ -71,7 +71,7 @@ struct tgs_ctx {
   uint32_t* sp_map = nullptr;     // host view
   uint32_t* dirty_map[2] = {nullptr, nullptr};  // host views (parity)
   uint32_t* ndirty = nullptr;     // host view [2]
-  float* planes_pinned = nullptr; // [kMaxCams*24] staging of the kernel parameter
+  float* planes_pinned = nullptr; // [2][kMaxCams*24] mapped staging of the camera batch
   // streams / events (ev_*[p]: last record by an activate of parity p)
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr, fix = nullptr;
   cudaEvent_t ev_plan = nullptr, ev_gstart = nullptr, ev_gdone = nullptr;
@@ -643,8 +643,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
       cudaHostAlloc((void**)&c->dirty_map[0], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[1], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * 2, cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * kMaxCams * 24,
-                    cudaHostAllocDefault) != cudaSuccess) {
+      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 2 * kMaxCams * 24,
+                    cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     return fail(TGS_ENOMEM);
   }
@@ -655,6 +655,11 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   cudaHostGetDevicePointer((void**)&d.dirty_map[0], c->dirty_map[0], 0);
   cudaHostGetDevicePointer((void**)&d.dirty_map[1], c->dirty_map[1], 0);
   cudaHostGetDevicePointer((void**)&d.ndirty_map, c->ndirty, 0);
+  for (int p = 0; p < 2; ++p) {
+    float* dp = nullptr;
+    cudaHostGetDevicePointer((void**)&dp, c->planes_pinned + (size_t)p * kMaxCams * 24, 0);
+    d.planes_map[p] = reinterpret_cast<const float4*>(dp);
+  }
 
   // ---- device state
   bool ok = true;
@@ -770,20 +775,20 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
 
   // ---- plan stream: a1 cull, a3 quota + fill, a2 delta, slots, A list.
   //      The lists of parity p are free once activate t-2's Adam, write-back
-  //      kernels and gather are done (GPU-side waits only).  Planes travel as
-  //      a kernel parameter: nothing here queues behind a copy engine.
+  //      kernels and gather are done (GPU-side waits only).  The camera batch is
+  //      read from mapped pinned memory by k_planes: nothing here queues behind
+  //      a copy engine.
   if (c->rec_lists[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_lists[p], 0));
   if (c->rec_ready[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_ready[p], 0));
   Timer tp;
-  static_assert(sizeof(PlanesArg) == sizeof(float) * kMaxCams * 24, "planes layout");
-  PlanesArg* pa = reinterpret_cast<PlanesArg*>(c->planes_pinned);
-  if (J) std::memcpy(pa, cams, sizeof(float) * 24 * J);
+  // the batch of t-2 (same staging buffer) was consumed before that plan's readback
+  if (J) std::memcpy(c->planes_pinned + (size_t)p * kMaxCams * 24, cams, sizeof(float) * 24 * J);
   prof_begin(c, c->plan, tp);
-  CK(launch_cull(d, *pa, J, T, p, c->plan));
+  CK(launch_cull(d, J, T, p, c->plan));
   CK(launch_quota(d, J, T, p, c->plan));
   CK(launch_plan(d, T, p, c->plan));
   prof_end(c, c->plan, tp, 2);
-  c->tm.kernel_launches += (d.Kloc ? 1 : 0) + ((J && d.Kloc) ? 1 : 0) + 1;
+  c->tm.kernel_launches += (d.Kloc ? 1 : 0) + ((J && d.Kloc) ? 2 : 0) + 1;
   CK(cudaEventRecord(c->ev_plan, c->plan));
   CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
   const PlanHdr h = *c->hdr;
