@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256) k_cull(Dev d, uint32_t J, int32_t T, int 
       if (dist < nr) vis = false;  // cull iff d < -r_k (NaN stays visible)
     }
     const uint32_t bits = __ballot_sync(kFull, vis);
-    if (lane == 0) d.percam[(size_t)j * d.W + w] = bits;
+    if (lane == 0 && w < d.W) d.percam[(size_t)j * d.W + w] = bits;  // tail warps own no word
     uni |= bits;
   }
   if (lane == 0 && w < d.W) {
