@@ -208,6 +208,8 @@ class Table:
             self._keep.append(cb)
             fill_p = C.cast(cb, C.c_void_p).value
         alloc = None
+        if os.environ.get("TGS_CUDAMALLOC") == "1":  # one cudaMalloc per buffer (sanitizer runs)
+            use_torch_allocator = False
         if use_torch_allocator:
             self._alloc = torch_allocator(cfg.device)
             alloc = C.byref(self._alloc)
