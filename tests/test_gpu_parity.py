@@ -293,3 +293,32 @@ def test_garbage_in_recycled_device_memory():
     pr = _pair(sc, capacity=cfg.capacity)
     _drive(pr, tr, cfg.J, 12, check_blocks_every=5)
     pr.close()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_shards_on_one_gpu(G):
+    """R17 sharding: every rank's context (world_size G, rank r,
+    capacity ceil(C/G)) matches the oracle's shard r bit-exactly -- K_loc is
+    then not a multiple of 32 (partial bitset words) -- and the shards' K
+    partition the single-GPU K."""
+    from paper_2605_20150_b200 import shard
+    cfg, sc, tr = tiny()
+    cap = shard.shard_capacity(cfg.capacity, G)
+    pairs = [_pair(sc, capacity=cap, world_size=G, rank=r) for r in range(G)]
+    single = O.Oracle(O.make_config(sc.N, sc.B, cfg.capacity), sc.bounds(), fill=None,
+                      track_all=False)
+    for t in range(16):
+        planes = tr.batch_planes(t, cfg.J)
+        single.activate(planes)
+        Ks = []
+        for pr in pairs:
+            act = pr.activate(planes)
+            pr.t = t
+            pr.compare_plan(cfg.J)
+            assert pr.step(act, t) == O.OK
+            Ks += pr.gpu.list("K").tolist()
+        assert sorted(Ks) == single.list("K").tolist()
+    for r, pr in enumerate(pairs):
+        pr.compare_stats()
+        assert pr.compare_blocks([k for k in range(sc.K) if k % G == r]) == 0
+        pr.close()
