@@ -322,3 +322,44 @@ def test_shards_on_one_gpu(G):
         pr.compare_stats()
         assert pr.compare_blocks([k for k in range(sc.K) if k % G == r]) == 0
         pr.close()
+
+
+class _RandomCams:
+    """Seeded random pinhole cameras inside a small scene (high churn)."""
+
+    def __init__(self, side, seed=11, far=25.0):
+        self.rng = np.random.default_rng(seed)
+        self.side, self.far = side, far
+
+    def batch_planes(self, t, J):
+        out = np.empty((J, 6, 4), np.float32)
+        for j in range(J):
+            pos = [*(self.rng.uniform(-0.5, 0.5, 2) * self.side), self.rng.uniform(1.0, 15.0)]
+            ang = self.rng.uniform(0, 2 * np.pi)
+            fwd = [np.cos(ang), np.sin(ang), -self.rng.uniform(0.1, 1.0)]
+            cam = W.look(pos, fwd, [0, 0, 1], 50.0, 640, 480, 0.1, self.far)
+            out[j] = W.camera_planes(cam)
+        return out
+
+
+@pytest.mark.parametrize("N,B,C,J,kw", [
+    (1, 4, 1, 1, {}),                                            # one Gaussian, one block
+    (37, 4, 2, 3, {"pool_slots": 2}),                            # ragged last block, P = C
+    (5000, 8, 1, 256, {"quota": (1, 1)}),                        # max cameras, C = 1, beta = 1
+    (20000, 36, 40, 17, {"max_age": 0, "lam": 0.0}),             # B % 32 != 0, recency off
+    (20000, 36, 40, 17, {"max_age": 1023, "gamma": 0.999999}),   # max age, gamma -> 1
+    (30000, 100, 7, 5, {"tide": 0, "moments": O.COLD_RESTART}),  # restage-all, cold
+    (30000, 100, 12, 4, {"quota": (1, 1), "lam": 1.0, "pool_slots": 13}),  # tight pool
+])
+def test_edge_configs(N, B, C, J, kw):
+    """Degenerate and extreme shapes under random (high-churn) cameras:
+    bit-exact lists/slots/counters and 0-ULP rows against the oracle."""
+    sc = W.Scene(N, B, side=60.0, lot=20.0, footprint=12.0, hmin=2.0, hmax=12.0)
+    tr = _RandomCams(60.0)
+    pr = _pair(sc, capacity=C, **kw)
+    _drive(pr, tr, J, 12, check_blocks_every=3)
+    pr.gpu.flush()
+    pr.orc.flush()
+    pr.compare_stats()
+    assert pr.compare_blocks(range(sc.K)) == 0
+    pr.close()
