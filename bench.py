@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="one process measures rank 0's shard of a G-way block-sharded table "
+                         "(per-GPU share of a G-GPU run, no collectives; e.g. --config 1b --shard-of 8)")
     ap.add_argument("--fine-filter", action="store_true",
                     help="NEXT f1: Level-2 filter -> I_t mask -> masked Adam in every step")
     return ap.parse_args()
@@ -194,6 +197,15 @@ def _synth_struct(sc):
 
 
 def _config_dict(args, wl, ws):
+    if getattr(args, "shard_of", 0) > 1 and ws == 1:
+        d = _config_dict_base(args, wl, args.shard_of)
+        d["shard"] = f"rank 0 of a {args.shard_of}-way block-sharded table, measured alone"
+        d["world_size"] = 1
+        return d
+    return _config_dict_base(args, wl, ws)
+
+
+def _config_dict_base(args, wl, ws):
     return {"workload": f"{wl.name}: {wl.n_gaussians:,} Gaussians, {wl.traj} trajectory "
                         f"({'random' if wl.shuffled else 'smooth'} order), J={wl.J} cameras/batch",
             "n_gaussians": wl.n_gaussians, "block_size": wl.block_size, "J": wl.J,
@@ -248,10 +260,11 @@ def main():
     wl = W.CONFIGS[args.config]
     sc = wl.scene()
     tr = wl.trajectory(sc)
-    cap = -(-wl.capacity // ws)
+    shard_ws, shard_rank = (args.shard_of, 0) if args.shard_of > 1 and ws == 1 else (ws, rank)
+    cap = -(-wl.capacity // shard_ws)
     moments = T.COLD_RESTART if args.moments == "cold" else T.PERSIST
     t_setup = time.perf_counter()
-    cfg = T.make_config(sc.N, sc.B, cap, moments=moments, world_size=ws, rank=rank,
+    cfg = T.make_config(sc.N, sc.B, cap, moments=moments, world_size=shard_ws, rank=shard_rank,
                         device=local)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
@@ -260,7 +273,7 @@ def main():
     # synthetic gradients for every slot, written once (renderer out of scope)
     P_ = table.P
     ids = torch.arange(P_, dtype=torch.int32, device=dev) % max(1, table.num_local_blocks)
-    ids = ids * ws + rank
+    ids = ids * shard_ws + shard_rank
     slots = torch.arange(P_, dtype=torch.int32, device=dev)
     act0 = table.activate(np.zeros((0, 6, 4), np.float32))
     W.cuda_lib().wl_cuda_synth_grads(act0.d_grads, act0.grad_stride, ids.data_ptr(),
@@ -392,7 +405,7 @@ def main():
                 "peak_kind": "measured in this run: pinned 1 GiB cudaMemcpy",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps}
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and shard_ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, wl, sc, tr, args.cpu_sample_s)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Gaussians/s", "n_gpus": ws,
