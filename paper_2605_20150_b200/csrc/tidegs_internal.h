@@ -33,6 +33,8 @@ struct PlanHdr {
 // per active (R n K) entry, written by k_adam_prologue
 struct AdamEnt {
   uint32_t step;   // new step count, 0 = no active row (block untouched)
+  uint16_t rows_hi_unused;
+  uint16_t fresh;  // cold restart and first update since admission: m = v = 0 implicitly
   uint32_t rows;   // logical rows of the block
   float bc1;       // 1 - beta1^step   (R9)
   float ibs;       // 1 / sqrt(1 - beta2^step)
@@ -106,7 +108,6 @@ cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
 cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t T, bool tag,
                                 cudaStream_t s);
 cudaError_t launch_readmit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s);
-cudaError_t launch_cold_init(const Dev& d, uint32_t nSp, int parity, cudaStream_t s);
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s);
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,

@@ -9,9 +9,10 @@
 //                        (Alg. 1 l.6-8), slot allocation /
 //                        eviction (R13), active list A = R n K
 //   k_evict          a4  dirty S- records -> write-back list
-//   k_cold_init      a4  cold restart: zero moments of admitted slots
 //   k_adam_prologue  a5  per-block active-row count, step, dirty bit
-//   k_adam           a5  fused masked Adam, 128-bit coalesced (Eq. masked_update)
+//   k_adam           a5  fused masked Adam, 128-bit coalesced (Eq. masked_update); a
+//                        cold-restarted block's moments are zero until its first update
+//                        (PAPER.md:327-328), which writes its whole m, v record
 //
 // Determinism: every choice (list order, Top-C, slot assignment) comes from
 // prefix sums over id-ordered bitsets, never from atomic arrival order; atomics
@@ -519,17 +520,6 @@ __global__ void __launch_bounds__(256) k_readmit(Dev d, int parity, int32_t T) {
     __stcs(dst + e, __ldcs(src + e));
 }
 
-// ---------------------------------- a4 cold restart: m = v = 0 in new slots
-__global__ void __launch_bounds__(256) k_cold_init(Dev d, int parity) {
-  const uint32_t i = blockIdx.y;
-  const uint32_t s = d.sp_slot[parity][i];
-  float4* mv = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * d.rec_floats + d.rec_floats);
-  const uint32_t n4 = (uint32_t)(2 * d.rec_floats / 4);
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += gridDim.x * blockDim.x)
-    __stcs(mv + e, z);
-}
-
 // ------------------------------------------------ a5 prologue (per block)
 __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int parity,
                                                        const uint32_t* __restrict__ mask) {
@@ -559,6 +549,9 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
         d.step[l] = ns;
         atomicOr(&d.dirty[s >> 5], 1u << (s & 31));
         e.step = ns;
+        // cold restart (R6): the moments of an admitted block are zero until its
+        // first update; k_adam writes that block's whole m, v record then
+        e.fresh = (d.cold && before == 0u) ? 1 : 0;
         e.bc1 = d.lut_bc1[ns];
         e.ibs = d.lut_ibs[ns];
         atomicAdd(&acc[0], 1ull);
@@ -742,7 +735,7 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   const size_t rf = d.rec_floats;
 
   uint32_t cur = 0xffffffffu;
-  uint32_t step = 0, rows = 0;
+  uint32_t step = 0, rows = 0, fresh = 0;
   float ss0[4], ss1[4];
   const float4* pg = nullptr;
   float4 *pt = nullptr, *pm = nullptr, *pv = nullptr;
@@ -756,6 +749,7 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       const AdamEnt ent = d.ent[i];
       step = ent.step;
       rows = ent.rows;
+      fresh = ent.fresh;
       K.ibs = ent.ibs;
       const uint32_t s = d.a_slot[parity][i];
       pt = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf);
@@ -776,10 +770,10 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       quad = 0;
       ++i;
     }
-    if (step == 0u || r0 >= rows) continue;  // no active row in this block / padding quad
-    uint32_t act = (rows - r0) >= 4u ? 0xFu : ((1u << (rows - r0)) - 1u);
+    if (step == 0u) continue;  // no active row in this block: untouched
+    uint32_t act = r0 >= rows ? 0u : (rows - r0) >= 4u ? 0xFu : ((1u << (rows - r0)) - 1u);
     if (pmask) act &= (pmask[r0 >> 5] >> (r0 & 31)) & 0xFu;
-    if (act == 0u) continue;  // warp-uniform
+    if (act == 0u && !fresh) continue;  // warp-uniform
     const size_t f0 = (size_t)(r0 / 4) * 59 + lane, f1 = f0 + 32;
     // components of float4 #lane / #lane+32 whose row is active: lanes whose
     // float4s hold only inactive rows skip their loads and stores (masked I_t)
@@ -794,14 +788,18 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
     if (sel0) {
       g0 = __ldcs(pg + f0);
       t0 = __ldcs(pt + f0);
-      m0 = __ldcs(pm + f0);
-      v0 = __ldcs(pv + f0);
+      if (!fresh) {
+        m0 = __ldcs(pm + f0);
+        v0 = __ldcs(pv + f0);
+      }
     }
     if (sel1) {
       g1 = __ldcs(pg + f1);
       t1 = __ldcs(pt + f1);
-      m1 = __ldcs(pm + f1);
-      v1 = __ldcs(pv + f1);
+      if (!fresh) {
+        m1 = __ldcs(pm + f1);
+        v1 = __ldcs(pv + f1);
+      }
     }
     const uint32_t nf0 = nonfinite4(g0) & sel0, nf1 = nonfinite4(g1) & sel1;
     if (__any_sync(kFull, (nf0 | nf1) != 0u)) {  // R20: rows with a non-finite g are skipped
@@ -836,15 +834,21 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
         if ((rowsel1 >> (4 * q)) & upd) sel1 |= 1u << q;
       }
     }
+    // a fresh (cold-restarted) block gets its whole m, v record written: the
+    // computed moments of updated rows, zeros for every other row
     if (sel0) {
       adam_f4(t0, m0, v0, g0, ss0, K, sel0);
       __stcs(pt + f0, t0);
+    }
+    if (sel0 || fresh) {
       __stcs(pm + f0, m0);
       __stcs(pv + f0, v0);
     }
     if (sel1) {
       adam_f4(t1, m1, v1, g1, ss1, K, sel1);
       __stcs(pt + f1, t1);
+    }
+    if (sel1 || (fresh && has1)) {
       __stcs(pm + f1, m1);
       __stcs(pv + f1, v1);
     }
@@ -895,13 +899,6 @@ cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) 
   if (nSm == 0) return cudaSuccess;
   dim3 grid(16, nSm);
   k_pack<<<grid, 256, 0, s>>>(d, parity);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_cold_init(const Dev& d, uint32_t nSp, int parity, cudaStream_t s) {
-  if (nSp == 0) return cudaSuccess;
-  dim3 grid(16, nSp);
-  k_cold_init<<<grid, 256, 0, s>>>(d, parity);
   return cudaGetLastError();
 }
 

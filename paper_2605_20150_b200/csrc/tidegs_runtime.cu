@@ -11,7 +11,7 @@
 //   h2d stream     : [slots freed by t-1, host records written by t-2]
 //                    one cudaMemcpyBatchAsync of S+ host tier -> slots (a4 gather)
 //                    -> k_readmit (S+ packed by t-1: newest copy in the ring)
-//                    -> k_cold_init -> ready[p]
+//                    -> ready[p]   (cold-restart zeros are folded into k_adam)
 //   compute stream : [after Adam(t-1)] k_evict (dirty S-) -> k_pack (slots ->
 //                    staging ring p) -> evict[p]                        (a4)
 //   I/O thread     : waits evict[p], reads the dirty list, one batch of
@@ -846,19 +846,12 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   // and patches re-admissions after it; the next gather does not wait for it
   cudaStream_t ready_on = c->h2d;
   if (h.nSp) {
-    const bool fixups = d.cold || c->prev_packed;
+    const bool fixups = c->prev_packed;  // cold restart needs no fix-up (see k_adam)
     if (fixups) {
       CK(cudaEventRecord(c->ev_gstart, c->h2d));
       CK(cudaStreamWaitEvent(c->fix, c->ev_gstart, 0));
       CK(cudaStreamWaitEvent(c->fix, c->ev_plan, 0));
       ready_on = c->fix;
-    }
-    if (d.cold) {
-      Timer tc;
-      prof_begin(c, c->fix, tc);
-      CK(launch_cold_init(d, h.nSp, p, c->fix));
-      prof_end(c, c->fix, tc, 6);
-      c->tm.kernel_launches++;
     }
     Timer th;
     prof_begin(c, c->h2d, th);
@@ -1143,12 +1136,19 @@ tgs_status tgs_read_block(tgs_ctx* c, uint64_t kg, float* theta, float* m, float
   st = sync_all(c);
   if (st != TGS_OK) return st;
   int32_t s = -1;
+  uint32_t stp = 0;
   CK(cudaMemcpy(&s, c->d.b2s + l, sizeof s, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&stp, c->d.step + l, sizeof stp, cudaMemcpyDeviceToHost));
+  // cold restart: a resident block not updated since admission has m = v = 0
+  // (k_adam writes its moment record at the first update)
+  const bool zero_moments = c->d.cold && s >= 0 && stp == 0;
   const size_t rb = c->rec_bytes, rf = c->d.rec_floats;
   float* outs[3] = {theta, m, v};
   for (int a = 0; a < 3; ++a) {
     if (!outs[a]) continue;
-    if (s >= 0) {
+    if (s >= 0 && a > 0 && zero_moments) {
+      std::memset(outs[a], 0, rb);
+    } else if (s >= 0) {
       CK(cudaMemcpy(outs[a], slot_rec(c, (uint32_t)s) + a * rf, rb, cudaMemcpyDeviceToHost));
     } else if (a < (int)c->d.n_arr) {
       std::memcpy(outs[a], host_rec(c, (uint32_t)l) + a * rf, rb);
