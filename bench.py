@@ -53,6 +53,12 @@ def parse():
     ap.add_argument("--shard-of", type=int, default=0,
                     help="one process measures rank 0's shard of a G-way block-sharded table "
                          "(per-GPU share of a G-GPU run, no collectives; e.g. --config 1b --shard-of 8)")
+    ap.add_argument("--no-tide", action="store_true",
+                    help="ablation w/o Tide (PAPER.md:570-573): restage R_{t+1} every batch")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="ablation w/o Overlap (PAPER.md:576-579): I/O and compute serialised")
+    ap.add_argument("--refresh-bounds", action="store_true",
+                    help="NEXT f2: conservative bound refresh after every update (R25)")
     ap.add_argument("--fine-filter", action="store_true",
                     help="NEXT f1: Level-2 filter -> I_t mask -> masked Adam in every step")
     return ap.parse_args()
@@ -210,7 +216,10 @@ def _config_dict_base(args, wl, ws):
                         f"({'random' if wl.shuffled else 'smooth'} order), J={wl.J} cameras/batch",
             "n_gaussians": wl.n_gaussians, "block_size": wl.block_size, "J": wl.J,
             "capacity_blocks_per_gpu": -(-wl.capacity // ws), "moments": args.moments,
-            "policy": "tide", "world_size": ws,
+            "policy": "restage-all (w/o Tide)" if getattr(args, "no_tide", False) else "tide",
+            "overlap": not getattr(args, "no_overlap", False),
+            "bound_refresh": bool(getattr(args, "refresh_bounds", False)),
+            "world_size": ws,
             "I_t": "Level-2 fine filter (f1)" if getattr(args, "fine_filter", False) else "all rows of R n K (mask NULL)",
             "l2": "inputs larger than L2 (Adam touches GBs per step)",
             "grads": "synthetic counter-hash gradients resident in the grad pool (renderer out of scope)",
@@ -265,7 +274,9 @@ def main():
     moments = T.COLD_RESTART if args.moments == "cold" else T.PERSIST
     t_setup = time.perf_counter()
     cfg = T.make_config(sc.N, sc.B, cap, moments=moments, world_size=shard_ws, rank=shard_rank,
-                        device=local)
+                        device=local, tide=0 if args.no_tide else 1,
+                        serialize=1 if args.no_overlap else 0,
+                        refresh_bounds=1 if args.refresh_bounds else 0)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
     table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream)

@@ -78,6 +78,8 @@ typedef struct {
                               writes them back straight from the slots instead  */
   int32_t refresh_bounds; /* NEXT f2 (R25): after each update grow r_k to hold every
                              Gaussian of the block; the cull of batch t+2 sees it  */
+  int32_t serialize;      /* ablation "w/o Overlap": activate returns
+                             after its gather and write-back, step_adam after Adam  */
 } tgs_config;
 
 /* Optional device allocator hooks (PyTorch's caching allocator from Python).

@@ -891,6 +891,10 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   c->parity = q;
   c->T = T + 1;
   c->can_step = true;
+  if (c->cfg.serialize) {  // ablation w/o Overlap: I/O completes before compute starts
+    st = sync_all(c);
+    if (st != TGS_OK) return st;
+  }
   if (out) {
     out->n_visible = h.nK;
     out->n_resident = h.nR;
@@ -943,6 +947,7 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
     CK(launch_refresh(c->d, nA, p, c->compute));
     c->tm.kernel_launches++;
   }
+  if (c->cfg.serialize) CK(cudaStreamSynchronize(c->compute));  // ablation w/o Overlap
   CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }

@@ -22,7 +22,7 @@ SEEDS = {"scene": 20150, "trajectory": 1, "shuffle": 7, "grads": 42, "mask": 43}
 
 
 class SceneParams(C.Structure):
-    _fields_ = [("n_gaussians", C.c_uint64), ("block_size", C.c_uint32), ("_pad", C.c_uint32),
+    _fields_ = [("n_gaussians", C.c_uint64), ("block_size", C.c_uint32), ("layout", C.c_uint32),
                 ("seed", C.c_uint64), ("side", C.c_double), ("lot", C.c_double),
                 ("footprint", C.c_double), ("hmin", C.c_double), ("hmax", C.c_double),
                 ("ground_h", C.c_double)]
@@ -101,9 +101,10 @@ class Scene:
 
     def __init__(self, n_gaussians: int, block_size: int = 4096, seed: int = SEEDS["scene"],
                  side: float = 2800.0, lot: float = 50.0, footprint: float = 30.0,
-                 hmin: float = 10.0, hmax: float = 100.0, ground_h: float = 0.5):
-        self.params = SceneParams(n_gaussians, block_size, 0, seed, side, lot, footprint, hmin,
-                                  hmax, ground_h)
+                 hmin: float = 10.0, hmax: float = 100.0, ground_h: float = 0.5,
+                 layout: int = 0):
+        self.params = SceneParams(n_gaussians, block_size, layout, seed, side, lot, footprint,
+                                  hmin, hmax, ground_h)
         self.handle = lib().wl_scene_create(C.byref(self.params))
         if not self.handle:
             raise ValueError("invalid scene parameters")
@@ -262,6 +263,9 @@ CONFIGS = {
     "300m": Workload("300m", 300_000_000, 4096, 2800.0, "aerial", 64, 6309, _AERIAL),
     "300m_random": Workload("300m_random", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
                             _AERIAL, True),
+    # ablation "w/o Morton": no spatial sort before blocking
+    "300m_nomorton": Workload("300m_nomorton", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
+                              _AERIAL, False, (("layout", 1),)),
 }
 
 

@@ -139,6 +139,18 @@ static float round_up_f(double v) {
 }
 
 void wl_bounds(const wl_scene* s, uint64_t k0, uint64_t k1, float* out) {
+  if (s->p.layout == 1) { /* unsorted: every block spans the city */
+    double half = 0.5 * s->p.side, hm = s->p.hmax;
+    double r = sqrt(2.0 * half * half + 0.25 * hm * hm) + 4.5 * s->sigma + 1e-3 * s->p.side;
+    for (uint64_t k = k0; k < k1; ++k) {
+      float* o = out + 4 * (k - k0);
+      o[0] = 0.0f;
+      o[1] = 0.0f;
+      o[2] = (float)(0.5 * hm);
+      o[3] = round_up_f(r);
+    }
+    return;
+  }
   for (uint64_t k = k0; k < k1; ++k) {
     int64_t ix, iy;
     double x0, y0, t, h;
@@ -175,6 +187,10 @@ void wl_block_theta(const wl_scene* s, uint64_t k, float* out) {
   for (uint32_t r = 0; r < rows; ++r) {
     uint64_t gid = k * (uint64_t)B + r;
     float* row = out + (size_t)r * WL_DIM;
+    if (s->p.layout == 1) { /* w/o Morton: the row lives in a random tile */
+      uint64_t kt = h3(seed, gid, 7) % s->K;
+      wl_block_tile(s, kt, &ix, &iy, &x0, &y0, &t, &h);
+    }
     row[0] = (float)(x0 + t * u01(h3(seed, gid, 1)));
     row[1] = (float)(y0 + t * u01(h3(seed, gid, 2)));
     row[2] = (float)(h * u01(h3(seed, gid, 3)));

@@ -31,7 +31,9 @@ extern "C" {
 typedef struct {
   uint64_t n_gaussians;   /* N >= 1 */
   uint32_t block_size;    /* B >= 4, B % 4 == 0 */
-  uint32_t _pad;
+  uint32_t layout;        /* 0: Morton-ordered tiles; 1: no spatial sort
+                             ("w/o Morton" ablation): every block's rows
+                             are scattered over the whole city */
   uint64_t seed;          /* scene seed (20150 in the bench) */
   double side;            /* city side length in metres */
   double lot;             /* lot pitch (50 m) */
