@@ -116,18 +116,18 @@ float exp_det(float x) {
   return p * two_k;
 }
 
-// Level-2 test of one Gaussian: the
-// sphere (mu_i, 3 * exp(max log-scale)) against each camera of the batch with
-// the Level-1 rule (cull iff d < -r on some plane, R2), visible if any camera
-// keeps it.
-bool gaussian_visible(const float* row, const std::vector<float>& planes) {
+// Level-2 test of one Gaussian (R24): the
+// sphere (mu_i, 3 * exp(max log-scale)) against the cameras whose Level-1 set
+// K^(j) holds its block -- camera j renders only its visible blocks -- with the
+// Level-1 rule (cull iff d < -r on some plane, R2); visible if one keeps it.
+bool gaussian_visible(const float* row, const std::vector<float>& planes,
+                      const std::vector<uint32_t>& cams) {
   float s = row[52];
   if (row[53] > s) s = row[53];
   if (row[54] > s) s = row[54];
   const float ext = 3.0f * exp_det(s);
   const float b[4] = {row[0], row[1], row[2], ext};
-  const size_t J = planes.size() / 24;
-  for (size_t j = 0; j < J; ++j)
+  for (uint32_t j : cams)
     if (sphere_visible(b, planes.data() + 24 * j)) return true;
   return false;
 }
@@ -578,8 +578,11 @@ int or_fine_filter(or_ctx* o, uint64_t kg, uint32_t* words) {
   if (!c.is_tracked((uint32_t)l)) return OR_EINVAL;
   const float* th = c.slot_data[c.slot_of[l]].data();
   const uint32_t nrows = c.rows((uint32_t)l);
+  std::vector<uint32_t> cams;  // cameras whose K^(j) holds block l
+  for (uint32_t j = 0; j < c.percam.size(); ++j)
+    if (contains(c.percam[j], (uint32_t)l)) cams.push_back(j);
   for (uint32_t r = 0; r < nrows; ++r)
-    if (gaussian_visible(th + (size_t)r * D, c.planes)) words[r / 32] |= 1u << (r % 32);
+    if (gaussian_visible(th + (size_t)r * D, c.planes, cams)) words[r / 32] |= 1u << (r % 32);
   return OR_OK;
 }
 

@@ -26,7 +26,10 @@ def _run(J=2, iters=5):
     for t in range(iters):
         planes = tr.batch_planes(t, J)
         o.activate(planes)
-        out.append((planes, o.list("A"), {int(k): o.fine_filter(int(k)) for k in o.list("A")}))
+        percam = [set(o.percam(j).tolist()) for j in range(J)]
+        cams = {int(k): [j for j in range(J) if int(k) in percam[j]] for k in o.list("A")}
+        out.append((planes, o.list("A"), {int(k): o.fine_filter(int(k)) for k in o.list("A")},
+                    cams))
     return cfg, sc, tr, o, out
 
 
@@ -34,11 +37,15 @@ def _bits(words, B):
     return np.unpackbits(words.view(np.uint8), bitorder="little")[:B].astype(bool)
 
 
-def _double_visible(rows, planes):
-    """Per-row sphere test in double with the true exp (brute force)."""
+def _double_visible(rows, planes, cams=None):
+    """Per-row sphere test in double with the true exp (brute force), against
+    the cameras `cams` (default: all)."""
     mu = rows[:, :3].astype(np.float64)
     ext = 3.0 * np.exp(rows[:, 52:55].astype(np.float64).max(1))
-    P = planes.astype(np.float64)
+    P = planes.astype(np.float64) if cams is None else planes[list(cams)].astype(np.float64)
+    if P.shape[0] == 0:
+        z = np.zeros(rows.shape[0], bool)
+        return z, z
     d = np.einsum("rk,jpk->rjp", mu, P[:, :, :3]) + P[None, :, :, 3]
     vis = ~(d < -ext[:, None, None]).any(2)
     band = (np.abs(d + ext[:, None, None]) <= 1e-4 * (1 + np.abs(mu).sum(1)[:, None, None] +
@@ -49,11 +56,11 @@ def _double_visible(rows, planes):
 def test_matches_double_brute_force_outside_rounding_band():
     cfg, sc, tr, o, out = _run()
     checked = 0
-    for planes, A, masks in out:
+    for planes, A, masks, cams in out:
         for k in A.tolist():
             rows = sc.block_theta(k)[: sc.rows(k)]
             got = _bits(masks[k], sc.B)[: sc.rows(k)]
-            ref, band = _double_visible(rows, planes)
+            ref, band = _double_visible(rows, planes, cams[k])
             bad = (got != ref) & ~band
             assert not bad.any(), (k, np.nonzero(bad)[0][:5])
             checked += rows.shape[0]
@@ -69,7 +76,7 @@ def test_centre_in_image_is_in_It_and_chain_is_conservative():
     cams_all = [tr.batch_cameras(t, 2) for t in range(3)]
     # K per batch from a bounds-only oracle for the chain check
     o2 = O.Oracle(O.make_config(sc.N, sc.B, 64), sc.bounds(), fill=None, track_all=False)
-    for t, ((planes, A, masks), cams) in enumerate(zip(out, cams_all)):
+    for t, ((planes, A, masks, _), cams) in enumerate(zip(out, cams_all)):
         o2.activate(planes)
         K = set(o2.list("K").tolist())
         for k in range(sc.K):
@@ -82,6 +89,10 @@ def test_centre_in_image_is_in_It_and_chain_is_conservative():
                 for r in range(0, rows.shape[0], 97):
                     if any(W.camera_sees(c, rows[r, :3].astype(np.float64)) for c in cams):
                         assert bits[r], (k, r)
+                # restricting camera j to its own K^(j) drops nothing (Level-1 is
+                # conservative per camera): the all-camera double test agrees
+                vis_all, band_all = _double_visible(rows, planes)
+                assert not ((vis_all != bits) & ~band_all).any(), k
 
 
 def test_outside_A_is_empty_and_far_behind_camera_is_culled():
