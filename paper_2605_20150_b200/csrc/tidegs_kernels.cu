@@ -592,19 +592,39 @@ __device__ __forceinline__ float exp_det(float x) {
 }
 
 // grid (ceil(B/256), nA): one thread per row of an A block.  The row's
-// extent sphere (mu, 3 exp(max log-scale)) against every camera of the batch
-// with the Level-1 rule; a ballot per 32
+// extent sphere (mu, 3 exp(max log-scale)) against every camera that sees the
+// block at Level 1, with the Level-1 rule; a ballot per 32
 // rows writes the I_t mask word of the slot.
 __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t J, int parity,
                                               uint32_t* __restrict__ mask) {
   __shared__ float4 pl[kMaxCams * 6];
-  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = d.last_planes[parity][i];
-  __syncthreads();
+  __shared__ uint32_t cams[kMaxCams];
+  __shared__ uint32_t wcount[8];
   const uint32_t i = blockIdx.y;
+  const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+  // cameras whose Level-1 set K^(j) holds block l (R24): camera j renders only
+  // its own visible blocks; compacted in camera order by warp ballots
+  const uint32_t j0 = threadIdx.x;  // blockDim 256 >= kMaxCams
+  const bool has = j0 < J && ((d.percam[(size_t)j0 * d.W + (l >> 5)] >> (l & 31)) & 1u);
+  const uint32_t bal = __ballot_sync(kFull, has);
+  if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
+  __syncthreads();
+  uint32_t base = 0, ncam = 0;
+  for (uint32_t w = 0; w < 8; ++w) {
+    if (w < (threadIdx.x >> 5)) base += wcount[w];
+    ncam += wcount[w];
+  }
+  if (has) {
+    const uint32_t pos = base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+    cams[pos] = j0;
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < ncam * 6; k += blockDim.x)
+    pl[k] = d.last_planes[parity][cams[k / 6] * 6 + k % 6];
+  __syncthreads();
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nw = (d.B + 31) / 32;
   if (r >= nw * 32) return;  // whole warps only
-  const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
   bool vis = false;
   if (r < block_rows(d, l)) {
     const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
@@ -613,7 +633,7 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t J, int parity,
     if (row[53] > sc) sc = row[53];
     if (row[54] > sc) sc = row[54];
     const float nr = -__fmul_rn(3.0f, exp_det(sc));
-    for (uint32_t j = 0; j < J && !vis; ++j) {
+    for (uint32_t j = 0; j < ncam && !vis; ++j) {
       bool in = true;
 #pragma unroll
       for (int p = 0; p < 6; ++p) {
