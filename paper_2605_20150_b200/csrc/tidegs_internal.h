@@ -57,7 +57,8 @@ struct Dev {
   uint8_t* evicted;      // [Kloc] evicted at least once (k_evict only; cold-restart count)
   int32_t* admit;        // [Kloc] activate index of last admission
   // bitsets over local blocks, [W] words each
-  uint32_t* percam;      // [J_max][W]
+  uint32_t* percam[2];   // [J_max][W] per-camera K^(j) (parity: k_fine of t reads it
+                         // while the plan of t+1 may already run)
   uint32_t *Kb, *cand, *Q, *Sp, *Sm, *Om, *Ab;
   uint32_t* R[2];        // R_t by parity
   // per slot

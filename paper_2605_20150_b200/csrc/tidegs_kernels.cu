@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256) k_cull(Dev d, uint32_t J, int32_t T, int 
       if (dist < nr) vis = false;  // cull iff d < -r_k (NaN stays visible)
     }
     const uint32_t bits = __ballot_sync(kFull, vis);
-    if (lane == 0 && w < d.W) d.percam[(size_t)j * d.W + w] = bits;  // tail warps own no word
+    if (lane == 0 && w < d.W) d.percam[parity][(size_t)j * d.W + w] = bits;  // tail warps own no word
     uni |= bits;
   }
   if (lane == 0 && w < d.W) {
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kQuotaNT) k_quota(Dev d, uint32_t J, int32_t T
   __shared__ uint32_t sh[40];
   if (d.cnt[CNT_CAND] <= d.C) return;  // #C_t <= C: nothing to select
   const uint32_t j = blockIdx.x;
-  const uint32_t* pc = d.percam + (size_t)j * d.W;
+  const uint32_t* pc = d.percam[parity] + (size_t)j * d.W;
   uint32_t mine = 0;
   for (uint32_t w = threadIdx.x; w < d.W; w += kQuotaNT) mine += __popc(pc[w]);
   const uint32_t nj = block_sum<kQuotaNT>(mine, sh);
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t J, int parity,
   // cameras whose Level-1 set K^(j) holds block l (R24): camera j renders only
   // its own visible blocks; compacted in camera order by warp ballots
   const uint32_t j0 = threadIdx.x;  // blockDim 256 >= kMaxCams
-  const bool has = j0 < J && ((d.percam[(size_t)j0 * d.W + (l >> 5)] >> (l & 31)) & 1u);
+  const bool has = j0 < J && ((d.percam[parity][(size_t)j0 * d.W + (l >> 5)] >> (l & 31)) & 1u);
   const uint32_t bal = __ballot_sync(kFull, has);
   if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
   __syncthreads();

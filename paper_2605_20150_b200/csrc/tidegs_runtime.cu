@@ -671,7 +671,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   d.ever = dalloc_t<uint8_t>(c, Kl, ok);
   d.evicted = dalloc_t<uint8_t>(c, Kl, ok);
   d.admit = dalloc_t<int32_t>(c, Kl, ok);
-  d.percam = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
+  d.percam[0] = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
+  d.percam[1] = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
   for (uint32_t** p : {&d.Kb, &d.cand, &d.Q, &d.Sp, &d.Sm, &d.Om, &d.Ab, &d.R[0], &d.R[1]})
     *p = dalloc_t<uint32_t>(c, Wd, ok);
   d.s2b = dalloc_t<int32_t>(c, P, ok);
@@ -735,7 +736,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * 2, s0));
   for (uint32_t* p : {d.Kb, d.cand, d.Q, d.Sp, d.Sm, d.Om, d.Ab, d.R[0], d.R[1]})
     CKI(cudaMemsetAsync(p, 0, sizeof(uint32_t) * Wd, s0));
-  CKI(cudaMemsetAsync(d.percam, 0, sizeof(uint32_t) * (size_t)d.J_max * Wd, s0));
+  for (int p = 0; p < 2; ++p)
+    CKI(cudaMemsetAsync(d.percam[p], 0, sizeof(uint32_t) * (size_t)d.J_max * Wd, s0));
   CKI(cudaMemsetAsync(d.s2b, 0xff, sizeof(int32_t) * P, s0));
   CKI(cudaMemsetAsync(d.occ, 0, sizeof(uint32_t) * d.PW, s0));
   CKI(cudaMemsetAsync(d.dirty, 0, sizeof(uint32_t) * d.PW, s0));
@@ -1090,7 +1092,7 @@ uint32_t tgs_get_percam(tgs_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap) 
   if (sync_all(c) != TGS_OK) return 0;
   Dev& d = c->d;
   std::vector<uint32_t> bits(std::max(d.W, 1u));
-  if (cudaMemcpy(bits.data(), d.percam + (size_t)j * d.W, sizeof(uint32_t) * d.W,
+  if (cudaMemcpy(bits.data(), d.percam[c->last_parity] + (size_t)j * d.W, sizeof(uint32_t) * d.W,
                  cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
   uint32_t n = 0;

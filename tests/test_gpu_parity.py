@@ -363,3 +363,54 @@ def test_edge_configs(N, B, C, J, kw):
     pr.compare_stats()
     assert pr.compare_blocks(range(sc.K)) == 0
     pr.close()
+
+
+@pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct"])
+def test_pipelined_run_matches_oracle(mode):
+    """The GPU runs ahead exactly as in bench.py -- no inspection call (hence no
+    host sync) between batches -- so every cross-batch hazard (plan of t+1 vs
+    Adam/filter/write-back of t) is exercised; the final state must still match
+    the oracle bit-exactly."""
+    import ctypes as C
+
+    import torch
+    from gpu_harness import GRAD_SEED, Synth, _cfn
+    cfg, sc, tr = tiny()
+    kw = {"plain": {}, "fine": {}, "fine_refresh_cold": {"refresh_bounds": 1,
+                                                          "moments": O.COLD_RESTART},
+          "mask_direct": {"staging_blocks": 1, "mask_p": 0.5}}[mode]
+    pr = _pair(sc, capacity=cfg.capacity, **kw)
+    if "refresh" in mode:
+        pr.lr[0:3] = 0.5
+    fine = mode.startswith("fine")
+    dmask = torch.zeros((pr.gpu.P, (sc.B + 31) // 32), dtype=torch.int32, device="cuda")
+    if pr.d_mask is not None:
+        dmask = pr.d_mask
+    n = 40
+    for t in range(n):  # GPU: back to back
+        planes = tr.batch_planes(t, cfg.J)
+        act = pr.gpu.activate(planes)
+        pr.grads_gpu_only(act, t)
+        if fine:
+            pr.gpu.fine_filter(dmask.data_ptr())
+        elif pr.msyn is not None:
+            W.synth_mask_cuda(dmask.data_ptr(), act, sc.B, sc.N, 43, t, pr.msyn.p32, pr.stream)
+        pr.gpu.step_adam(pr.lr, mask_ptr=dmask.data_ptr() if (fine or pr.msyn) else None)
+    g = (_cfn("wl_grad_cb"), C.addressof(pr.gsyn))
+    for t in range(n):  # oracle
+        assert pr.orc.activate(tr.batch_planes(t, cfg.J)) == O.OK
+        m = pr.orc.fine_filter_mask if fine else (
+            (_cfn("wl_mask_cb"), C.addressof(pr.msyn)) if pr.msyn is not None else None)
+        assert pr.orc.step_adam(pr.lr, grad=g, mask=m) == O.OK
+    pr.t = n
+    pr.compare_plan(cfg.J)
+    pr.compare_stats()
+    assert pr.compare_blocks(range(sc.K)) == 0
+    pr.gpu.flush()
+    pr.orc.flush()
+    pr.compare_stats()
+    if "refresh" in mode:
+        gb = np.stack([pr.gpu.bound(k) for k in range(sc.K)])
+        ob = np.stack([pr.orc.bound(k) for k in range(sc.K)])
+        np.testing.assert_array_equal(gb.view(np.uint32), ob.view(np.uint32))
+    pr.close()
