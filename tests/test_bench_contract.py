@@ -1,0 +1,44 @@
+"""bench.py keeps the driver's JSON contract: one JSON line with the required
+keys, on CPU for the reference arm (the oracle) and on a GPU for our arm."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+             "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+             "cpu_baseline"}
+
+
+def _run(args, timeout=600):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args,
+                       capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    d = _run(["--impl", "reference", "--config", "tiny", "--steps", "3", "--warmup", "3"])
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert "workload" in d["config"]
+
+
+@pytest.mark.gpu
+def test_our_arm_contract():
+    d = _run(["--config", "tiny", "--steps", "4", "--warmup", "3", "--cpu-sample-s", "1"])
+    assert BASE_KEYS | {"roofline", "clocks", "gpu_launches", "link_roofline"} <= set(d)
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["n_gpus"] == 1
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["peak"] > 0 and 0 < r["frac"] == pytest.approx(
+        r["achieved"] / r["peak"])
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["cpu_baseline"]["kind"] == "oracle"
