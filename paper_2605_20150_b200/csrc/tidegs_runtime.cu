@@ -27,6 +27,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <climits>
+#include <cstdint>
 #include <cstdlib>
 #include <condition_variable>
 #include <cstring>
@@ -92,6 +93,7 @@ struct tgs_ctx {
   std::string io_err;
   uint32_t last_ndirty = 0;
   std::mutex prof_mu;
+  size_t d2h_max_merge = SIZE_MAX;  // TGS_D2H_MERGE=<records> caps merged write-back copies
   // Adam LUT (bias corrections, R9)
   std::vector<float> lut_bc1_h, lut_ibs_h;
   float* lut_pinned = nullptr;     // [2][lut_cap]
@@ -304,9 +306,11 @@ struct CopyBatch {
   std::vector<void*> src;
   std::vector<size_t> size;
   uint64_t bytes = 0;
+  size_t max_merge = SIZE_MAX;  // largest merged copy (bytes)
   void add(void* d, const void* s, size_t n) {
     bytes += n;
-    if (!dst.empty() && (char*)dst.back() + size.back() == (char*)d &&
+    if (!dst.empty() && size.back() + n <= max_merge &&
+        (char*)dst.back() + size.back() == (char*)d &&
         (char*)src.back() + size.back() == (const char*)s) {
       size.back() += n;
       return;
@@ -401,6 +405,7 @@ void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
   const uint32_t* dl = c->dirty_map[p];
   const size_t w = (size_t)d.n_arr * c->rec_bytes;
   CopyBatch b;
+  b.max_merge = c->d2h_max_merge;
   for (uint32_t k = 0; k < nd; ++k) {
     float* h = host_rec(c, dl[2 * k]);
     const float* src = j.direct ? slot_rec(c, dl[2 * k + 1])
@@ -751,6 +756,8 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
 #undef CKI
   int dev = g.device;
   c->adam_grid = adam_grid(dev);
+  if (const char* m = getenv("TGS_D2H_MERGE"))
+    c->d2h_max_merge = (size_t)std::max(1, atoi(m)) * d.n_arr * c->rec_bytes;
   c->io = std::thread(io_main, c);
   *out = c;
   return TGS_OK;
