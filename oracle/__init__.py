@@ -79,6 +79,10 @@ def lib():
         L.or_step_count.argtypes = [vp, C.c_uint64]
         L.or_fine_filter.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint32)]
         L.or_get_bound.argtypes = [vp, C.c_uint64, C.POINTER(C.c_float)]
+        L.or_build_layout.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32,
+                                      C.POINTER(C.c_uint64), C.POINTER(C.c_float)]
+        L.or_morton3.restype = C.c_uint64
+        L.or_morton3.argtypes = [C.c_uint32] * 3
         L.or_exp_det.restype = C.c_float
         L.or_exp_det.argtypes = [C.c_float]
         _lib = L
@@ -238,6 +242,25 @@ class Oracle:
 
 def exp_det(x: float) -> float:
     return float(lib().or_exp_det(x))
+
+
+def morton3(x: int, y: int, z: int) -> int:
+    return int(lib().or_morton3(x, y, z))
+
+
+def build_layout(cs: np.ndarray, B: int):
+    """NEXT f2b: (perm, bounds) for Gaussians given as n x 4 (cx, cy, cz, max
+    log-scale) -- Morton sort + blocking."""
+    cs = np.ascontiguousarray(cs, np.float32)
+    n = cs.shape[0]
+    K = (n + B - 1) // B
+    perm = np.empty(n, np.uint64)
+    bounds = np.empty((K, 4), np.float32)
+    rc = lib().or_build_layout(_f(cs), n, B, perm.ctypes.data_as(C.POINTER(C.c_uint64)),
+                               _f(bounds))
+    if rc != OK:
+        raise OracleError(rc, "or_build_layout")
+    return perm, bounds
 
     @property
     def num_local_blocks(self) -> int:

@@ -559,6 +559,89 @@ uint32_t or_num_local_blocks(or_ctx* o) { return o->c.Kloc; }
 
 float or_exp_det(float x) { return exp_det(x); }
 
+// ---- NEXT f2b: Morton sort + blocking ("we Morton-sort
+// Gaussians by the codes of their centers before blocking", 375-376; SPEC.md:
+// 81-145, readings R26).  Step by step:
+//  1. quantisation box = AABB of all centres; per axis q = min(2^21-1,
+//     floor(((double)p - lo) * (2^21-1) / (hi - lo))) (0 if hi == lo)
+//  2. code = bit-interleave of q, x lowest (bit 3i = x_i, 3i+1 = y_i, 3i+2 = z_i)
+//  3. stable sort by code (ties keep the original index order)
+//  4. block k = sorted positions [kB, min(N, (k+1)B))
+//  5. c_k = centroid of its centres, summed in double in sorted order, rounded
+//     to fp32; r_k = max_i (|mu_i - c_k| in double + 3 * exp_det(max log-scale_i))
+//     rounded up to fp32 (conservative)
+uint64_t or_morton3(uint32_t x, uint32_t y, uint32_t z) {
+  uint64_t c = 0;
+  for (int b = 0; b < 21; ++b) {
+    c |= (uint64_t)((x >> b) & 1u) << (3 * b);
+    c |= (uint64_t)((y >> b) & 1u) << (3 * b + 1);
+    c |= (uint64_t)((z >> b) & 1u) << (3 * b + 2);
+  }
+  return c;
+}
+
+int or_build_layout(const float* cs /* n x 4 */, uint64_t n, uint32_t B, uint64_t* perm,
+                    float* bounds /* ceil(n/B) x 4 */) {
+  if (!cs || n == 0 || B == 0 || !perm || !bounds) return OR_EINVAL;
+  float lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) lo[a] = hi[a] = cs[a];
+  for (uint64_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      const float v = cs[4 * i + a];
+      if (!std::isfinite(v)) return OR_EINVAL;
+      if (v < lo[a]) lo[a] = v;
+      if (v > hi[a]) hi[a] = v;
+    }
+  const double qmax = 2097151.0;  // 2^21 - 1
+  double inv[3];
+  for (int a = 0; a < 3; ++a)
+    inv[a] = hi[a] > lo[a] ? qmax / ((double)hi[a] - (double)lo[a]) : 0.0;
+  std::vector<std::pair<uint64_t, uint64_t>> key(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t q[3];
+    for (int a = 0; a < 3; ++a) {
+      double t = std::floor(((double)cs[4 * i + a] - (double)lo[a]) * inv[a]);
+      if (t > qmax) t = qmax;
+      if (t < 0.0) t = 0.0;
+      q[a] = (uint32_t)t;
+    }
+    key[i] = {or_morton3(q[0], q[1], q[2]), i};
+  }
+  std::stable_sort(key.begin(), key.end(),
+                   [](const std::pair<uint64_t, uint64_t>& a,
+                      const std::pair<uint64_t, uint64_t>& b) { return a.first < b.first; });
+  for (uint64_t i = 0; i < n; ++i) perm[i] = key[i].second;
+  const uint64_t K = (n + B - 1) / B;
+  for (uint64_t k = 0; k < K; ++k) {
+    const uint64_t a0 = k * B, a1 = std::min<uint64_t>(n, a0 + B);
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    for (uint64_t p = a0; p < a1; ++p) {
+      const float* r = cs + 4 * perm[p];
+      sx += (double)r[0];
+      sy += (double)r[1];
+      sz += (double)r[2];
+    }
+    const double cnt = (double)(a1 - a0);
+    const float cx = (float)(sx / cnt), cy = (float)(sy / cnt), cz = (float)(sz / cnt);
+    double rad = 0.0;
+    for (uint64_t p = a0; p < a1; ++p) {
+      const float* r = cs + 4 * perm[p];
+      const double dx = (double)r[0] - (double)cx, dy = (double)r[1] - (double)cy,
+                   dz = (double)r[2] - (double)cz;
+      const double dist = std::sqrt(dx * dx + dy * dy + dz * dz);
+      const double e = dist + (double)(3.0f * exp_det(r[3]));
+      if (e > rad) rad = e;
+    }
+    float rf = (float)rad;
+    if ((double)rf < rad) rf = std::nextafterf(rf, INFINITY);
+    bounds[4 * k] = cx;
+    bounds[4 * k + 1] = cy;
+    bounds[4 * k + 2] = cz;
+    bounds[4 * k + 3] = rf;
+  }
+  return OR_OK;
+}
+
 int or_get_bound(or_ctx* o, uint64_t kg, float* out4) {
   Ctx& c = o->c;
   if (kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;

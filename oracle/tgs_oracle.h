@@ -89,6 +89,11 @@ int or_fine_filter(or_ctx* c, uint64_t k_global, uint32_t* words);
 void or_fine_filter_cb(void* ctx, uint64_t k_global, uint64_t t, uint32_t* words);
 /* current bound (cx, cy, cz, r) of a global block of this shard */
 int or_get_bound(or_ctx* c, uint64_t k_global, float* out4);
+/* NEXT f2b (R26): Morton sort + blocking of n Gaussians given as (cx, cy, cz,
+ * max log-scale) rows: perm[sorted position] = original index, bounds per
+ * block of B consecutive sorted Gaussians (centroid, conservative radius). */
+int or_build_layout(const float* cs, uint64_t n, uint32_t B, uint64_t* perm, float* bounds);
+uint64_t or_morton3(uint32_t x, uint32_t y, uint32_t z);
 /* the deterministic exp of R24 (exported for its pins) */
 float or_exp_det(float x);
 
