@@ -228,6 +228,22 @@ tgs_status tgs_read_bound(tgs_ctx* ctx, uint64_t k_global, float* out4);
 uint32_t tgs_num_local_blocks(const tgs_ctx* ctx);
 uint32_t tgs_pool_slots(const tgs_ctx* ctx);
 
+/* NEXT f2b -- Morton sort + blocking ("we Morton-sort
+ * Gaussians by the codes of their centers before blocking", 375-376; SPEC.md:
+ * 81-145; reading R26 in DESIGN.md §3).  cs: host [n][4] fp32 (cx, cy, cz,
+ * max log-scale) of n <= 2^32-1 Gaussians in any order.  On the GPU: AABB,
+ * 21-bit-per-axis quantisation in double, x-lowest bit interleave, stable radix
+ * sort of the 63-bit codes (ties keep index order), then per block of
+ * block_size consecutive sorted Gaussians: centroid (double, sorted order,
+ * rounded to fp32) and radius max(|mu - c| (double) + 3*exp(max log-scale))
+ * rounded up to fp32.  Outputs (host, caller-owned): perm[n] = original index
+ * of sorted position i; bounds[ceil(n/B)][4] -- the tgs_init_table bounds of
+ * the table whose row i is original row perm[i].  gpu_ms (may be NULL): device
+ * time of the sort and bounds.  EINVAL: n == 0 or > 2^32-1, B == 0,
+ * non-finite centre.  Stateless; allocates and frees its own device memory. */
+tgs_status tgs_build_layout(const float* cs, uint64_t n, uint32_t block_size, int device,
+                            uint64_t* perm, float* bounds, double* gpu_ms);
+
 /* Frustum planes of a pinhole camera (R1): w2c row-major 4x4 world->camera
  * (camera +z forward, +x right, +y down), intrinsics fx, fy, cx, cy, image
  * width x height, near/far.  Computed in double, rounded to fp32. */

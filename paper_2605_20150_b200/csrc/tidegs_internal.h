@@ -118,4 +118,20 @@ cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint3
 cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s);
 int adam_grid(int device);
 
+// NEXT f2b: Morton sort + blocking
+struct LayoutBufs {
+  float* cs;                      // [n][4] (cx, cy, cz, max log-scale)
+  unsigned long long* k[2];       // [n] codes (ping-pong)
+  uint32_t* v[2];                 // [n] indices (ping-pong)
+  uint32_t* counts;               // [layout_scan_len(n)]
+  uint32_t* sums;                 // [layout_nsums(n)]
+  float* part;                    // [part_grid][6]
+  float* bounds;                  // [K][4]
+};
+uint32_t layout_ntile(uint64_t n);
+uint64_t layout_scan_len(uint64_t n);
+uint32_t layout_nsums(uint64_t n);
+cudaError_t layout_run(const LayoutBufs& b, uint64_t n, uint32_t B, cudaStream_t s, int part_grid,
+                       int* perm_buf);
+
 }  // namespace tgs

@@ -19,7 +19,9 @@
 // only carry commutative effects (or/and on bitmaps, integer adds, min).
 // Floating point: IEEE RN intrinsics in the exact order DESIGN.md §3 (R2, R9)
 // fixes; compiled without fast-math, FTZ off.
+#include <cmath>
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "tidegs_internal.h"
@@ -875,6 +877,205 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   }
 }
 
+
+// ============================================================================
+// NEXT f2b: Morton sort + blocking (
+// reading R26).  Input: n Gaussians as (cx, cy, cz, max log-scale).
+// ============================================================================
+constexpr int kRsNT = 256, kRsItems = 16, kRsTile = kRsNT * kRsItems;
+
+__global__ void __launch_bounds__(256) k_lay_aabb(const float4* __restrict__ cs, uint64_t n,
+                                                  float* __restrict__ part) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float4 c = cs[i];
+    lo[0] = fminf(lo[0], c.x); lo[1] = fminf(lo[1], c.y); lo[2] = fminf(lo[2], c.z);
+    hi[0] = fmaxf(hi[0], c.x); hi[1] = fmaxf(hi[1], c.y); hi[2] = fmaxf(hi[2], c.z);
+  }
+  __shared__ float sh[6][256];
+  for (int a = 0; a < 3; ++a) {
+    sh[a][threadIdx.x] = lo[a];
+    sh[3 + a][threadIdx.x] = hi[a];
+  }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      for (int a = 0; a < 3; ++a) {
+        sh[a][threadIdx.x] = fminf(sh[a][threadIdx.x], sh[a][threadIdx.x + w]);
+        sh[3 + a][threadIdx.x] = fmaxf(sh[3 + a][threadIdx.x], sh[3 + a][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {  // 21 bits -> every third bit
+  uint64_t x = v & 0x1fffffu;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+// R26 quantisation: q = min(2^21-1, floor(((double)p - lo) * inv)), in double
+__device__ __forceinline__ uint32_t quant(float p, double lo, double inv) {
+  double t = floor(__dmul_rn(__dsub_rn((double)p, lo), inv));
+  t = t > 2097151.0 ? 2097151.0 : (t < 0.0 ? 0.0 : t);
+  return (uint32_t)t;
+}
+
+__global__ void __launch_bounds__(256) k_lay_codes(const float4* __restrict__ cs, uint64_t n,
+                                                   double lx, double ly, double lz, double ix,
+                                                   double iy, double iz,
+                                                   unsigned long long* __restrict__ keys,
+                                                   uint32_t* __restrict__ vals) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 c = cs[i];
+  keys[i] = spread3(quant(c.x, lx, ix)) | (spread3(quant(c.y, ly, iy)) << 1) |
+            (spread3(quant(c.z, lz, iz)) << 2);
+  vals[i] = (uint32_t)i;
+}
+
+// LSD radix sort pass, 8-bit digit: per-tile digit histogram (digit-major layout)
+__global__ void __launch_bounds__(kRsNT) k_rs_hist(const unsigned long long* __restrict__ keys,
+                                                   uint64_t n, int shift, uint32_t ntile,
+                                                   uint32_t* __restrict__ counts) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
+  for (int r = 0; r < kRsItems; ++r) {
+    const uint64_t i = base + (uint64_t)r * kRsNT + threadIdx.x;
+    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  counts[(size_t)threadIdx.x * ntile + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of m u32 values: per-CTA scan of kRsTile, block sums, fix-up
+__global__ void __launch_bounds__(kRsNT) k_scan_local(uint32_t* __restrict__ v, uint64_t m,
+                                                      uint32_t* __restrict__ sums) {
+  __shared__ uint32_t sh[40];
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile + (uint64_t)threadIdx.x * kRsItems;
+  uint32_t loc[kRsItems], acc = 0;
+#pragma unroll
+  for (int k = 0; k < kRsItems; ++k) {
+    const uint64_t i = base + k;
+    loc[k] = i < m ? v[i] : 0u;
+    const uint32_t x = loc[k];
+    loc[k] = acc;
+    acc += x;
+  }
+  uint32_t tot;
+  const uint32_t pre = block_scan<kRsNT>(acc, tot, sh);
+#pragma unroll
+  for (int k = 0; k < kRsItems; ++k)
+    if (base + k < m) v[base + k] = pre + loc[k];
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* __restrict__ sums, uint32_t m) {
+  __shared__ uint32_t sh[40];
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < m; b += 1024) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t x = i < m ? sums[i] : 0u;
+    uint32_t tot;
+    const uint32_t pre = block_scan<1024>(x, tot, sh);
+    if (i < m) sums[i] = carry + pre;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kRsNT) k_scan_add(uint32_t* __restrict__ v, uint64_t m,
+                                                    const uint32_t* __restrict__ sums) {
+  const uint32_t add = sums[blockIdx.x];
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
+  for (int k = 0; k < kRsItems; ++k) {
+    const uint64_t i = base + (uint64_t)k * kRsNT + threadIdx.x;
+    if (i < m) v[i] += add;
+  }
+}
+
+// stable scatter: items of a tile in index order; the rank among equal digits
+// comes from __match_any_sync within a warp, per-warp counts across warps and
+// a running count across the tile's rounds
+__global__ void __launch_bounds__(kRsNT) k_rs_scatter(
+    const unsigned long long* __restrict__ kin, const uint32_t* __restrict__ vin,
+    unsigned long long* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n, int shift,
+    uint32_t ntile, const uint32_t* __restrict__ offs) {
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wcnt[kRsNT / 32][256];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  run[threadIdx.x] = 0;
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
+  for (int r = 0; r < kRsItems; ++r) {
+    for (int w = 0; w < kRsNT / 32; ++w) wcnt[w][threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t i = base + (uint64_t)r * kRsNT + threadIdx.x;
+    const bool valid = i < n;
+    unsigned long long key = 0;
+    uint32_t val = 0, dig = 256 + lane;  // invalid lanes never match a real digit
+    if (valid) {
+      key = kin[i];
+      val = vin[i];
+      dig = (uint32_t)(key >> shift) & 255u;
+    }
+    const uint32_t peers = __match_any_sync(kFull, dig);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank == 0) wcnt[warp][dig] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      uint32_t pre = 0;
+      for (uint32_t w = 0; w < warp; ++w) pre += wcnt[w][dig];
+      const uint32_t pos = offs[(size_t)dig * ntile + blockIdx.x] + run[dig] + pre + rank;
+      kout[pos] = key;
+      vout[pos] = val;
+    }
+    __syncthreads();
+    uint32_t add = 0;
+    for (int w = 0; w < kRsNT / 32; ++w) add += wcnt[w][threadIdx.x];
+    run[threadIdx.x] += add;
+    __syncthreads();
+  }
+}
+
+// one thread per block: centroid (double, sorted order) and conservative radius
+__global__ void __launch_bounds__(128) k_lay_bounds(const float4* __restrict__ cs, uint64_t n,
+                                                    uint32_t B, const uint32_t* __restrict__ perm,
+                                                    float4* __restrict__ bounds, uint64_t K) {
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const uint64_t a0 = k * B, a1 = a0 + B < n ? a0 + B : n;
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  for (uint64_t p = a0; p < a1; ++p) {
+    const float4 c = cs[perm[p]];
+    sx = __dadd_rn(sx, (double)c.x);
+    sy = __dadd_rn(sy, (double)c.y);
+    sz = __dadd_rn(sz, (double)c.z);
+  }
+  const double cnt = (double)(a1 - a0);
+  const float cx = __double2float_rn(__ddiv_rn(sx, cnt)), cy = __double2float_rn(__ddiv_rn(sy, cnt)),
+              cz = __double2float_rn(__ddiv_rn(sz, cnt));
+  double rad = 0.0;
+  for (uint64_t p = a0; p < a1; ++p) {
+    const float4 c = cs[perm[p]];
+    const double dx = __dsub_rn((double)c.x, (double)cx), dy = __dsub_rn((double)c.y, (double)cy),
+                 dz = __dsub_rn((double)c.z, (double)cz);
+    const double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                             __dmul_rn(dz, dz)));
+    const double e = __dadd_rn(dist, (double)__fmul_rn(3.0f, exp_det(c.w)));
+    if (e > rad) rad = e;
+  }
+  float rf = __double2float_rn(rad);
+  if ((double)rf < rad) rf = nextafterf(rf, INFINITY);
+  bounds[k] = make_float4(cx, cy, cz, rf);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- launchers
@@ -953,6 +1154,54 @@ cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s
   if (nA == 0) return cudaSuccess;
   dim3 grid((d.B + 255) / 256, nA);
   k_refresh<<<grid, 256, 0, s>>>(d, parity);
+  return cudaGetLastError();
+}
+
+uint32_t layout_ntile(uint64_t n) { return (uint32_t)((n + kRsTile - 1) / kRsTile); }
+uint64_t layout_scan_len(uint64_t n) { return 256ull * layout_ntile(n); }
+uint32_t layout_nsums(uint64_t n) { return (uint32_t)((layout_scan_len(n) + kRsTile - 1) / kRsTile); }
+
+// The whole GPU part of tgs_build_layout: AABB (partials reduced on the host,
+// exact and order-free), codes, 8 stable 8-bit LSD radix passes over the
+// 63-bit codes (ties keep index order), per-block bounds.  *perm_buf returns
+// which of b.v[0], b.v[1] holds the sorted indices.
+cudaError_t layout_run(const LayoutBufs& b, uint64_t n, uint32_t B, cudaStream_t s,
+                       int part_grid, int* perm_buf) {
+  k_lay_aabb<<<part_grid, 256, 0, s>>>(reinterpret_cast<const float4*>(b.cs), n, b.part);
+  std::vector<float> part((size_t)part_grid * 6);
+  cudaError_t e = cudaMemcpyAsync(part.data(), b.part, sizeof(float) * part.size(),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int g = 0; g < part_grid; ++g)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::fmin(lo[a], part[6 * g + a]);
+      hi[a] = std::fmax(hi[a], part[6 * g + 3 + a]);
+    }
+  double inv[3];
+  for (int a = 0; a < 3; ++a)
+    inv[a] = hi[a] > lo[a] ? 2097151.0 / ((double)hi[a] - (double)lo[a]) : 0.0;
+  const unsigned gridn = (unsigned)((n + 255) / 256);
+  k_lay_codes<<<gridn, 256, 0, s>>>(reinterpret_cast<const float4*>(b.cs), n, lo[0], lo[1],
+                                    lo[2], inv[0], inv[1], inv[2], b.k[0], b.v[0]);
+  const uint32_t ntile = layout_ntile(n);
+  const uint64_t m = layout_scan_len(n);
+  const uint32_t nsums = layout_nsums(n);
+  int cur = 0;
+  for (int shift = 0; shift < 64; shift += 8) {
+    k_rs_hist<<<ntile, kRsNT, 0, s>>>(b.k[cur], n, shift, ntile, b.counts);
+    k_scan_local<<<nsums, kRsNT, 0, s>>>(b.counts, m, b.sums);
+    k_scan_sums<<<1, 1024, 0, s>>>(b.sums, nsums);
+    k_scan_add<<<nsums, kRsNT, 0, s>>>(b.counts, m, b.sums);
+    k_rs_scatter<<<ntile, kRsNT, 0, s>>>(b.k[cur], b.v[cur], b.k[cur ^ 1], b.v[cur ^ 1], n,
+                                         shift, ntile, b.counts);
+    cur ^= 1;
+  }
+  const uint64_t K = (n + B - 1) / B;
+  k_lay_bounds<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(
+      reinterpret_cast<const float4*>(b.cs), n, B, b.v[cur], reinterpret_cast<float4*>(b.bounds), K);
+  *perm_buf = cur;
   return cudaGetLastError();
 }
 

@@ -1197,6 +1197,78 @@ tgs_status tgs_read_bound(tgs_ctx* c, uint64_t kg, float* out4) {
 uint32_t tgs_num_local_blocks(const tgs_ctx* c) { return c ? c->d.Kloc : 0; }
 uint32_t tgs_pool_slots(const tgs_ctx* c) { return c ? c->d.P : 0; }
 
+tgs_status tgs_build_layout(const float* cs, uint64_t n, uint32_t block_size, int device,
+                            uint64_t* perm, float* bounds, double* gpu_ms) {
+  if (!cs || n == 0 || n > 0xffffffffull || block_size == 0 || !perm || !bounds)
+    return TGS_EINVAL;
+  for (uint64_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a)
+      if (!std::isfinite(cs[4 * i + a])) return TGS_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TGS_ECUDA;
+  const uint64_t K = (n + block_size - 1) / block_size;
+  const int part_grid = 592;
+  LayoutBufs b{};
+  std::vector<void*> allocs;
+  bool ok = true;
+  auto get = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) {
+      ok = false;
+      return nullptr;
+    }
+    allocs.push_back(p);
+    return p;
+  };
+  b.cs = (float*)get(n * 16);
+  b.k[0] = (unsigned long long*)get(n * 8);
+  b.k[1] = (unsigned long long*)get(n * 8);
+  b.v[0] = (uint32_t*)get(n * 4);
+  b.v[1] = (uint32_t*)get(n * 4);
+  b.counts = (uint32_t*)get(layout_scan_len(n) * 4);
+  b.sums = (uint32_t*)get((size_t)layout_nsums(n) * 4);
+  b.part = (float*)get((size_t)part_grid * 6 * 4);
+  b.bounds = (float*)get(K * 16);
+  auto release = [&]() {
+    for (void* p : allocs) cudaFree(p);
+    cudaGetLastError();
+  };
+  if (!ok) {
+    release();
+    return TGS_ENOMEM;
+  }
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  tgs_status st = TGS_OK;
+  int cur = 0;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess ||
+      cudaMemcpyAsync(b.cs, cs, n * 16, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaEventRecord(e0, s) != cudaSuccess ||
+      layout_run(b, n, block_size, s, part_grid, &cur) != cudaSuccess ||
+      cudaEventRecord(e1, s) != cudaSuccess) {
+    st = TGS_ECUDA;
+  }
+  std::vector<uint32_t> p32;
+  if (st == TGS_OK) {
+    p32.resize(n);
+    if (cudaMemcpyAsync(p32.data(), b.v[cur], n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(bounds, b.bounds, K * 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      st = TGS_ECUDA;
+  }
+  if (st == TGS_OK) {
+    for (uint64_t i = 0; i < n; ++i) perm[i] = p32[i];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (gpu_ms) *gpu_ms = ms;
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (s) cudaStreamDestroy(s);
+  release();
+  return st;
+}
+
 tgs_status tgs_frustum_planes(const double w2c[16], double fx, double fy, double cx, double cy,
                               uint32_t width, uint32_t height, double znear, double zfar,
                               tgs_camera* out) {

@@ -28,7 +28,7 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_get_stats", "tgs_get_stats_async", "tgs_get_timing", "tgs_set_profiling", "tgs_get_list",
            "tgs_get_percam", "tgs_get_evicted_dirty", "tgs_get_slot_map",
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
-           "tgs_pool_slots", "tgs_read_bound", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error")
+           "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error")
 
 
 class Config(C.Structure):
@@ -137,6 +137,9 @@ def lib():
         L.tgs_num_local_blocks.argtypes = [vp]
         L.tgs_pool_slots.restype = u32
         L.tgs_pool_slots.argtypes = [vp]
+        L.tgs_build_layout.argtypes = [C.POINTER(C.c_float), u64, u32, C.c_int,
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_float),
+                                       C.POINTER(C.c_double)]
         L.tgs_frustum_planes.argtypes = [C.POINTER(C.c_double)] + [C.c_double] * 4 + [
             u32, u32, C.c_double, C.c_double, C.POINTER(Camera)]
         L.tgs_status_string.restype = C.c_char_p
@@ -341,3 +344,20 @@ def frustum_planes(w2c, fx, fy, cx, cy, width, height, znear, zfar) -> np.ndarra
     if rc != OK:
         raise TgsError(rc, "tgs_frustum_planes")
     return np.array([[cam.plane[p][i] for i in range(4)] for p in range(6)], np.float32)
+
+
+def build_layout(cs: np.ndarray, block_size: int, device: int = 0):
+    """NEXT f2b on the GPU: (perm, bounds, gpu_ms) for n x 4 (cx, cy, cz, max
+    log-scale) -- Morton sort + blocking (tgs_build_layout)."""
+    cs = np.ascontiguousarray(cs, np.float32)
+    n = cs.shape[0]
+    K = (n + block_size - 1) // block_size
+    perm = np.empty(n, np.uint64)
+    bounds = np.empty((K, 4), np.float32)
+    ms = C.c_double(0.0)
+    rc = lib().tgs_build_layout(_fp(cs), n, block_size, device,
+                                perm.ctypes.data_as(C.POINTER(C.c_uint64)), _fp(bounds),
+                                C.byref(ms))
+    if rc != OK:
+        raise TgsError(rc, "tgs_build_layout")
+    return perm, bounds, ms.value
