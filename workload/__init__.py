@@ -65,6 +65,7 @@ def lib():
         L.wl_bounds.argtypes = [vp, u64, u64, f32p]
         L.wl_block_theta.argtypes = [vp, u64, f32p]
         L.wl_table.argtypes = [vp, f32p, C.c_int]
+        L.wl_table_cs.argtypes = [vp, f32p, C.c_int]
         L.wl_block_tile.argtypes = [vp, u64] + [C.POINTER(C.c_int64)] * 2 + [C.POINTER(C.c_double)] * 4
         L.wl_camera_look.argtypes = [C.POINTER(Camera)] + [C.c_double * 3] * 3 + [
             C.c_double, u32, u32, C.c_double, C.c_double]
@@ -137,6 +138,12 @@ class Scene:
     def table(self, nthreads: int | None = None) -> np.ndarray:
         out = np.empty((self.K * self.B, DIM), np.float32)
         lib().wl_table(self.handle, fptr(out), nthreads or os.cpu_count() or 1)
+        return out
+
+    def table_cs(self, nthreads: int | None = None) -> np.ndarray:
+        """[N][4] (cx, cy, cz, max log-scale) of every Gaussian, block order."""
+        out = np.empty((self.N, 4), np.float32)
+        lib().wl_table_cs(self.handle, fptr(out), nthreads or os.cpu_count() or 1)
         return out
 
     def tile(self, k: int):

@@ -215,6 +215,60 @@ void wl_block_theta(const wl_scene* s, uint64_t k, float* out) {
   }
 }
 
+/* (cx, cy, cz, max log-scale) of every logical row of block k: the same values
+   wl_block_theta produces for attrs 0..2 and max(52..54), without the rest */
+void wl_block_cs(const wl_scene* s, uint64_t k, float* out) {
+  const uint32_t B = s->p.block_size;
+  const uint32_t rows = wl_block_rows(s, k);
+  int64_t ix, iy;
+  double x0, y0, t, h;
+  wl_block_tile(s, k, &ix, &iy, &x0, &y0, &t, &h);
+  const uint64_t seed = s->p.seed;
+  const double sig = s->sigma;
+  for (uint32_t r = 0; r < rows; ++r) {
+    uint64_t gid = k * (uint64_t)B + r;
+    float* o = out + 4 * (size_t)r;
+    if (s->p.layout == 1) {
+      uint64_t kt = h3(seed, gid, 7) % s->K;
+      wl_block_tile(s, kt, &ix, &iy, &x0, &y0, &t, &h);
+    }
+    o[0] = (float)(x0 + t * u01(h3(seed, gid, 1)));
+    o[1] = (float)(y0 + t * u01(h3(seed, gid, 2)));
+    o[2] = (float)(h * u01(h3(seed, gid, 3)));
+    float a = (float)log(sig * (0.5 + u01(h3(seed, gid, 80))));
+    float b = (float)log(sig * (0.5 + u01(h3(seed, gid, 81))));
+    float c = (float)log(0.1 * sig);
+    float m = a;
+    if (b > m) m = b;
+    if (c > m) m = c;
+    o[3] = m;
+  }
+}
+
+typedef struct { const wl_scene* s; float* out; uint64_t k0, k1; } cs_job;
+static void* cs_worker(void* arg) {
+  cs_job* j = (cs_job*)arg;
+  for (uint64_t k = j->k0; k < j->k1; ++k)
+    wl_block_cs(j->s, k, j->out + 4 * (size_t)k * j->s->p.block_size);
+  return NULL;
+}
+
+/* all N rows as [N][4] (rows in block order, padding excluded) */
+void wl_table_cs(const wl_scene* s, float* out, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  cs_job jobs[256];
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i].s = s;
+    jobs[i].out = out;
+    jobs[i].k0 = s->K * (uint64_t)i / (uint64_t)nthreads;
+    jobs[i].k1 = s->K * (uint64_t)(i + 1) / (uint64_t)nthreads;
+    pthread_create(&th[i], NULL, cs_worker, &jobs[i]);
+  }
+  for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+}
+
 void wl_block_theta_cb(void* scene, uint64_t k, float* out) {
   wl_block_theta((const wl_scene*)scene, k, out);
 }

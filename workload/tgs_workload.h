@@ -56,6 +56,9 @@ double    wl_sigma(const wl_scene* s);                  /* mean Gaussian spacing
 void      wl_bounds(const wl_scene* s, uint64_t k0, uint64_t k1, float* out);
 /* Theta rows of one global block: B x 59 fp32, rows >= rows(k) zero */
 void      wl_block_theta(const wl_scene* s, uint64_t k, float* out);
+/* (cx, cy, cz, max log-scale) of block k's rows / of all N rows [N][4] */
+void      wl_block_cs(const wl_scene* s, uint64_t k, float* out);
+void      wl_table_cs(const wl_scene* s, float* out, int nthreads);
 /* callback form for the oracle's lazily materialised host tier */
 void      wl_block_theta_cb(void* scene, uint64_t k, float* out);
 /* the whole table [K*B][59] (padding rows zero), nthreads workers */
