@@ -368,15 +368,20 @@ def main():
         torch.cuda.synchronize()
         table.stats_async(res[0].data_ptr())
         torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        e0.record(stream)
         for i in range(n_e):
             act = table.activate(host_planes[i].numpy())
             if fmask is not None:
                 table.fine_filter(fmask.data_ptr())
             table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
             table.stats_async(res[i + 1].data_ptr())
+        e1.record(stream)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        dev_s = e0.elapsed_time(e1) / 1e3
         fi = {n: j for j, n in enumerate(T.STAT_FIELDS)}
         d_rows = int(res[n_e, fi["n_active_rows"]] - res[0, fi["n_active_rows"]])
         d_h2d = int(res[n_e, fi["h2d_bytes"]] - res[0, fi["h2d_bytes"]])
@@ -385,6 +390,7 @@ def main():
                "h2d_bytes_per_step": int((d_h2d + n_e * J * 96) / n_e),
                "d2h_bytes_per_step": int((d_d2h + n_e * nf * 8) / n_e),
                "ms_per_step": 1e3 * dt / n_e,
+               "device_value_same_steps": d_rows / dev_s,
                "how": "wall clock over %d steps: pinned host planes in, per-step async stats "
                       "readback to pinned host memory, one sync at the end" % n_e}
 
