@@ -279,7 +279,12 @@ def main():
                         refresh_bounds=1 if args.refresh_bounds else 0)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
-    table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream)
+    build_ms = None
+    if wl.build:  # f2b: Morton-sort + block the unsorted scene on the GPU
+        perm, bounds, build_ms = T.build_layout(sc.table_cs(), sc.B, local)
+        table = T.Table(cfg, bounds, fill=sc.perm_fill(perm), stream=stream.cuda_stream)
+    else:
+        table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream)
     setup_s = time.perf_counter() - t_setup
     # synthetic gradients for every slot, written once (renderer out of scope)
     P_ = table.P
@@ -444,7 +449,7 @@ def main():
                            "h2d_ms_per_step": tm["h2d_ms"] / args.steps,
                            "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
                            "copy_calls_per_step": tm["copy_calls"] / args.steps,
-                           "setup_s": setup_s}}
+                           "setup_s": setup_s, "layout_build_gpu_ms": build_ms}}
         print(json.dumps(line), flush=True)
     table.close()
     if ws > 1:

@@ -30,7 +30,8 @@ class Pair:
 
     def __init__(self, scene, *, capacity, pool_slots=0, max_cameras=256, max_age=255,
                  quota=(1, 2), lam=0.7, gamma=0.9, moments=O.PERSIST, tide=1, world_size=1,
-                 rank=0, track_all=True, mask_p=None, staging_blocks=0, refresh_bounds=0):
+                 rank=0, track_all=True, mask_p=None, staging_blocks=0, refresh_bounds=0,
+                 bounds=None, fill=None):
         import torch
         from paper_2605_20150_b200 import tidegs as T
 
@@ -40,12 +41,13 @@ class Pair:
         kw = dict(pool_slots=pool_slots, max_cameras=max_cameras, max_age=max_age, quota=quota,
                   lam=lam, gamma=gamma, moments=moments, tide=tide, world_size=world_size,
                   rank=rank)
-        bounds = scene.bounds()
+        bounds = scene.bounds() if bounds is None else bounds
+        fill = scene.fill_fn if fill is None else fill
         self.gpu = T.Table(T.make_config(scene.N, scene.B, capacity, staging_blocks=staging_blocks,
                                          refresh_bounds=refresh_bounds, **kw), bounds,
-                           fill=scene.fill_fn)
+                           fill=fill)
         self.orc = O.Oracle(O.make_config(scene.N, scene.B, capacity, refresh_bounds=refresh_bounds,
-                                          **kw), bounds, fill=scene.fill_fn, track_all=track_all)
+                                          **kw), bounds, fill=fill, track_all=track_all)
         self.gsyn = Synth(GRAD_SEED, scene.N, scene.B, 0)
         self.mask_p = mask_p
         self.msyn = None

@@ -47,3 +47,31 @@ def test_degenerate_axis_and_extremes():
     cs[:, 0] = rng.uniform(-1e6, 1e6, n)      # z = y = 0: zero-extent axes (inv = 0)
     cs[:, 3] = rng.uniform(-80, 5, n)
     _check(cs, 64)
+
+
+def test_unsorted_scene_built_then_trained():
+    """The whole pipeline on an unsorted scene: GPU Morton build (f2b) -> table
+    re-blocked by its permutation -> working-set steps, bit-exact with the
+    oracle driven by its own build of the same scene."""
+    from gpu_harness import Pair
+    from paper_2605_20150_b200 import tidegs as T
+    sc = W.Scene(100_000, 1568, side=80.0, lot=20.0, footprint=12.0, hmin=2.0, hmax=12.0,
+                 layout=1)
+    cs = sc.table_cs()
+    p_gpu, b_gpu, _ = T.build_layout(cs, sc.B)
+    p_ref, b_ref = O.build_layout(cs, sc.B)
+    np.testing.assert_array_equal(p_gpu, p_ref)
+    tr = W.Trajectory(sc, "orbit", n_views=16, altitude=40.0, fovx_deg=25.0, znear=0.05,
+                      zfar=1.8, radius_scale=1.0)
+    pr = Pair(sc, capacity=24, bounds=b_gpu, fill=sc.perm_fill(p_gpu))
+    ks = []
+    for t in range(16):
+        act = pr.activate(tr.batch_planes(t, 2))
+        pr.t = t
+        pr.compare_plan(2)
+        ks.append(act.n_visible)
+        assert pr.step(act, t) == O.OK
+    assert max(ks) < sc.K  # re-blocked bounds cull again
+    pr.compare_stats()
+    assert pr.compare_blocks(range(sc.K)) == 0
+    pr.close()

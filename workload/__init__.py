@@ -28,6 +28,10 @@ class SceneParams(C.Structure):
                 ("ground_h", C.c_double)]
 
 
+class _PermFill(C.Structure):
+    _fields_ = [("scene", C.c_void_p), ("perm", C.c_void_p), ("n", C.c_uint64)]
+
+
 class Camera(C.Structure):
     _fields_ = [("pos", C.c_double * 3), ("fwd", C.c_double * 3), ("right", C.c_double * 3),
                 ("down", C.c_double * 3), ("fx", C.c_double), ("fy", C.c_double),
@@ -153,6 +157,14 @@ class Scene:
                             C.byref(t), C.byref(h))
         return ix.value, iy.value, x0.value, y0.value, t.value, h.value
 
+    def perm_fill(self, perm: np.ndarray):
+        """(C fn, user) filling block k of the table re-blocked by `perm` (row i
+        of the new table = generator row perm[i]); keeps its buffers alive."""
+        perm = np.ascontiguousarray(perm, np.uint64)
+        st = _PermFill(C.c_void_p(self.handle), perm.ctypes.data, len(perm))
+        self._perm_keep = (perm, st)
+        return C.cast(lib().wl_perm_fill_cb, C.c_void_p).value, C.addressof(st)
+
     @property
     def fill_fn(self):
         """(C function pointer, user pointer) for the oracle's lazy host tier."""
@@ -241,6 +253,7 @@ class Workload:
     traj_kw: tuple = ()
     shuffled: bool = False
     scene_kw: tuple = ()
+    build: bool = False      # NEXT f2b: Morton-build the (unsorted) table at setup
 
     def scene(self) -> Scene:
         return Scene(self.n_gaussians, self.block_size, side=self.side, **dict(self.scene_kw))
@@ -273,6 +286,9 @@ CONFIGS = {
     # ablation "w/o Morton": no spatial sort before blocking
     "300m_nomorton": Workload("300m_nomorton", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
                               _AERIAL, False, (("layout", 1),)),
+    # the same unsorted scene, Morton-sorted and blocked on the GPU at setup (f2b)
+    "300m_built": Workload("300m_built", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
+                           _AERIAL, False, (("layout", 1),), True),
 }
 
 

@@ -175,43 +175,55 @@ void wl_bounds(const wl_scene* s, uint64_t k0, uint64_t k1, float* out) {
   }
 }
 
+/* one row (gid = k*B + r) of the table; layout 1 places it in a random tile */
+void wl_row_theta(const wl_scene* s, uint64_t gid, float* row) {
+  const uint32_t B = s->p.block_size;
+  int64_t ix, iy;
+  double x0, y0, t, h;
+  wl_block_tile(s, s->p.layout == 1 ? h3(s->p.seed, gid, 7) % s->K : gid / B, &ix, &iy, &x0,
+                &y0, &t, &h);
+  const uint64_t seed = s->p.seed;
+  const double sig = s->sigma;
+  row[0] = (float)(x0 + t * u01(h3(seed, gid, 1)));
+  row[1] = (float)(y0 + t * u01(h3(seed, gid, 2)));
+  row[2] = (float)(h * u01(h3(seed, gid, 3)));
+  for (int a = 0; a < 3; ++a) row[3 + a] = (float)(0.3 * nrm(seed, gid, 10 + a));
+  for (int a = 0; a < 45; ++a) row[6 + a] = (float)(0.02 * nrm(seed, gid, 20 + a));
+  row[51] = (float)(1.5 * nrm(seed, gid, 70));
+  row[52] = (float)log(sig * (0.5 + u01(h3(seed, gid, 80))));
+  row[53] = (float)log(sig * (0.5 + u01(h3(seed, gid, 81))));
+  row[54] = (float)log(0.1 * sig);
+  double q[4], n2 = 0.0;
+  for (int a = 0; a < 4; ++a) {
+    q[a] = nrm(seed, gid, 90 + a);
+    n2 += q[a] * q[a];
+  }
+  if (n2 < 1e-12) {
+    q[0] = 1.0;
+    q[1] = q[2] = q[3] = 0.0;
+    n2 = 1.0;
+  }
+  double inv = 1.0 / sqrt(n2);
+  for (int a = 0; a < 4; ++a) row[55 + a] = (float)(q[a] * inv);
+}
+
 void wl_block_theta(const wl_scene* s, uint64_t k, float* out) {
   const uint32_t B = s->p.block_size;
   const uint32_t rows = wl_block_rows(s, k);
   memset(out, 0, sizeof(float) * (size_t)B * WL_DIM);
-  int64_t ix, iy;
-  double x0, y0, t, h;
-  wl_block_tile(s, k, &ix, &iy, &x0, &y0, &t, &h);
-  const uint64_t seed = s->p.seed;
-  const double sig = s->sigma;
-  for (uint32_t r = 0; r < rows; ++r) {
-    uint64_t gid = k * (uint64_t)B + r;
-    float* row = out + (size_t)r * WL_DIM;
-    if (s->p.layout == 1) { /* w/o Morton: the row lives in a random tile */
-      uint64_t kt = h3(seed, gid, 7) % s->K;
-      wl_block_tile(s, kt, &ix, &iy, &x0, &y0, &t, &h);
-    }
-    row[0] = (float)(x0 + t * u01(h3(seed, gid, 1)));
-    row[1] = (float)(y0 + t * u01(h3(seed, gid, 2)));
-    row[2] = (float)(h * u01(h3(seed, gid, 3)));
-    for (int a = 0; a < 3; ++a) row[3 + a] = (float)(0.3 * nrm(seed, gid, 10 + a));
-    for (int a = 0; a < 45; ++a) row[6 + a] = (float)(0.02 * nrm(seed, gid, 20 + a));
-    row[51] = (float)(1.5 * nrm(seed, gid, 70));
-    row[52] = (float)log(sig * (0.5 + u01(h3(seed, gid, 80))));
-    row[53] = (float)log(sig * (0.5 + u01(h3(seed, gid, 81))));
-    row[54] = (float)log(0.1 * sig);
-    double q[4], n2 = 0.0;
-    for (int a = 0; a < 4; ++a) {
-      q[a] = nrm(seed, gid, 90 + a);
-      n2 += q[a] * q[a];
-    }
-    if (n2 < 1e-12) {
-      q[0] = 1.0;
-      q[1] = q[2] = q[3] = 0.0;
-      n2 = 1.0;
-    }
-    double inv = 1.0 / sqrt(n2);
-    for (int a = 0; a < 4; ++a) row[55 + a] = (float)(q[a] * inv);
+  for (uint32_t r = 0; r < rows; ++r) wl_row_theta(s, k * (uint64_t)B + r, out + (size_t)r * WL_DIM);
+}
+
+/* block k of the table whose row i is the generator's row perm[i] (a Morton
+   layout built by tgs_build_layout / or_build_layout over an unsorted scene) */
+void wl_perm_fill_cb(void* user, uint64_t k, float* out) {
+  const wl_perm_fill* f = (const wl_perm_fill*)user;
+  const uint32_t B = f->scene->p.block_size;
+  memset(out, 0, sizeof(float) * (size_t)B * WL_DIM);
+  for (uint32_t r = 0; r < B; ++r) {
+    const uint64_t p = k * (uint64_t)B + r;
+    if (p >= f->n) break;
+    wl_row_theta(f->scene, f->perm[p], out + (size_t)r * WL_DIM);
   }
 }
 

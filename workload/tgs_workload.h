@@ -59,6 +59,11 @@ void      wl_block_theta(const wl_scene* s, uint64_t k, float* out);
 /* (cx, cy, cz, max log-scale) of block k's rows / of all N rows [N][4] */
 void      wl_block_cs(const wl_scene* s, uint64_t k, float* out);
 void      wl_table_cs(const wl_scene* s, float* out, int nthreads);
+/* one generator row by its global row id */
+void      wl_row_theta(const wl_scene* s, uint64_t gid, float* row);
+/* fill callback of a permuted (re-blocked) table: block k = rows perm[kB ..] */
+typedef struct { const wl_scene* scene; const uint64_t* perm; uint64_t n; } wl_perm_fill;
+void      wl_perm_fill_cb(void* user, uint64_t k, float* out);
 /* callback form for the oracle's lazily materialised host tier */
 void      wl_block_theta_cb(void* scene, uint64_t k, float* out);
 /* the whole table [K*B][59] (padding rows zero), nthreads workers */
