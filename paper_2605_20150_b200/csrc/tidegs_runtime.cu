@@ -332,7 +332,10 @@ tgs_status submit(tgs_ctx* c, CopyBatch& b, cudaStream_t s) {
     CK(cudaMemcpyBatchAsync(b.dst.data(), b.src.data(), b.size.data(), b.dst.size(), &at, &aidx,
                             1, &fail, s));
   }
-  c->tm.copy_calls += b.dst.size();
+  {
+    std::lock_guard<std::mutex> g(c->mu);  // the I/O thread counts its copies too
+    c->tm.copy_calls += b.dst.size();
+  }
   return TGS_OK;
 }
 
