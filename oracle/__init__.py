@@ -16,6 +16,8 @@ DIM = 59
 OK, EINVAL, ESTATE, ENONFINITE = 0, 1, 2, 6
 PERSIST, COLD_RESTART = 0, 1
 LISTS = {"K": 0, "R": 1, "S+": 2, "S-": 3, "Omega": 4, "A": 5}
+STORE_STATS = ("hits", "misses", "evictions", "dirty_evictions", "flush_appends", "read_bytes",
+               "write_bytes", "segments", "cached", "cached_dirty")
 
 
 class Config(C.Structure):
@@ -85,6 +87,11 @@ def lib():
         L.or_morton3.argtypes = [C.c_uint32] * 3
         L.or_exp_det.restype = C.c_float
         L.or_exp_det.argtypes = [C.c_float]
+        L.or_store_open.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
+        L.or_store_index.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.or_store_stats.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.or_store_lru.restype = C.c_uint32
+        L.or_store_lru.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), C.c_uint32]
         _lib = L
     return _lib
 
@@ -235,6 +242,42 @@ class Oracle:
         return out
 
     @property
+    def num_local_blocks(self) -> int:
+        return int(lib().or_num_local_blocks(self.h))
+
+    # ---- NEXT f3: CPU cache + log-structured store (R27, R28)
+    def store_open(self, dir, cache_blocks, segment_bytes=0):
+        """dir=None: metadata only (Index, LRU, counters)."""
+        d = None if dir is None else os.fsencode(str(dir))
+        rc = lib().or_store_open(self.h, d, cache_blocks, segment_bytes)
+        if rc != OK:
+            raise OracleError(rc, "or_store_open")
+
+    def store_index(self, k):
+        """Index[k] = (file_id, offset, size, version) (PAPER.md:233)."""
+        out = (C.c_uint64 * 4)()
+        rc = lib().or_store_index(self.h, k, out)
+        if rc != OK:
+            raise OracleError(rc, "or_store_index")
+        return tuple(int(x) for x in out)
+
+    def store_stats(self) -> dict:
+        out = (C.c_uint64 * 10)()
+        rc = lib().or_store_stats(self.h, out)
+        if rc != OK:
+            raise OracleError(rc, "or_store_stats")
+        return dict(zip(STORE_STATS, (int(x) for x in out)))
+
+    def store_lru(self):
+        """cached global ids, least recently used first, and their dirty flags"""
+        n = lib().or_store_lru(self.h, None, None, 0)
+        b = np.empty(n, np.uint32)
+        d = np.empty(n, np.uint8)
+        lib().or_store_lru(self.h, b.ctypes.data_as(C.POINTER(C.c_uint32)),
+                           d.ctypes.data_as(C.POINTER(C.c_uint8)), n)
+        return b, d.astype(bool)
+
+    @property
     def fine_filter_mask(self):
         """(C fn, user) mask callback: step_adam with I_t from the fine filter."""
         return C.cast(lib().or_fine_filter_cb, C.c_void_p).value, self.h.value
@@ -262,6 +305,3 @@ def build_layout(cs: np.ndarray, B: int):
         raise OracleError(rc, "or_build_layout")
     return perm, bounds
 
-    @property
-    def num_local_blocks(self) -> int:
-        return int(lib().or_num_local_blocks(self.h))

@@ -7,7 +7,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <limits>
 #include <map>
 #include <set>
@@ -17,6 +19,37 @@
 namespace {
 
 constexpr uint32_t D = 59;  // PAPER.md:101-103 "D = 59"
+
+
+// ---- NEXT f3: the tier below the host (§3.4), readings
+// R27 (cache events) and R28 (segment format) of DESIGN.md §3.
+struct IndexEntry {     // PAPER.md:233 "Index[k] = (file_id, offset, size, version)"
+  uint32_t file_id = 0;  // 0 = base segment
+  uint64_t offset = 0;   // byte offset of the payload in that file
+  uint64_t size = 0;     // payload bytes (n_arr * B * 59 * 4)
+  uint64_t version = 0;  // 0 = base, +1 per appended version
+};
+struct CacheEntry {     // PAPER.md:239-240 "an LRU cache over blocks together with a per-block dirty bit"
+  std::vector<float> payload;  // theta | m | v (persist) or theta; empty in metadata-only mode
+  bool dirty = false;
+  uint64_t stamp = 0;          // LRU clock of the last access
+};
+struct Store {
+  bool on = false;
+  bool data = false;           // files written / read (needs every block tracked)
+  std::string dir;
+  uint32_t H = 0;              // cache capacity in block records
+  uint64_t seg_budget = 0;     // patch segment rollover budget (bytes)
+  uint64_t S = 0;              // payload bytes padded to 4096 (record slot)
+  uint64_t payload = 0;        // n_arr * rec_bytes
+  std::vector<IndexEntry> index;   // per local block
+  std::map<uint32_t, CacheEntry> cache;
+  uint64_t clock = 0;
+  uint32_t cur_file = 0;       // 0 = no patch segment open yet
+  uint64_t cur_size = 0;       // bytes in the current patch segment
+  uint64_t hits = 0, misses = 0, evictions = 0, dirty_evictions = 0, flush_appends = 0,
+           read_bytes = 0, write_bytes = 0, segments = 0;
+};
 
 struct Ctx {
   or_config cfg{};
@@ -56,6 +89,7 @@ struct Ctx {
   bool can_step = false;  // one step_adam per activate
   uint64_t nonfinite = std::numeric_limits<uint64_t>::max();
   or_stats st{};
+  Store sto;
 
   uint64_t gid_block(uint32_t l) const { return (uint64_t)l * cfg.world_size + cfg.rank; }
   uint32_t rows(uint32_t l) const {
@@ -172,6 +206,146 @@ bool contains(const std::vector<uint32_t>& s, uint32_t x) {
   return std::binary_search(s.begin(), s.end(), x);
 }
 
+
+// ---- NEXT f3 store tier helpers (R28 format: little-endian, every header a
+// 4096-byte page so payloads start page-aligned -- PAPER.md:187-188 "236
+// contiguous 4 KB pages ... aligns the dominant block records with common
+// filesystem/page-cache granularities").
+constexpr uint64_t kPage = 4096;
+uint64_t pad_page(uint64_t x) { return (x + kPage - 1) / kPage * kPage; }
+
+void put32(unsigned char* p, uint32_t v) {
+  for (int i = 0; i < 4; ++i) p[i] = (unsigned char)(v >> (8 * i));
+}
+void put64(unsigned char* p, uint64_t v) {
+  for (int i = 0; i < 8; ++i) p[i] = (unsigned char)(v >> (8 * i));
+}
+
+std::string seg_path(const Store& s, uint32_t fid) {
+  char b[64];
+  if (fid == 0)
+    std::snprintf(b, sizeof b, "/base.tdgs");
+  else
+    std::snprintf(b, sizeof b, "/patch-%06u.tdgp", fid);
+  return s.dir + b;
+}
+
+// segment header page: magic, format 1, file id, n_arr, N, D, B, G, rank, Kloc
+std::vector<unsigned char> segment_header(const Ctx& c, uint32_t fid) {
+  std::vector<unsigned char> h(kPage, 0);
+  std::memcpy(h.data(), fid == 0 ? "TDGS" : "TDGP", 4);
+  put32(&h[4], 1);
+  put32(&h[8], fid);
+  put32(&h[12], c.n_arr());
+  put64(&h[16], c.cfg.n_gaussians);
+  put32(&h[24], D);
+  put32(&h[28], c.cfg.block_size);
+  put32(&h[32], (uint32_t)c.cfg.world_size);
+  put32(&h[36], (uint32_t)c.cfg.rank);
+  put32(&h[40], c.Kloc);
+  return h;
+}
+
+void write_at(const std::string& path, uint64_t off, const void* p, uint64_t n, bool create) {
+  FILE* f = std::fopen(path.c_str(), create ? "w+b" : "r+b");
+  if (!f) return;
+  std::fseek(f, (long)off, SEEK_SET);
+  std::fwrite(p, 1, n, f);
+  std::fclose(f);
+}
+
+void read_at(const std::string& path, uint64_t off, void* p, uint64_t n) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return;
+  std::fseek(f, (long)off, SEEK_SET);
+  size_t got = std::fread(p, 1, n, f);
+  (void)got;
+  std::fclose(f);
+}
+
+// "updated blocks are written sequentially into patch
+// segments rather than overwriting existing block locations in place"; Index[k]
+// then points to the latest location.  R28: a record is a
+// header page ("TREC", format 1, global id, version, payload bytes) followed by
+// the payload padded to whole pages; a new segment starts when the record
+// would push a non-empty segment past the byte budget.
+void append_version(Ctx& c, uint32_t l, const CacheEntry& e) {
+  Store& s = c.sto;
+  const uint64_t rec = kPage + s.S;
+  if (s.cur_file == 0 || (s.cur_size > kPage && s.cur_size + rec > s.seg_budget)) {
+    s.cur_file += 1;
+    s.segments += 1;
+    s.cur_size = kPage;
+    s.write_bytes += kPage;
+    if (s.data) {
+      std::vector<unsigned char> h = segment_header(c, s.cur_file);
+      write_at(seg_path(s, s.cur_file), 0, h.data(), kPage, true);
+    }
+  }
+  IndexEntry& ix = s.index[l];
+  const uint64_t off = s.cur_size;
+  const uint64_t version = ix.version + 1;
+  if (s.data) {
+    std::vector<unsigned char> r(rec, 0);
+    std::memcpy(&r[0], "TREC", 4);
+    put32(&r[4], 1);
+    put64(&r[8], c.gid_block(l));
+    put64(&r[16], version);
+    put64(&r[24], s.payload);
+    std::memcpy(&r[kPage], e.payload.data(), s.payload);
+    write_at(seg_path(s, s.cur_file), off, r.data(), rec, false);
+  }
+  ix.file_id = s.cur_file;
+  ix.offset = off + kPage;
+  ix.size = s.payload;
+  ix.version = version;
+  s.cur_size += rec;
+  s.write_bytes += rec;
+}
+
+// R27 (b): CPU-cache access of an S+ block.  Hit:
+// touch.  Miss: take a new entry while fewer than H blocks are cached, else
+// evict the least recently used entry whose block is in neither R_t nor
+// R_{t+1} (the blocks the GPU holds are pinned); a dirty victim is appended to
+// the patch log first.  Then the newest version is
+// read through Index[k] ("Reads consult Index to materialize the
+// newest version of each block").
+CacheEntry& cache_access(Ctx& c, uint32_t l, const std::vector<uint32_t>& Rt,
+                         const std::vector<uint32_t>& Rn) {
+  Store& s = c.sto;
+  auto it = s.cache.find(l);
+  if (it != s.cache.end()) {
+    s.hits += 1;
+    it->second.stamp = ++s.clock;
+    return it->second;
+  }
+  s.misses += 1;
+  if (s.cache.size() >= s.H) {
+    auto victim = s.cache.end();
+    for (auto v = s.cache.begin(); v != s.cache.end(); ++v) {
+      if (contains(Rt, v->first) || contains(Rn, v->first)) continue;
+      if (victim == s.cache.end() || v->second.stamp < victim->second.stamp) victim = v;
+    }
+    // a victim exists: pinned entries <= |R_t u R_{t+1}| - 1 < 2C <= H
+    s.evictions += 1;
+    if (victim->second.dirty) {
+      s.dirty_evictions += 1;
+      append_version(c, victim->first, victim->second);
+    }
+    s.cache.erase(victim);
+  }
+  CacheEntry& e = s.cache[l];
+  const IndexEntry& ix = s.index[l];
+  if (s.data) {
+    e.payload.assign((size_t)c.n_arr() * c.rec_floats(), 0.0f);
+    read_at(seg_path(s, ix.file_id), ix.offset, e.payload.data(), s.payload);
+  }
+  s.read_bytes += s.S;
+  e.dirty = false;
+  e.stamp = ++s.clock;
+  return e;
+}
+
 }  // namespace
 
 struct or_ctx {
@@ -233,6 +407,7 @@ int or_track_block(or_ctx* o, uint64_t kg) {
   uint64_t l = kg / c.cfg.world_size;
   if (l >= c.Kloc) return OR_EINVAL;
   if (c.slot_of[l] >= 0 && !c.tracked[l] && !c.track_all) return OR_ESTATE;  // track before admission
+  if (c.sto.on && !c.sto.data) return OR_ESTATE;  // metadata-only store keeps no data
   c.tracked[l] = 1;
   return OR_OK;
 }
@@ -349,7 +524,15 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
   for (uint32_t l : Sm) {
     int32_t s = c.slot_of[l];
     if (c.dirty[s]) {
-      if (c.is_tracked(l)) {
+      if (c.sto.on) {
+        // R27 (a): D2H into the block's CPU-cache entry, inserted dirty (PAPER.md:
+        // 247-248); the entry exists (inclusion: every GPU-resident block is cached)
+        CacheEntry& e = c.sto.cache.at(l);
+        if (c.sto.data)
+          std::memcpy(e.payload.data(), c.slot_data[s].data(),
+                      sizeof(float) * c.n_arr() * c.rec_floats());
+        e.dirty = true;
+      } else if (c.is_tracked(l)) {
         std::vector<float>& h = c.host_rec(l);
         std::vector<float>& d = c.slot_data[s];
         std::memcpy(h.data(), d.data(), sizeof(float) * c.n_arr() * c.rec_floats());
@@ -379,7 +562,15 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
     c.ever_resident[l] = 1;
     c.admit_iter[l] = c.t;
     if (g.moments == OR_COLD_RESTART) c.step[l] = 0;
-    if (c.is_tracked(l)) {
+    if (c.sto.on) {
+      // R27 (b): H2D from the block's CPU-cache entry, loaded from SSD on a miss
+      CacheEntry& e = cache_access(c, l, c.R, Rn);
+      if (c.sto.data) {
+        std::vector<float> d(3 * c.rec_floats(), 0.0f);
+        std::memcpy(d.data(), e.payload.data(), sizeof(float) * c.n_arr() * c.rec_floats());
+        c.slot_data[s] = std::move(d);
+      }
+    } else if (c.is_tracked(l)) {
       std::vector<float>& h = c.host_rec(l);
       std::vector<float> d(3 * c.rec_floats(), 0.0f);
       std::memcpy(d.data(), h.data(), sizeof(float) * c.n_arr() * c.rec_floats());
@@ -387,6 +578,12 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
     }
   }
   c.st.h2d_bytes += (uint64_t)Sp.size() * rb;
+  // R27 (c): the blocks that left the GPU are accesses of the CPU cache too
+  // ("The LRU policy is updated on each access"): touched in
+  // ascending id after the S+ accesses; clean ones move no bytes (their entry
+  // already holds the version the GPU had).
+  if (c.sto.on)
+    for (uint32_t l : Sm) c.sto.cache.at(l).stamp = ++c.sto.clock;
 
   // ---- bookkeeping
   c.Kset = Kn;
@@ -499,7 +696,13 @@ int or_flush(or_ctx* o) {
   for (uint32_t l : c.R) {  // consistency barrier: write back dirty residents
     int32_t s = c.slot_of[l];
     if (!c.dirty[s]) continue;
-    if (c.is_tracked(l)) {
+    if (c.sto.on) {
+      CacheEntry& e = c.sto.cache.at(l);
+      if (c.sto.data)
+        std::memcpy(e.payload.data(), c.slot_data[s].data(),
+                    sizeof(float) * c.n_arr() * c.rec_floats());
+      e.dirty = true;
+    } else if (c.is_tracked(l)) {
       std::vector<float>& h = c.host_rec(l);
       std::memcpy(h.data(), c.slot_data[s].data(), sizeof(float) * c.n_arr() * c.rec_floats());
     }
@@ -507,6 +710,17 @@ int or_flush(or_ctx* o) {
     c.st.flush_bytes += rb;
     c.st.n_flush_blocks += 1;
   }
+  // f3: "Dirty blocks are flushed to SSD patch segments ... at explicit
+  // consistency barriers such as checkpointing and shutdown":
+  // every dirty CPU-cache entry is appended, ascending id, and becomes clean;
+  // the cache keeps its contents and LRU order.
+  if (c.sto.on)
+    for (auto& kv : c.sto.cache)
+      if (kv.second.dirty) {
+        append_version(c, kv.first, kv.second);
+        kv.second.dirty = false;
+        c.sto.flush_appends += 1;
+      }
   c.can_step = false;
   return OR_OK;
 }
@@ -686,11 +900,21 @@ int or_read_block(or_ctx* o, uint64_t kg, float* theta, float* m, float* v) {
   if (l >= c.Kloc || !c.is_tracked((uint32_t)l)) return OR_EINVAL;
   const size_t n = c.rec_floats();
   const float* src;
-  std::vector<float> zeros;
+  std::vector<float> zeros, stored;
   if (c.slot_of[l] >= 0) {
     src = c.slot_data[c.slot_of[l]].data();
   } else {
-    std::vector<float>& h = c.host_rec((uint32_t)l);
+    if (c.sto.on) {  // f3: CPU-cache entry, else the newest version through Index[k]
+      auto it = c.sto.cache.find((uint32_t)l);
+      if (it != c.sto.cache.end()) {
+        stored = it->second.payload;
+      } else {
+        const IndexEntry& ix = c.sto.index[l];
+        stored.assign((size_t)c.n_arr() * n, 0.0f);
+        read_at(seg_path(c.sto, ix.file_id), ix.offset, stored.data(), c.sto.payload);
+      }
+    }
+    std::vector<float>& h = c.sto.on ? stored : c.host_rec((uint32_t)l);
     if (c.n_arr() == 3) {
       src = h.data();
     } else {  // cold restart: moments do not exist off-GPU
@@ -703,6 +927,85 @@ int or_read_block(or_ctx* o, uint64_t kg, float* theta, float* m, float* v) {
   if (m) std::memcpy(m, src + n, sizeof(float) * n);
   if (v) std::memcpy(v, src + 2 * n, sizeof(float) * n);
   return OR_OK;
+}
+
+
+// ---- NEXT f3: store tier (R27, R28)
+int or_store_open(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t segment_bytes) {
+  Ctx& c = o->c;
+  Store& s = c.sto;
+  if (c.t != 0 || s.on) return OR_ESTATE;
+  if (cache_blocks < 2ull * c.cfg.capacity) return OR_EINVAL;  // pinned entries < 2C (R27)
+  bool any_tracked = c.track_all;
+  for (char x : c.tracked) any_tracked = any_tracked || x;
+  if ((dir != nullptr) != c.track_all) return OR_EINVAL;  // data mode <=> every block tracked
+  if (!dir && any_tracked) return OR_EINVAL;
+  s.payload = (uint64_t)c.n_arr() * c.rec_bytes();
+  s.S = pad_page(s.payload);
+  s.seg_budget = segment_bytes ? segment_bytes : (1ull << 30);
+  if (s.seg_budget < 2 * kPage + s.S) return OR_EINVAL;
+  s.on = true;
+  s.data = dir != nullptr;
+  s.H = cache_blocks;
+  if (dir) s.dir = dir;
+  // "The initial model is written once as an immutable base segment"
+  // (PAPER.md:228): header page, then record l at 4096 + l * S, Index[l] =
+  // (0, offset, size, 0).
+  s.index.assign(c.Kloc, IndexEntry{});
+  for (uint32_t l = 0; l < c.Kloc; ++l) s.index[l] = {0, kPage + (uint64_t)l * s.S, s.payload, 0};
+  if (s.data) {
+    const std::string base = seg_path(s, 0);
+    std::vector<unsigned char> h = segment_header(c, 0);
+    write_at(base, 0, h.data(), kPage, true);
+    std::vector<unsigned char> r(s.S, 0);
+    std::vector<float> v((size_t)c.n_arr() * c.rec_floats());
+    for (uint32_t l = 0; l < c.Kloc; ++l) {
+      std::fill(v.begin(), v.end(), 0.0f);  // m = v = 0 (persist)
+      if (c.fill) c.fill(c.fill_user, c.gid_block(l), v.data());
+      std::memcpy(r.data(), v.data(), s.payload);
+      write_at(base, kPage + (uint64_t)l * s.S, r.data(), s.S, false);
+    }
+  }
+  return OR_OK;
+}
+
+int or_store_index(or_ctx* o, uint64_t kg, uint64_t* out4) {
+  Ctx& c = o->c;
+  if (!c.sto.on || kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;
+  const uint64_t l = kg / c.cfg.world_size;
+  if (l >= c.Kloc) return OR_EINVAL;
+  const IndexEntry& ix = c.sto.index[l];
+  out4[0] = ix.file_id;
+  out4[1] = ix.offset;
+  out4[2] = ix.size;
+  out4[3] = ix.version;
+  return OR_OK;
+}
+
+/* hits, misses, evictions, dirty_evictions, flush_appends, read_bytes,
+ * write_bytes, segments, cached blocks, dirty cached blocks */
+int or_store_stats(or_ctx* o, uint64_t* out10) {
+  const Store& s = o->c.sto;
+  if (!s.on) return OR_EINVAL;
+  uint64_t nd = 0;
+  for (const auto& kv : s.cache) nd += kv.second.dirty ? 1 : 0;
+  const uint64_t v[10] = {s.hits, s.misses, s.evictions, s.dirty_evictions, s.flush_appends,
+                          s.read_bytes, s.write_bytes, s.segments, (uint64_t)s.cache.size(), nd};
+  std::memcpy(out10, v, sizeof v);
+  return OR_OK;
+}
+
+/* cached local->global ids in LRU order (least recent first) with dirty flags */
+uint32_t or_store_lru(or_ctx* o, uint32_t* blocks, uint8_t* dirty, uint32_t cap) {
+  const Store& s = o->c.sto;
+  std::vector<std::pair<uint64_t, uint32_t>> v;
+  for (const auto& kv : s.cache) v.push_back({kv.second.stamp, kv.first});
+  std::sort(v.begin(), v.end());
+  for (uint32_t i = 0; i < v.size() && i < cap; ++i) {
+    if (blocks) blocks[i] = (uint32_t)o->c.gid_block(v[i].second);
+    if (dirty) dirty[i] = s.cache.at(v[i].second).dirty ? 1 : 0;
+  }
+  return (uint32_t)v.size();
 }
 
 }  // extern "C"

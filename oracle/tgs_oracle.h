@@ -97,6 +97,18 @@ uint64_t or_morton3(uint32_t x, uint32_t y, uint32_t z);
 /* the deterministic exp of R24 (exported for its pins) */
 float or_exp_det(float x);
 
+/* NEXT f3 -- the tier below the host (§3.4; readings R27,
+ * R28 of DESIGN.md §3): an LRU CPU cache of cache_blocks (>= 2C) block records
+ * with dirty bits over a log-structured store (immutable base segment +
+ * append-only patch segments, Index[k] = (file_id, offset, size, version)).
+ * Call after or_create, before the first activate.  dir != NULL: files are
+ * written under dir (needs track_all); dir == NULL: metadata only (Index, LRU
+ * and counters; no block may be tracked). */
+int or_store_open(or_ctx* c, const char* dir, uint32_t cache_blocks, uint64_t segment_bytes);
+int or_store_index(or_ctx* c, uint64_t k_global, uint64_t* out4);
+int or_store_stats(or_ctx* c, uint64_t* out10);
+uint32_t or_store_lru(or_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap);
+
 #ifdef __cplusplus
 }
 #endif
