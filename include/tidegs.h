@@ -52,7 +52,8 @@ typedef enum {
   TGS_ECUDA = 4,       /* CUDA runtime error; context poisoned                      */
   TGS_ENCCL = 5,       /* reserved for collective errors                            */
   TGS_ENONFINITE = 6,  /* a non-finite gradient was seen in an active row (R20)     */
-  TGS_EPOISONED = 7    /* an earlier CUDA error poisoned this context               */
+  TGS_EPOISONED = 7,   /* an earlier CUDA error poisoned this context               */
+  TGS_EIO = 8          /* storage (f3 store tier) read/write failed; context poisoned */
 } tgs_status;
 
 typedef enum { TGS_MOMENTS_PERSIST = 0, TGS_MOMENTS_COLD_RESTART = 1 } tgs_moments;
@@ -157,6 +158,56 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
                           void* compute_stream, tgs_ctx** out);
 
 tgs_status tgs_destroy(tgs_ctx* ctx);
+
+/* NEXT f3 -- the tier below the host tier (§3.4 "SSD
+ * Storage, CPU Tiered Cache"; readings R27, R28 of DESIGN.md §3).  Instead of a
+ * pinned host copy of the whole shard, the shard lives in a log-structured
+ * store under dir: an immutable base segment (base.tdgs, written here from
+ * theta_rows / fill, m = v = 0) and append-only patch segments
+ * (patch-NNNNNN.tdgp) with a per-block Index[k] = (file_id, offset, size,
+ * version).  Above it sits a CPU cache of cache_blocks
+ * pinned block records (LRU with a dirty bit per entry),
+ * inclusive of the GPU working set: the S+ gather reads from, and the dirty
+ * S- write-back lands in, the block's entry; a dirty entry reaches the SSD
+ * when the cache evicts it (LRU among blocks outside R_t u R_{t+1}) or at
+ * tgs_flush.  Misses are read through Index[k] inside
+ * tgs_activate (overlapping the previous Adam on the device).  File format:
+ * little-endian, 4096-byte header pages, payloads page-aligned (R28).
+ * Every other call behaves exactly as with tgs_init_table. */
+typedef struct {
+  const char* dir;         /* directory (created if absent; one store per dir: its stale
+                              patch segments are removed); must not be NULL        */
+  uint32_t cache_blocks;   /* H >= 2 * capacity block records (EINVAL otherwise)    */
+  uint64_t segment_bytes;  /* patch segment rollover budget; 0 -> 1 GiB             */
+  int32_t direct_io;       /* 1: O_DIRECT reads/writes (page cache bypassed)        */
+  int32_t io_threads;      /* parallel SSD requests; 0 -> 8                         */
+} tgs_store_config;
+
+/* As tgs_init_table, with the store tier.  TGS_EIO: the store could not be
+ * created (a message is printed to stderr; *out is not set). */
+tgs_status tgs_init_table_store(const tgs_config* cfg, const tgs_store_config* store,
+                                const float* theta_rows, tgs_fill_fn fill, void* fill_user,
+                                const float* bounds, const tgs_allocator* alloc,
+                                void* compute_stream, tgs_ctx** out);
+
+typedef struct {
+  uint64_t hits, misses;        /* CPU-cache lookups of S+ blocks                          */
+  uint64_t evictions;           /* CPU-cache evictions (LRU victims)                       */
+  uint64_t dirty_evictions;     /* victims appended to the patch log during training       */
+  uint64_t flush_appends;       /* records appended by tgs_flush                           */
+  uint64_t read_bytes;          /* SSD bytes read (misses x padded payload)                */
+  uint64_t write_bytes;         /* SSD bytes appended (record + segment header pages incl.) */
+  uint64_t segments;            /* patch segments created                                  */
+  uint64_t cached, cached_dirty;/* current CPU-cache occupancy                             */
+  double read_ms, write_ms;     /* host wall time spent in SSD reads / appends             */
+} tgs_store_stats;
+/* ESTATE without a store.  Synchronising. */
+tgs_status tgs_get_store_stats(tgs_ctx* ctx, tgs_store_stats* out);
+/* Index[k] of global block k: out4 = (file_id, payload offset, payload bytes, version) */
+tgs_status tgs_store_index(tgs_ctx* ctx, uint64_t k_global, uint64_t* out4);
+/* cached global ids, least recently used first, and their dirty flags (either may
+ * be NULL); returns the number cached (writes at most cap) */
+uint32_t tgs_store_lru(tgs_ctx* ctx, uint32_t* blocks, uint8_t* dirty, uint32_t cap);
 
 /* ------------------------------------------------------------ the hot path */
 

@@ -71,6 +71,7 @@ struct Dev {
   PlanHdr* hdr_dev;      // device copy of the header
   PlanHdr* hdr_map;      // device alias of the mapped host header
   uint32_t* sp_map;      // mapped host [C][2] (local id, slot) of S+
+  uint32_t* sm_map;      // mapped host [C] S- local ids (store mode only, else nullptr)
   uint32_t* dirty_map[2];  // mapped host [C][2] (local id, slot) of dirty S- (parity)
   uint32_t* ndirty_map;    // mapped host [2] |dirty S-| (parity)
   uint32_t* ndirty_dev;    // [2] |dirty S-| (parity), read by k_pack

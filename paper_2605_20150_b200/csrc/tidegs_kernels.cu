@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
   unsigned long long streak = 0;
   for (uint32_t i = tid; i < nSm; i += kPlanNT) {
     const uint32_t l = smb[i], s = sms[i];
+    if (d.sm_map) d.sm_map[i] = l;  // f3: the host touches the CPU-cache entries of S-
     d.b2s[l] = -1;
     d.s2b[s] = -1;
     atomicAnd(&d.occ[s >> 5], ~(1u << (s & 31)));

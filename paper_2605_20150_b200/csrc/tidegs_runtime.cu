@@ -42,6 +42,7 @@
 
 #include "tidegs.h"
 #include "tidegs_internal.h"
+#include "tidegs_store.h"
 
 using namespace tgs;
 
@@ -64,9 +65,13 @@ struct tgs_ctx {
   tgs_allocator alloc{};
   bool has_alloc = false;
   std::vector<void*> dev_allocs;
-  // host tier: [Kloc][n_arr][B][59]
+  // host tier: [Kloc][n_arr][B][59]; or (NEXT f3) a CPU cache of H records over
+  // the log-structured store on SSD
   float* host = nullptr;
   size_t host_bytes = 0;
+  tgs::BlockStore* store = nullptr;
+  char* cache_pool = nullptr;     // [H][S] pinned (store mode)
+  uint32_t* sm_map = nullptr;     // mapped host [C] S- local ids (store mode, written by k_plan)
   // mapped pinned
   PlanHdr* hdr = nullptr;         // host view
   uint32_t* sp_map = nullptr;     // host view
@@ -77,6 +82,7 @@ struct tgs_ctx {
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr, fix = nullptr;
   cudaEvent_t ev_plan = nullptr, ev_gstart = nullptr, ev_gdone = nullptr;
   cudaEvent_t ev_ready[2] = {}, ev_evict[2] = {}, ev_d2h[2] = {}, ev_lists[2] = {};
+  cudaEvent_t ev_job[4] = {};      // write-back of activate J done: ev_job[J & 3] (store mode)
   bool rec_ready[2] = {}, rec_evict[2] = {}, rec_lists[2] = {};
   int32_t d2h_job[2] = {-1, -1};   // activate index of the last write-back job of parity p
   bool prev_direct = false;        // previous activate wrote back straight from its slots
@@ -289,6 +295,7 @@ tgs_status ensure_lut(tgs_ctx* c, float b1, float b2, uint32_t need) {
 }
 
 inline float* host_rec(tgs_ctx* c, uint32_t l) {
+  if (c->store) return c->store->entry_of(l);  // cached by inclusion whenever it moves (R27)
   return c->host + (size_t)l * c->d.n_arr * c->d.rec_floats;
 }
 inline float* slot_rec(tgs_ctx* c, uint32_t s) {
@@ -360,28 +367,32 @@ tgs_status issue_copies(tgs_ctx* c, const uint32_t* pairs, uint32_t n, bool to_d
   return submit(c, b, s);
 }
 
-void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user, int nthreads) {
-  const uint32_t Kloc = c->d.Kloc;
+// initial record of local block l: theta from the caller's rows or fill, m = v = 0
+void fill_record(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user, uint32_t l,
+                 float* dst) {
   const size_t rf = c->d.rec_floats;
   const uint32_t B = c->d.B;
+  const uint64_t k = (uint64_t)l * c->cfg.world_size + c->cfg.rank;
+  if (rows) {
+    const uint64_t lo = k * B;
+    const uint64_t nr = std::min<uint64_t>(B, c->cfg.n_gaussians - lo);
+    std::memcpy(dst, rows + lo * kDim, nr * kDim * sizeof(float));
+    std::memset(dst + nr * kDim, 0, (rf - nr * kDim) * sizeof(float));
+  } else {
+    fill(user, k, dst);
+  }
+  if (c->d.n_arr == 3) std::memset(dst + rf, 0, 2 * rf * sizeof(float));  // m = v = 0
+}
+
+void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user, int nthreads) {
+  const uint32_t Kloc = c->d.Kloc;
   std::atomic<uint32_t> next{0};
   auto work = [&]() {
     for (;;) {
       const uint32_t l0 = next.fetch_add(16);
       if (l0 >= Kloc) break;
-      for (uint32_t l = l0; l < std::min<uint32_t>(l0 + 16, Kloc); ++l) {
-        float* dst = host_rec(c, l);
-        const uint64_t k = (uint64_t)l * c->cfg.world_size + c->cfg.rank;
-        if (rows) {
-          const uint64_t lo = k * B;
-          const uint64_t nr = std::min<uint64_t>(B, c->cfg.n_gaussians - lo);
-          std::memcpy(dst, rows + lo * kDim, nr * kDim * sizeof(float));
-          std::memset(dst + nr * kDim, 0, (rf - nr * kDim) * sizeof(float));
-        } else {
-          fill(user, k, dst);
-        }
-        if (c->d.n_arr == 3) std::memset(dst + rf, 0, 2 * rf * sizeof(float));  // m = v = 0
-      }
+      for (uint32_t l = l0; l < std::min<uint32_t>(l0 + 16, Kloc); ++l)
+        fill_record(c, rows, fill, user, l, host_rec(c, l));
     }
   };
   std::vector<std::thread> th;
@@ -410,6 +421,7 @@ void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
   CopyBatch b;
   b.max_merge = c->d2h_max_merge;
   for (uint32_t k = 0; k < nd; ++k) {
+    if (c->store) c->store->mark_dirty(dl[2 * k], j.T);  // R27 (a): inserted dirty
     float* h = host_rec(c, dl[2 * k]);
     const float* src = j.direct ? slot_rec(c, dl[2 * k + 1])
                                 : d.staging[p] + (size_t)k * d.n_arr * d.rec_floats;
@@ -432,6 +444,10 @@ void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
   prof_end(c, c->d2h, td, 4, (uint64_t)nd * w);
   e = cudaEventRecord(c->ev_d2h[p], c->d2h);
   if (e != cudaSuccess) return fail("io: cudaEventRecord(d2h)", e);
+  if (c->store) {
+    e = cudaEventRecord(c->ev_job[j.T & 3], c->d2h);
+    if (e != cudaSuccess) return fail("io: cudaEventRecord(job)", e);
+  }
   std::lock_guard<std::mutex> g(c->mu);
   c->tm.copy_calls += b.dst.size();
   c->last_ndirty = nd;
@@ -520,9 +536,14 @@ void destroy_impl(tgs_ctx* c) {
       cudaFree(p);
   }
   if (c->host) cudaFreeHost(c->host);
+  delete c->store;
+  if (c->cache_pool) cudaFreeHost(c->cache_pool);
+  if (c->sm_map) cudaFreeHost(c->sm_map);
   for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
                   (void*)c->ndirty, (void*)c->planes_pinned, (void*)c->lut_pinned})
     if (h) cudaFreeHost(h);
+  for (cudaEvent_t e : c->ev_job)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_plan, c->ev_gstart, c->ev_gdone, c->ev_ready[0], c->ev_ready[1],
                         c->ev_evict[0],
                         c->ev_evict[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_lists[0],
@@ -549,15 +570,20 @@ const char* tgs_status_string(tgs_status s) {
     case TGS_ENCCL: return "NCCL error";
     case TGS_ENONFINITE: return "non-finite gradient";
     case TGS_EPOISONED: return "context poisoned by an earlier CUDA error";
+    case TGS_EIO: return "storage I/O error";
   }
   return "unknown status";
 }
 
 const char* tgs_last_error(const tgs_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
-tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fill_fn fill,
-                          void* fill_user, const float* bounds, const tgs_allocator* alloc,
-                          void* compute_stream, tgs_ctx** out) {
+}  // extern "C"
+
+namespace {
+
+tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const float* theta_rows,
+                     tgs_fill_fn fill, void* fill_user, const float* bounds,
+                     const tgs_allocator* alloc, void* compute_stream, tgs_ctx** out) {
   if (!cfg || !out || !bounds) return TGS_EINVAL;
   const tgs_config& g = *cfg;
   if (g.dim != kDim || g.block_size < 4 || g.block_size % 4 != 0 || g.capacity == 0 ||
@@ -572,6 +598,7 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   if ((theta_rows == nullptr) == (fill == nullptr)) return TGS_EINVAL;
   const uint32_t P = g.pool_slots ? g.pool_slots : 2u * g.capacity;
   if (P < g.capacity) return TGS_EINVAL;
+  if (scfg && (!scfg->dir || scfg->cache_blocks < 2ull * g.capacity)) return TGS_EINVAL;  // R27
   const uint64_t K = (g.n_gaussians + g.block_size - 1) / g.block_size;
   const uint64_t Kloc64 = K > (uint64_t)g.rank ? (K - g.rank + g.world_size - 1) / g.world_size : 0;
   if (Kloc64 > (1ull << 31) / 32) return TGS_EINVAL;
@@ -629,20 +656,44 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   for (cudaEvent_t* e : {&c->ev_plan, &c->ev_gstart, &c->ev_gdone, &c->ev_ready[0],
                          &c->ev_ready[1], &c->ev_evict[0],
                          &c->ev_evict[1], &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_lists[0],
-                         &c->ev_lists[1]})
+                         &c->ev_lists[1], &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
+                         &c->ev_job[3]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
 
   // ---- host tier (pinned, block records)
-  c->host_bytes = (size_t)d.Kloc * d.n_arr * c->rec_bytes;
-  if (c->host_bytes &&
-      cudaHostAlloc((void**)&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess) {
-    c->host = nullptr;
-    cudaGetLastError();
-    return fail(TGS_ENOMEM);
-  }
   int nth = g.init_threads > 0 ? g.init_threads : (int)std::thread::hardware_concurrency();
   nth = std::max(1, std::min(nth, 128));
-  fill_host_tier(c, theta_rows, fill, fill_user, nth);
+  if (scfg) {
+    // NEXT f3: CPU cache of H records over the log-structured store
+    const uint64_t S = (d.n_arr * c->rec_bytes + 4095) / 4096 * 4096;
+    if (cudaHostAlloc((void**)&c->cache_pool, (size_t)scfg->cache_blocks * S,
+                      cudaHostAllocPortable) != cudaSuccess) {
+      c->cache_pool = nullptr;
+      cudaGetLastError();
+      return fail(TGS_ENOMEM);
+    }
+    tgs::BlockStore::Geometry geo{d.N, d.B, d.n_arr, d.G, d.rank, d.Kloc, c->rec_bytes};
+    c->store = new tgs::BlockStore();
+    const int io_threads = scfg->io_threads > 0 ? std::min(scfg->io_threads, 64) : 8;
+    const std::string e = c->store->open(
+        scfg->dir, geo, scfg->cache_blocks, c->cache_pool,
+        scfg->segment_bytes ? scfg->segment_bytes : (1ull << 30), scfg->direct_io != 0,
+        std::max(io_threads, std::min(nth, 32)),
+        [&](uint32_t l, float* dst) { fill_record(c, theta_rows, fill, fill_user, l, dst); });
+    if (!e.empty()) {
+      fprintf(stderr, "tidegs: store: %s\n", e.c_str());  // the context is gone on return
+      return fail(TGS_EIO);
+    }
+  } else {
+    c->host_bytes = (size_t)d.Kloc * d.n_arr * c->rec_bytes;
+    if (c->host_bytes &&
+        cudaHostAlloc((void**)&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess) {
+      c->host = nullptr;
+      cudaGetLastError();
+      return fail(TGS_ENOMEM);
+    }
+    fill_host_tier(c, theta_rows, fill, fill_user, nth);
+  }
 
   // ---- mapped pinned plan readback
   const size_t list_bytes = sizeof(uint32_t) * 2 * (size_t)std::max(d.C, 1u);
@@ -655,6 +706,15 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
                     cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     return fail(TGS_ENOMEM);
+  }
+  if (c->store) {
+    if (cudaHostAlloc((void**)&c->sm_map, sizeof(uint32_t) * std::max(d.C, 1u),
+                      cudaHostAllocMapped) != cudaSuccess) {
+      c->sm_map = nullptr;
+      cudaGetLastError();
+      return fail(TGS_ENOMEM);
+    }
+    cudaHostGetDevicePointer((void**)&d.sm_map, c->sm_map, 0);
   }
   std::memset(c->hdr, 0, sizeof(PlanHdr));
   std::memset(c->ndirty, 0, sizeof(uint32_t) * 2);
@@ -766,6 +826,24 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
   return TGS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fill_fn fill,
+                          void* fill_user, const float* bounds, const tgs_allocator* alloc,
+                          void* compute_stream, tgs_ctx** out) {
+  return init_impl(cfg, nullptr, theta_rows, fill, fill_user, bounds, alloc, compute_stream, out);
+}
+
+tgs_status tgs_init_table_store(const tgs_config* cfg, const tgs_store_config* store,
+                                const float* theta_rows, tgs_fill_fn fill, void* fill_user,
+                                const float* bounds, const tgs_allocator* alloc,
+                                void* compute_stream, tgs_ctx** out) {
+  if (!store) return TGS_EINVAL;
+  return init_impl(cfg, store, theta_rows, fill, fill_user, bounds, alloc, compute_stream, out);
+}
+
 tgs_status tgs_destroy(tgs_ctx* c) {
   if (!c) return TGS_EINVAL;
   destroy_impl(c);
@@ -865,6 +943,26 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
       CK(cudaStreamWaitEvent(c->fix, c->ev_plan, 0));
       ready_on = c->fix;
     }
+    if (c->store) {
+      // NEXT f3, R27 (b): S+ records come from their CPU-cache entries; misses
+      // are read from SSD through Index[k] after a dirty LRU victim (if any) is
+      // appended to the patch log.  Needs the dirty marks of activate T-1.
+      io_join(c, T - 1);
+      if (c->io_failed) return check(c);
+      auto wait_d2h = [&](int32_t job) {
+        // the plan of T waited (GPU-side) for the gather of T-2, which waited
+        // for the write-back of T-4: older jobs have landed
+        if (job + 4 <= T) return;
+        io_join(c, job);
+        cudaEventSynchronize(c->ev_job[job & 3]);
+      };
+      const std::string e = c->store->gather(c->sp_map, h.nSp, T, wait_d2h);
+      if (!e.empty()) {
+        c->poisoned = true;
+        set_err(c, "store: %s", e.c_str());
+        return TGS_EIO;
+      }
+    }
     Timer th;
     prof_begin(c, c->h2d, th);
     CopyBatch b;
@@ -887,6 +985,8 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   }
   CK(cudaEventRecord(c->ev_ready[p], ready_on));
   c->rec_ready[p] = true;
+  // R27 (c): the blocks that left the GPU are accesses of the CPU cache too
+  if (c->store && h.nSm) c->store->touch_evicted(c->sm_map, h.nSm, T);
 
   if (!reuse_now && h.nSm) {
     st = writeback();
@@ -1003,6 +1103,17 @@ tgs_status tgs_flush(tgs_ctx* c) {
   CK(cudaStreamSynchronize(c->d2h));
   CK(cudaMemset(d.dirty, 0, sizeof(uint32_t) * d.PW));
   CK(cudaDeviceSynchronize());
+  if (c->store) {
+    // NEXT f3: the barrier reaches the SSD too: the dirty
+    // residents just landed in their entries, then every dirty entry is appended
+    for (auto& e : list) c->store->mark_dirty(e.first, -1);
+    const std::string e = c->store->flush_all([](int32_t) {});
+    if (!e.empty()) {
+      c->poisoned = true;
+      set_err(c, "store: %s", e.c_str());
+      return TGS_EIO;
+    }
+  }
   c->host_flush_blocks += list.size();
   c->host_flush_bytes += (uint64_t)list.size() * d.n_arr * c->rec_bytes;
   c->can_step = false;
@@ -1161,6 +1272,19 @@ tgs_status tgs_read_block(tgs_ctx* c, uint64_t kg, float* theta, float* m, float
   const bool zero_moments = c->d.cold && s >= 0 && stp == 0;
   const size_t rb = c->rec_bytes, rf = c->d.rec_floats;
   float* outs[3] = {theta, m, v};
+  std::vector<float> stored;
+  const float* hrec = nullptr;
+  if (s < 0 && c->store) {  // f3: CPU-cache entry, else the newest version through Index[k]
+    stored.resize((size_t)c->d.n_arr * rf);
+    const std::string e = c->store->read_block((uint32_t)l, stored.data());
+    if (!e.empty()) {
+      set_err(c, "store: %s", e.c_str());
+      return TGS_EIO;
+    }
+    hrec = stored.data();
+  } else if (s < 0) {
+    hrec = host_rec(c, (uint32_t)l);
+  }
   for (int a = 0; a < 3; ++a) {
     if (!outs[a]) continue;
     if (s >= 0 && a > 0 && zero_moments) {
@@ -1168,7 +1292,7 @@ tgs_status tgs_read_block(tgs_ctx* c, uint64_t kg, float* theta, float* m, float
     } else if (s >= 0) {
       CK(cudaMemcpy(outs[a], slot_rec(c, (uint32_t)s) + a * rf, rb, cudaMemcpyDeviceToHost));
     } else if (a < (int)c->d.n_arr) {
-      std::memcpy(outs[a], host_rec(c, (uint32_t)l) + a * rf, rb);
+      std::memcpy(outs[a], hrec + a * rf, rb);
     } else {
       std::memset(outs[a], 0, rb);  // cold restart: moments do not exist off the device
     }
@@ -1297,6 +1421,59 @@ tgs_status tgs_frustum_planes(const double w2c[16], double fx, double fy, double
     out->plane[p][3] = (float)(dw / len);
   }
   return TGS_OK;
+}
+
+// ---- NEXT f3 inspection
+tgs_status tgs_get_store_stats(tgs_ctx* c, tgs_store_stats* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out) return TGS_EINVAL;
+  if (!c->store) return TGS_ESTATE;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  const tgs::StoreCounters& k = c->store->counters();
+  out->hits = k.hits;
+  out->misses = k.misses;
+  out->evictions = k.evictions;
+  out->dirty_evictions = k.dirty_evictions;
+  out->flush_appends = k.flush_appends;
+  out->read_bytes = k.read_bytes;
+  out->write_bytes = k.write_bytes;
+  out->segments = k.segments;
+  out->cached = c->store->cached();
+  out->cached_dirty = c->store->cached_dirty();
+  out->read_ms = k.read_ms;
+  out->write_ms = k.write_ms;
+  return TGS_OK;
+}
+
+tgs_status tgs_store_index(tgs_ctx* c, uint64_t kg, uint64_t* out4) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!c->store) return TGS_ESTATE;
+  if (!out4 || kg % c->cfg.world_size != (uint64_t)c->cfg.rank) return TGS_EINVAL;
+  const uint64_t l = kg / c->cfg.world_size;
+  if (l >= c->d.Kloc) return TGS_EINVAL;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  const tgs::StoreIndex& ix = c->store->index((uint32_t)l);
+  out4[0] = ix.file_id;
+  out4[1] = ix.offset;
+  out4[2] = ix.size;
+  out4[3] = ix.version;
+  return TGS_OK;
+}
+
+uint32_t tgs_store_lru(tgs_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap) {
+  if (check(c) != TGS_OK || !c->store || sync_all(c) != TGS_OK) return 0;
+  std::vector<uint32_t> b;
+  std::vector<uint8_t> d;
+  c->store->lru_order(b, d);
+  for (uint32_t i = 0; i < b.size() && i < cap; ++i) {
+    if (blocks) blocks[i] = b[i] * c->cfg.world_size + c->cfg.rank;
+    if (dirty) dirty[i] = d[i];
+  }
+  return (uint32_t)b.size();
 }
 
 }  // extern "C"

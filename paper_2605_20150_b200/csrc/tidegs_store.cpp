@@ -1,0 +1,468 @@
+// tidegs_store.cpp -- NEXT f3 store tier (see tidegs_store.h; PAPER.md:224-251,
+// readings R27/R28 of DESIGN.md §3).
+#include "tidegs_store.h"
+
+#include <algorithm>
+#include <cerrno>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+
+#include <dirent.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <sys/uio.h>
+#include <unistd.h>
+
+namespace tgs {
+
+// ------------------------------------------------------------------ IoPool
+IoPool::IoPool(int n) {
+  for (int i = 1; i < n; ++i) th_.emplace_back([this] { worker(); });
+}
+
+IoPool::~IoPool() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : th_) t.join();
+}
+
+void IoPool::worker() {
+  uint64_t seen = 0;
+  for (;;) {
+    const std::function<void(uint32_t)>* fn;
+    uint32_t n;
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      fn = fn_;
+      n = n_;
+      ++busy_;
+    }
+    for (uint32_t i; (i = next_.fetch_add(1)) < n;) (*fn)(i);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      --busy_;
+    }
+    done_cv_.notify_all();
+  }
+}
+
+void IoPool::parallel_for(uint32_t n, const std::function<void(uint32_t)>& fn) {
+  if (n == 0) return;
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    fn_ = &fn;
+    n_ = n;
+    next_ = 0;
+    ++gen_;
+  }
+  cv_.notify_all();
+  for (uint32_t i; (i = next_.fetch_add(1)) < n;) fn(i);
+  std::unique_lock<std::mutex> g(mu_);
+  done_cv_.wait(g, [&] { return busy_ == 0; });
+  fn_ = nullptr;
+}
+
+// -------------------------------------------------------------- helpers
+namespace {
+
+void put32(unsigned char* p, uint32_t v) {
+  for (int i = 0; i < 4; ++i) p[i] = (unsigned char)(v >> (8 * i));
+}
+void put64(unsigned char* p, uint64_t v) {
+  for (int i = 0; i < 8; ++i) p[i] = (unsigned char)(v >> (8 * i));
+}
+
+char* aligned_pages(size_t bytes) {
+  void* p = nullptr;
+  if (posix_memalign(&p, BlockStore::kPage, std::max<size_t>(bytes, BlockStore::kPage)) != 0)
+    return nullptr;
+  return static_cast<char*>(p);
+}
+
+std::string errno_str(const char* what) {
+  return std::string(what) + ": " + std::strerror(errno);
+}
+
+// full-length positional I/O (short counts retried)
+bool pwrite_all(int fd, const void* p, uint64_t n, uint64_t off) {
+  const char* c = static_cast<const char*>(p);
+  while (n) {
+    const ssize_t w = ::pwrite(fd, c, n, (off_t)off);
+    if (w <= 0) {
+      if (w < 0 && errno == EINTR) continue;
+      return false;
+    }
+    c += w, n -= (uint64_t)w, off += (uint64_t)w;
+  }
+  return true;
+}
+bool pread_all(int fd, void* p, uint64_t n, uint64_t off) {
+  char* c = static_cast<char*>(p);
+  while (n) {
+    const ssize_t r = ::pread(fd, c, n, (off_t)off);
+    if (r <= 0) {
+      if (r < 0 && errno == EINTR) continue;
+      return false;
+    }
+    c += r, n -= (uint64_t)r, off += (uint64_t)r;
+  }
+  return true;
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- BlockStore
+BlockStore::~BlockStore() {
+  delete pool_io_;
+  for (int fd : fds_)
+    if (fd >= 0) ::close(fd);
+  free(hdr_pages_);
+}
+
+int BlockStore::fd_of(uint32_t fid) {
+  if (fid < fds_.size() && fds_[fid] >= 0) return fds_[fid];
+  char name[64];
+  std::snprintf(name, sizeof name, fid == 0 ? "/base.tdgs" : "/patch-%06u.tdgp", fid);
+  const int fd = ::open((dir_ + name).c_str(), O_RDWR | (direct_ ? O_DIRECT : 0));
+  if (fid >= fds_.size()) fds_.resize(fid + 1, -1);
+  fds_[fid] = fd;
+  return fd;
+}
+
+// R28 segment header page: magic, format 1, file id, n_arr, N, D, B, G, rank, Kloc
+static void segment_header(unsigned char* h, uint32_t fid, const BlockStore::Geometry& g) {
+  std::memset(h, 0, BlockStore::kPage);
+  std::memcpy(h, fid == 0 ? "TDGS" : "TDGP", 4);
+  put32(h + 4, 1);
+  put32(h + 8, fid);
+  put32(h + 12, g.n_arr);
+  put64(h + 16, g.N);
+  put32(h + 24, 59);
+  put32(h + 28, g.B);
+  put32(h + 32, g.G);
+  put32(h + 36, g.rank);
+  put32(h + 40, g.Kloc);
+}
+
+std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t H, char* pool,
+                             uint64_t seg_budget, bool direct, int threads,
+                             const std::function<void(uint32_t, float*)>& fill) {
+  g_ = g;
+  dir_ = dir;
+  H_ = H;
+  pool_ = pool;
+  direct_ = direct;
+  payload_ = (uint64_t)g.n_arr * g.rec_bytes;
+  S_ = (payload_ + kPage - 1) / kPage * kPage;
+  seg_budget_ = seg_budget;
+  if (seg_budget_ < 2 * kPage + S_) return "segment budget below one record";
+  if (::mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST) return errno_str("mkdir");
+  // the directory holds one store: stale patch segments of an earlier store go
+  if (DIR* dp = ::opendir(dir.c_str())) {
+    while (dirent* e = ::readdir(dp)) {
+      const std::string n = e->d_name;
+      if (n.size() == 17 && n.compare(0, 6, "patch-") == 0 && n.compare(12, 5, ".tdgp") == 0)
+        ::unlink((dir + "/" + n).c_str());
+    }
+    ::closedir(dp);
+  }
+  pool_io_ = new IoPool(std::max(1, threads));
+
+  // "The initial model is written once as an immutable base segment"
+  // (PAPER.md:228): header page, record l at 4096 + l*S; Index[l] = (0, off, size, 0)
+  const int fd = ::open((dir + "/base.tdgs").c_str(),
+                        O_RDWR | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
+  if (fd < 0) return errno_str(direct ? "open base.tdgs (O_DIRECT)" : "open base.tdgs");
+  fds_.assign(1, fd);
+  std::unique_ptr<char, decltype(&free)> hp(aligned_pages(kPage), &free);
+  segment_header(reinterpret_cast<unsigned char*>(hp.get()), 0, g);
+  if (!pwrite_all(fd, hp.get(), kPage, 0)) return errno_str("write base header");
+  std::atomic<bool> bad{false};
+  pool_io_->parallel_for(g.Kloc, [&](uint32_t l) {
+    thread_local std::unique_ptr<char, decltype(&free)> buf(nullptr, &free);
+    thread_local uint64_t cap = 0;
+    if (cap < S_) {
+      buf.reset(aligned_pages(S_));
+      cap = S_;
+    }
+    std::memset(buf.get(), 0, S_);
+    fill(l, reinterpret_cast<float*>(buf.get()));
+    if (!pwrite_all(fd, buf.get(), S_, kPage + (uint64_t)l * S_)) bad = true;
+  });
+  if (bad) return errno_str("write base record");
+  index_.resize(g.Kloc);
+  for (uint32_t l = 0; l < g.Kloc; ++l) index_[l] = {0, kPage + (uint64_t)l * S_, payload_, 0};
+  ent_of_.assign(g.Kloc, -1);
+  ents_.assign(H, Ent{});
+  free_.clear();
+  for (uint32_t e = H; e-- > 0;) free_.push_back((int32_t)e);
+  return "";
+}
+
+void BlockStore::unlink(int32_t e) {
+  Ent& x = ents_[e];
+  if (!x.listed) return;
+  if (x.prev >= 0) ents_[x.prev].next = x.next; else head_ = x.next;
+  if (x.next >= 0) ents_[x.next].prev = x.prev; else tail_ = x.prev;
+  x.prev = x.next = -1;
+  x.listed = false;
+}
+
+void BlockStore::push_mru(int32_t e) {
+  Ent& x = ents_[e];
+  x.prev = tail_;
+  x.next = -1;
+  if (tail_ >= 0) ents_[tail_].next = e; else head_ = e;
+  tail_ = e;
+  x.listed = true;
+}
+
+std::string BlockStore::new_segment() {
+  cur_file_ += 1;
+  char name[64];
+  std::snprintf(name, sizeof name, "/patch-%06u.tdgp", cur_file_);
+  const int fd = ::open((dir_ + name).c_str(), O_RDWR | O_CREAT | O_TRUNC | (direct_ ? O_DIRECT : 0),
+                        0644);
+  if (fd < 0) return errno_str("open patch segment");
+  if (cur_file_ >= fds_.size()) fds_.resize(cur_file_ + 1, -1);
+  fds_[cur_file_] = fd;
+  std::unique_ptr<char, decltype(&free)> hp(aligned_pages(kPage), &free);
+  segment_header(reinterpret_cast<unsigned char*>(hp.get()), cur_file_, g_);
+  if (!pwrite_all(fd, hp.get(), kPage, 0)) return errno_str("write patch header");
+  cur_size_ = kPage;
+  cnt_.segments += 1;
+  cnt_.write_bytes += kPage;
+  return "";
+}
+
+// updated blocks are appended to patch segments, never
+// written in place; Index[k] then points to the latest location.  R28: a new
+// segment starts when the record would push a non-empty segment past the budget.
+std::string BlockStore::reserve_append(uint32_t l, int& fd, uint64_t& rec_off) {
+  const uint64_t rec = kPage + S_;
+  if (cur_file_ == 0 || (cur_size_ > kPage && cur_size_ + rec > seg_budget_)) {
+    std::string err = new_segment();
+    if (!err.empty()) return err;
+  }
+  fd = fds_[cur_file_];
+  rec_off = cur_size_;
+  StoreIndex& ix = index_[l];
+  ix = {cur_file_, rec_off + kPage, payload_, ix.version + 1};
+  cur_size_ += rec;
+  cnt_.write_bytes += rec;
+  return "";
+}
+
+// appends the given (block, entry) records in order: offsets are reserved
+// sequentially, then the header page + payload of every record is written in
+// parallel (pwritev straight from the pinned entry).
+std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int32_t>>& recs) {
+  if (recs.empty()) return "";
+  const size_t need = recs.size() * kPage;
+  if (hdr_cap_ < need) {
+    free(hdr_pages_);
+    hdr_pages_ = aligned_pages(need);
+    hdr_cap_ = need;
+  }
+  std::vector<int> fd(recs.size());
+  std::vector<uint64_t> off(recs.size());
+  for (size_t i = 0; i < recs.size(); ++i) {
+    std::string err = reserve_append(recs[i].first, fd[i], off[i]);
+    if (!err.empty()) return err;
+    unsigned char* h = reinterpret_cast<unsigned char*>(hdr_pages_ + i * kPage);
+    std::memset(h, 0, kPage);
+    std::memcpy(h, "TREC", 4);
+    put32(h + 4, 1);
+    put64(h + 8, (uint64_t)recs[i].first * g_.G + g_.rank);
+    put64(h + 16, index_[recs[i].first].version);
+    put64(h + 24, payload_);
+  }
+  std::atomic<bool> bad{false};
+  pool_io_->parallel_for((uint32_t)recs.size(), [&](uint32_t i) {
+    iovec iov[2];
+    iov[0].iov_base = hdr_pages_ + i * kPage;
+    iov[0].iov_len = kPage;
+    iov[1].iov_base = pool_ + (uint64_t)recs[i].second * S_;
+    iov[1].iov_len = S_;
+    uint64_t done = 0, total = kPage + S_;
+    while (done < total) {
+      const ssize_t w = ::pwritev(fd[i], iov, 2, (off_t)(off[i] + done));
+      if (w <= 0) {
+        if (w < 0 && errno == EINTR) continue;
+        bad = true;
+        return;
+      }
+      done += (uint64_t)w;
+      if (done < total) {  // short write: finish the rest with plain pwrite
+        const uint64_t o = off[i] + done;
+        if (done < kPage) {
+          if (!pwrite_all(fd[i], hdr_pages_ + i * kPage + done, kPage - done, o) ||
+              !pwrite_all(fd[i], iov[1].iov_base, S_, off[i] + kPage))
+            bad = true;
+        } else if (!pwrite_all(fd[i], (char*)iov[1].iov_base + (done - kPage), total - done, o)) {
+          bad = true;
+        }
+        return;
+      }
+    }
+  });
+  return bad ? errno_str("append patch record") : "";
+}
+
+std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
+                               const std::function<void(int32_t)>& wait_d2h) {
+  // every S+ block is in R_{t+1}: its entry (if cached) is not evictable (R27)
+  for (uint32_t i = 0; i < n; ++i) {
+    const int32_t e = ent_of_[sp[2 * i]];
+    if (e >= 0) unlink(e);
+  }
+  std::vector<std::pair<uint32_t, int32_t>> victims, misses;  // (block, entry)
+  std::vector<int32_t> jobs;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t l = sp[2 * i];
+    int32_t e = ent_of_[l];
+    if (e >= 0) {
+      cnt_.hits += 1;
+    } else {
+      cnt_.misses += 1;
+      if (!free_.empty()) {
+        e = free_.back();
+        free_.pop_back();
+      } else {
+        e = head_;  // least recently used entry outside R_t u R_{t+1}
+        if (e < 0) return "CPU cache: no evictable entry (cache_blocks < 2C?)";
+        unlink(e);
+        Ent& v = ents_[e];
+        cnt_.evictions += 1;
+        if (v.dirty) {  // two-step write-back, step 2
+          cnt_.dirty_evictions += 1;
+          victims.push_back({(uint32_t)v.blk, e});
+          if (v.wb_job >= 0) jobs.push_back(v.wb_job);
+        }
+        ent_of_[v.blk] = -1;
+      }
+      ent_of_[l] = e;
+      misses.push_back({l, e});
+      ents_[e].dirty = false;
+      ents_[e].wb_job = -1;
+    }
+    Ent& x = ents_[e];
+    x.blk = (int32_t)l;
+    x.resident = true;
+    x.admitted = T;
+    x.stamp = ++clock_;
+  }
+  if (!victims.empty()) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::sort(jobs.begin(), jobs.end());
+    jobs.erase(std::unique(jobs.begin(), jobs.end()), jobs.end());
+    for (int32_t j : jobs) wait_d2h(j);  // the victim's newest record has landed
+    std::string err = write_records(victims);
+    if (!err.empty()) return err;
+    cnt_.write_ms += ms_since(t0);
+  }
+  if (!misses.empty()) {  // fetched through Index[k]
+    const auto t0 = std::chrono::steady_clock::now();
+    std::atomic<bool> bad{false};
+    pool_io_->parallel_for((uint32_t)misses.size(), [&](uint32_t i) {
+      const StoreIndex& ix = index_[misses[i].first];
+      const int fd = fd_of(ix.file_id);
+      if (fd < 0 || !pread_all(fd, pool_ + (uint64_t)misses[i].second * S_, S_, ix.offset))
+        bad = true;
+    });
+    if (bad) return errno_str("read block record");
+    cnt_.read_bytes += misses.size() * S_;
+    cnt_.read_ms += ms_since(t0);
+  }
+  return "";
+}
+
+void BlockStore::touch_evicted(const uint32_t* sm, uint32_t n, int32_t T) {
+  for (uint32_t i = 0; i < n; ++i) {
+    const int32_t e = ent_of_[sm[i]];
+    if (e < 0) continue;  // cannot happen (inclusion)
+    Ent& x = ents_[e];
+    x.stamp = ++clock_;
+    if (x.admitted == T) continue;  // re-admitted by this activate (tide off): still pinned
+    x.resident = false;
+    unlink(e);
+    push_mru(e);
+  }
+}
+
+void BlockStore::mark_dirty(uint32_t l, int32_t T) {
+  const int32_t e = ent_of_[l];
+  if (e < 0) return;
+  ents_[e].dirty = true;
+  ents_[e].wb_job = T;
+}
+
+std::string BlockStore::flush_all(const std::function<void(int32_t)>& wait_d2h) {
+  std::vector<std::pair<uint32_t, int32_t>> recs;
+  for (uint32_t l = 0; l < g_.Kloc; ++l) {
+    const int32_t e = ent_of_[l];
+    if (e >= 0 && ents_[e].dirty) {
+      recs.push_back({l, e});
+      if (ents_[e].wb_job >= 0) wait_d2h(ents_[e].wb_job);
+    }
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::string err = write_records(recs);
+  if (!err.empty()) return err;
+  for (auto& r : recs) {
+    ents_[r.second].dirty = false;
+    ents_[r.second].wb_job = -1;
+  }
+  cnt_.flush_appends += recs.size();
+  for (int fd : fds_)  // a consistency barrier: durable on return
+    if (fd >= 0 && ::fdatasync(fd) != 0) return errno_str("fdatasync");
+  cnt_.write_ms += ms_since(t0);
+  return "";
+}
+
+std::string BlockStore::read_block(uint32_t l, void* dst) {
+  if (const float* p = entry_of(l)) {
+    std::memcpy(dst, p, payload_);
+    return "";
+  }
+  std::unique_ptr<char, decltype(&free)> buf(aligned_pages(S_), &free);
+  const StoreIndex& ix = index_[l];
+  const int fd = fd_of(ix.file_id);
+  if (fd < 0 || !pread_all(fd, buf.get(), S_, ix.offset)) return errno_str("read block record");
+  std::memcpy(dst, buf.get(), payload_);
+  return "";
+}
+
+uint32_t BlockStore::cached_dirty() const {
+  uint32_t n = 0;
+  for (const Ent& e : ents_) n += (e.blk >= 0 && ent_of_[e.blk] >= 0 && e.dirty) ? 1 : 0;
+  return n;
+}
+
+void BlockStore::lru_order(std::vector<uint32_t>& blocks, std::vector<uint8_t>& dirty) const {
+  std::vector<std::pair<uint64_t, int32_t>> v;
+  for (uint32_t l = 0; l < g_.Kloc; ++l)
+    if (ent_of_[l] >= 0) v.push_back({ents_[ent_of_[l]].stamp, ent_of_[l]});
+  std::sort(v.begin(), v.end());
+  blocks.clear();
+  dirty.clear();
+  for (auto& x : v) {
+    blocks.push_back((uint32_t)ents_[x.second].blk);
+    dirty.push_back(ents_[x.second].dirty ? 1 : 0);
+  }
+}
+
+}  // namespace tgs

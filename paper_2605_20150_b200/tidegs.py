@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TGS_LIB") or os.path.join(_HERE, "libtidegs.so")
 DIM = 59
 
-OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENONFINITE, EPOISONED = range(8)
+OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENONFINITE, EPOISONED, EIO = range(9)
 PERSIST, COLD_RESTART = 0, 1
 LISTS = {"K": 0, "R": 1, "S+": 2, "S-": 3, "Omega": 4, "A": 5}
 
@@ -28,7 +28,8 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_get_stats", "tgs_get_stats_async", "tgs_get_timing", "tgs_set_profiling", "tgs_get_list",
            "tgs_get_percam", "tgs_get_evicted_dirty", "tgs_get_slot_map",
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
-           "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error")
+           "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error",
+           "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru")
 
 
 class Config(C.Structure):
@@ -92,6 +93,23 @@ class Timing(C.Structure):
                 for n, t in self._fields_}
 
 
+class StoreConfig(C.Structure):
+    _fields_ = [("dir", C.c_char_p), ("cache_blocks", C.c_uint32), ("segment_bytes", C.c_uint64),
+                ("direct_io", C.c_int32), ("io_threads", C.c_int32)]
+
+
+STORE_FIELDS = ("hits", "misses", "evictions", "dirty_evictions", "flush_appends", "read_bytes",
+                "write_bytes", "segments", "cached", "cached_dirty")
+
+
+class StoreStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in STORE_FIELDS] + [("read_ms", C.c_double),
+                                                          ("write_ms", C.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 class Camera(C.Structure):
     _fields_ = [("plane", (C.c_float * 4) * 6)]
 
@@ -111,6 +129,13 @@ def lib():
         L.tgs_init_table.argtypes = [C.POINTER(Config), C.c_void_p, C.c_void_p, vp,
                                      C.POINTER(C.c_float), C.POINTER(Allocator), vp,
                                      C.POINTER(vp)]
+        L.tgs_init_table_store.argtypes = [C.POINTER(Config), C.POINTER(StoreConfig), C.c_void_p,
+                                           C.c_void_p, vp, C.POINTER(C.c_float),
+                                           C.POINTER(Allocator), vp, C.POINTER(vp)]
+        L.tgs_get_store_stats.argtypes = [vp, C.POINTER(StoreStats)]
+        L.tgs_store_index.argtypes = [vp, u64, C.POINTER(C.c_uint64)]
+        L.tgs_store_lru.restype = u32
+        L.tgs_store_lru.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), u32]
         L.tgs_destroy.argtypes = [vp]
         L.tgs_activate.argtypes = [vp, C.c_void_p, u32, C.POINTER(Activation)]
         L.tgs_step_adam.argtypes = [vp, C.POINTER(Adam), vp]
@@ -192,7 +217,9 @@ class Table:
     """One shard of the block-virtualized Gaussian table (tgs_ctx)."""
 
     def __init__(self, cfg: Config, bounds: np.ndarray, *, theta_rows: np.ndarray | None = None,
-                 fill=None, stream=None, use_torch_allocator=True):
+                 fill=None, stream=None, use_torch_allocator=True, store: dict | None = None):
+        """store: None (flat pinned host tier) or the NEXT f3 store tier,
+        dict(dir=..., cache_blocks=H, segment_bytes=0, direct_io=1, io_threads=0)."""
         self.cfg = cfg
         self.B = cfg.block_size
         self._bounds = np.ascontiguousarray(bounds, np.float32)
@@ -221,10 +248,18 @@ class Table:
             stream = torch.cuda.current_stream(cfg.device).cuda_stream
         self.stream = int(stream)
         h = C.c_void_p()
-        rc = lib().tgs_init_table(C.byref(cfg), rows_p, fill_p, fill_u, _fp(self._bounds), alloc,
-                                  self.stream or None, C.byref(h))
+        if store is None:
+            rc = lib().tgs_init_table(C.byref(cfg), rows_p, fill_p, fill_u, _fp(self._bounds),
+                                      alloc, self.stream or None, C.byref(h))
+        else:
+            self._store_cfg = StoreConfig(os.fsencode(str(store["dir"])), store["cache_blocks"],
+                                          store.get("segment_bytes", 0),
+                                          store.get("direct_io", 1), store.get("io_threads", 0))
+            rc = lib().tgs_init_table_store(C.byref(cfg), C.byref(self._store_cfg), rows_p,
+                                            fill_p, fill_u, _fp(self._bounds), alloc,
+                                            self.stream or None, C.byref(h))
         if rc != OK:
-            raise TgsError(rc, "tgs_init_table")
+            raise TgsError(rc, "tgs_init_table" + ("" if store is None else "_store"))
         self.h = h
         self.P = int(lib().tgs_pool_slots(h))
         self.last = None
@@ -335,6 +370,25 @@ class Table:
     @property
     def num_local_blocks(self) -> int:
         return int(lib().tgs_num_local_blocks(self.h))
+
+    # ---- NEXT f3 store tier
+    def store_stats(self) -> dict:
+        s = StoreStats()
+        self._err(lib().tgs_get_store_stats(self.h, C.byref(s)), "tgs_get_store_stats")
+        return s.as_dict()
+
+    def store_index(self, k):
+        out = (C.c_uint64 * 4)()
+        self._err(lib().tgs_store_index(self.h, k, out), "tgs_store_index")
+        return tuple(int(x) for x in out)
+
+    def store_lru(self):
+        n = lib().tgs_store_lru(self.h, None, None, 0)
+        b = np.empty(n, np.uint32)
+        d = np.empty(n, np.uint8)
+        lib().tgs_store_lru(self.h, b.ctypes.data_as(C.POINTER(C.c_uint32)),
+                            d.ctypes.data_as(C.POINTER(C.c_uint8)), n)
+        return b, d.astype(bool)
 
 
 def frustum_planes(w2c, fx, fy, cx, cy, width, height, znear, zfar) -> np.ndarray:

@@ -31,7 +31,10 @@ class Pair:
     def __init__(self, scene, *, capacity, pool_slots=0, max_cameras=256, max_age=255,
                  quota=(1, 2), lam=0.7, gamma=0.9, moments=O.PERSIST, tide=1, world_size=1,
                  rank=0, track_all=True, mask_p=None, staging_blocks=0, refresh_bounds=0,
-                 bounds=None, fill=None):
+                 bounds=None, fill=None, store=None):
+        """store (NEXT f3): dict(gpu_dir, orc_dir, cache_blocks, segment_bytes=0,
+        direct_io=0) -- the GPU table and the oracle each get their own store
+        directory (orc_dir None: oracle metadata only)."""
         import torch
         from paper_2605_20150_b200 import tidegs as T
 
@@ -43,11 +46,20 @@ class Pair:
                   rank=rank)
         bounds = scene.bounds() if bounds is None else bounds
         fill = scene.fill_fn if fill is None else fill
+        gstore = None
+        if store is not None:
+            gstore = dict(dir=store["gpu_dir"], cache_blocks=store["cache_blocks"],
+                          segment_bytes=store.get("segment_bytes", 0),
+                          direct_io=store.get("direct_io", 0))
         self.gpu = T.Table(T.make_config(scene.N, scene.B, capacity, staging_blocks=staging_blocks,
                                          refresh_bounds=refresh_bounds, **kw), bounds,
-                           fill=fill)
+                           fill=fill, store=gstore)
         self.orc = O.Oracle(O.make_config(scene.N, scene.B, capacity, refresh_bounds=refresh_bounds,
                                           **kw), bounds, fill=fill, track_all=track_all)
+        self.store = store
+        if store is not None:
+            self.orc.store_open(store.get("orc_dir"), store["cache_blocks"],
+                                store.get("segment_bytes", 0))
         self.gsyn = Synth(GRAD_SEED, scene.N, scene.B, 0)
         self.mask_p = mask_p
         self.msyn = None
@@ -144,6 +156,19 @@ class Pair:
                 worst = max(worst, max_ulp(a, b))
             assert self.gpu.step_count(k) == self.orc.step_count(k), k
         return worst
+
+    def compare_store(self, index_blocks=()):
+        """f3: CPU-cache counters, LRU order with dirty flags and Index[k] bit-exact"""
+        g, o = self.gpu.store_stats(), self.orc.store_stats()
+        diff = {k: (g[k], o[k]) for k in o if g[k] != o[k]}
+        assert not diff, f"store counters t={self.t}: {diff}"
+        gb, gd = self.gpu.store_lru()
+        ob, od = self.orc.store_lru()
+        np.testing.assert_array_equal(gb, ob, err_msg=f"LRU order t={self.t}")
+        np.testing.assert_array_equal(gd, od, err_msg=f"LRU dirty flags t={self.t}")
+        for k in index_blocks:
+            assert self.gpu.store_index(int(k)) == self.orc.store_index(int(k)), (k, self.t)
+        return g
 
     def close(self):
         self.gpu.close()

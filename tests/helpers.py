@@ -43,3 +43,26 @@ def synth_mask(seed, N, B, p32):
 def mask_rows(words, B):
     bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:B]
     return bits.astype(bool)
+
+
+def box_planes(lo, hi):
+    """one 'camera' whose frustum is the axis-aligned box [lo, hi] (inside iff n.p + d0 >= 0)"""
+    p = np.zeros((1, 6, 4), np.float32)
+    for a in range(3):
+        n = np.zeros(3)
+        n[a] = 1
+        p[0, 2 * a, :3], p[0, 2 * a, 3] = n, -lo[a]
+        p[0, 2 * a + 1, :3], p[0, 2 * a + 1, 3] = -n, hi[a]
+    return p
+
+
+def random_boxes(sc, n, seed=5):
+    """batches that jump across the scene, each seeing a handful of blocks"""
+    b = sc.bounds()
+    rng = np.random.default_rng(seed)
+    ext = (b[:, :3].max(0) - b[:, :3].min(0)) / 5
+    out = []
+    for _ in range(n):
+        c = b[rng.integers(len(b)), :3]
+        out.append(box_planes(c - ext / 2, c + ext / 2))
+    return out

@@ -17,7 +17,7 @@ import pytest
 
 import oracle as O
 import workload as W
-from helpers import lr_3dgs, synth_grad, synth_mask, tiny
+from helpers import lr_3dgs, random_boxes, synth_grad, synth_mask, tiny
 
 PAGE = 4096
 REC = 966_656  # B=4096 record: 4096*59*4 bytes = 236 pages
@@ -118,29 +118,6 @@ def test_persist_payload_and_padding(tmp_path):
         assert off % PAGE == 0 and size == payload and ver == 0
         p = payload_at(segs, fid, off, size).reshape(3, sc.B, 59)
         assert np.array_equal(p[0], sc.block_theta(k)) and not p[1:].any()
-
-
-def box_planes(lo, hi):
-    """one 'camera' whose frustum is the axis-aligned box [lo, hi] (inside iff n.p + d0 >= 0)"""
-    p = np.zeros((1, 6, 4), np.float32)
-    for a in range(3):
-        n = np.zeros(3)
-        n[a] = 1
-        p[0, 2 * a, :3], p[0, 2 * a, 3] = n, -lo[a]
-        p[0, 2 * a + 1, :3], p[0, 2 * a + 1, 3] = -n, hi[a]
-    return p
-
-
-def random_boxes(sc, n, seed=5):
-    """batches that jump across the scene, each seeing a handful of blocks"""
-    b = sc.bounds()
-    rng = np.random.default_rng(seed)
-    ext = (b[:, :3].max(0) - b[:, :3].min(0)) / 5
-    out = []
-    for _ in range(n):
-        c = b[rng.integers(len(b)), :3]
-        out.append(box_planes(c - ext / 2, c + ext / 2))
-    return out
 
 
 def lru_model(trace, H):
