@@ -87,6 +87,9 @@ def lib():
         L.or_morton3.argtypes = [C.c_uint32] * 3
         L.or_exp_det.restype = C.c_float
         L.or_exp_det.argtypes = [C.c_float]
+        L.or_order_views.argtypes = [C.POINTER(C.c_double), C.c_uint32, C.c_uint32,
+                                     C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.or_store_open.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
         L.or_store_index.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint64)]
         L.or_store_stats.argtypes = [vp, C.POINTER(C.c_uint64)]
@@ -305,3 +308,19 @@ def build_layout(cs: np.ndarray, B: int):
         raise OracleError(rc, "or_build_layout")
     return perm, bounds
 
+
+def order_views(feat: np.ndarray):
+    """NEXT f4: clustered-TSP view order (R29) of M views with D features:
+    (perm, cluster, k, lloyd_iterations)."""
+    f = np.ascontiguousarray(feat, np.float64)
+    M, D = f.shape
+    perm = np.empty(M, np.uint32)
+    cl = np.empty(M, np.uint32)
+    k = C.c_uint32()
+    it = C.c_uint32()
+    u32p = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint32))
+    rc = lib().or_order_views(f.ctypes.data_as(C.POINTER(C.c_double)), M, D, u32p(perm), u32p(cl),
+                              C.byref(k), C.byref(it))
+    if rc != OK:
+        raise OracleError(rc, "or_order_views")
+    return perm, cl, int(k.value), int(it.value)

@@ -1008,4 +1008,150 @@ uint32_t or_store_lru(or_ctx* o, uint32_t* blocks, uint8_t* dirty, uint32_t cap)
   return (uint32_t)v.size();
 }
 
+
+// ---- NEXT f4: clustered-TSP view ordering ("We use a clustered
+// TSP-ordered (no-shuffle) camera sequence", 709-712 "applying a clustered
+// traveling-salesperson (TSP) ordering over camera poses"
+// order_views).  Reading R29, step by step (all arithmetic in double, no FMA):
+//  d2(a, b) = sum over the D feature coordinates, in order, of (a_i - b_i)^2
+//  1. k = ceil(sqrt(M)) (smallest k with k*k >= M)
+//  2. maximin initialisation: centre 0 = the lexicographically smallest view
+//     (features compared in order, then index); centre j = the view maximising
+//     the min d2 to the centres so far (ties: lowest index)
+//  3. Lloyd iterations (at most 100): assign every view to the nearest centre
+//     (ties: lowest centre); stop when no assignment changed; otherwise every
+//     non-empty cluster's centre becomes the mean of its members (summed in
+//     ascending view index, then divided by the count)
+//  4. cluster tour: nearest-neighbour over the non-empty clusters' centres,
+//     starting at the cluster of the lexicographically smallest view (ties:
+//     lowest cluster)
+//  5. tour inside each cluster: nearest-neighbour over its members, starting
+//     at the lexicographically smallest view (first cluster) or at the member
+//     nearest to the preceding cluster's centre (ties: lowest index)
+//  6. pi = the concatenation, cluster by cluster in tour order
+static double d2(const double* a, const double* b, uint32_t D) {
+  double s = 0.0;
+  for (uint32_t i = 0; i < D; ++i) {
+    const double t = a[i] - b[i];
+    s = s + t * t;
+  }
+  return s;
+}
+
+static bool lex_less(const double* f, uint32_t D, uint32_t a, uint32_t b) {
+  for (uint32_t i = 0; i < D; ++i) {
+    if (f[(size_t)a * D + i] < f[(size_t)b * D + i]) return true;
+    if (f[(size_t)a * D + i] > f[(size_t)b * D + i]) return false;
+  }
+  return a < b;
+}
+
+int or_order_views(const double* feat, uint32_t M, uint32_t D, uint32_t* perm,
+                   uint32_t* cluster_out, uint32_t* k_out, uint32_t* iters_out) {
+  if (!feat || !perm || M == 0 || D == 0 || D > 8) return OR_EINVAL;
+  for (size_t i = 0; i < (size_t)M * D; ++i)
+    if (!std::isfinite(feat[i])) return OR_EINVAL;
+  uint32_t k = 1;
+  while ((uint64_t)k * k < M) ++k;  // step 1
+  uint32_t v0 = 0;
+  for (uint32_t i = 1; i < M; ++i)
+    if (lex_less(feat, D, i, v0)) v0 = i;
+  // step 2
+  std::vector<double> cen((size_t)k * D);
+  std::vector<double> mind(M);
+  for (uint32_t i = 0; i < D; ++i) cen[i] = feat[(size_t)v0 * D + i];
+  for (uint32_t v = 0; v < M; ++v) mind[v] = d2(feat + (size_t)v * D, cen.data(), D);
+  for (uint32_t j = 1; j < k; ++j) {
+    uint32_t best = 0;
+    for (uint32_t v = 1; v < M; ++v)
+      if (mind[v] > mind[best]) best = v;
+    for (uint32_t i = 0; i < D; ++i) cen[(size_t)j * D + i] = feat[(size_t)best * D + i];
+    for (uint32_t v = 0; v < M; ++v) {
+      const double e = d2(feat + (size_t)v * D, cen.data() + (size_t)j * D, D);
+      if (e < mind[v]) mind[v] = e;
+    }
+  }
+  // step 3
+  std::vector<uint32_t> asg(M, UINT32_MAX);
+  uint32_t it = 0;
+  for (; it < 100; ++it) {
+    bool changed = false;
+    for (uint32_t v = 0; v < M; ++v) {
+      uint32_t bj = 0;
+      double bd = d2(feat + (size_t)v * D, cen.data(), D);
+      for (uint32_t j = 1; j < k; ++j) {
+        const double e = d2(feat + (size_t)v * D, cen.data() + (size_t)j * D, D);
+        if (e < bd) bd = e, bj = j;
+      }
+      if (asg[v] != bj) changed = true;
+      asg[v] = bj;
+    }
+    if (!changed) break;
+    std::vector<double> sum((size_t)k * D, 0.0);
+    std::vector<uint32_t> cnt(k, 0);
+    for (uint32_t v = 0; v < M; ++v) {
+      for (uint32_t i = 0; i < D; ++i) sum[(size_t)asg[v] * D + i] += feat[(size_t)v * D + i];
+      cnt[asg[v]] += 1;
+    }
+    for (uint32_t j = 0; j < k; ++j)
+      if (cnt[j])
+        for (uint32_t i = 0; i < D; ++i) cen[(size_t)j * D + i] = sum[(size_t)j * D + i] / (double)cnt[j];
+  }
+  // step 4
+  std::vector<std::vector<uint32_t>> mem(k);
+  for (uint32_t v = 0; v < M; ++v) mem[asg[v]].push_back(v);
+  std::vector<char> done(k, 0);
+  for (uint32_t j = 0; j < k; ++j) done[j] = mem[j].empty();
+  std::vector<uint32_t> tour{asg[v0]};
+  done[asg[v0]] = 1;
+  for (;;) {
+    const uint32_t cur = tour.back();
+    uint32_t best = UINT32_MAX;
+    double bd = 0.0;
+    for (uint32_t j = 0; j < k; ++j) {
+      if (done[j]) continue;
+      const double e = d2(cen.data() + (size_t)cur * D, cen.data() + (size_t)j * D, D);
+      if (best == UINT32_MAX || e < bd) bd = e, best = j;
+    }
+    if (best == UINT32_MAX) break;
+    done[best] = 1;
+    tour.push_back(best);
+  }
+  // steps 5-6
+  uint32_t n = 0;
+  for (size_t ci = 0; ci < tour.size(); ++ci) {
+    const std::vector<uint32_t>& ms = mem[tour[ci]];
+    std::vector<char> used(ms.size(), 0);
+    size_t cur = 0;
+    if (ci == 0) {
+      while (ms[cur] != v0) ++cur;
+    } else {
+      const double* pc = cen.data() + (size_t)tour[ci - 1] * D;
+      double bd = d2(feat + (size_t)ms[0] * D, pc, D);
+      for (size_t m = 1; m < ms.size(); ++m) {
+        const double e = d2(feat + (size_t)ms[m] * D, pc, D);
+        if (e < bd) bd = e, cur = m;
+      }
+    }
+    for (size_t step = 0; step < ms.size(); ++step) {
+      used[cur] = 1;
+      perm[n++] = ms[cur];
+      size_t nb = SIZE_MAX;
+      double bd = 0.0;
+      for (size_t m = 0; m < ms.size(); ++m) {
+        if (used[m]) continue;
+        const double e = d2(feat + (size_t)ms[m] * D, feat + (size_t)ms[cur] * D, D);
+        if (nb == SIZE_MAX || e < bd) bd = e, nb = m;
+      }
+      if (nb == SIZE_MAX) break;
+      cur = nb;
+    }
+  }
+  if (cluster_out)
+    for (uint32_t v = 0; v < M; ++v) cluster_out[v] = asg[v];
+  if (k_out) *k_out = k;
+  if (iters_out) *iters_out = it;
+  return OR_OK;
+}
+
 }  // extern "C"

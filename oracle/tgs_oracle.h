@@ -109,6 +109,14 @@ int or_store_index(or_ctx* c, uint64_t k_global, uint64_t* out4);
 int or_store_stats(or_ctx* c, uint64_t* out10);
 uint32_t or_store_lru(or_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap);
 
+/* NEXT f4 -- clustered-TSP view ordering (reading R29):
+ * perm[M] = the order in which to present M views described by D <= 8
+ * features each (feat: M x D doubles, e.g. camera centre and a point on the
+ * optical axis); cluster (may be NULL) = k-means cluster of each view,
+ * k_out = number of clusters, iters_out = Lloyd iterations. */
+int or_order_views(const double* feat, uint32_t M, uint32_t D, uint32_t* perm,
+                   uint32_t* cluster, uint32_t* k_out, uint32_t* iters_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,8 @@ def lib():
         L.wl_traj_num_views.argtypes = [vp]
         L.wl_traj_view.argtypes = [vp, u64, C.POINTER(Camera)]
         L.wl_traj_set_order.argtypes = [vp, C.c_int, u64]
+        L.wl_traj_set_perm.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.wl_traj_features.argtypes = [vp, C.c_double, C.POINTER(C.c_double)]
         L.wl_traj_batch_planes.argtypes = [vp, u64, u32, f32p]
         L.wl_traj_batch_cameras.argtypes = [vp, u64, u32, C.POINTER(Camera)]
         L.wl_grad.restype = C.c_float
@@ -192,6 +194,18 @@ class Trajectory:
         if getattr(self, "handle", None) and _lib is not None:
             _lib.wl_traj_destroy(self.handle)
             self.handle = None
+
+    def features(self, focus: float) -> np.ndarray:
+        """(n_views, 6) pose features in the current order: centre, centre + focus * forward"""
+        out = np.empty((self.n_views, 6), np.float64)
+        lib().wl_traj_features(self.handle, focus, out.ctypes.data_as(C.POINTER(C.c_double)))
+        return out
+
+    def reorder(self, perm):
+        """present the views in order perm (indices into the current order)"""
+        p = np.ascontiguousarray(perm, np.uint64)
+        assert p.shape == (self.n_views,)
+        lib().wl_traj_set_perm(self.handle, p.ctypes.data_as(C.POINTER(C.c_uint64)))
 
     def batch_planes(self, b: int, J: int) -> np.ndarray:
         out = np.empty((J, 6, 4), np.float32)

@@ -522,6 +522,25 @@ void wl_traj_set_order(wl_traj* t, int shuffled, uint64_t seed) {
   }
 }
 
+void wl_traj_set_perm(wl_traj* t, const uint64_t* perm) {
+  uint64_t n = t->n_views;
+  uint64_t* o = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  for (uint64_t i = 0; i < n; ++i) o[i] = t->order ? t->order[perm[i]] : perm[i];
+  free(t->order);
+  t->order = o;
+}
+
+void wl_traj_features(const wl_traj* t, double focus, double* out) {
+  for (uint64_t i = 0; i < t->n_views; ++i) {
+    wl_camera c;
+    wl_traj_view(t, t->order ? t->order[i] : i, &c);
+    for (int a = 0; a < 3; ++a) {
+      out[6 * i + a] = c.pos[a];
+      out[6 * i + 3 + a] = c.pos[a] + focus * c.fwd[a];
+    }
+  }
+}
+
 void wl_traj_batch_cameras(const wl_traj* t, uint64_t b, uint32_t J, wl_camera* out) {
   for (uint32_t j = 0; j < J; ++j) {
     uint64_t idx = (b * (uint64_t)J + j) % t->n_views;

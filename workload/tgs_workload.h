@@ -110,6 +110,11 @@ uint64_t  wl_traj_num_views(const wl_traj* t);
 void      wl_traj_view(const wl_traj* t, uint64_t i, wl_camera* out);
 /* view order: 0 = smooth (path order), 1 = seeded Fisher-Yates shuffle */
 void      wl_traj_set_order(wl_traj* t, int shuffled, uint64_t seed);
+/* compose the current view order with perm (new position i = old position perm[i]) */
+void      wl_traj_set_perm(wl_traj* t, const uint64_t* perm);
+/* pose features of the views in the current order, out[M][6] = (centre,
+ * centre + focus * forward): inputs of the f4 view ordering (no method arithmetic) */
+void      wl_traj_features(const wl_traj* t, double focus, double* out);
 /* planes of batch b: views order[b*J .. b*J+J) (wrapping), out[J][6][4] */
 void      wl_traj_batch_planes(const wl_traj* t, uint64_t b, uint32_t J, float* out);
 void      wl_traj_batch_cameras(const wl_traj* t, uint64_t b, uint32_t J, wl_camera* out);
