@@ -24,9 +24,11 @@ oracle/libtgsoracle.so: oracle/tgs_oracle.cpp oracle/tgs_oracle.h
 # the product: CUDA kernels + C++ runtime behind the C ABI (include/tidegs.h)
 $(PKG)/libtidegs.so: $(PKG)/csrc/tidegs_kernels.cu $(PKG)/csrc/tidegs_runtime.cu \
                      $(PKG)/csrc/tidegs_store.cpp $(PKG)/csrc/tidegs_store.h \
+                     $(PKG)/csrc/tidegs_order.cu \
                      $(PKG)/csrc/tidegs_internal.h include/tidegs.h
 	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(PKG)/csrc/tidegs_kernels.cu \
-	    $(PKG)/csrc/tidegs_runtime.cu $(PKG)/csrc/tidegs_store.cpp -lpthread 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
+	    $(PKG)/csrc/tidegs_runtime.cu $(PKG)/csrc/tidegs_store.cpp $(PKG)/csrc/tidegs_order.cu \
+	    -lpthread 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
 
 clean:
 	rm -f workload/*.so oracle/*.so $(PKG)/*.so

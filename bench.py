@@ -61,6 +61,13 @@ def parse():
                     help="NEXT f2: conservative bound refresh after every update (R25)")
     ap.add_argument("--fine-filter", action="store_true",
                     help="NEXT f1: Level-2 filter -> I_t mask -> masked Adam in every step")
+    ap.add_argument("--store", default=None, metavar="DIR",
+                    help="NEXT f3: the shard lives in a log-structured store under DIR (SSD) "
+                         "below a CPU cache of --cache-blocks records (PAPER.md:224-251)")
+    ap.add_argument("--cache-blocks", type=int, default=0,
+                    help="CPU-cache records for --store (0 -> 3x the GPU capacity)")
+    ap.add_argument("--store-buffered", action="store_true",
+                    help="--store through the page cache instead of O_DIRECT")
     return ap.parse_args()
 
 
@@ -223,6 +230,10 @@ def _config_dict_base(args, wl, ws):
             "I_t": "Level-2 fine filter (f1)" if getattr(args, "fine_filter", False) else "all rows of R n K (mask NULL)",
             "l2": "inputs larger than L2 (Adam touches GBs per step)",
             "grads": "synthetic counter-hash gradients resident in the grad pool (renderer out of scope)",
+            "host_tier": ("pinned host copy of the shard" if not getattr(args, "store", None) else
+                          f"NEXT f3 store: CPU cache of {args.cache_blocks} block records over "
+                          f"{'buffered' if args.store_buffered else 'O_DIRECT'} log-structured "
+                          "segments (base + patches) on local disk"),
             "seeds": W.SEEDS}
 
 
@@ -280,11 +291,20 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
     build_ms = None
+    store = None
+    if args.store:
+        if not args.cache_blocks:
+            args.cache_blocks = 3 * cap
+        store = dict(dir=os.path.join(args.store, f"rank{shard_rank:03d}"),
+                     cache_blocks=args.cache_blocks, direct_io=0 if args.store_buffered else 1)
+        os.makedirs(args.store, exist_ok=True)
     if wl.build:  # f2b: Morton-sort + block the unsorted scene on the GPU
         perm, bounds, build_ms = T.build_layout(sc.table_cs(), sc.B, local)
-        table = T.Table(cfg, bounds, fill=sc.perm_fill(perm), stream=stream.cuda_stream)
+        table = T.Table(cfg, bounds, fill=sc.perm_fill(perm), stream=stream.cuda_stream,
+                        store=store)
     else:
-        table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream)
+        table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream,
+                        store=store)
     setup_s = time.perf_counter() - t_setup
     # synthetic gradients for every slot, written once (renderer out of scope)
     P_ = table.P
@@ -331,6 +351,7 @@ def main():
     torch.cuda.synchronize()
     table.set_profiling(True)
     st0 = table.stats()
+    ss0 = table.store_stats() if store else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -343,6 +364,17 @@ def main():
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
     st1 = table.stats()
+    store_detail = None
+    if store:
+        ss1 = table.store_stats()
+        dd = {k: ss1[k] - ss0[k] for k in ss1 if k not in ("cached", "cached_dirty")}
+        store_detail = {"per_step": {k: v / args.steps for k, v in dd.items()},
+                        "hit_rate": dd["hits"] / max(1, dd["hits"] + dd["misses"]),
+                        "ssd_read_GBps_in_reads": (dd["read_bytes"] / (dd["read_ms"] / 1e3) / 1e9
+                                                   if dd["read_ms"] else None),
+                        "ssd_write_GBps_in_appends": (dd["write_bytes"] / (dd["write_ms"] / 1e3)
+                                                      / 1e9 if dd["write_ms"] else None),
+                        "cached": ss1["cached"], "cached_dirty": ss1["cached_dirty"]}
     tm = table.timing()
     rows = st1["n_active_rows"] - st0["n_active_rows"]
     h2d = st1["h2d_bytes"] - st0["h2d_bytes"]
@@ -449,9 +481,13 @@ def main():
                            "h2d_ms_per_step": tm["h2d_ms"] / args.steps,
                            "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
                            "copy_calls_per_step": tm["copy_calls"] / args.steps,
-                           "setup_s": setup_s, "layout_build_gpu_ms": build_ms}}
+                           "setup_s": setup_s, "layout_build_gpu_ms": build_ms,
+                           "store": store_detail}}
         print(json.dumps(line), flush=True)
     table.close()
+    if store:
+        import shutil
+        shutil.rmtree(store["dir"], ignore_errors=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 

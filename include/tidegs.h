@@ -295,6 +295,24 @@ uint32_t tgs_pool_slots(const tgs_ctx* ctx);
 tgs_status tgs_build_layout(const float* cs, uint64_t n, uint32_t block_size, int device,
                             uint64_t* perm, float* bounds, double* gpu_ms);
 
+/* NEXT f4 -- clustered-TSP view ordering ("We use a clustered
+ * TSP-ordered (no-shuffle) camera sequence to increase overlap between
+ * consecutive block working sets", 709-712; reading R29 of DESIGN.md §3), on
+ * the GPU.  feat: host [M][D] doubles (D in [1, 8]) describing each training
+ * view's pose (e.g. camera centre and a point on its optical axis).  k =
+ * ceil(sqrt(M)) k-means clusters (maximin initialisation from the
+ * lexicographically smallest view, Lloyd iterations until no assignment
+ * changes, at most 100), a nearest-neighbour tour over the cluster centres and
+ * nearest-neighbour tours inside each cluster; every distance a
+ * feature-ordered sum of squares in double without FMA, every tie to the
+ * lowest index.  Outputs (host, caller-owned): perm[M] = the view to present
+ * at position i; cluster[M] (may be NULL); k_out, iters_out (Lloyd passes that
+ * changed something), gpu_ms (device time; each may be NULL).  EINVAL: M == 0,
+ * D outside [1, 8], non-finite feature, k*D doubles over 200 KB.  Stateless. */
+tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D, int device, uint32_t* perm,
+                           uint32_t* cluster, uint32_t* k_out, uint32_t* iters_out,
+                           double* gpu_ms);
+
 /* Frustum planes of a pinhole camera (R1): w2c row-major 4x4 world->camera
  * (camera +z forward, +x right, +y down), intrinsics fx, fy, cx, cy, image
  * width x height, near/far.  Computed in double, rounded to fp32. */

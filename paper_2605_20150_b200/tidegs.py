@@ -29,7 +29,8 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_get_percam", "tgs_get_evicted_dirty", "tgs_get_slot_map",
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
            "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error",
-           "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru")
+           "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru",
+           "tgs_order_views")
 
 
 class Config(C.Structure):
@@ -167,6 +168,10 @@ def lib():
                                        C.POINTER(C.c_double)]
         L.tgs_frustum_planes.argtypes = [C.POINTER(C.c_double)] + [C.c_double] * 4 + [
             u32, u32, C.c_double, C.c_double, C.POINTER(Camera)]
+        L.tgs_order_views.argtypes = [C.POINTER(C.c_double), u32, u32, C.c_int,
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_double)]
         L.tgs_status_string.restype = C.c_char_p
         L.tgs_status_string.argtypes = [C.c_int]
         L.tgs_last_error.restype = C.c_char_p
@@ -415,3 +420,19 @@ def build_layout(cs: np.ndarray, block_size: int, device: int = 0):
     if rc != OK:
         raise TgsError(rc, "tgs_build_layout")
     return perm, bounds, ms.value
+
+
+def order_views(feat: np.ndarray, device: int = 0):
+    """NEXT f4 on the GPU: clustered-TSP view order (tgs_order_views):
+    (perm, cluster, k, lloyd_iterations, gpu_ms)."""
+    f = np.ascontiguousarray(feat, np.float64)
+    M, D = f.shape
+    perm = np.empty(M, np.uint32)
+    cl = np.empty(M, np.uint32)
+    k, it, ms = C.c_uint32(), C.c_uint32(), C.c_double()
+    u32p = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint32))
+    rc = lib().tgs_order_views(f.ctypes.data_as(C.POINTER(C.c_double)), M, D, device, u32p(perm),
+                               u32p(cl), C.byref(k), C.byref(it), C.byref(ms))
+    if rc != OK:
+        raise TgsError(rc, "tgs_order_views")
+    return perm, cl, int(k.value), int(it.value), ms.value
