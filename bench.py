@@ -68,6 +68,8 @@ def parse():
                     help="CPU-cache records for --store (0 -> 3x the GPU capacity)")
     ap.add_argument("--store-buffered", action="store_true",
                     help="--store through the page cache instead of O_DIRECT")
+    ap.add_argument("--io-threads", type=int, default=0,
+                    help="parallel SSD requests of the --store tier (0 -> library default)")
     return ap.parse_args()
 
 
@@ -142,6 +144,20 @@ def link_peak(torch, dev):
     return best
 
 
+def ssd_read_peak(path, gib=4):
+    """Measured sequential O_DIRECT read bandwidth (GB/s) of the store's disk:
+    dd of the first GiBs of the base segment in 16 MiB requests."""
+    try:
+        out = subprocess.run(["dd", f"if={path}", "of=/dev/null", "bs=16M", f"count={64 * gib}",
+                              "iflag=direct"], capture_output=True, text=True, timeout=120).stderr
+        line = [x for x in out.splitlines() if "copied" in x][-1]
+        nbytes = float(line.split()[0])
+        secs = float(line.split(",")[-2].split()[0])
+        return nbytes / secs / 1e9
+    except Exception:
+        return None
+
+
 def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -161,6 +177,8 @@ def run_reference(args, ws, rank):
     wl = W.CONFIGS[args.config]
     sc = wl.scene()
     tr = wl.trajectory(sc)
+    if wl.tsp:  # f4 on the reference arm: the oracle's clustered-TSP order
+        tr.reorder(O.order_views(tr.features(150.0 if wl.traj == "aerial" else 20.0))[0])
     moments = O.COLD_RESTART if args.moments == "cold" else O.PERSIST
     o = O.Oracle(O.make_config(sc.N, sc.B, wl.capacity, moments=moments), sc.bounds(),
                  fill=None, track_all=True)
@@ -219,8 +237,10 @@ def _config_dict(args, wl, ws):
 
 
 def _config_dict_base(args, wl, ws):
+    order = ("shuffled, then clustered-TSP order (f4)" if wl.tsp else
+             "random" if wl.shuffled else "smooth")
     return {"workload": f"{wl.name}: {wl.n_gaussians:,} Gaussians, {wl.traj} trajectory "
-                        f"({'random' if wl.shuffled else 'smooth'} order), J={wl.J} cameras/batch",
+                        f"({order} order), J={wl.J} cameras/batch",
             "n_gaussians": wl.n_gaussians, "block_size": wl.block_size, "J": wl.J,
             "capacity_blocks_per_gpu": -(-wl.capacity // ws), "moments": args.moments,
             "policy": "restage-all (w/o Tide)" if getattr(args, "no_tide", False) else "tide",
@@ -280,6 +300,11 @@ def main():
     wl = W.CONFIGS[args.config]
     sc = wl.scene()
     tr = wl.trajectory(sc)
+    order_ms = None
+    if wl.tsp:  # f4: clustered-TSP order of the (shuffled) views, on the GPU
+        focus = 150.0 if wl.traj == "aerial" else 20.0
+        perm, _, _, _, order_ms = T.order_views(tr.features(focus), local)
+        tr.reorder(perm)
     shard_ws, shard_rank = (args.shard_of, 0) if args.shard_of > 1 and ws == 1 else (ws, rank)
     cap = -(-wl.capacity // shard_ws)
     moments = T.COLD_RESTART if args.moments == "cold" else T.PERSIST
@@ -296,7 +321,8 @@ def main():
         if not args.cache_blocks:
             args.cache_blocks = 3 * cap
         store = dict(dir=os.path.join(args.store, f"rank{shard_rank:03d}"),
-                     cache_blocks=args.cache_blocks, direct_io=0 if args.store_buffered else 1)
+                     cache_blocks=args.cache_blocks, direct_io=0 if args.store_buffered else 1,
+                     io_threads=args.io_threads)
         os.makedirs(args.store, exist_ok=True)
     if wl.build:  # f2b: Morton-sort + block the unsorted scene on the GPU
         perm, bounds, build_ms = T.build_layout(sc.table_cs(), sc.B, local)
@@ -448,6 +474,8 @@ def main():
             "algorithmic_bytes_per_launch": (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM,
             "avg_launch_ms": adam_ms}
     lp = link_peak(torch, dev) if rank == 0 else None
+    if store and store_detail is not None:
+        store_detail["ssd_read_peak_GBps"] = ssd_read_peak(os.path.join(store["dir"], "base.tdgs"))
     link = None
     if rank == 0:
         h2d_rate = tm["h2d_bytes"] / (tm["h2d_ms"] / 1e3) / 1e9 if tm["h2d_ms"] else None
@@ -482,6 +510,7 @@ def main():
                            "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
                            "copy_calls_per_step": tm["copy_calls"] / args.steps,
                            "setup_s": setup_s, "layout_build_gpu_ms": build_ms,
+                           "view_order_gpu_ms": order_ms,
                            "store": store_detail}}
         print(json.dumps(line), flush=True)
     table.close()

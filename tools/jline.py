@@ -1,0 +1,18 @@
+"""Print the key numbers of one bench JSON line: python tools/jline.py FILE"""
+import json
+import sys
+
+d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+det = d.get("detail", {})
+out = {"value_G/s": round(d["value"] / 1e9, 4), "ms/step": round(d["ms_per_step"], 3),
+       "adam_frac": round(d["roofline"]["frac"], 3), "S+/step": det.get("stage_in_blocks_per_step"),
+       "active/step": det.get("active_blocks_per_step"),
+       "e2e_G/s": round(d["e2e"]["value"] / 1e9, 4) if d.get("e2e") else None,
+       "order_ms": det.get("view_order_gpu_ms")}
+st = det.get("store")
+if st:
+    out.update({"hit_rate": round(st["hit_rate"], 3), "ssd_read_GBps": st["ssd_read_GBps_in_reads"],
+                "ssd_peak": st.get("ssd_read_peak_GBps"),
+                "read_ms/step": st["per_step"]["read_ms"], "misses/step": st["per_step"]["misses"],
+                "dirty_evict/step": st["per_step"]["dirty_evictions"]})
+print(json.dumps(out))

@@ -268,6 +268,7 @@ class Workload:
     shuffled: bool = False
     scene_kw: tuple = ()
     build: bool = False      # NEXT f2b: Morton-build the (unsorted) table at setup
+    tsp: bool = False        # NEXT f4: reorder the views by the clustered TSP at setup
 
     def scene(self) -> Scene:
         return Scene(self.n_gaussians, self.block_size, side=self.side, **dict(self.scene_kw))
@@ -297,6 +298,9 @@ CONFIGS = {
     "300m": Workload("300m", 300_000_000, 4096, 2800.0, "aerial", 64, 6309, _AERIAL),
     "300m_random": Workload("300m_random", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
                             _AERIAL, True),
+    # the shuffled views re-ordered by the clustered TSP on the GPU at setup (f4)
+    "300m_tsp": Workload("300m_tsp", 300_000_000, 4096, 2800.0, "aerial", 64, 6309, _AERIAL,
+                         True, (), False, True),
     # ablation "w/o Morton": no spatial sort before blocking
     "300m_nomorton": Workload("300m_nomorton", 300_000_000, 4096, 2800.0, "aerial", 64, 6309,
                               _AERIAL, False, (("layout", 1),)),
