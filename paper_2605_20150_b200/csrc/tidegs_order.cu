@@ -84,6 +84,8 @@ struct Ctl {
   uint32_t changed;     // Lloyd: an assignment changed in this pass
   uint32_t done_ctas;   // last-CTA-done counter
   uint32_t n_tour;      // non-empty clusters in the tour
+  uint32_t stop;        // Lloyd converged
+  uint32_t iters;       // Lloyd passes that changed an assignment
 };
 
 __device__ __forceinline__ bool lex_less(const double* f, int D, uint32_t a, uint32_t b) {
@@ -161,9 +163,12 @@ __global__ void k_init_step(const double* f, uint32_t M, int D, double* mind, do
   }
 }
 
-// Lloyd assignment: nearest centre (ties lowest), change flag
+// Lloyd assignment: nearest centre (ties lowest), change flag.  Every Lloyd
+// pass is enqueued up front; once a pass changes nothing (ctl->stop) the
+// remaining launches return at once, so the host never waits per pass.
 __global__ void k_assign(const double* f, uint32_t M, int D, const double* cen, uint32_t k,
                          uint32_t* asg, Ctl* ctl) {
+  if (ctl->stop) return;
   extern __shared__ double sc[];
   for (uint32_t i = threadIdx.x; i < k * D; i += blockDim.x) sc[i] = cen[i];
   __syncthreads();
@@ -183,33 +188,57 @@ __global__ void k_assign(const double* f, uint32_t M, int D, const double* cen, 
   if (__syncthreads_or(ch) && threadIdx.x == 0) atomicOr(&ctl->changed, 1u);
 }
 
-// Lloyd update: cluster j's centre = mean of its members, summed in ascending
-// view index (one thread per cluster; the warp reads asg[v] as a broadcast)
-__global__ void k_update(const double* f, uint32_t M, int D, double* cen, uint32_t k,
-                         const uint32_t* asg, uint32_t* cnt_out) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= k) return;
-  double s[kMaxD];
-  for (int i = 0; i < D; ++i) s[i] = 0.0;
-  uint32_t n = 0;
-  for (uint32_t v = 0; v < M; ++v) {
-    if (__ldg(asg + v) != j) continue;
-    for (int i = 0; i < D; ++i) s[i] = __dadd_rn(s[i], f[(size_t)v * D + i]);
-    ++n;
+// end of a pass: stop when nothing changed, else count the pass and re-arm
+__global__ void k_lloyd_check(Ctl* ctl) {
+  if (ctl->stop) return;
+  if (!ctl->changed) {
+    ctl->stop = 1u;
+  } else {
+    ctl->iters += 1;
+    ctl->changed = 0u;
   }
-  if (n && cen)
-    for (int i = 0; i < D; ++i) cen[(size_t)j * D + i] = __ddiv_rn(s[i], (double)n);
-  if (cnt_out) cnt_out[j] = n;
 }
 
-// ascending member list of cluster j at off[j]
+// Lloyd update: cluster j's centre = mean of its members, summed in ascending
+// view index.  One warp per cluster: 32 assignments per ballot, then lane i
+// (i < D) adds feature i of each member in ascending order -- the sequential
+// sum of R29, 32x fewer serial steps than a thread scanning every view.
+__global__ void k_update(const double* f, uint32_t M, int D, double* cen, uint32_t k,
+                         const uint32_t* asg, uint32_t* cnt_out, const Ctl* ctl) {
+  if (ctl && ctl->stop) return;
+  const uint32_t j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (j >= k) return;
+  double s = 0.0;
+  uint32_t n = 0;
+  for (uint32_t base = 0; base < M; base += 32) {
+    const uint32_t v = base + lane;
+    uint32_t hit = __ballot_sync(0xffffffffu, v < M && __ldg(asg + v) == j);
+    n += __popc(hit);
+    while (hit) {
+      const uint32_t u = base + __ffs(hit) - 1;
+      hit &= hit - 1;
+      if (lane < (uint32_t)D) s = __dadd_rn(s, f[(size_t)u * D + lane]);
+    }
+  }
+  if (n && cen && lane < (uint32_t)D) cen[(size_t)j * D + lane] = __ddiv_rn(s, (double)n);
+  if (cnt_out && lane == 0) cnt_out[j] = n;
+}
+
+// ascending member list of cluster j at off[j] (one warp per cluster, ballot compaction)
 __global__ void k_members(uint32_t M, uint32_t k, const uint32_t* asg, const uint32_t* off,
                           uint32_t* mem) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
   if (j >= k) return;
   uint32_t o = off[j];
-  for (uint32_t v = 0; v < M; ++v)
-    if (__ldg(asg + v) == j) mem[o++] = v;
+  for (uint32_t base = 0; base < M; base += 32) {
+    const uint32_t v = base + lane;
+    const bool in = v < M && __ldg(asg + v) == j;
+    const uint32_t hit = __ballot_sync(0xffffffffu, in);
+    if (in) mem[o + __popc(hit & ((1u << lane) - 1u))] = v;
+    o += __popc(hit);
+  }
 }
 
 // nearest-neighbour tour over the non-empty centres from the cluster of v0
@@ -348,30 +377,28 @@ extern "C" tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D
   for (uint32_t j = 0; j < k; ++j)  // R29 step 2
     k_init_step<<<grid, kNT, 0, s>>>(d_f, M, (int)D, d_mind, d_cen, j, (Best*)d_part, d_ctl);
   CKO(cudaGetLastError());
-  for (it = 0; it < 100; ++it) {  // R29 step 3
-    CKO(cudaMemsetAsync(&d_ctl->changed, 0, 4, s));
+  for (uint32_t pass = 0; pass < 100; ++pass) {  // R29 step 3, no host round trip per pass
     k_assign<<<grid, kNT, smem, s>>>(d_f, M, (int)D, d_cen, k, d_asg, d_ctl);
-    CKO(cudaMemcpyAsync(&h_ctl->changed, &d_ctl->changed, 4, cudaMemcpyDeviceToHost, s));
-    CKO(cudaStreamSynchronize(s));
-    if (!h_ctl->changed) break;
-    k_update<<<(k + 127) / 128, 128, 0, s>>>(d_f, M, (int)D, d_cen, k, d_asg, nullptr);
-    CKO(cudaGetLastError());
+    k_lloyd_check<<<1, 1, 0, s>>>(d_ctl);
+    k_update<<<(k + 7) / 8, 256, 0, s>>>(d_f, M, (int)D, d_cen, k, d_asg, nullptr, d_ctl);
   }
+  CKO(cudaGetLastError());
   {
     // member lists (counting-sort offsets), cluster tour, tours inside clusters
-    k_update<<<(k + 127) / 128, 128, 0, s>>>(d_f, M, (int)D, nullptr, k, d_asg, d_cnt);
+    k_update<<<(k + 7) / 8, 256, 0, s>>>(d_f, M, (int)D, nullptr, k, d_asg, d_cnt, nullptr);
     std::vector<uint32_t> cnt(k), off(k);
     CKO(cudaMemcpyAsync(cnt.data(), d_cnt, k * 4, cudaMemcpyDeviceToHost, s));
     CKO(cudaStreamSynchronize(s));
     uint32_t acc = 0;
     for (uint32_t j = 0; j < k; ++j) off[j] = acc, acc += cnt[j];
     CKO(cudaMemcpyAsync(d_off, off.data(), k * 4, cudaMemcpyHostToDevice, s));
-    k_members<<<(k + 127) / 128, 128, 0, s>>>(M, k, d_asg, d_off, d_mem);
+    k_members<<<(k + 7) / 8, 256, 0, s>>>(M, k, d_asg, d_off, d_mem);
     k_cluster_tour<<<1, 1024, 0, s>>>(d_cen, (int)D, k, d_cnt, d_asg, d_tour, d_used + M, d_ctl);
     std::vector<uint32_t> tour(k);
     CKO(cudaMemcpyAsync(tour.data(), d_tour, k * 4, cudaMemcpyDeviceToHost, s));
     CKO(cudaMemcpyAsync(h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
     CKO(cudaStreamSynchronize(s));
+    it = h_ctl->iters;
     std::vector<uint32_t> toff(k, 0);
     acc = 0;
     for (uint32_t c = 0; c < h_ctl->n_tour; ++c) toff[c] = acc, acc += cnt[tour[c]];

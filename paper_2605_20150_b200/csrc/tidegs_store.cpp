@@ -290,34 +290,40 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
     put64(h + 16, index_[recs[i].first].version);
     put64(h + 24, payload_);
   }
+  // consecutive records of one segment form one pwritev (header page +
+  // payload per record, up to 16 MiB); the runs are spread over the pool
+  constexpr uint64_t kRunBytes = 16ull << 20;
+  constexpr size_t kMaxRec = 64;
+  std::vector<std::pair<size_t, size_t>> runs;
+  for (size_t i = 0; i < recs.size();) {
+    size_t j = i + 1;
+    while (j < recs.size() && j - i < kMaxRec && fd[j] == fd[i] &&
+           off[j] == off[j - 1] + kPage + S_ && (j - i + 1) * (kPage + S_) <= kRunBytes)
+      ++j;
+    runs.push_back({i, j});
+    i = j;
+  }
   std::atomic<bool> bad{false};
-  pool_io_->parallel_for((uint32_t)recs.size(), [&](uint32_t i) {
-    iovec iov[2];
-    iov[0].iov_base = hdr_pages_ + i * kPage;
-    iov[0].iov_len = kPage;
-    iov[1].iov_base = pool_ + (uint64_t)recs[i].second * S_;
-    iov[1].iov_len = S_;
-    uint64_t done = 0, total = kPage + S_;
-    while (done < total) {
-      const ssize_t w = ::pwritev(fd[i], iov, 2, (off_t)(off[i] + done));
-      if (w <= 0) {
-        if (w < 0 && errno == EINTR) continue;
-        bad = true;
-        return;
-      }
-      done += (uint64_t)w;
-      if (done < total) {  // short write: finish the rest with plain pwrite
-        const uint64_t o = off[i] + done;
-        if (done < kPage) {
-          if (!pwrite_all(fd[i], hdr_pages_ + i * kPage + done, kPage - done, o) ||
-              !pwrite_all(fd[i], iov[1].iov_base, S_, off[i] + kPage))
-            bad = true;
-        } else if (!pwrite_all(fd[i], (char*)iov[1].iov_base + (done - kPage), total - done, o)) {
-          bad = true;
-        }
-        return;
-      }
+  pool_io_->parallel_for((uint32_t)runs.size(), [&](uint32_t r) {
+    const size_t b = runs[r].first, e = runs[r].second;
+    iovec iov[2 * kMaxRec];
+    int n = 0;
+    for (size_t i = b; i < e; ++i) {
+      iov[n].iov_base = hdr_pages_ + i * kPage;
+      iov[n++].iov_len = kPage;
+      iov[n].iov_base = pool_ + (uint64_t)recs[i].second * S_;
+      iov[n++].iov_len = S_;
     }
+    const uint64_t total = (uint64_t)(e - b) * (kPage + S_);
+    ssize_t w;
+    do {
+      w = ::pwritev(fd[b], iov, n, (off_t)off[b]);
+    } while (w < 0 && errno == EINTR);
+    if (w == (ssize_t)total) return;
+    for (size_t i = b; i < e; ++i)  // short or failed vector write: record by record
+      if (!pwrite_all(fd[i], hdr_pages_ + i * kPage, kPage, off[i]) ||
+          !pwrite_all(fd[i], pool_ + (uint64_t)recs[i].second * S_, S_, off[i] + kPage))
+        bad = true;
   });
   return bad ? errno_str("append patch record") : "";
 }
@@ -376,18 +382,74 @@ std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
   }
   if (!misses.empty()) {  // fetched through Index[k]
     const auto t0 = std::chrono::steady_clock::now();
-    std::atomic<bool> bad{false};
-    pool_io_->parallel_for((uint32_t)misses.size(), [&](uint32_t i) {
-      const StoreIndex& ix = index_[misses[i].first];
-      const int fd = fd_of(ix.file_id);
-      if (fd < 0 || !pread_all(fd, pool_ + (uint64_t)misses[i].second * S_, S_, ix.offset))
-        bad = true;
-    });
-    if (bad) return errno_str("read block record");
+    std::string err = read_records(misses);
+    if (!err.empty()) return err;
     cnt_.read_bytes += misses.size() * S_;
     cnt_.read_ms += ms_since(t0);
   }
   return "";
+}
+
+// Reads the newest version of each (block, entry) into its entry.  Records
+// that are neighbours in one segment (consecutive base records, or patch
+// records separated only by their header page) are read by one preadv into
+// the scattered entries (header pages into a scratch page), up to kRunBytes,
+// so the device sees large requests; the runs are spread over the pool.
+std::string BlockStore::read_records(const std::vector<std::pair<uint32_t, int32_t>>& recs) {
+  constexpr uint64_t kRunBytes = 16ull << 20;
+  constexpr int kMaxIov = 256;
+  struct Item { uint32_t fid; uint64_t off; int32_t e; };
+  std::vector<Item> it(recs.size());
+  for (size_t i = 0; i < recs.size(); ++i) {
+    const StoreIndex& ix = index_[recs[i].first];
+    it[i] = {ix.file_id, ix.offset, recs[i].second};
+    if (fd_of(ix.file_id) < 0) return errno_str("open segment");  // opened serially
+  }
+  std::sort(it.begin(), it.end(), [](const Item& a, const Item& b) {
+    return a.fid != b.fid ? a.fid < b.fid : a.off < b.off;
+  });
+  std::vector<std::pair<size_t, size_t>> runs;  // [begin, end) into it
+  for (size_t i = 0; i < it.size();) {
+    size_t j = i + 1;
+    uint64_t end = it[i].off + S_;
+    int iov = 1;
+    while (j < it.size() && it[j].fid == it[i].fid && end - it[i].off + S_ + kPage <= kRunBytes &&
+           iov + 2 <= kMaxIov && (it[j].off == end || it[j].off == end + kPage)) {
+      iov += it[j].off == end ? 1 : 2;
+      end = it[j].off + S_;
+      ++j;
+    }
+    runs.push_back({i, j});
+    i = j;
+  }
+  std::atomic<bool> bad{false};
+  pool_io_->parallel_for((uint32_t)runs.size(), [&](uint32_t r) {
+    thread_local std::unique_ptr<char, decltype(&free)> scratch(aligned_pages(kPage), &free);
+    const size_t b = runs[r].first, e = runs[r].second;
+    const int fd = fds_[it[b].fid];
+    iovec iov[kMaxIov];
+    int n = 0;
+    uint64_t total = 0, pos = it[b].off;
+    for (size_t i = b; i < e; ++i) {
+      if (it[i].off != pos) {  // a patch record's header page between two payloads
+        iov[n].iov_base = scratch.get();
+        iov[n++].iov_len = kPage;
+        total += kPage;
+      }
+      iov[n].iov_base = pool_ + (uint64_t)it[i].e * S_;
+      iov[n++].iov_len = S_;
+      total += S_;
+      pos = it[i].off + S_;
+    }
+    ssize_t got;
+    do {
+      got = ::preadv(fd, iov, n, (off_t)it[b].off);
+    } while (got < 0 && errno == EINTR);
+    if (got == (ssize_t)total) return;
+    for (size_t i = b; i < e; ++i)  // short or failed vector read: record by record
+      if (!pread_all(fd, pool_ + (uint64_t)it[i].e * S_, S_, it[i].off)) bad = true;
+  });
+  return bad ? errno_str("read block record") : "";
 }
 
 void BlockStore::touch_evicted(const uint32_t* sm, uint32_t n, int32_t T) {

@@ -129,6 +129,7 @@ class BlockStore {
   // reserves the next record of the patch log for block l: (fd, file offset of the record)
   std::string reserve_append(uint32_t l, int& fd, uint64_t& rec_off);
   std::string write_records(const std::vector<std::pair<uint32_t, int32_t>>& recs /* (l, entry) */);
+  std::string read_records(const std::vector<std::pair<uint32_t, int32_t>>& recs /* (l, entry) */);
 
   Geometry g_{};
   std::string dir_;
