@@ -1,0 +1,47 @@
+"""SSD roofline for the f3 store's access pattern: O_DIRECT reads of whole
+block records (the payload S of one cache entry) at random record offsets of a
+base segment, at several queue depths (threads), against one large sequential
+stream.  python tools/ssd_probe.py BASE_SEGMENT RECORD_BYTES"""
+import mmap
+import os
+import random
+import sys
+import threading
+import time
+
+path, S = sys.argv[1], int(sys.argv[2])
+size = os.path.getsize(path)
+n_rec = (size - 4096) // S
+fd = os.open(path, os.O_RDONLY | os.O_DIRECT)
+
+
+def run(qd, n_reads, seq=False, req=S):
+    offs = [4096 + i * req for i in range(n_reads)] if seq else \
+        [4096 + random.Random(qd).randrange(n_rec) * S for _ in range(n_reads)]
+    bufs = [mmap.mmap(-1, req) for _ in range(qd)]
+    nxt = [0]
+    lock = threading.Lock()
+
+    def work(b):
+        while True:
+            with lock:
+                i = nxt[0]
+                nxt[0] += 1
+            if i >= len(offs):
+                return
+            os.preadv(fd, [b], offs[i])
+
+    th = [threading.Thread(target=work, args=(bufs[q],)) for q in range(qd)]
+    t = time.perf_counter()
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    dt = time.perf_counter() - t
+    return len(offs) * req / dt / 1e9
+
+
+print(f"records {n_rec} x {S} B")
+print(f"sequential 16 MiB QD1: {run(1, 256, True, 16 << 20):.2f} GB/s")
+for qd in (1, 2, 4, 8, 16, 32):
+    print(f"random records QD{qd}: {run(qd, 400):.2f} GB/s")
