@@ -10,6 +10,17 @@ import threading
 import time
 
 path, S = sys.argv[1], int(sys.argv[2])
+if len(sys.argv) > 3:  # create a test file of that many GiB (incompressible data, O_DIRECT)
+    gib = int(sys.argv[3])
+    buf = mmap.mmap(-1, 16 << 20)
+    buf.write(os.urandom(16 << 20))
+    wfd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC | os.O_DIRECT, 0o644)
+    t = time.perf_counter()
+    for i in range(gib * 64):
+        os.pwritev(wfd, [buf], i * (16 << 20))
+    os.fsync(wfd)
+    os.close(wfd)
+    print(f"created {gib} GiB: sequential O_DIRECT write {gib * 2**30 / (time.perf_counter() - t) / 1e9:.2f} GB/s")
 size = os.path.getsize(path)
 n_rec = (size - 4096) // S
 fd = os.open(path, os.O_RDONLY | os.O_DIRECT)
