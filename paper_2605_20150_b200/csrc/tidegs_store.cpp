@@ -183,9 +183,15 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
 
   // "The initial model is written once as an immutable base segment"
   // (PAPER.md:228): header page, record l at 4096 + l*S; Index[l] = (0, off, size, 0)
-  const int fd = ::open((dir + "/base.tdgs").c_str(),
-                        O_RDWR | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
-  if (fd < 0) return errno_str(direct ? "open base.tdgs (O_DIRECT)" : "open base.tdgs");
+  int fd = ::open((dir + "/base.tdgs").c_str(),
+                  O_RDWR | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
+  if (fd < 0 && direct && errno == EINVAL) {  // e.g. tmpfs: no O_DIRECT, use the page cache
+    std::fprintf(stderr, "tidegs: store: %s does not support O_DIRECT; using buffered I/O\n",
+                 dir.c_str());
+    direct_ = false;
+    fd = ::open((dir + "/base.tdgs").c_str(), O_RDWR | O_CREAT | O_TRUNC, 0644);
+  }
+  if (fd < 0) return errno_str("open base.tdgs");
   fds_.assign(1, fd);
   std::unique_ptr<char, decltype(&free)> hp(aligned_pages(kPage), &free);
   segment_header(reinterpret_cast<unsigned char*>(hp.get()), 0, g);
