@@ -32,6 +32,9 @@ IoPool::~IoPool() {
   for (auto& t : th_) t.join();
 }
 
+// Every worker takes part in every generation and acknowledges it; the caller
+// returns only after all of them have, so no worker can still hold the
+// previous generation's function when the next parallel_for starts.
 void IoPool::worker() {
   uint64_t seen = 0;
   for (;;) {
@@ -44,12 +47,11 @@ void IoPool::worker() {
       seen = gen_;
       fn = fn_;
       n = n_;
-      ++busy_;
     }
     for (uint32_t i; (i = next_.fetch_add(1)) < n;) (*fn)(i);
     {
       std::lock_guard<std::mutex> g(mu_);
-      --busy_;
+      ++acked_;
     }
     done_cv_.notify_all();
   }
@@ -62,12 +64,13 @@ void IoPool::parallel_for(uint32_t n, const std::function<void(uint32_t)>& fn) {
     fn_ = &fn;
     n_ = n;
     next_ = 0;
+    acked_ = 0;
     ++gen_;
   }
   cv_.notify_all();
   for (uint32_t i; (i = next_.fetch_add(1)) < n;) fn(i);
   std::unique_lock<std::mutex> g(mu_);
-  done_cv_.wait(g, [&] { return busy_ == 0; });
+  done_cv_.wait(g, [&] { return acked_ == th_.size(); });
   fn_ = nullptr;
 }
 

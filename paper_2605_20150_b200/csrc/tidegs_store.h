@@ -43,7 +43,7 @@ class IoPool {
   const std::function<void(uint32_t)>* fn_ = nullptr;
   uint32_t n_ = 0;
   std::atomic<uint32_t> next_{0};
-  uint32_t busy_ = 0;
+  size_t acked_ = 0;  // workers done with the current generation
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
