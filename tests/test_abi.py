@@ -100,3 +100,34 @@ def test_frustum_planes_helper_matches_pinhole_geometry():
         elif (d > margin).all():
             raise AssertionError(f"point {p} outside the frustum is inside all planes")
     assert T.lib().tgs_frustum_planes(None, 1, 1, 0, 0, 1, 1, 0.1, 1.0, None) == T.EINVAL
+
+
+def test_store_config_is_validated_before_the_device(tmp_path):
+    """f3: NULL store / dir, or a CPU cache smaller than 2C (R27), is EINVAL."""
+    cfg = T.make_config(64, 16, 2)
+    b = np.zeros((4, 4), np.float32)
+    rows = np.zeros((64, 59), np.float32)
+    h = C.c_void_p()
+    bp = b.ctypes.data_as(C.POINTER(C.c_float))
+    L = T.lib()
+    assert L.tgs_init_table_store(C.byref(cfg), None, rows.ctypes.data, None, None, bp, None, None,
+                                  C.byref(h)) == T.EINVAL
+    for d, H in ((None, 4), (os.fsencode(str(tmp_path)), 3)):
+        sc = T.StoreConfig(d, H, 0, 1, 0)
+        assert L.tgs_init_table_store(C.byref(cfg), C.byref(sc), rows.ctypes.data, None, None, bp,
+                                      None, None, C.byref(h)) == T.EINVAL
+    assert not os.listdir(tmp_path)  # nothing written
+
+
+def test_order_views_validates_inputs():
+    """f4: M = 0, D outside [1, 8], non-finite features are EINVAL (before the device)."""
+    L = T.lib()
+    u = (C.c_uint32 * 4)()
+    f = np.zeros((4, 3))
+    fp = f.ctypes.data_as(C.POINTER(C.c_double))
+    assert L.tgs_order_views(fp, 0, 3, 0, u, None, None, None, None) == T.EINVAL
+    assert L.tgs_order_views(fp, 4, 0, 0, u, None, None, None, None) == T.EINVAL
+    assert L.tgs_order_views(fp, 1, 9, 0, u, None, None, None, None) == T.EINVAL
+    f[1, 2] = np.inf
+    assert L.tgs_order_views(fp, 4, 3, 0, u, None, None, None, None) == T.EINVAL
+    assert L.tgs_order_views(None, 4, 3, 0, u, None, None, None, None) == T.EINVAL
