@@ -17,6 +17,7 @@
 //   k_members      : thread per cluster: ascending member lists (counting-sort offsets)
 //   k_cluster_tour : one CTA, nearest-neighbour over the non-empty centres
 //   k_inner_tour   : one CTA per cluster, nearest-neighbour over its members
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <vector>
@@ -103,24 +104,42 @@ __global__ void k_lex(const double* f, uint32_t M, int D, uint32_t* part, Ctl* c
   uint32_t best = UINT32_MAX;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x)
     if (best == UINT32_MAX || lex_less(f, D, v, best)) best = v;
+  // tree reduction of the lexicographic minimum inside the CTA
   sb[threadIdx.x] = best;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t b = UINT32_MAX;
-    for (int t = 0; t < blockDim.x; ++t)
-      if (sb[t] != UINT32_MAX && (b == UINT32_MAX || lex_less(f, D, sb[t], b))) b = sb[t];
-    part[blockIdx.x] = b;
-    __threadfence();
-    if (atomicAdd(&ctl->done_ctas, 1u) == gridDim.x - 1) {
-      uint32_t g = UINT32_MAX;
-      const volatile uint32_t* vp = part;
-      for (uint32_t c = 0; c < gridDim.x; ++c) {
-        const uint32_t x = vp[c];
-        if (x != UINT32_MAX && (g == UINT32_MAX || lex_less(f, D, x, g))) g = x;
-      }
-      ctl->v0 = g;
-      ctl->done_ctas = 0;
+  for (int w = kNT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const uint32_t a = sb[threadIdx.x], c = sb[threadIdx.x + w];
+      if (c != UINT32_MAX && (a == UINT32_MAX || lex_less(f, D, c, a))) sb[threadIdx.x] = c;
     }
+    __syncthreads();
+  }
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = sb[0];
+    __threadfence();
+    last = atomicAdd(&ctl->done_ctas, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  const volatile uint32_t* vp = part;
+  uint32_t g = UINT32_MAX;
+  for (uint32_t c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
+    const uint32_t x = vp[c];
+    if (x != UINT32_MAX && (g == UINT32_MAX || lex_less(f, D, x, g))) g = x;
+  }
+  sb[threadIdx.x] = g;
+  __syncthreads();
+  for (int w = kNT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const uint32_t a = sb[threadIdx.x], c = sb[threadIdx.x + w];
+      if (c != UINT32_MAX && (a == UINT32_MAX || lex_less(f, D, c, a))) sb[threadIdx.x] = c;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ctl->v0 = sb[0];
+    ctl->done_ctas = 0;
   }
 }
 
@@ -147,20 +166,24 @@ __global__ void k_init_step(const double* f, uint32_t M, int D, double* mind, do
     if (better_max(x, b)) b = x;
   }
   b = block_best<true>(b);
+  __shared__ bool last;
   if (threadIdx.x == 0) {
     part[blockIdx.x] = b;
     __threadfence();
-    if (atomicAdd(&ctl->done_ctas, 1u) == gridDim.x - 1) {
-      const volatile Best* vp = part;
-      Best g{vp[0].v, vp[0].i};
-      for (uint32_t q = 1; q < gridDim.x; ++q) {
-        const Best x{vp[q].v, vp[q].i};
-        if (better_max(x, g)) g = x;
-      }
-      for (int i = 0; i < D; ++i) cen[(size_t)j * D + i] = f[(size_t)g.i * D + i];
-      ctl->done_ctas = 0;
-    }
+    last = atomicAdd(&ctl->done_ctas, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  // the last CTA reduces the per-CTA candidates with all its threads
+  const volatile Best* vp = part;
+  Best g{-1.0, UINT32_MAX};
+  for (uint32_t q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+    const Best x{vp[q].v, vp[q].i};
+    if (better_max(x, g)) g = x;
+  }
+  g = block_best<true>(g);
+  if (threadIdx.x < D) cen[(size_t)j * D + threadIdx.x] = f[(size_t)g.i * D + threadIdx.x];
+  if (threadIdx.x == 0) ctl->done_ctas = 0;
 }
 
 // Lloyd assignment: nearest centre (ties lowest), change flag.  Every Lloyd
@@ -324,7 +347,7 @@ extern "C" tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D
   while ((uint64_t)k * k < M) ++k;  // R29 step 1
   if ((size_t)k * D * sizeof(double) > 200 * 1024) return TGS_EINVAL;  // centres must fit smem
   if (cudaSetDevice(device) != cudaSuccess) return TGS_ECUDA;
-  const int grid = 148 * 4;
+  const int grid = (int)std::min<uint64_t>(148 * 4, ((uint64_t)M + kNT - 1) / kNT);
   std::vector<void*> allocs;
   bool ok = true;
   auto get = [&](size_t bytes) -> void* {

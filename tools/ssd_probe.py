@@ -26,10 +26,24 @@ n_rec = (size - 4096) // S
 fd = os.open(path, os.O_RDONLY | os.O_DIRECT)
 
 
-def run(qd, n_reads, seq=False, req=S):
+PINNED = []
+
+
+def pinned(n):
+    """page-aligned pinned (cudaHostAlloc) buffer, as the store's cache entries are"""
+    import ctypes
+    import torch
+    t = torch.empty(n + 4096, dtype=torch.uint8).pin_memory()
+    PINNED.append(t)
+    a = (t.data_ptr() + 4095) // 4096 * 4096
+    return (ctypes.c_char * n).from_address(a)
+
+
+def run(qd, n_reads, seq=False, req=S, pin=False, seed=0):
+    rng = random.Random(seed * 1000 + qd)
     offs = [4096 + i * req for i in range(n_reads)] if seq else \
-        [4096 + random.Random(qd).randrange(n_rec) * S for _ in range(n_reads)]
-    bufs = [mmap.mmap(-1, req) for _ in range(qd)]
+        [4096 + rng.randrange(n_rec) * S for _ in range(n_reads)]
+    bufs = [pinned(req) if pin else mmap.mmap(-1, req) for _ in range(qd)]
     nxt = [0]
     lock = threading.Lock()
 
@@ -52,7 +66,9 @@ def run(qd, n_reads, seq=False, req=S):
     return len(offs) * req / dt / 1e9
 
 
-print(f"records {n_rec} x {S} B")
+print(f"records {n_rec} x {S} B ({size / 2**30:.1f} GiB file)")
 print(f"sequential 16 MiB QD1: {run(1, 256, True, 16 << 20):.2f} GB/s")
-for qd in (1, 2, 4, 8, 16, 32):
-    print(f"random records QD{qd}: {run(qd, 400):.2f} GB/s")
+for pin in (False, True):
+    for qd in (1, 4, 8, 16):
+        print(f"random records QD{qd} {'pinned' if pin else 'pageable'}: "
+              f"{run(qd, 600, pin=pin, seed=qd + 10 * pin):.2f} GB/s")
