@@ -678,7 +678,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     const std::string e = c->store->open(
         scfg->dir, geo, scfg->cache_blocks, c->cache_pool,
         scfg->segment_bytes ? scfg->segment_bytes : (1ull << 30), scfg->direct_io != 0,
-        std::max(io_threads, std::min(nth, 32)),
+        io_threads,
         [&](uint32_t l, float* dst) { fill_record(c, theta_rows, fill, fill_user, l, dst); });
     if (!e.empty()) {
       fprintf(stderr, "tidegs: store: %s\n", e.c_str());  // the context is gone on return
@@ -943,10 +943,13 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
       CK(cudaStreamWaitEvent(c->fix, c->ev_plan, 0));
       ready_on = c->fix;
     }
+    Timer th;
+    CopyBatch b;
     if (c->store) {
       // NEXT f3, R27 (b): S+ records come from their CPU-cache entries; misses
       // are read from SSD through Index[k] after a dirty LRU victim (if any) is
       // appended to the patch log.  Needs the dirty marks of activate T-1.
+      // The hits move over PCIe while the SSD reads the misses.
       io_join(c, T - 1);
       if (c->io_failed) return check(c);
       auto wait_d2h = [&](int32_t job) {
@@ -956,20 +959,39 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
         io_join(c, job);
         cudaEventSynchronize(c->ev_job[job & 3]);
       };
-      const std::string e = c->store->gather(c->sp_map, h.nSp, T, wait_d2h);
+      std::vector<uint32_t> pairs[2];  // (local id, slot) of hits / misses
+      tgs_status hst = TGS_OK;
+      auto hits_ready = [&](const std::vector<uint8_t>& miss) {
+        for (uint32_t i = 0; i < h.nSp; ++i) {
+          pairs[miss[i]].push_back(c->sp_map[2 * i]);
+          pairs[miss[i]].push_back(c->sp_map[2 * i + 1]);
+        }
+        Timer t1;
+        prof_begin(c, c->h2d, t1);
+        add_records(c, b, pairs[0].data(), (uint32_t)pairs[0].size() / 2, true);
+        hst = submit(c, b, c->h2d);
+        prof_end(c, c->h2d, t1, 3, (uint64_t)pairs[0].size() / 2 * d.n_arr * c->rec_bytes);
+        b = CopyBatch{};
+      };
+      const std::string e = c->store->gather(c->sp_map, h.nSp, T, wait_d2h, hits_ready);
       if (!e.empty()) {
         c->poisoned = true;
         set_err(c, "store: %s", e.c_str());
         return TGS_EIO;
       }
+      if (hst != TGS_OK) return hst;
+      prof_begin(c, c->h2d, th);
+      add_records(c, b, pairs[1].data(), (uint32_t)pairs[1].size() / 2, true);
+      st = submit(c, b, c->h2d);
+      if (st != TGS_OK) return st;
+      prof_end(c, c->h2d, th, 3, (uint64_t)pairs[1].size() / 2 * d.n_arr * c->rec_bytes);
+    } else {
+      prof_begin(c, c->h2d, th);
+      add_records(c, b, c->sp_map, h.nSp, true);
+      st = submit(c, b, c->h2d);
+      if (st != TGS_OK) return st;
+      prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
     }
-    Timer th;
-    prof_begin(c, c->h2d, th);
-    CopyBatch b;
-    add_records(c, b, c->sp_map, h.nSp, true);
-    st = submit(c, b, c->h2d);
-    if (st != TGS_OK) return st;
-    prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
     if (c->prev_packed) {  // S+ blocks the previous batch packed: newest copy is in its ring
       CK(cudaEventRecord(c->ev_gdone, c->h2d));
       CK(cudaStreamWaitEvent(c->fix, c->ev_gdone, 0));

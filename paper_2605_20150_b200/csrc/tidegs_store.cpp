@@ -183,6 +183,9 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
     ::closedir(dp);
   }
   pool_io_ = new IoPool(std::max(1, threads));
+  // the base segment is built by every host core (generation is CPU work); the
+  // training reads and appends use the `threads` of pool_io_ (queue depth)
+  IoPool build_pool(std::max(threads, std::min<int>(32, (int)std::thread::hardware_concurrency())));
 
   // "The initial model is written once as an immutable base segment"
   // (PAPER.md:228): header page, record l at 4096 + l*S; Index[l] = (0, off, size, 0)
@@ -200,7 +203,7 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
   segment_header(reinterpret_cast<unsigned char*>(hp.get()), 0, g);
   if (!pwrite_all(fd, hp.get(), kPage, 0)) return errno_str("write base header");
   std::atomic<bool> bad{false};
-  pool_io_->parallel_for(g.Kloc, [&](uint32_t l) {
+  build_pool.parallel_for(g.Kloc, [&](uint32_t l) {
     thread_local std::unique_ptr<char, decltype(&free)> buf(nullptr, &free);
     thread_local uint64_t cap = 0;
     if (cap < S_) {
@@ -338,7 +341,8 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
 }
 
 std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
-                               const std::function<void(int32_t)>& wait_d2h) {
+                               const std::function<void(int32_t)>& wait_d2h,
+                               const std::function<void(const std::vector<uint8_t>&)>& hits_ready) {
   // every S+ block is in R_{t+1}: its entry (if cached) is not evictable (R27)
   for (uint32_t i = 0; i < n; ++i) {
     const int32_t e = ent_of_[sp[2 * i]];
@@ -346,6 +350,7 @@ std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
   }
   std::vector<std::pair<uint32_t, int32_t>> victims, misses;  // (block, entry)
   std::vector<int32_t> jobs;
+  std::vector<uint8_t> miss(n, 0);
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t l = sp[2 * i];
     int32_t e = ent_of_[l];
@@ -353,6 +358,7 @@ std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
       cnt_.hits += 1;
     } else {
       cnt_.misses += 1;
+      miss[i] = 1;
       if (!free_.empty()) {
         e = free_.back();
         free_.pop_back();
@@ -380,6 +386,9 @@ std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
     x.admitted = T;
     x.stamp = ++clock_;
   }
+  // the hits' records are final: the caller can start moving them while the
+  // victims are appended and the misses read
+  if (hits_ready) hits_ready(miss);
   if (!victims.empty()) {
     const auto t0 = std::chrono::steady_clock::now();
     std::sort(jobs.begin(), jobs.end());

@@ -87,8 +87,11 @@ class BlockStore {
 
   // R27 (b): S+ (local ids, ascending) of activate T.  wait_d2h(job) must
   // return once the write-back of that activate into the cache has landed.
+  // hits_ready(miss flags per S+ entry), if set, is called once the cache
+  // decisions are made and before any SSD I/O: the hits' entries are final.
   std::string gather(const uint32_t* sp_pairs /* (l, slot) */, uint32_t n, int32_t T,
-                     const std::function<void(int32_t)>& wait_d2h);
+                     const std::function<void(int32_t)>& wait_d2h,
+                     const std::function<void(const std::vector<uint8_t>&)>& hits_ready = nullptr);
   // R27 (c): S- of activate T, ascending (after gather of the same activate)
   void touch_evicted(const uint32_t* sm, uint32_t n, int32_t T);
   // R27 (a): the D2H write-back of activate T put block l's dirty record into its entry
