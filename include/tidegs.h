@@ -200,6 +200,8 @@ typedef struct {
   uint64_t segments;            /* patch segments created                                  */
   uint64_t cached, cached_dirty;/* current CPU-cache occupancy                             */
   double read_ms, write_ms;     /* host wall time spent in SSD reads / appends             */
+  uint64_t read_calls;          /* vector reads issued (runs of neighbouring records)      */
+  double read_busy_ms;          /* summed over the I/O threads: time inside the reads      */
 } tgs_store_stats;
 /* ESTATE without a store.  Synchronising. */
 tgs_status tgs_get_store_stats(tgs_ctx* ctx, tgs_store_stats* out);

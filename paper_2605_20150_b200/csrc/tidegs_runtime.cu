@@ -1466,6 +1466,8 @@ tgs_status tgs_get_store_stats(tgs_ctx* c, tgs_store_stats* out) {
   out->cached_dirty = c->store->cached_dirty();
   out->read_ms = k.read_ms;
   out->write_ms = k.write_ms;
+  out->read_calls = k.read_calls;
+  out->read_busy_ms = k.read_busy_ms;
   return TGS_OK;
 }
 

@@ -441,6 +441,9 @@ std::string BlockStore::read_records(const std::vector<std::pair<uint32_t, int32
     i = j;
   }
   std::atomic<bool> bad{false};
+  std::mutex busy_mu;
+  double busy = 0.0;
+  cnt_.read_calls += runs.size();
   pool_io_->parallel_for((uint32_t)runs.size(), [&](uint32_t r) {
     thread_local std::unique_ptr<char, decltype(&free)> scratch(aligned_pages(kPage), &free);
     const size_t b = runs[r].first, e = runs[r].second;
@@ -460,13 +463,19 @@ std::string BlockStore::read_records(const std::vector<std::pair<uint32_t, int32
       pos = it[i].off + S_;
     }
     ssize_t got;
+    const auto t0 = std::chrono::steady_clock::now();
     do {
       got = ::preadv(fd, iov, n, (off_t)it[b].off);
     } while (got < 0 && errno == EINTR);
+    {
+      std::lock_guard<std::mutex> g(busy_mu);
+      busy += ms_since(t0);
+    }
     if (got == (ssize_t)total) return;
     for (size_t i = b; i < e; ++i)  // short or failed vector read: record by record
       if (!pread_all(fd, pool_ + (uint64_t)it[i].e * S_, S_, it[i].off)) bad = true;
   });
+  cnt_.read_busy_ms += busy;
   return bad ? errno_str("read block record") : "";
 }
 

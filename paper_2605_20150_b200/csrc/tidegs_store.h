@@ -59,6 +59,8 @@ struct StoreCounters {
   uint64_t hits = 0, misses = 0, evictions = 0, dirty_evictions = 0, flush_appends = 0,
            read_bytes = 0, write_bytes = 0, segments = 0;
   double read_ms = 0.0, write_ms = 0.0;  // wall time of the SSD phases
+  uint64_t read_calls = 0;               // vector reads issued (runs of neighbouring records)
+  double read_busy_ms = 0.0;             // sum over threads of time inside preadv
 };
 
 class BlockStore {

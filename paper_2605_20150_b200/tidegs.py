@@ -105,7 +105,9 @@ STORE_FIELDS = ("hits", "misses", "evictions", "dirty_evictions", "flush_appends
 
 class StoreStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in STORE_FIELDS] + [("read_ms", C.c_double),
-                                                          ("write_ms", C.c_double)]
+                                                          ("write_ms", C.c_double),
+                                                          ("read_calls", C.c_uint64),
+                                                          ("read_busy_ms", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -14,5 +14,7 @@ if st:
     out.update({"hit_rate": round(st["hit_rate"], 3), "ssd_read_GBps": st["ssd_read_GBps_in_reads"],
                 "ssd_peak": st.get("ssd_read_peak_GBps"),
                 "read_ms/step": st["per_step"]["read_ms"], "misses/step": st["per_step"]["misses"],
-                "dirty_evict/step": st["per_step"]["dirty_evictions"]})
+                "dirty_evict/step": st["per_step"]["dirty_evictions"],
+                "read_calls/step": st["per_step"].get("read_calls"),
+                "read_busy_ms/step": st["per_step"].get("read_busy_ms")})
 print(json.dumps(out))

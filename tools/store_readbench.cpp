@@ -3,8 +3,9 @@
 // step whose ids follow a sliding window (like the aerial path entering new
 // territory), reading into a pinned-or-pageable cache.  Prints the SSD GB/s the
 // store's own read path reaches, per thread count.
-//   g++ -O2 -std=c++17 -pthread tools/store_readbench.cpp paper_2605_20150_b200/csrc/tidegs_store.cpp
-//   ./a.out DIR K MISSES STEPS THREADS [direct=1]
+//   g++ -O2 -std=c++17 -pthread -I/usr/local/cuda/include tools/store_readbench.cpp \
+//       paper_2605_20150_b200/csrc/tidegs_store.cpp -L/usr/local/cuda/lib64 -lcudart
+//   ./a.out DIR K MISSES STEPS THREADS [direct=1] [pinned=0]
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -12,6 +13,8 @@
 #include <random>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "../paper_2605_20150_b200/csrc/tidegs_store.h"
 
@@ -21,11 +24,14 @@ int main(int argc, char** argv) {
   const uint32_t K = std::atoi(argv[2]), misses = std::atoi(argv[3]), steps = std::atoi(argv[4]);
   const int threads = std::atoi(argv[5]);
   const int direct = argc > 6 ? std::atoi(argv[6]) : 1;
+  const int pinned = argc > 7 ? std::atoi(argv[7]) : 0;  // cudaHostAlloc cache, as the library
   const uint32_t B = 4096, H = misses * 4 + 64;
   tgs::BlockStore::Geometry geo{(uint64_t)B * K, B, 1, 1, 0, K, (uint64_t)B * 59 * 4};
   const uint64_t S = (geo.rec_bytes + 4095) / 4096 * 4096;
   char* pool = nullptr;
-  if (posix_memalign((void**)&pool, 4096, (size_t)H * S) != 0) return 3;
+  if (pinned ? cudaHostAlloc((void**)&pool, (size_t)H * S, cudaHostAllocPortable) != cudaSuccess
+             : posix_memalign((void**)&pool, 4096, (size_t)H * S) != 0)
+    return 3;
   std::memset(pool, 0, (size_t)H * S);
   tgs::BlockStore st;
   auto t0 = std::chrono::steady_clock::now();
@@ -74,8 +80,8 @@ int main(int argc, char** argv) {
   }
   const double ms = st.counters().read_ms - read_ms0;
   const double gb = (st.counters().read_bytes - read_b0) / 1e9;
-  std::printf("threads %d direct %d: %u misses/step, %.2f ms/step in reads, %.2f GB/s\n", threads,
-              direct, misses, ms / (steps - 5), gb / (ms / 1e3));
-  free(pool);
+  std::printf("threads %d direct %d pinned %d: %u misses/step, %.2f ms/step in reads, %.2f GB/s\n",
+              threads, direct, pinned, misses, ms / (steps - 5), gb / (ms / 1e3));
+  if (pinned) cudaFreeHost(pool); else free(pool);
   return 0;
 }
