@@ -5,7 +5,7 @@
 // store's own read path reaches, per thread count.
 //   g++ -O2 -std=c++17 -pthread -I/usr/local/cuda/include tools/store_readbench.cpp \
 //       paper_2605_20150_b200/csrc/tidegs_store.cpp -L/usr/local/cuda/lib64 -lcudart
-//   ./a.out DIR K MISSES STEPS THREADS [direct=1] [pinned=0]
+//   ./a.out DIR K MISSES STEPS THREADS [direct=1] [pinned=0] [run=1]
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +25,7 @@ int main(int argc, char** argv) {
   const int threads = std::atoi(argv[5]);
   const int direct = argc > 6 ? std::atoi(argv[6]) : 1;
   const int pinned = argc > 7 ? std::atoi(argv[7]) : 0;  // cudaHostAlloc cache, as the library
+  const uint32_t run = argc > 8 ? std::atoi(argv[8]) : 1;   // neighbouring misses per run
   const uint32_t B = 4096, H = misses * 4 + 64;
   tgs::BlockStore::Geometry geo{(uint64_t)B * K, B, 1, 1, 0, K, (uint64_t)B * 59 * 4};
   const uint64_t S = (geo.rec_bytes + 4095) / 4096 * 4096;
@@ -44,7 +45,6 @@ int main(int argc, char** argv) {
   const double wsec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   std::printf("base: %u records, %.1f GB written in %.1f s (%.2f GB/s)\n", K, K * S / 1e9, wsec,
               K * S / 1e9 / wsec);
-  std::mt19937 rng(3);
   std::vector<uint32_t> resident;
   uint32_t window = 0;
   auto noop = [](int32_t) {};
@@ -54,8 +54,8 @@ int main(int argc, char** argv) {
     // S+ = `misses` never-seen blocks from a window sliding over the id space
     // (spread like a Morton-ordered strip edge), S- = the previous batch
     std::vector<uint32_t> sp;
-    for (uint32_t i = 0; i < misses; ++i) {
-      const uint32_t l = (window + i * 7 + (rng() % 5)) % K;
+    for (uint32_t i = 0; i < misses; ++i) {  // runs of `run` neighbouring records
+      const uint32_t l = (window + (i / run) * 7 * run + i % run) % K;
       if (std::find(sp.begin(), sp.end(), l) == sp.end()) sp.push_back(l);
     }
     window = (window + misses * 7) % K;
@@ -80,8 +80,9 @@ int main(int argc, char** argv) {
   }
   const double ms = st.counters().read_ms - read_ms0;
   const double gb = (st.counters().read_bytes - read_b0) / 1e9;
-  std::printf("threads %d direct %d pinned %d: %u misses/step, %.2f ms/step in reads, %.2f GB/s\n",
-              threads, direct, pinned, misses, ms / (steps - 5), gb / (ms / 1e3));
+  std::printf("threads %d direct %d pinned %d run %u: %u misses/step, %.2f ms/step in reads, "
+              "%.2f GB/s, %.1f read calls/step\n", threads, direct, pinned, run, misses,
+              ms / (steps - 5), gb / (ms / 1e3), (double)st.counters().read_calls / steps);
   if (pinned) cudaFreeHost(pool); else free(pool);
   return 0;
 }
