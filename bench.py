@@ -514,7 +514,7 @@ def main():
                            "store": store_detail}}
         print(json.dumps(line), flush=True)
     table.close()
-    if store:
+    if store and os.environ.get("TGS_KEEP_STORE") != "1":
         import shutil
         shutil.rmtree(store["dir"], ignore_errors=True)
     if ws > 1:
