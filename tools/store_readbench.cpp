@@ -5,7 +5,7 @@
 // store's own read path reaches, per thread count.
 //   g++ -O2 -std=c++17 -pthread -I/usr/local/cuda/include tools/store_readbench.cpp \
 //       paper_2605_20150_b200/csrc/tidegs_store.cpp -L/usr/local/cuda/lib64 -lcudart
-//   ./a.out DIR K MISSES STEPS THREADS [direct=1] [pinned=0] [run=1]
+//   ./a.out DIR K MISSES STEPS THREADS [direct=1] [pinned=0] [run=1] [H]
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -26,7 +26,8 @@ int main(int argc, char** argv) {
   const int direct = argc > 6 ? std::atoi(argv[6]) : 1;
   const int pinned = argc > 7 ? std::atoi(argv[7]) : 0;  // cudaHostAlloc cache, as the library
   const uint32_t run = argc > 8 ? std::atoi(argv[8]) : 1;   // neighbouring misses per run
-  const uint32_t B = 4096, H = misses * 4 + 64;
+  const uint32_t B = 4096;
+  const uint32_t H = argc > 9 ? std::atoi(argv[9]) : misses * 4 + 64;  // cache records
   tgs::BlockStore::Geometry geo{(uint64_t)B * K, B, 1, 1, 0, K, (uint64_t)B * 59 * 4};
   const uint64_t S = (geo.rec_bytes + 4095) / 4096 * 4096;
   char* pool = nullptr;
@@ -80,8 +81,8 @@ int main(int argc, char** argv) {
   }
   const double ms = st.counters().read_ms - read_ms0;
   const double gb = (st.counters().read_bytes - read_b0) / 1e9;
-  std::printf("threads %d direct %d pinned %d run %u: %u misses/step, %.2f ms/step in reads, "
-              "%.2f GB/s, %.1f read calls/step\n", threads, direct, pinned, run, misses,
+  std::printf("H %u threads %d direct %d pinned %d run %u: %u misses/step, %.2f ms/step in reads, "
+              "%.2f GB/s, %.1f read calls/step\n", H, threads, direct, pinned, run, misses,
               ms / (steps - 5), gb / (ms / 1e3), (double)st.counters().read_calls / steps);
   if (pinned) cudaFreeHost(pool); else free(pool);
   return 0;
