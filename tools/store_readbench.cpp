@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <sys/mman.h>
+
 #include <cuda_runtime.h>
 
 #include "../paper_2605_20150_b200/csrc/tidegs_store.h"
@@ -30,11 +32,21 @@ int main(int argc, char** argv) {
   const uint32_t H = argc > 9 ? std::atoi(argv[9]) : misses * 4 + 64;  // cache records
   tgs::BlockStore::Geometry geo{(uint64_t)B * K, B, 1, 1, 0, K, (uint64_t)B * 59 * 4};
   const uint64_t S = (geo.rec_bytes + 4095) / 4096 * 4096;
+  // pinned: 1 cudaHostAlloc, 2 THP-backed anonymous memory + cudaHostRegister, 3 THP only
   char* pool = nullptr;
-  if (pinned ? cudaHostAlloc((void**)&pool, (size_t)H * S, cudaHostAllocPortable) != cudaSuccess
-             : posix_memalign((void**)&pool, 4096, (size_t)H * S) != 0)
+  const size_t bytes = ((size_t)H * S + (2u << 20) - 1) / (2u << 20) * (2u << 20);
+  if (pinned == 1) {
+    if (cudaHostAlloc((void**)&pool, bytes, cudaHostAllocPortable) != cudaSuccess) return 3;
+  } else if (pinned >= 2) {
+    pool = (char*)mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (pool == MAP_FAILED) return 3;
+    madvise(pool, bytes, MADV_HUGEPAGE);
+    std::memset(pool, 0, bytes);
+    if (pinned == 2 && cudaHostRegister(pool, bytes, cudaHostRegisterPortable) != cudaSuccess) return 3;
+  } else if (posix_memalign((void**)&pool, 4096, bytes) != 0) {
     return 3;
-  std::memset(pool, 0, (size_t)H * S);
+  }
+  std::memset(pool, getenv("SRB_FILL") ? atoi(getenv("SRB_FILL")) : 0, bytes);
   tgs::BlockStore st;
   auto t0 = std::chrono::steady_clock::now();
   std::string err = st.open(dir, geo, H, pool, 1ull << 30, direct != 0, threads,
@@ -84,6 +96,8 @@ int main(int argc, char** argv) {
   std::printf("H %u threads %d direct %d pinned %d run %u: %u misses/step, %.2f ms/step in reads, "
               "%.2f GB/s, %.1f read calls/step\n", H, threads, direct, pinned, run, misses,
               ms / (steps - 5), gb / (ms / 1e3), (double)st.counters().read_calls / steps);
-  if (pinned) cudaFreeHost(pool); else free(pool);
+  if (pinned == 1) cudaFreeHost(pool);
+  else if (pinned >= 2) { if (pinned == 2) cudaHostUnregister(pool); munmap(pool, bytes); }
+  else free(pool);
   return 0;
 }
