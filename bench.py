@@ -164,7 +164,10 @@ def dist_init(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        # TGS_BENCH_BACKEND=gloo: functional run of the multi-rank path with
+        # several ranks sharing one GPU (NCCL refuses duplicate GPUs)
+        backend = os.environ.get("TGS_BENCH_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
+        dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -295,6 +298,8 @@ def main():
     import paper_2605_20150_b200 as P
     from paper_2605_20150_b200 import tidegs as T
 
+    if os.environ.get("TGS_BENCH_BACKEND") == "gloo":
+        local = 0  # every rank on cuda:0 (functional multi-rank run on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     wl = W.CONFIGS[args.config]
@@ -356,6 +361,9 @@ def main():
 
     fmask = torch.zeros((table.P, (sc.B + 31) // 32), dtype=torch.int32, device=dev) \
         if args.fine_filter else None
+    # C2 inputs: a ring of pinned rows (the host runs at most ~2 batches ahead)
+    cnt_host = torch.zeros((8, 8), dtype=torch.int64).pin_memory() if ws > 1 else None
+    cnt_dev = torch.zeros((8, 8), dtype=torch.int64, device=dev) if ws > 1 else None
 
     def step(i):
         act = table.activate(planes[i])
@@ -365,9 +373,12 @@ def main():
             n = act.n_active_blocks
             A = torch.as_tensor(_CudaView(act.d_active_blocks, n), device=dev) if n else \
                 torch.empty(0, dtype=torch.int32, device=dev)
-            shard.exchange_active(A, cap)
-            shard.reduce_counts(torch.tensor([act.n_visible, act.n_resident, act.n_stage_in,
-                                              act.n_evict, n], dtype=torch.int64, device=dev))
+            shard.exchange_active(A, cap, union=False)
+            row = i % 8
+            cnt_host[row, :5] = torch.tensor([act.n_visible, act.n_resident, act.n_stage_in,
+                                              act.n_evict, n], dtype=torch.int64)
+            cnt_dev[row].copy_(cnt_host[row], non_blocking=True)
+            shard.reduce_counts(cnt_dev[row])
         table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
 
     for i in range(args.warmup):
@@ -449,6 +460,14 @@ def main():
         d_rows = int(res[n_e, fi["n_active_rows"]] - res[0, fi["n_active_rows"]])
         d_h2d = int(res[n_e, fi["h2d_bytes"]] - res[0, fi["h2d_bytes"]])
         d_d2h = int(res[n_e, fi["d2h_bytes"]] - res[0, fi["d2h_bytes"]])
+        if ws > 1:  # whole job: rows and bytes summed over ranks, the slowest rank's clock
+            import torch.distributed as dist
+            tsum = torch.tensor([d_rows, d_h2d, d_d2h], dtype=torch.float64, device=dev)
+            tmax = torch.tensor([dt, dev_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tsum)
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            d_rows, d_h2d, d_d2h = (int(x) for x in tsum.tolist())
+            dt, dev_s = tmax.tolist()
         e2e = {"value": d_rows / dt, "unit": "Gaussians/s",
                "h2d_bytes_per_step": int((d_h2d + n_e * J * 96) / n_e),
                "d2h_bytes_per_step": int((d_d2h + n_e * nf * 8) / n_e),

@@ -34,11 +34,13 @@ def shard_capacity(C: int, world_size: int) -> int:
     return -(-int(C) // world_size)
 
 
-def exchange_active(active, cap: int, group=None):
+def exchange_active(active, cap: int, group=None, union=True):
     """C1: all-gather every rank's A list (global ids, ascending, <= cap
     entries).  `active` is a 1-D int32/int64 torch tensor (CUDA under NCCL, CPU
-    under gloo).  Returns the [G, cap] gathered tensor (PAD-padded) and the
-    sorted global active set as a 1-D tensor."""
+    under gloo).  Returns the [G, cap] gathered tensor (PAD-padded) and, if
+    `union`, the sorted global active set as a 1-D tensor (that compaction
+    needs its size on the host, i.e. a stream sync: the bench skips it so the
+    host never waits for the device).  Nothing here synchronises otherwise."""
     import torch
     import torch.distributed as dist
 
@@ -49,15 +51,16 @@ def exchange_active(active, cap: int, group=None):
     buf = torch.full((cap,), PAD, dtype=torch.int64, device=active.device)
     buf[:n] = active.to(torch.int64)
     out = torch.empty((G, cap), dtype=torch.int64, device=active.device)
-    if active.device.type == "cuda":
+    if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, buf, group=group)
-    else:
+    else:  # gloo (CPU tests, or a one-GPU functional run of the multi-rank bench)
         parts = [torch.empty_like(buf) for _ in range(G)]
         dist.all_gather(parts, buf, group=group)
         out = torch.stack(parts)
+    if not union:
+        return out, None
     flat = out.reshape(-1)
-    union = torch.sort(flat[flat != PAD]).values
-    return out, union
+    return out, torch.sort(flat[flat != PAD]).values
 
 
 def reduce_counts(counts, group=None):
