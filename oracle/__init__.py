@@ -91,6 +91,7 @@ def lib():
                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.or_store_open.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
+        L.or_store_reopen.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
         L.or_store_index.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint64)]
         L.or_store_stats.argtypes = [vp, C.POINTER(C.c_uint64)]
         L.or_store_lru.restype = C.c_uint32
@@ -255,6 +256,12 @@ class Oracle:
         rc = lib().or_store_open(self.h, d, cache_blocks, segment_bytes)
         if rc != OK:
             raise OracleError(rc, "or_store_open")
+
+    def store_reopen(self, dir, cache_blocks, segment_bytes=0):
+        """R30: resume over the segment files of an earlier session."""
+        rc = lib().or_store_reopen(self.h, os.fsencode(str(dir)), cache_blocks, segment_bytes)
+        if rc != OK:
+            raise OracleError(rc, "or_store_reopen")
 
     def store_index(self, k):
         """Index[k] = (file_id, offset, size, version) (PAPER.md:233)."""

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <string>
 #include <limits>
 #include <map>
@@ -966,6 +967,75 @@ int or_store_open(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t se
       write_at(base, kPage + (uint64_t)l * s.S, r.data(), s.S, false);
     }
   }
+  return OR_OK;
+}
+
+
+// Checkpoint/resume of the store tier (reading R30): a new session over the
+// files a barrier left.  SPEC.md log_store recover_index: scan the segments
+// in file_id order, later records win; a truncated trailing record of the
+// newest patch is dropped (the segment is cut back to the last whole record).
+// Everything else starts afresh: an empty CPU cache, no resident block, step
+// counters and recency at zero.
+static uint64_t get64(const unsigned char* p) {
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+static uint32_t get32(const unsigned char* p) {
+  uint32_t v = 0;
+  for (int i = 3; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+int or_store_reopen(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t segment_bytes) {
+  Ctx& c = o->c;
+  Store& s = c.sto;
+  if (c.t != 0 || s.on) return OR_ESTATE;
+  if (!dir || !c.track_all || cache_blocks < 2ull * c.cfg.capacity) return OR_EINVAL;
+  s.payload = (uint64_t)c.n_arr() * c.rec_bytes();
+  s.S = pad_page(s.payload);
+  s.seg_budget = segment_bytes ? segment_bytes : (1ull << 30);
+  if (s.seg_budget < 2 * kPage + s.S) return OR_EINVAL;
+  s.dir = dir;
+  // the base header must describe this shard
+  std::vector<unsigned char> want = segment_header(c, 0), got(kPage, 0);
+  read_at(seg_path(s, 0), 0, got.data(), kPage);
+  if (got != want) return OR_EINVAL;
+  s.index.assign(c.Kloc, IndexEntry{});
+  for (uint32_t l = 0; l < c.Kloc; ++l) s.index[l] = {0, kPage + (uint64_t)l * s.S, s.payload, 0};
+  uint32_t last = 0;
+  uint64_t end = 0;
+  for (uint32_t fid = 1;; ++fid) {
+    const std::string path = seg_path(s, fid);
+    std::error_code ec;
+    const uint64_t size = std::filesystem::file_size(path, ec);
+    if (ec) break;
+    std::vector<unsigned char> h(kPage, 0);
+    read_at(path, 0, h.data(), kPage);
+    if (h != segment_header(c, fid)) return OR_EINVAL;
+    uint64_t off = kPage;
+    while (off + kPage + s.S <= size) {
+      std::vector<unsigned char> r(kPage, 0);
+      read_at(path, off, r.data(), kPage);
+      const uint64_t gid = get64(&r[8]);
+      if (std::memcmp(r.data(), "TREC", 4) != 0 || get32(&r[4]) != 1 ||
+          get64(&r[24]) != s.payload || gid % c.cfg.world_size != (uint64_t)c.cfg.rank ||
+          gid / c.cfg.world_size >= c.Kloc)
+        break;
+      s.index[gid / c.cfg.world_size] = {fid, off + kPage, s.payload, get64(&r[16])};
+      off += kPage + s.S;
+    }
+    last = fid;
+    end = off;
+  }
+  if (last) std::filesystem::resize_file(seg_path(s, last), end);  // drop a torn tail
+  s.cur_file = last;
+  s.cur_size = last ? end : 0;
+  s.segments = 0;
+  s.on = true;
+  s.data = true;
+  s.H = cache_blocks;
   return OR_OK;
 }
 

@@ -105,6 +105,10 @@ float or_exp_det(float x);
  * written under dir (needs track_all); dir == NULL: metadata only (Index, LRU
  * and counters; no block may be tracked). */
 int or_store_open(or_ctx* c, const char* dir, uint32_t cache_blocks, uint64_t segment_bytes);
+/* R30 checkpoint/resume: a new session over the files of an earlier one
+ * (after its barrier): Index recovered by scanning the segments (later
+ * records win, a torn tail record dropped), empty cache; needs track_all. */
+int or_store_reopen(or_ctx* c, const char* dir, uint32_t cache_blocks, uint64_t segment_bytes);
 int or_store_index(or_ctx* c, uint64_t k_global, uint64_t* out4);
 int or_store_stats(or_ctx* c, uint64_t* out10);
 uint32_t or_store_lru(or_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap);

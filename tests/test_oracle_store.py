@@ -350,3 +350,48 @@ def test_store_errors(tmp_path):
         o.store_open(tmp_path, 2 * cfg.capacity)
     with pytest.raises(O.OracleError):          # segment budget below one record
         mk(True).store_open(tmp_path, 2 * cfg.capacity, 2 * PAGE)
+
+
+def test_reopen_recovers_index_and_table(tmp_path):
+    """R30 checkpoint/resume (SPEC.md recover_index 'random session replayed
+    from disk -> index equals live index'): a new session over the files left
+    by a barrier recovers every Index[k] and serves every block's newest
+    version; a torn trailing record is dropped and cut off the segment; a store
+    of another shape is refused."""
+    cfg, sc, tr = tiny()
+    S = _pad(3 * sc.B * 59 * 4)
+    budget = PAGE + 4 * (PAGE + S)
+    sc, ((flat, _), (st, _)) = _flat_and_store(tmp_path, O.PERSIST, False, 16, budget)
+    live = {k: st.store_index(k) for k in range(sc.K)}
+    table = {k: flat.read_block(k) for k in range(sc.K)}
+    last = max(int(n[6:12]) for n in os.listdir(tmp_path) if n.startswith("patch-"))
+    lp = tmp_path / f"patch-{last:06d}.tdgp"
+    size = lp.stat().st_size
+    with open(lp, "ab") as f:  # a record whose payload never made it to disk
+        f.write(b"TREC" + b"\0" * 5000)
+    o = O.Oracle(O.make_config(sc.N, sc.B, 8), sc.bounds(), fill=None, track_all=True)
+    o.store_reopen(tmp_path, 16, budget)
+    assert lp.stat().st_size == size
+    for k in range(sc.K):
+        assert o.store_index(k) == live[k], k
+        th, m, v = o.read_block(k)
+        assert np.array_equal(th.view(np.uint32), table[k][0].view(np.uint32)), k
+        assert np.array_equal(m.view(np.uint32), table[k][1].view(np.uint32)), k
+    # the resumed session keeps appending after the last whole record
+    lr = lr_3dgs()
+    grad = synth_grad(W.SEEDS["grads"], sc.N, sc.B)
+    for planes in random_boxes(sc, 12, seed=21):
+        o.activate(planes)
+        o.step_adam(lr, grad=grad)
+    o.flush()
+    segs = read_segments(tmp_path)
+    assert max(segs) >= last
+    for k in range(sc.K):  # the parser (later records win) agrees with the live index
+        fid, off, n, ver = o.store_index(k)
+        assert ver >= live[k][3]
+        if fid:
+            assert (off, k, ver, n) in [(r[0], r[1], r[2], r[3]) for r in segs[fid][2]]
+    bad = O.Oracle(O.make_config(sc.N, sc.B - 4, 8), W.Scene(sc.N, sc.B - 4).bounds(), fill=None,
+                   track_all=True)
+    with pytest.raises(O.OracleError):
+        bad.store_reopen(tmp_path, 16, budget)
