@@ -181,6 +181,13 @@ typedef struct {
   uint64_t segment_bytes;  /* patch segment rollover budget; 0 -> 1 GiB             */
   int32_t direct_io;       /* 1: O_DIRECT reads/writes (page cache bypassed)        */
   int32_t io_threads;      /* parallel SSD requests; 0 -> 8                         */
+  int32_t reopen;          /* 1: resume over the segments an earlier session left at its
+                              barrier (checkpoint/resume, reading R30): no base is
+                              written (theta_rows and fill may both be NULL), Index is
+                              recovered by scanning the segments (later records win, a
+                              torn trailing record is cut off), the cache starts empty and
+                              Adam step counters / recency start at zero; TGS_EIO if the
+                              base header does not describe this shard               */
 } tgs_store_config;
 
 /* As tgs_init_table, with the store tier.  TGS_EIO: the store could not be

@@ -595,7 +595,9 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (g.world_size < 1 || g.rank < 0 || g.rank >= g.world_size) return TGS_EINVAL;
   if (g.moments != TGS_MOMENTS_PERSIST && g.moments != TGS_MOMENTS_COLD_RESTART) return TGS_EINVAL;
   if (g.max_cameras < 1 || g.max_cameras > kMaxCams || g.max_age > kMaxAge) return TGS_EINVAL;
-  if ((theta_rows == nullptr) == (fill == nullptr)) return TGS_EINVAL;
+  const bool reopen = scfg && scfg->reopen;
+  if (!reopen && (theta_rows == nullptr) == (fill == nullptr)) return TGS_EINVAL;
+  if (reopen && theta_rows && fill) return TGS_EINVAL;
   const uint32_t P = g.pool_slots ? g.pool_slots : 2u * g.capacity;
   if (P < g.capacity) return TGS_EINVAL;
   if (scfg && (!scfg->dir || scfg->cache_blocks < 2ull * g.capacity)) return TGS_EINVAL;  // R27
@@ -679,7 +681,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
         scfg->dir, geo, scfg->cache_blocks, c->cache_pool,
         scfg->segment_bytes ? scfg->segment_bytes : (1ull << 30), scfg->direct_io != 0,
         io_threads,
-        [&](uint32_t l, float* dst) { fill_record(c, theta_rows, fill, fill_user, l, dst); });
+        [&](uint32_t l, float* dst) { fill_record(c, theta_rows, fill, fill_user, l, dst); },
+        reopen);
     if (!e.empty()) {
       fprintf(stderr, "tidegs: store: %s\n", e.c_str());  // the context is gone on return
       return fail(TGS_EIO);

@@ -162,7 +162,7 @@ static void segment_header(unsigned char* h, uint32_t fid, const BlockStore::Geo
 
 std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t H, char* pool,
                              uint64_t seg_budget, bool direct, int threads,
-                             const std::function<void(uint32_t, float*)>& fill) {
+                             const std::function<void(uint32_t, float*)>& fill, bool reopen) {
   g_ = g;
   dir_ = dir;
   H_ = H;
@@ -172,6 +172,16 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
   S_ = (payload_ + kPage - 1) / kPage * kPage;
   seg_budget_ = seg_budget;
   if (seg_budget_ < 2 * kPage + S_) return "segment budget below one record";
+  if (reopen) {
+    pool_io_ = new IoPool(std::max(1, threads));
+    std::string err = recover();
+    if (!err.empty()) return err;
+    ent_of_.assign(g.Kloc, -1);
+    ents_.assign(H, Ent{});
+    free_.clear();
+    for (uint32_t e = H; e-- > 0;) free_.push_back((int32_t)e);
+    return "";
+  }
   if (::mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST) return errno_str("mkdir");
   // the directory holds one store: stale patch segments of an earlier store go
   if (DIR* dp = ::opendir(dir.c_str())) {
@@ -221,6 +231,59 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
   ents_.assign(H, Ent{});
   free_.clear();
   for (uint32_t e = H; e-- > 0;) free_.push_back((int32_t)e);
+  return "";
+}
+
+// R30 checkpoint/resume: Index recovered from the segments a barrier left --
+// the base header must describe this shard; patch segments are scanned in
+// file_id order, later records win; a torn trailing record of the newest
+// segment is dropped and the segment cut back to its last whole record.
+std::string BlockStore::recover() {
+  std::unique_ptr<char, decltype(&free)> want(aligned_pages(kPage), &free), got(aligned_pages(kPage), &free);
+  if (fd_of(0) < 0 && direct_ && errno == EINVAL) {  // no O_DIRECT here: page cache
+    direct_ = false;
+    fds_.clear();
+  }
+  if (fd_of(0) < 0) return errno_str("open base.tdgs");
+  segment_header(reinterpret_cast<unsigned char*>(want.get()), 0, g_);
+  if (!pread_all(fds_[0], got.get(), kPage, 0) || std::memcmp(want.get(), got.get(), kPage) != 0)
+    return "base.tdgs does not hold this shard (header mismatch)";
+  index_.resize(g_.Kloc);
+  for (uint32_t l = 0; l < g_.Kloc; ++l) index_[l] = {0, kPage + (uint64_t)l * S_, payload_, 0};
+  uint32_t last = 0;
+  uint64_t end = 0;
+  for (uint32_t fid = 1;; ++fid) {
+    char name[64];
+    std::snprintf(name, sizeof name, "/patch-%06u.tdgp", fid);
+    struct stat sb;
+    if (::stat((dir_ + name).c_str(), &sb) != 0) break;
+    const int fd = fd_of(fid);
+    if (fd < 0) return errno_str("open patch segment");
+    segment_header(reinterpret_cast<unsigned char*>(want.get()), fid, g_);
+    if (!pread_all(fd, got.get(), kPage, 0) || std::memcmp(want.get(), got.get(), kPage) != 0)
+      return std::string("patch segment header mismatch: ") + name;
+    const uint64_t size = (uint64_t)sb.st_size;
+    uint64_t off = kPage;
+    while (off + kPage + S_ <= size) {
+      if (!pread_all(fd, got.get(), kPage, off)) return errno_str("read record header");
+      const unsigned char* r = reinterpret_cast<const unsigned char*>(got.get());
+      uint64_t gid = 0, ver = 0, n = 0;
+      uint32_t fmt = 0;
+      for (int i = 7; i >= 0; --i) gid = (gid << 8) | r[8 + i], ver = (ver << 8) | r[16 + i],
+                                   n = (n << 8) | r[24 + i];
+      for (int i = 3; i >= 0; --i) fmt = (fmt << 8) | r[4 + i];
+      if (std::memcmp(r, "TREC", 4) != 0 || fmt != 1 || n != payload_ || gid % g_.G != g_.rank ||
+          gid / g_.G >= g_.Kloc)
+        break;
+      index_[gid / g_.G] = {fid, off + kPage, payload_, ver};
+      off += kPage + S_;
+    }
+    last = fid;
+    end = off;
+  }
+  if (last && ::ftruncate(fds_[last], (off_t)end) != 0) return errno_str("truncate torn tail");
+  cur_file_ = last;
+  cur_size_ = last ? end : 0;
   return "";
 }
 

@@ -81,9 +81,10 @@ class BlockStore {
   // beyond what fill writes) and sets up an empty cache over pool (H entries
   // of entry_bytes(), pinned, page-aligned; owned by the caller).  Returns an
   // error string or "".
+  // reopen (R30): no base is written; Index is recovered from the files.
   std::string open(const std::string& dir, const Geometry& g, uint32_t H, char* pool,
                    uint64_t seg_budget, bool direct, int threads,
-                   const std::function<void(uint32_t, float*)>& fill);
+                   const std::function<void(uint32_t, float*)>& fill, bool reopen = false);
   uint64_t entry_bytes() const { return S_; }
   uint64_t payload_bytes() const { return payload_; }
 
@@ -131,6 +132,7 @@ class BlockStore {
   void push_mru(int32_t e);
   int fd_of(uint32_t fid);
   std::string new_segment();
+  std::string recover();
   // reserves the next record of the patch log for block l: (fd, file offset of the record)
   std::string reserve_append(uint32_t l, int& fd, uint64_t& rec_off);
   std::string write_records(const std::vector<std::pair<uint32_t, int32_t>>& recs /* (l, entry) */);

@@ -96,7 +96,7 @@ class Timing(C.Structure):
 
 class StoreConfig(C.Structure):
     _fields_ = [("dir", C.c_char_p), ("cache_blocks", C.c_uint32), ("segment_bytes", C.c_uint64),
-                ("direct_io", C.c_int32), ("io_threads", C.c_int32)]
+                ("direct_io", C.c_int32), ("io_threads", C.c_int32), ("reopen", C.c_int32)]
 
 
 STORE_FIELDS = ("hits", "misses", "evictions", "dirty_evictions", "flush_appends", "read_bytes",
@@ -226,7 +226,7 @@ class Table:
     def __init__(self, cfg: Config, bounds: np.ndarray, *, theta_rows: np.ndarray | None = None,
                  fill=None, stream=None, use_torch_allocator=True, store: dict | None = None):
         """store: None (flat pinned host tier) or the NEXT f3 store tier,
-        dict(dir=..., cache_blocks=H, segment_bytes=0, direct_io=1, io_threads=0)."""
+        dict(dir=..., cache_blocks=H, segment_bytes=0, direct_io=1, io_threads=0, reopen=0)."""
         self.cfg = cfg
         self.B = cfg.block_size
         self._bounds = np.ascontiguousarray(bounds, np.float32)
@@ -261,7 +261,8 @@ class Table:
         else:
             self._store_cfg = StoreConfig(os.fsencode(str(store["dir"])), store["cache_blocks"],
                                           store.get("segment_bytes", 0),
-                                          store.get("direct_io", 1), store.get("io_threads", 0))
+                                          store.get("direct_io", 1), store.get("io_threads", 0),
+                                          store.get("reopen", 0))
             rc = lib().tgs_init_table_store(C.byref(cfg), C.byref(self._store_cfg), rows_p,
                                             fill_p, fill_u, _fp(self._bounds), alloc,
                                             self.stream or None, C.byref(h))

@@ -50,7 +50,7 @@ class Pair:
         if store is not None:
             gstore = dict(dir=store["gpu_dir"], cache_blocks=store["cache_blocks"],
                           segment_bytes=store.get("segment_bytes", 0),
-                          direct_io=store.get("direct_io", 0))
+                          direct_io=store.get("direct_io", 0), reopen=store.get("reopen", 0))
         self.gpu = T.Table(T.make_config(scene.N, scene.B, capacity, staging_blocks=staging_blocks,
                                          refresh_bounds=refresh_bounds, **kw), bounds,
                            fill=fill, store=gstore)
@@ -58,8 +58,8 @@ class Pair:
                                           **kw), bounds, fill=fill, track_all=track_all)
         self.store = store
         if store is not None:
-            self.orc.store_open(store.get("orc_dir"), store["cache_blocks"],
-                                store.get("segment_bytes", 0))
+            (self.orc.store_reopen if store.get("reopen") else self.orc.store_open)(
+                store.get("orc_dir"), store["cache_blocks"], store.get("segment_bytes", 0))
         self.gsyn = Synth(GRAD_SEED, scene.N, scene.B, 0)
         self.mask_p = mask_p
         self.msyn = None

@@ -108,6 +108,27 @@ int main(int argc, char** argv) {
     CHECK(st.index(l).version <= v);
     for (uint32_t k = 0; k < B * 59; k += 13) CHECK(buf[k] == val(l, v, k));
   }
+  // ---- R30 resume: a second store over the same files recovers every Index
+  //      entry and serves the same newest versions
+  {
+    char* pool2 = nullptr;
+    if (posix_memalign((void**)&pool2, 4096, H * S) != 0) return 2;
+    BlockStore st2;
+    err = st2.open(dir, geo, H, pool2, 4096 + 3 * (4096 + S), direct != 0, 3,
+                   [](uint32_t, float*) {}, true);
+    CHECK(err.empty());
+    if (!err.empty()) std::fprintf(stderr, "%s\n", err.c_str());
+    for (uint32_t l = 0; l < K; ++l) {
+      const tgs::StoreIndex a = st.index(l), b = st2.index(l);
+      CHECK(a.file_id == b.file_id && a.offset == b.offset && a.size == b.size &&
+            a.version == b.version);
+      err = st2.read_block(l, buf.data());
+      CHECK(err.empty());
+      const uint32_t v = ver.count(l) ? ver[l] : 0;
+      for (uint32_t k = 0; k < B * 59; k += 13) CHECK(buf[k] == val(l, v, k));
+    }
+    free(pool2);
+  }
   std::printf("store host test: %d failures; hits %llu misses %llu dirty evictions %llu segments %llu\n",
               fails, (unsigned long long)st.counters().hits, (unsigned long long)st.counters().misses,
               (unsigned long long)st.counters().dirty_evictions,

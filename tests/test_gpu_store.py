@@ -132,6 +132,38 @@ def test_store_pipelined_matches_oracle(tmp_path, H):
     pr.close()
 
 
+@pytest.mark.parametrize("moments", [O.PERSIST, O.COLD_RESTART])
+def test_store_resume_after_barrier(tmp_path, moments):
+    """R30 checkpoint/resume: a second GPU context reopens the segment files
+    the first one left at its barrier; its recovered Index[k] equals the
+    oracle's (each side reopens its own files), and 20 more batches stay
+    bit-exact, ending with byte-identical files."""
+    from gpu_harness import Pair
+    cfg, sc, tr = tiny()
+    seg = 6 << 20
+    pr, g, o = _pair(sc, tmp_path, 16, seg, 1, capacity=8, moments=moments)
+    for t, planes in enumerate(random_boxes(sc, 24, seed=13)):
+        act = pr.activate(planes)
+        assert pr.step(act, t) == O.OK
+    pr.gpu.flush()
+    pr.orc.flush()
+    live = {k: pr.orc.store_index(k) for k in range(sc.K)}
+    pr.close()
+    st = dict(gpu_dir=str(g), orc_dir=str(o), cache_blocks=16, segment_bytes=seg, direct_io=1,
+              reopen=1)
+    pr = Pair(sc, capacity=8, moments=moments, store=st)
+    for k in range(sc.K):
+        assert pr.gpu.store_index(k) == pr.orc.store_index(k) == live[k], k
+    for t, planes in enumerate(random_boxes(sc, 20, seed=14)):
+        act = pr.activate(planes)
+        pr.t = t
+        pr.compare_plan(1)
+        pr.compare_store(pr.orc.list("S+"))
+        assert pr.step(act, t) == O.OK
+    _finish(pr, sc, g, o)
+    pr.close()
+
+
 def test_store_conservation_without_updates(tmp_path):
     """Empty masks: nothing is dirty, nothing is appended, every block read back
     through the store equals the generated table."""
