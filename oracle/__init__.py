@@ -91,6 +91,7 @@ def lib():
                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.or_store_open.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
+        L.or_store_compact.argtypes = [vp]
         L.or_store_reopen.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
         L.or_store_index.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint64)]
         L.or_store_stats.argtypes = [vp, C.POINTER(C.c_uint64)]
@@ -262,6 +263,12 @@ class Oracle:
         rc = lib().or_store_reopen(self.h, os.fsencode(str(dir)), cache_blocks, segment_bytes)
         if rc != OK:
             raise OracleError(rc, "or_store_reopen")
+
+    def store_compact(self):
+        """R31: merge the patch segments into a new base (after flush)."""
+        rc = lib().or_store_compact(self.h)
+        if rc != OK:
+            raise OracleError(rc, "or_store_compact")
 
     def store_index(self, k):
         """Index[k] = (file_id, offset, size, version) (PAPER.md:233)."""

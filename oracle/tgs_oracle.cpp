@@ -1039,6 +1039,43 @@ int or_store_reopen(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t 
   return OR_OK;
 }
 
+
+// Compaction ("Optional compaction can merge patch segments into
+// a new base segment, but this is outside the training critical path";
+// SPEC.md log_store compact; reading R31): at a barrier (the caller flushes
+// first), a new base segment holds every block's newest version at the base
+// offsets; it replaces the old base, the patch segments are removed, Index[k]
+// becomes (0, base offset, size, version) -- versions keep counting -- and the
+// next append opens patch segment 1 again.
+int or_store_compact(or_ctx* o) {
+  Ctx& c = o->c;
+  Store& s = c.sto;
+  if (!s.on || !s.data) return OR_EINVAL;
+  for (const auto& kv : s.cache)
+    if (kv.second.dirty) return OR_ESTATE;  // barrier first
+  for (uint32_t l : c.R)
+    if (c.dirty[c.slot_of[l]]) return OR_ESTATE;
+  const std::string tmp = s.dir + "/base.tdgs.tmp";
+  std::vector<unsigned char> h = segment_header(c, 0);
+  write_at(tmp, 0, h.data(), kPage, true);
+  std::vector<unsigned char> r(s.S, 0);
+  for (uint32_t l = 0; l < c.Kloc; ++l) {
+    std::fill(r.begin(), r.end(), 0);
+    const IndexEntry& ix = s.index[l];
+    read_at(seg_path(s, ix.file_id), ix.offset, r.data(), s.payload);
+    write_at(tmp, kPage + (uint64_t)l * s.S, r.data(), s.S, false);
+  }
+  std::filesystem::rename(tmp, seg_path(s, 0));
+  for (uint32_t fid = 1; fid <= s.cur_file; ++fid) std::filesystem::remove(seg_path(s, fid));
+  for (uint32_t l = 0; l < c.Kloc; ++l) {
+    s.index[l].file_id = 0;
+    s.index[l].offset = kPage + (uint64_t)l * s.S;
+  }
+  s.cur_file = 0;
+  s.cur_size = 0;
+  return OR_OK;
+}
+
 int or_store_index(or_ctx* o, uint64_t kg, uint64_t* out4) {
   Ctx& c = o->c;
   if (!c.sto.on || kg % c.cfg.world_size != (uint64_t)c.cfg.rank) return OR_EINVAL;

@@ -109,6 +109,10 @@ int or_store_open(or_ctx* c, const char* dir, uint32_t cache_blocks, uint64_t se
  * (after its barrier): Index recovered by scanning the segments (later
  * records win, a torn tail record dropped), empty cache; needs track_all. */
 int or_store_reopen(or_ctx* c, const char* dir, uint32_t cache_blocks, uint64_t segment_bytes);
+/* R31 compaction at a barrier (flush first; ESTATE otherwise): a new base
+ * segment with every block's newest version replaces the old one, the patch
+ * segments are removed, Index points into the base again (versions kept). */
+int or_store_compact(or_ctx* c);
 int or_store_index(or_ctx* c, uint64_t k_global, uint64_t* out4);
 int or_store_stats(or_ctx* c, uint64_t* out10);
 uint32_t or_store_lru(or_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap);

@@ -395,3 +395,38 @@ def test_reopen_recovers_index_and_table(tmp_path):
                    track_all=True)
     with pytest.raises(O.OracleError):
         bad.store_reopen(tmp_path, 16, budget)
+
+
+def test_compaction_keeps_every_newest_version(tmp_path):
+    """R31 (SPEC.md log_store compact): after the barrier the
+    patches merge into a new base -- every block's payload byte-identical to
+    before, Index[k] = (0, base offset, size, same version), no patch segment
+    left, the base the same size; training then appends from patch 1 with
+    versions counting on.  Compaction with dirty data pending is refused."""
+    cfg, sc, tr = tiny()
+    S = _pad(3 * sc.B * 59 * 4)
+    sc, ((flat, _), (st, _)) = _flat_and_store(tmp_path, O.PERSIST, False, 16, PAGE + 4 * (PAGE + S))
+    before = read_segments(tmp_path)
+    assert len(before) > 2
+    idx = {k: st.store_index(k) for k in range(sc.K)}
+    pay = {k: payload_at(before, *idx[k][:2], idx[k][2]).copy() for k in range(sc.K)}
+    base_size = (tmp_path / "base.tdgs").stat().st_size
+    st.store_compact()
+    after = read_segments(tmp_path)
+    assert list(after) == [0] and (tmp_path / "base.tdgs").stat().st_size == base_size
+    for k in range(sc.K):
+        fid, off, n, ver = st.store_index(k)
+        assert (fid, off, n, ver) == (0, PAGE + k * S, idx[k][2], idx[k][3])
+        assert np.array_equal(payload_at(after, 0, off, n), pay[k]), k
+    lr = lr_3dgs()
+    grad = synth_grad(W.SEEDS["grads"], sc.N, sc.B)
+    for planes in random_boxes(sc, 10, seed=31):
+        st.activate(planes)
+        st.step_adam(lr, grad=grad)
+    with pytest.raises(O.OracleError):  # dirty blocks on the GPU: barrier first
+        st.store_compact()
+    st.flush()
+    segs = read_segments(tmp_path)
+    assert 1 in segs
+    for off, gid, ver, n in segs[1][2]:
+        assert ver > idx[gid][3]
