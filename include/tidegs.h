@@ -214,6 +214,14 @@ typedef struct {
 tgs_status tgs_get_store_stats(tgs_ctx* ctx, tgs_store_stats* out);
 /* Index[k] of global block k: out4 = (file_id, payload offset, payload bytes, version) */
 tgs_status tgs_store_index(tgs_ctx* ctx, uint64_t k_global, uint64_t* out4);
+/* Compaction ("Optional compaction can merge patch segments into a
+ * new base segment, but this is outside the training critical path"; reading
+ * R31): performs the tgs_flush barrier, then writes every block's newest version
+ * into a new base segment (base.tdgs.tmp, made durable, renamed over base.tdgs),
+ * removes the patch segments and points Index[k] into the base again (versions
+ * kept; the next append opens patch segment 1).  ESTATE without a store; TGS_EIO
+ * on an I/O failure (the old files stay valid until the rename). */
+tgs_status tgs_store_compact(tgs_ctx* ctx);
 /* cached global ids, least recently used first, and their dirty flags (either may
  * be NULL); returns the number cached (writes at most cap) */
 uint32_t tgs_store_lru(tgs_ctx* ctx, uint32_t* blocks, uint8_t* dirty, uint32_t cap);

@@ -1491,6 +1491,21 @@ tgs_status tgs_store_index(tgs_ctx* c, uint64_t kg, uint64_t* out4) {
   return TGS_OK;
 }
 
+tgs_status tgs_store_compact(tgs_ctx* c) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!c->store) return TGS_ESTATE;
+  st = tgs_flush(c);  // the barrier
+  if (st != TGS_OK) return st;
+  const std::string e = c->store->compact();
+  if (!e.empty()) {
+    c->poisoned = true;
+    set_err(c, "store: %s", e.c_str());
+    return TGS_EIO;
+  }
+  return TGS_OK;
+}
+
 uint32_t tgs_store_lru(tgs_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap) {
   if (check(c) != TGS_OK || !c->store || sync_all(c) != TGS_OK) return 0;
   std::vector<uint32_t> b;

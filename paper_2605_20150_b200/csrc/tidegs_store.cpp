@@ -287,6 +287,67 @@ std::string BlockStore::recover() {
   return "";
 }
 
+// R31 compaction, at a barrier: every block's newest version
+// is copied to base.tdgs.tmp at the base offsets (reads through Index, writes
+// in parallel), which is made durable and renamed over the base; the patch
+// segments are removed and Index points into the base again.
+std::string BlockStore::compact() {
+  for (const Ent& e : ents_)
+    if (e.blk >= 0 && ent_of_[e.blk] >= 0 && e.dirty) return "compact: dirty entries (barrier first)";
+  const std::string tmp = dir_ + "/base.tdgs.tmp";
+  int fd = ::open(tmp.c_str(), O_RDWR | O_CREAT | O_TRUNC | (direct_ ? O_DIRECT : 0), 0644);
+  if (fd < 0) return errno_str("open base.tdgs.tmp");
+  std::unique_ptr<char, decltype(&free)> hp(aligned_pages(kPage), &free);
+  segment_header(reinterpret_cast<unsigned char*>(hp.get()), 0, g_);
+  if (!pwrite_all(fd, hp.get(), kPage, 0)) {
+    ::close(fd);
+    return errno_str("write base header");
+  }
+  for (uint32_t f = 0; f <= cur_file_; ++f)
+    if (fd_of(f) < 0) {
+      ::close(fd);
+      return errno_str("open segment");
+    }
+  std::atomic<bool> bad{false};
+  pool_io_->parallel_for(g_.Kloc, [&](uint32_t l) {
+    thread_local std::unique_ptr<char, decltype(&free)> buf(nullptr, &free);
+    thread_local uint64_t cap = 0;
+    if (cap < S_) {
+      buf.reset(aligned_pages(S_));
+      cap = S_;
+    }
+    const StoreIndex& ix = index_[l];
+    std::memset(buf.get(), 0, S_);
+    if (!pread_all(fds_[ix.file_id], buf.get(), S_, ix.offset) ||
+        !pwrite_all(fd, buf.get(), S_, kPage + (uint64_t)l * S_))
+      bad = true;
+  });
+  if (bad || ::fdatasync(fd) != 0) {
+    ::close(fd);
+    return errno_str("write compacted base");
+  }
+  if (::rename(tmp.c_str(), (dir_ + "/base.tdgs").c_str()) != 0) {
+    ::close(fd);
+    return errno_str("rename compacted base");
+  }
+  for (uint32_t f = 0; f < fds_.size(); ++f) {
+    if (fds_[f] >= 0) ::close(fds_[f]);
+    if (f > 0) {
+      char name[64];
+      std::snprintf(name, sizeof name, "/patch-%06u.tdgp", f);
+      ::unlink((dir_ + name).c_str());
+    }
+  }
+  fds_.assign(1, fd);
+  for (uint32_t l = 0; l < g_.Kloc; ++l) {
+    index_[l].file_id = 0;
+    index_[l].offset = kPage + (uint64_t)l * S_;
+  }
+  cur_file_ = 0;
+  cur_size_ = 0;
+  return "";
+}
+
 void BlockStore::unlink(int32_t e) {
   Ent& x = ents_[e];
   if (!x.listed) return;

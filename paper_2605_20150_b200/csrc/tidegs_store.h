@@ -101,6 +101,8 @@ class BlockStore {
   void mark_dirty(uint32_t l, int32_t T);
   // the barrier: append every dirty entry (ascending id), clear dirty, fdatasync
   std::string flush_all(const std::function<void(int32_t)>& wait_d2h);
+  // R31: merge the patch segments into a new base (after flush_all)
+  std::string compact();
 
   // host address of block l's cached record, nullptr if not cached
   float* entry_of(uint32_t l) const {

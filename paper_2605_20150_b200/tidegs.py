@@ -30,7 +30,7 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
            "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error",
            "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru",
-           "tgs_order_views")
+           "tgs_order_views", "tgs_store_compact")
 
 
 class Config(C.Structure):
@@ -137,6 +137,7 @@ def lib():
                                            C.POINTER(Allocator), vp, C.POINTER(vp)]
         L.tgs_get_store_stats.argtypes = [vp, C.POINTER(StoreStats)]
         L.tgs_store_index.argtypes = [vp, u64, C.POINTER(C.c_uint64)]
+        L.tgs_store_compact.argtypes = [vp]
         L.tgs_store_lru.restype = u32
         L.tgs_store_lru.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), u32]
         L.tgs_destroy.argtypes = [vp]
@@ -389,6 +390,10 @@ class Table:
         out = (C.c_uint64 * 4)()
         self._err(lib().tgs_store_index(self.h, k, out), "tgs_store_index")
         return tuple(int(x) for x in out)
+
+    def store_compact(self):
+        """R31: barrier, then merge the patch segments into a new base."""
+        self._err(lib().tgs_store_compact(self.h), "tgs_store_compact")
 
     def store_lru(self):
         n = lib().tgs_store_lru(self.h, None, None, 0)

@@ -164,6 +164,31 @@ def test_store_resume_after_barrier(tmp_path, moments):
     pr.close()
 
 
+def test_store_compaction(tmp_path):
+    """R31: compaction at a barrier on both sides -> byte-identical base
+    segments, no patch left, identical Index; training then continues
+    bit-exact (patch segment 1 again, versions counting on)."""
+    cfg, sc, tr = tiny()
+    pr, g, o = _pair(sc, tmp_path, 16, 6 << 20, 1, capacity=8)
+    boxes = random_boxes(sc, 40, seed=17)
+    for t, planes in enumerate(boxes[:28]):
+        act = pr.activate(planes)
+        assert pr.step(act, t) == O.OK
+    pr.gpu.store_compact()
+    pr.orc.flush()
+    pr.orc.store_compact()
+    assert _compare_files(g, o) == 1
+    pr.compare_store(range(sc.K))
+    for t, planes in enumerate(boxes[28:], 28):
+        act = pr.activate(planes)
+        pr.t = t
+        pr.compare_plan(1)
+        pr.compare_store(pr.orc.list("S+"))
+        assert pr.step(act, t) == O.OK
+    _finish(pr, sc, g, o)
+    pr.close()
+
+
 def test_store_conservation_without_updates(tmp_path):
     """Empty masks: nothing is dirty, nothing is appended, every block read back
     through the store equals the generated table."""
