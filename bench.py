@@ -418,13 +418,15 @@ def main():
     d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
     stage_in = st1["n_stage_in"] - st0["n_stage_in"]
     visible = st1["n_visible"] - st0["n_visible"]
-    if ws > 1:
-        t = torch.tensor([rows, ms, h2d, d2h, stage_in, visible, tm["adam_ms"]],
+    active_blocks = st1["n_active_blocks"] - st0["n_active_blocks"]
+    if ws > 1:  # whole job: counts summed over ranks, the slowest rank's clock
+        t = torch.tensor([rows, ms, h2d, d2h, stage_in, visible, tm["adam_ms"], active_blocks],
                          dtype=torch.float64, device=dev)
         mx = t.clone()
         torch.distributed.all_reduce(t)
         torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        rows, h2d, d2h, stage_in, visible = (float(x) for x in (t[0], t[2], t[3], t[4], t[5]))
+        rows, h2d, d2h, stage_in, visible, active_blocks = (
+            float(x) for x in (t[0], t[2], t[3], t[4], t[5], t[7]))
         ms = float(mx[1])
     value = rows / (ms / 1e3)
 
@@ -517,7 +519,7 @@ def main():
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": tm["kernel_launches"],
                 "roofline": roof, "link_roofline": link, "cpu_baseline": cpu,
                 "detail": {"active_blocks_per_step": None if not args.steps else
-                           (st1["n_active_blocks"] - st0["n_active_blocks"]) / args.steps,
+                           active_blocks / args.steps,
                            "visible_blocks_per_step": visible / args.steps,
                            "stage_in_blocks_per_step": stage_in / args.steps,
                            "h2d_GB_per_step": h2d / args.steps / 1e9,
