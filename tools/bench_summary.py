@@ -8,7 +8,10 @@ DESC = {"default": "300m aerial smooth, J=64, C=6309, cold restart (the N=1 head
         "fine": "same + Level-2 fine filter (f1) as I_t",
         "100m_persist": "100m street, J=64, C=2103, moments persist (after 400 warm-up batches)",
         "11m": "11m aerial, J=4, C=K (in-memory)",
-        "300m_random": "300m aerial, shuffled views (w/o trajectory order)"}
+        "300m_random": "300m aerial, shuffled views (w/o trajectory order)",
+        "300m_tsp": "300m aerial, shuffled views re-ordered by the GPU clustered TSP (f4)",
+        "1b_shard8": "1B aerial, one GPU's share of the 8-way block-sharded table (--shard-of 8)",
+        "store_1b_shard8": "the same shard on the f3 store tier (O_DIRECT segments on local disk, CPU cache 3C)"}
 
 tag, names = sys.argv[1], sys.argv[2:]
 rows = []
@@ -39,5 +42,12 @@ d = lines.get("default")
 if d:
     out += ["", f"* default: clocks {d['clocks']}; cpu_baseline {d['cpu_baseline']}; "
                 f"gpu_launches {d['gpu_launches']} over {d['steps']} steps."]
+for f, d in lines.items():
+    st = (d.get("detail") or {}).get("store")
+    if st:
+        out += [f"* {f}: CPU-cache hit rate {st['hit_rate']:.2f}, "
+                f"{st['per_step']['misses']:.1f} misses/step read at "
+                f"{st['ssd_read_GBps_in_reads']:.2f} GB/s (dd sequential peak "
+                f"{st.get('ssd_read_peak_GBps') or 0:.2f} GB/s); see profiles/store_r01.md."]
 open(f"profiles/bench_{tag}.md", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
