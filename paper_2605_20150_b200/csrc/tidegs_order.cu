@@ -12,9 +12,10 @@
 //
 //   k_lex          : lexicographically smallest view v0 (grid argmin + last-CTA finish)
 //   k_init_step x k: maximin initialisation, one centre per launch
-//   Lloyd          : k_assign (grid, centres in smem, change flag) then
-//                    k_update (thread per cluster: ascending-index sums -> means)
-//   k_members      : thread per cluster: ascending member lists (counting-sort offsets)
+//   Lloyd          : k_assign (grid, centres in smem, change flag), then a stable
+//                    counting sort of the views by cluster (k_chunk_count, k_chunk_scan,
+//                    k_offsets, k_scatter: ascending member lists) and k_update_lists (warp per
+//                    cluster: each member in ascending view index added in turn -> means)
 //   k_cluster_tour : one CTA, nearest-neighbour over the non-empty centres
 //   k_inner_tour   : one CTA per cluster, nearest-neighbour over its members
 #include <algorithm>
@@ -222,46 +223,92 @@ __global__ void k_lloyd_check(Ctl* ctl) {
   }
 }
 
-// Lloyd update: cluster j's centre = mean of its members, summed in ascending
-// view index.  One warp per cluster: 32 assignments per ballot, then lane i
-// (i < D) adds feature i of each member in ascending order -- the sequential
-// sum of R29, 32x fewer serial steps than a thread scanning every view.
-__global__ void k_update(const double* f, uint32_t M, int D, double* cen, uint32_t k,
-                         const uint32_t* asg, uint32_t* cnt_out, const Ctl* ctl) {
-  if (ctl && ctl->stop) return;
-  const uint32_t j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const uint32_t lane = threadIdx.x & 31;
-  if (j >= k) return;
-  double s = 0.0;
-  uint32_t n = 0;
-  for (uint32_t base = 0; base < M; base += 32) {
-    const uint32_t v = base + lane;
-    uint32_t hit = __ballot_sync(0xffffffffu, v < M && __ldg(asg + v) == j);
-    n += __popc(hit);
-    while (hit) {
-      const uint32_t u = base + __ffs(hit) - 1;
-      hit &= hit - 1;
-      if (lane < (uint32_t)D) s = __dadd_rn(s, f[(size_t)u * D + lane]);
-    }
-  }
-  if (n && cen && lane < (uint32_t)D) cen[(size_t)j * D + lane] = __ddiv_rn(s, (double)n);
-  if (cnt_out && lane == 0) cnt_out[j] = n;
+// ---- stable counting sort of the views by cluster (chunks of kChunk views)
+constexpr int kChunk = 256;
+constexpr uint32_t kMaxK = 8192;
+
+// per chunk: how many of its views each cluster holds
+__global__ void k_chunk_count(uint32_t M, uint32_t k, const uint32_t* asg, uint32_t* chunk_cnt,
+                              const Ctl* ctl) {
+  if (ctl->stop) return;
+  extern __shared__ uint32_t sc_cnt[];
+  for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) sc_cnt[j] = 0;
+  __syncthreads();
+  const uint32_t v = blockIdx.x * kChunk + threadIdx.x;
+  if (v < M) atomicAdd(&sc_cnt[asg[v]], 1u);  // a count: order-free
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < k; j += blockDim.x)
+    chunk_cnt[(size_t)blockIdx.x * k + j] = sc_cnt[j];
 }
 
-// ascending member list of cluster j at off[j] (one warp per cluster, ballot compaction)
-__global__ void k_members(uint32_t M, uint32_t k, const uint32_t* asg, const uint32_t* off,
-                          uint32_t* mem) {
+// per cluster: exclusive scan over the chunks (in place) and the cluster size
+__global__ void k_chunk_scan(uint32_t nchunks, uint32_t k, uint32_t* chunk_cnt, uint32_t* cnt,
+                             const Ctl* ctl) {
+  if (ctl->stop) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  uint32_t run = 0;
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    const uint32_t x = chunk_cnt[(size_t)c * k + j];
+    chunk_cnt[(size_t)c * k + j] = run;
+    run += x;
+  }
+  cnt[j] = run;
+}
+
+// cluster offsets: exclusive scan of the sizes (one CTA of 1024)
+__global__ void k_offsets(uint32_t k, const uint32_t* cnt, uint32_t* off, const Ctl* ctl) {
+  if (ctl->stop) return;
+  __shared__ uint32_t part[1024];
+  const uint32_t per = (k + blockDim.x - 1) / blockDim.x;
+  const uint32_t a = threadIdx.x * per, b = min(k, a + per);
+  uint32_t sum = 0;
+  for (uint32_t j = a; j < b; ++j) sum += cnt[j];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (uint32_t w = 1; w < blockDim.x; w <<= 1) {  // inclusive Hillis-Steele scan
+    const uint32_t x = threadIdx.x >= w ? part[threadIdx.x - w] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += x;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - sum;
+  for (uint32_t j = a; j < b; ++j) {
+    off[j] = run;
+    run += cnt[j];
+  }
+}
+
+// each chunk places its views in ascending order (one thread walks the chunk,
+// so equal clusters keep index order): member lists ascending per cluster
+__global__ void k_scatter(uint32_t M, uint32_t k, const uint32_t* asg, const uint32_t* chunk_off,
+                          const uint32_t* off, uint32_t* mem, const Ctl* ctl) {
+  if (ctl->stop) return;
+  extern __shared__ uint32_t sc_pos[];
+  for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) sc_pos[j] = 0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint32_t v0 = blockIdx.x * kChunk, v1 = min(M, v0 + kChunk);
+  for (uint32_t v = v0; v < v1; ++v) {
+    const uint32_t j = asg[v];
+    mem[off[j] + chunk_off[(size_t)blockIdx.x * k + j] + sc_pos[j]++] = v;
+  }
+}
+
+// Lloyd update from the member lists: warp per cluster, lane i (< D) adds
+// feature i of each member in ascending view index (R29's sequential sum)
+__global__ void k_update_lists(const double* f, int D, double* cen, uint32_t k,
+                               const uint32_t* cnt, const uint32_t* off, const uint32_t* mem,
+                               const Ctl* ctl) {
+  if (ctl->stop) return;
   const uint32_t j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const uint32_t lane = threadIdx.x & 31;
-  if (j >= k) return;
-  uint32_t o = off[j];
-  for (uint32_t base = 0; base < M; base += 32) {
-    const uint32_t v = base + lane;
-    const bool in = v < M && __ldg(asg + v) == j;
-    const uint32_t hit = __ballot_sync(0xffffffffu, in);
-    if (in) mem[o + __popc(hit & ((1u << lane) - 1u))] = v;
-    o += __popc(hit);
-  }
+  if (j >= k || lane >= (uint32_t)D) return;
+  const uint32_t n = cnt[j], o = off[j];
+  if (n == 0) return;
+  double s = 0.0;
+  for (uint32_t m = 0; m < n; ++m) s = __dadd_rn(s, f[(size_t)mem[o + m] * D + lane]);
+  cen[(size_t)j * D + lane] = __ddiv_rn(s, (double)n);
 }
 
 // nearest-neighbour tour over the non-empty centres from the cluster of v0
@@ -345,7 +392,7 @@ extern "C" tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D
     if (!(feat[i] - feat[i] == 0.0)) return TGS_EINVAL;  // non-finite
   uint32_t k = 1;
   while ((uint64_t)k * k < M) ++k;  // R29 step 1
-  if ((size_t)k * D * sizeof(double) > 200 * 1024) return TGS_EINVAL;  // centres must fit smem
+  if ((size_t)k * D * sizeof(double) > 200 * 1024 || k > kMaxK) return TGS_EINVAL;  // smem
   if (cudaSetDevice(device) != cudaSuccess) return TGS_ECUDA;
   const int grid = (int)std::min<uint64_t>(148 * 4, ((uint64_t)M + kNT - 1) / kNT);
   std::vector<void*> allocs;
@@ -370,6 +417,8 @@ extern "C" tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D
   uint32_t* d_toff = (uint32_t*)get((size_t)k * 4);
   uint8_t* d_used = (uint8_t*)get((size_t)M + k);
   uint32_t* d_perm = (uint32_t*)get((size_t)M * 4);
+  const uint32_t nchunks = (M + kChunk - 1) / kChunk;
+  uint32_t* d_chunk = (uint32_t*)get((size_t)nchunks * k * 4);
   uint32_t* d_part = (uint32_t*)get((size_t)grid * 16);
   Ctl* d_ctl = (Ctl*)get(sizeof(Ctl));
   Ctl* h_ctl = nullptr;
@@ -403,19 +452,19 @@ extern "C" tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D
   for (uint32_t pass = 0; pass < 100; ++pass) {  // R29 step 3, no host round trip per pass
     k_assign<<<grid, kNT, smem, s>>>(d_f, M, (int)D, d_cen, k, d_asg, d_ctl);
     k_lloyd_check<<<1, 1, 0, s>>>(d_ctl);
-    k_update<<<(k + 7) / 8, 256, 0, s>>>(d_f, M, (int)D, d_cen, k, d_asg, nullptr, d_ctl);
+    // members of every cluster in ascending index, then the ordered-sum means;
+    // after the last pass that changed something these lists are the final ones
+    k_chunk_count<<<nchunks, kChunk, k * 4, s>>>(M, k, d_asg, d_chunk, d_ctl);
+    k_chunk_scan<<<(k + 127) / 128, 128, 0, s>>>(nchunks, k, d_chunk, d_cnt, d_ctl);
+    k_offsets<<<1, 1024, 0, s>>>(k, d_cnt, d_off, d_ctl);
+    k_scatter<<<nchunks, kChunk, k * 4, s>>>(M, k, d_asg, d_chunk, d_off, d_mem, d_ctl);
+    k_update_lists<<<(k + 7) / 8, 256, 0, s>>>(d_f, (int)D, d_cen, k, d_cnt, d_off, d_mem, d_ctl);
   }
   CKO(cudaGetLastError());
   {
-    // member lists (counting-sort offsets), cluster tour, tours inside clusters
-    k_update<<<(k + 7) / 8, 256, 0, s>>>(d_f, M, (int)D, nullptr, k, d_asg, d_cnt, nullptr);
-    std::vector<uint32_t> cnt(k), off(k);
+    // cluster tour, tours inside clusters (member lists of the final assignment)
+    std::vector<uint32_t> cnt(k);
     CKO(cudaMemcpyAsync(cnt.data(), d_cnt, k * 4, cudaMemcpyDeviceToHost, s));
-    CKO(cudaStreamSynchronize(s));
-    uint32_t acc = 0;
-    for (uint32_t j = 0; j < k; ++j) off[j] = acc, acc += cnt[j];
-    CKO(cudaMemcpyAsync(d_off, off.data(), k * 4, cudaMemcpyHostToDevice, s));
-    k_members<<<(k + 7) / 8, 256, 0, s>>>(M, k, d_asg, d_off, d_mem);
     k_cluster_tour<<<1, 1024, 0, s>>>(d_cen, (int)D, k, d_cnt, d_asg, d_tour, d_used + M, d_ctl);
     std::vector<uint32_t> tour(k);
     CKO(cudaMemcpyAsync(tour.data(), d_tour, k * 4, cudaMemcpyDeviceToHost, s));
@@ -423,7 +472,7 @@ extern "C" tgs_status tgs_order_views(const double* feat, uint32_t M, uint32_t D
     CKO(cudaStreamSynchronize(s));
     it = h_ctl->iters;
     std::vector<uint32_t> toff(k, 0);
-    acc = 0;
+    uint32_t acc = 0;
     for (uint32_t c = 0; c < h_ctl->n_tour; ++c) toff[c] = acc, acc += cnt[tour[c]];
     CKO(cudaMemcpyAsync(d_toff, toff.data(), k * 4, cudaMemcpyHostToDevice, s));
     k_inner_tour<<<h_ctl->n_tour, 256, 0, s>>>(d_f, (int)D, d_cen, d_tour, d_cnt, d_off, d_mem,
