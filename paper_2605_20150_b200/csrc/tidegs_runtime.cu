@@ -70,6 +70,9 @@ struct tgs_ctx {
   float* host = nullptr;
   size_t host_bytes = 0;
   tgs::BlockStore* store = nullptr;
+  // A = R n K lists of the last three activates (index T % 3): the plan of t+2
+  // may then overwrite its parity's other lists while Adam(t) still reads its A
+  uint32_t *a3_blk[3] = {}, *a3_slot[3] = {}, *a3_gid[3] = {};
   char* cache_pool = nullptr;     // [H][S] pinned (store mode)
   uint32_t* sm_map = nullptr;     // mapped host [C] S- local ids (store mode, written by k_plan)
   // mapped pinned
@@ -292,6 +295,17 @@ tgs_status ensure_lut(tgs_ctx* c, float b1, float b2, uint32_t need) {
     c->lut_n = c->lut_cap;
   }
   return TGS_OK;
+}
+
+// the device state as the kernels of activate T (parity p) see it: its A lists
+// come from the 3-deep ring
+inline Dev dev_for(const tgs_ctx* c, int p, int32_t T) {
+  Dev x = c->d;
+  const int r = (int)(((uint32_t)T) % 3u);
+  x.a_blk[p] = c->a3_blk[r];
+  x.a_slot[p] = c->a3_slot[r];
+  x.a_gid[p] = c->a3_gid[r];
+  return x;
 }
 
 inline float* host_rec(tgs_ctx* c, uint32_t l) {
@@ -755,14 +769,17 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     d.sp_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
     d.sm_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
     d.sm_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
-    d.a_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
-    d.a_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
-    d.a_gid[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.a_blk[p] = d.a_slot[p] = d.a_gid[p] = nullptr;  // per launch, from the ring below
   }
   d.hdr_dev = dalloc_t<PlanHdr>(c, 1, ok);
   d.cnt = dalloc_t<uint32_t>(c, CNT_N, ok);
   d.stats = dalloc_t<unsigned long long>(c, ST_N, ok);
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
+  for (int r = 0; r < 3; ++r) {
+    c->a3_blk[r] = dalloc_t<uint32_t>(c, Cc, ok);
+    c->a3_slot[r] = dalloc_t<uint32_t>(c, Cc, ok);
+    c->a3_gid[r] = dalloc_t<uint32_t>(c, Cc, ok);
+  }
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
   d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
   d.pend[0] = dalloc_t<uint32_t>(c, Kl, ok);
@@ -877,9 +894,10 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   // the batch of t-2 (same staging buffer) was consumed before that plan's readback
   if (J) std::memcpy(c->planes_pinned + (size_t)p * kMaxCams * 24, cams, sizeof(float) * 24 * J);
   prof_begin(c, c->plan, tp);
-  CK(launch_cull(d, J, T, p, c->plan));
-  CK(launch_quota(d, J, T, p, c->plan));
-  CK(launch_plan(d, T, p, c->plan));
+  const Dev dk = dev_for(c, p, T);
+  CK(launch_cull(dk, J, T, p, c->plan));
+  CK(launch_quota(dk, J, T, p, c->plan));
+  CK(launch_plan(dk, T, p, c->plan));
   prof_end(c, c->plan, tp, 2);
   c->tm.kernel_launches += (d.Kloc ? 1 : 0) + ((J && d.Kloc) ? 2 : 0) + 1;
   CK(cudaEventRecord(c->ev_plan, c->plan));
@@ -1040,8 +1058,8 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     out->n_evict = h.nSm;
     out->n_evict_dirty = 0;  // decided after the previous Adam; see tgs_get_stats
     out->h2d_bytes = (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
-    out->d_active_blocks = d.a_gid[p];
-    out->d_active_slots = d.a_slot[p];
+    out->d_active_blocks = c->a3_gid[(uint32_t)T % 3u];
+    out->d_active_slots = c->a3_slot[(uint32_t)T % 3u];
     out->d_params = d.params;
     out->d_grads = d.grads;
     out->slot_stride = 3 * d.rec_floats;
@@ -1072,20 +1090,27 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
   CK(cudaStreamWaitEvent(c->compute, c->ev_ready[p], 0));
   if (nA == 0) return TGS_OK;
+  const Dev dk = dev_for(c, p, c->T - 1);
   Timer t1, t2;
   prof_begin(c, c->compute, t1);
-  CK(launch_adam_prologue(c->d, nA, p, d_row_mask, c->compute));
+  CK(launch_adam_prologue(dk, nA, p, d_row_mask, c->compute));
   prof_end(c, c->compute, t1, 1);
+  // After the prologue, Adam reads only its A lists (3-deep ring), the per-
+  // entry constants and slots the plan never hands out while R_{t+1} holds
+  // them: the plan of t+2 may overwrite this parity's other lists now.  With
+  // the bound refresh on, that plan also merges k_refresh's radii (R25), so
+  // the lists stay in use until after it.
+  if (!c->d.refresh) CK(cudaEventRecord(c->ev_lists[p], c->compute));
   prof_begin(c, c->compute, t2);
-  CK(launch_adam(c->d, nA, p, d_row_mask, h, c->adam_grid, c->compute));
+  CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
   c->tm.kernel_launches += 2;
   if (c->d.refresh) {
-    CK(launch_refresh(c->d, nA, p, c->compute));
+    CK(launch_refresh(dk, nA, p, c->compute));
     c->tm.kernel_launches++;
+    CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   }
   if (c->cfg.serialize) CK(cudaStreamSynchronize(c->compute));  // ablation w/o Overlap
-  CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }
 
@@ -1101,9 +1126,10 @@ tgs_status tgs_fine_filter(tgs_ctx* c, uint32_t* d_row_mask) {
   if (c->last.nA == 0 || c->d.Kloc == 0) return TGS_OK;
   Timer tf;
   prof_begin(c, c->compute, tf);
-  CK(launch_fine(c->d, c->last.nA, c->last_J, p, d_row_mask, c->compute));
+  CK(launch_fine(dev_for(c, p, c->T - 1), c->last.nA, c->last_J, p, d_row_mask, c->compute));
   prof_end(c, c->compute, tf, 8);
   c->tm.kernel_launches++;
+  CK(cudaEventRecord(c->ev_lists[p], c->compute));  // k_fine reads this parity's K^(j)
   return TGS_OK;
 }
 
