@@ -68,6 +68,10 @@ def parse():
                     help="CPU-cache records for --store (0 -> 3x the GPU capacity)")
     ap.add_argument("--store-buffered", action="store_true",
                     help="--store through the page cache instead of O_DIRECT")
+    ap.add_argument("--capacity", type=int, default=0,
+                    help="override the config's capacity C (blocks, world size 1; C_g = ceil(C/G))")
+    ap.add_argument("--pool-slots", type=int, default=0,
+                    help="device slot pool P per GPU (0 -> 2 C_g, R13)")
     ap.add_argument("--io-threads", type=int, default=0,
                     help="parallel SSD requests of the --store tier (0 -> library default)")
     return ap.parse_args()
@@ -158,6 +162,16 @@ def ssd_read_peak(path, gib=4):
         return None
 
 
+def _workload(args):
+    """The named config, with --capacity overriding its C (the capacity sweep of
+    SURVEY §8d: C as a multiple of the mean #K_t)."""
+    wl = W.CONFIGS[args.config]
+    if args.capacity:
+        import dataclasses
+        wl = dataclasses.replace(wl, capacity=int(args.capacity))
+    return wl
+
+
 def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -177,7 +191,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return
     import oracle as O
-    wl = W.CONFIGS[args.config]
+    wl = _workload(args)
     sc = wl.scene()
     tr = wl.trajectory(sc)
     if wl.tsp:  # f4 on the reference arm: the oracle's clustered-TSP order
@@ -246,6 +260,7 @@ def _config_dict_base(args, wl, ws):
                         f"({order} order), J={wl.J} cameras/batch",
             "n_gaussians": wl.n_gaussians, "block_size": wl.block_size, "J": wl.J,
             "capacity_blocks_per_gpu": -(-wl.capacity // ws), "moments": args.moments,
+            **({"pool_slots_per_gpu": args.pool_slots} if getattr(args, "pool_slots", 0) else {}),
             "policy": "restage-all (w/o Tide)" if getattr(args, "no_tide", False) else "tide",
             "overlap": not getattr(args, "no_overlap", False),
             "bound_refresh": bool(getattr(args, "refresh_bounds", False)),
@@ -302,7 +317,7 @@ def main():
         local = 0  # every rank on cuda:0 (functional multi-rank run on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    wl = W.CONFIGS[args.config]
+    wl = _workload(args)
     sc = wl.scene()
     tr = wl.trajectory(sc)
     order_ms = None
@@ -314,7 +329,7 @@ def main():
     cap = -(-wl.capacity // shard_ws)
     moments = T.COLD_RESTART if args.moments == "cold" else T.PERSIST
     t_setup = time.perf_counter()
-    cfg = T.make_config(sc.N, sc.B, cap, moments=moments, world_size=shard_ws, rank=shard_rank,
+    cfg = T.make_config(sc.N, sc.B, cap, pool_slots=args.pool_slots, moments=moments, world_size=shard_ws, rank=shard_rank,
                         device=local, tide=0 if args.no_tide else 1,
                         serialize=1 if args.no_overlap else 0,
                         refresh_bounds=1 if args.refresh_bounds else 0)
@@ -393,10 +408,14 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         ev0.record(stream)
-        for i in range(args.warmup, total):
+        # per-step cadence on the compute stream (no host sync): p50 / p99 of T_iter
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for j, i in enumerate(range(args.warmup, total)):
             step(i)
+            evs[j].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
+    step_ms = np.diff(np.array([0.0] + [ev0.elapsed_time(e) for e in evs]))
     if ws > 1:
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -524,6 +543,10 @@ def main():
                            "stage_in_blocks_per_step": stage_in / args.steps,
                            "h2d_GB_per_step": h2d / args.steps / 1e9,
                            "d2h_GB_per_step": d2h / args.steps / 1e9,
+                           "step_ms": {"p50": float(np.percentile(step_ms, 50)),
+                                       "p99": float(np.percentile(step_ms, 99)),
+                                       "max": float(step_ms.max()),
+                                       "how": "compute-stream event after each step (rank 0)"},
                            "plan_ms_per_step": tm["plan_ms"] / args.steps,
                            "fine_ms_per_step": tm["fine_ms"] / args.steps,
                            "adam_prologue_ms_per_step": tm["adam_prologue_ms"] / args.steps,

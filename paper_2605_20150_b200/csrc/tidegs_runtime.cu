@@ -103,6 +103,12 @@ struct tgs_ctx {
   uint32_t last_ndirty = 0;
   std::mutex prof_mu;
   size_t d2h_max_merge = SIZE_MAX;  // TGS_D2H_MERGE=<records> caps merged write-back copies
+  // The plan of t+2 waits for all of Adam(t) (default), or with
+  // TGS_LISTS_AFTER_ADAM=0 only for its prologue (the A lists then come from
+  // the 3-deep ring).  The early release lets the high-priority plan kernels
+  // run inside Adam, which costs Adam ~5% of its HBM rate and gains the
+  // link-bound step nothing (profiles/ab_lists_r01.md): off by default.
+  bool lists_after_adam = true;
   // Adam LUT (bias corrections, R9)
   std::vector<float> lut_bc1_h, lut_ibs_h;
   float* lut_pinned = nullptr;     // [2][lut_cap]
@@ -841,6 +847,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   c->adam_grid = adam_grid(dev);
   if (const char* m = getenv("TGS_D2H_MERGE"))
     c->d2h_max_merge = (size_t)std::max(1, atoi(m)) * d.n_arr * c->rec_bytes;
+  if (const char* m = getenv("TGS_LISTS_AFTER_ADAM")) c->lists_after_adam = atoi(m) != 0;
   c->io = std::thread(io_main, c);
   *out = c;
   return TGS_OK;
@@ -1097,10 +1104,12 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   prof_end(c, c->compute, t1, 1);
   // After the prologue, Adam reads only its A lists (3-deep ring), the per-
   // entry constants and slots the plan never hands out while R_{t+1} holds
-  // them: the plan of t+2 may overwrite this parity's other lists now.  With
-  // the bound refresh on, that plan also merges k_refresh's radii (R25), so
-  // the lists stay in use until after it.
-  if (!c->d.refresh) CK(cudaEventRecord(c->ev_lists[p], c->compute));
+  // them: the plan of t+2 could overwrite this parity's other lists now
+  // (TGS_LISTS_AFTER_ADAM=0).  By default, and always with the bound refresh
+  // on (that plan merges k_refresh's radii, R25), they stay in use until the
+  // end of this step's compute work.
+  const bool lists_late = c->d.refresh || c->lists_after_adam;
+  if (!lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));
   prof_begin(c, c->compute, t2);
   CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
@@ -1108,8 +1117,8 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   if (c->d.refresh) {
     CK(launch_refresh(dk, nA, p, c->compute));
     c->tm.kernel_launches++;
-    CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   }
+  if (lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   if (c->cfg.serialize) CK(cudaStreamSynchronize(c->compute));  // ablation w/o Overlap
   return TGS_OK;
 }

@@ -365,8 +365,9 @@ def test_edge_configs(N, B, C, J, kw):
     pr.close()
 
 
-@pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct"])
-def test_pipelined_run_matches_oracle(mode):
+@pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct",
+                                  "plain_early_lists", "fine_early_lists"])
+def test_pipelined_run_matches_oracle(mode, monkeypatch):
     """The GPU runs ahead exactly as in bench.py -- no inspection call (hence no
     host sync) between batches -- so every cross-batch hazard (plan of t+1 vs
     Adam/filter/write-back of t) is exercised; the final state must still match
@@ -376,6 +377,9 @@ def test_pipelined_run_matches_oracle(mode):
     import torch
     from gpu_harness import GRAD_SEED, Synth, _cfn
     cfg, sc, tr = tiny()
+    if mode.endswith("_early_lists"):  # plan of t+2 released after Adam(t)'s prologue
+        monkeypatch.setenv("TGS_LISTS_AFTER_ADAM", "0")
+        mode = mode[: -len("_early_lists")]
     kw = {"plain": {}, "fine": {}, "fine_refresh_cold": {"refresh_bounds": 1,
                                                           "moments": O.COLD_RESTART},
           "mask_direct": {"staging_blocks": 1, "mask_p": 0.5}}[mode]

@@ -14,14 +14,18 @@ DESC = {"default": "300m aerial smooth, J=64, C=6309, cold restart (the N=1 head
         "store_1b_shard8": "the same shard on the f3 store tier (O_DIRECT segments on local disk, CPU cache 3C)"}
 
 tag, names = sys.argv[1], sys.argv[2:]
+src = "gpurun_out"
+if names and names[0].startswith("--src="):
+    src, names = names[0][6:], names[1:]
 rows = []
 lines = {}
 for f in names:
-    shutil.copy(f"gpurun_out/bench_{f}.json", f"profiles/bench_{tag}_{f}.json")
-    d = json.loads(open(f"gpurun_out/bench_{f}.json").read().strip().splitlines()[-1])
+    shutil.copy(f"{src}/bench_{f}.json", f"profiles/bench_{tag}_{f}.json")
+    d = json.loads(open(f"{src}/bench_{f}.json").read().strip().splitlines()[-1])
     lines[f] = d
     r, l, det, e = d["roofline"], d["link_roofline"], d["detail"], d.get("e2e")
     e2e = f"{e['value'] / 1e9:.3f} ({e['ms_per_step']:.2f} ms)" if e else "-"
+    peak = r["peak"]
     rows.append(f"| {f} | {DESC.get(f, f)} | {d['value'] / 1e9:.3f} | {d['ms_per_step']:.2f} | {e2e} | "
                 f"{det['active_blocks_per_step']:.0f} | {det['stage_in_blocks_per_step']:.0f} | "
                 f"{det['h2d_GB_per_step']:.3f} / {det['d2h_GB_per_step']:.3f} | "
@@ -32,11 +36,11 @@ out = [f"# bench.py results, round {tag[1:]} (one B200, fresh gpurun box)", "",
        "second of device time (CUDA events on the compute stream); one step = tgs_activate + "
        "tgs_step_adam (a1-a5). e2e = the same loop through the public API with pinned host camera "
        "planes in and an async per-step counter readback, wall clock. Adam GB/s = algorithmic 1652 "
-       "B/row / event-timed k_adam launch vs the measured 6551 GB/s HBM copy peak. Link GB/s = "
+       "B/row / event-timed k_adam launch vs the measured HBM copy peak of MEASURED_PEAKS.json (%.0f GB/s). Link GB/s = "
        "copy-batch bytes / event-timed span on the h2d / d2h streams vs the pinned 1 GiB copy "
-       "peak measured in the same run." % tag, "",
+       "peak measured in the same run." % (tag, peak), "",
        "| run | workload | G Gaussians/s | ms/step | e2e G/s | active blocks/step | S+ blocks/step | "
-       "H2D / D2H GB/step | k_adam GB/s (of 6551) | link GB/s h2d / d2h |",
+       "H2D / D2H GB/step | k_adam GB/s (% of peak) | link GB/s h2d / d2h |",
        "|---|---|---|---|---|---|---|---|---|---|"] + rows
 d = lines.get("default")
 if d:

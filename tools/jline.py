@@ -8,7 +8,10 @@ out = {"value_G/s": round(d["value"] / 1e9, 4), "ms/step": round(d["ms_per_step"
        "adam_frac": round(d["roofline"]["frac"], 3), "S+/step": det.get("stage_in_blocks_per_step"),
        "active/step": det.get("active_blocks_per_step"),
        "e2e_G/s": round(d["e2e"]["value"] / 1e9, 4) if d.get("e2e") else None,
-       "order_ms": det.get("view_order_gpu_ms")}
+       "order_ms": det.get("view_order_gpu_ms"),
+       "d2h_GB": det.get("d2h_GB_per_step"),
+       "p50/p99_ms": [round(det["step_ms"]["p50"], 3), round(det["step_ms"]["p99"], 3)]
+       if det.get("step_ms") else None}
 st = det.get("store")
 if st:
     out.update({"hit_rate": round(st["hit_rate"], 3), "ssd_read_GBps": st["ssd_read_GBps_in_reads"],
