@@ -162,6 +162,20 @@ def ssd_read_peak(path, gib=4):
         return None
 
 
+def _churn(st0, st1, steps):
+    """SURVEY §8d churn over the timed steps (this rank): evictions, dirty
+    evictions and re-admissions per step, the share of block updates that
+    cold-restarted their moments, and the mean length of a finished residency."""
+    d = {k: st1[k] - st0[k] for k in st1}
+    return {"evict_per_step": d["n_evict"] / steps,
+            "evict_dirty_per_step": d["n_evict_dirty"] / steps,
+            "readmissions_per_step": d["readmissions"] / steps,
+            "cold_restart_ratio": (d["cold_restart_updates"] / d["total_updates"]
+                                   if d["total_updates"] else None),
+            "mean_resident_streak": (d["resident_streak_sum"] / d["streak_count"]
+                                     if d["streak_count"] else None)}
+
+
 def _workload(args):
     """The named config, with --capacity overriding its C (the capacity sweep of
     SURVEY §8d: C as a multiple of the mean #K_t)."""
@@ -543,6 +557,7 @@ def main():
                            "stage_in_blocks_per_step": stage_in / args.steps,
                            "h2d_GB_per_step": h2d / args.steps / 1e9,
                            "d2h_GB_per_step": d2h / args.steps / 1e9,
+                           "churn": _churn(st0, st1, args.steps),
                            "step_ms": {"p50": float(np.percentile(step_ms, 50)),
                                        "p99": float(np.percentile(step_ms, 99)),
                                        "max": float(step_ms.max()),

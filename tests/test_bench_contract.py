@@ -31,6 +31,13 @@ def test_reference_arm_contract():
     assert "workload" in d["config"]
 
 
+def test_capacity_override_reaches_the_run():
+    """--capacity (the SURVEY §8d C sweep) replaces the config's C on both arms."""
+    d = _run(["--impl", "reference", "--config", "tiny", "--steps", "2", "--warmup", "3",
+              "--capacity", "64"])
+    assert d["config"]["capacity_blocks_per_gpu"] == 64 and d["value"] > 0
+
+
 @pytest.mark.gpu
 def test_our_arm_contract():
     d = _run(["--config", "tiny", "--steps", "4", "--warmup", "3", "--cpu-sample-s", "1"])
