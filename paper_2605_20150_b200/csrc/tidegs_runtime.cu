@@ -670,7 +670,10 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   // the plan is latency-critical (the host waits for it): highest priority
-  if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+  // (TGS_PLAN_PRIO=0: default priority, for A/B measurements)
+  const char* pp = getenv("TGS_PLAN_PRIO");
+  const int plan_prio = (pp && atoi(pp) == 0) ? prio_lo : prio_hi;
+  if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, plan_prio) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->fix, cudaStreamNonBlocking) != cudaSuccess)
