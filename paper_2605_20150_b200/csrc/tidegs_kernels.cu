@@ -727,6 +727,37 @@ __device__ __forceinline__ uint32_t nonfinite4(const float4& g) {
          ((__float_as_uint(g.z) & e) == e ? 4u : 0u) | ((__float_as_uint(g.w) & e) == e ? 8u : 0u);
 }
 
+// R20 slow path of k_adam (warp-collective; rare): the rows of the quad whose
+// gradient has a non-finite component, and the lowest gid*59+attr among them
+// reported to d.nonfinite.  Out of line so that the fast path keeps its
+// registers (inlined, it spilled the loop state to local memory).
+__device__ __noinline__ uint32_t adam_nonfinite(uint32_t nf0, uint32_t nf1, uint32_t rowsel0,
+                                                uint32_t rowsel1, uint32_t lane, uint64_t gid0,
+                                                unsigned long long* nonfinite) {
+  uint32_t bad = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if ((nf0 >> q) & 1u) bad |= (rowsel0 >> (4 * q)) & 0xFu;
+    if ((nf1 >> q) & 1u) bad |= (rowsel1 >> (4 * q)) & 0xFu;
+  }
+  bad = __reduce_or_sync(kFull, bad);
+  unsigned long long best = ~0ull;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
+    if ((nf0 >> q) & 1u) {
+      const unsigned long long idx = (gid0 + e0 / 59) * 59ull + e0 % 59;
+      best = idx < best ? idx : best;
+    }
+    if ((nf1 >> q) & 1u) {
+      const unsigned long long idx = (gid0 + e1 / 59) * 59ull + e1 % 59;
+      best = idx < best ? idx : best;
+    }
+  }
+  if (best != ~0ull) atomicMin(nonfinite, best);
+  return bad;
+}
+
 __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t nA, int parity,
                                                      const uint32_t* __restrict__ mask,
                                                      AdamHyper hp) {
@@ -759,14 +790,22 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
 
   uint32_t cur = 0xffffffffu;
   uint32_t step = 0, rows = 0, fresh = 0;
-  float ss0[4], ss1[4];
+  // per-lane step sizes ss_a = lr[a] / (1 - beta1^s) of float4 #lane and
+  // #lane+32, kept in shared memory (each lane reads back only what it wrote):
+  // in registers they pushed the loop past the 80-register budget into spills
+  __shared__ float4 ss_tab[kAdamNT / 32][64];
+  float4* const my_ss = ss_tab[threadIdx.x >> 5];
+  // one base pointer per block record: theta at pt, m at pt + rf4, v at
+  // pt + 2 rf4 (registers: the loop runs at the 80-register budget of 3 CTAs/SM)
+  float4* pt = nullptr;
   const float4* pg = nullptr;
-  float4 *pt = nullptr, *pm = nullptr, *pv = nullptr;
   const uint32_t* pmask = nullptr;
+  const size_t rf4 = rf / 4;
 
   uint32_t i = (uint32_t)(q0 / QB);
   uint32_t quad = (uint32_t)(q0 - (uint64_t)i * QB);
-  for (uint64_t qi = q0; qi < q1; ++qi) {
+  const uint32_t nq = (uint32_t)(q1 - q0);  // <= kAdamQPW
+  for (uint32_t k = 0; k < nq; ++k) {
     if (i != cur) {
       cur = i;
       const AdamEnt ent = d.ent[i];
@@ -776,15 +815,13 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       K.ibs = ent.ibs;
       const uint32_t s = d.a_slot[parity][i];
       pt = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf);
-      pm = pt + rf / 4;
-      pv = pt + rf / 2;
       pg = reinterpret_cast<const float4*>(d.grads + (size_t)s * rf);
       pmask = mask ? mask + (size_t)s * nw : nullptr;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // ss_a = lr[a] / (1 - beta1^s)  (R9)
         const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
-        ss0[q] = __fdiv_rn(lr[e0 % 59], ent.bc1);
-        ss1[q] = __fdiv_rn(lr[has1 ? e1 % 59 : 0], ent.bc1);
+        reinterpret_cast<float*>(&my_ss[lane])[q] = __fdiv_rn(lr[e0 % 59], ent.bc1);
+        reinterpret_cast<float*>(&my_ss[lane + 32])[q] = __fdiv_rn(lr[has1 ? e1 % 59 : 0], ent.bc1);
       }
     }
     const uint32_t r0 = 4u * quad;
@@ -812,43 +849,22 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       g0 = __ldcs(pg + f0);
       t0 = __ldcs(pt + f0);
       if (!fresh) {
-        m0 = __ldcs(pm + f0);
-        v0 = __ldcs(pv + f0);
+        m0 = __ldcs(pt + rf4 + f0);
+        v0 = __ldcs(pt + 2 * rf4 + f0);
       }
     }
     if (sel1) {
       g1 = __ldcs(pg + f1);
       t1 = __ldcs(pt + f1);
       if (!fresh) {
-        m1 = __ldcs(pm + f1);
-        v1 = __ldcs(pv + f1);
+        m1 = __ldcs(pt + rf4 + f1);
+        v1 = __ldcs(pt + 2 * rf4 + f1);
       }
     }
     const uint32_t nf0 = nonfinite4(g0) & sel0, nf1 = nonfinite4(g1) & sel1;
     if (__any_sync(kFull, (nf0 | nf1) != 0u)) {  // R20: rows with a non-finite g are skipped
-      uint32_t bad = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((nf0 >> q) & 1u) bad |= (rowsel0 >> (4 * q)) & 0xFu;
-        if ((nf1 >> q) & 1u) bad |= (rowsel1 >> (4 * q)) & 0xFu;
-      }
-      bad = __reduce_or_sync(kFull, bad);
-      // report the lowest gid*59+attr over the active rows
-      const uint64_t gid0 = (uint64_t)d.a_gid[parity][cur] * d.B + r0;
-      unsigned long long best = ~0ull;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
-        if ((nf0 >> q) & 1u) {
-          const unsigned long long idx = (gid0 + e0 / 59) * 59ull + e0 % 59;
-          best = idx < best ? idx : best;
-        }
-        if ((nf1 >> q) & 1u) {
-          const unsigned long long idx = (gid0 + e1 / 59) * 59ull + e1 % 59;
-          best = idx < best ? idx : best;
-        }
-      }
-      if (best != ~0ull) atomicMin(d.nonfinite, best);
+      const uint32_t bad = adam_nonfinite(nf0, nf1, rowsel0, rowsel1, lane,
+                                          (uint64_t)d.a_gid[parity][cur] * d.B + r0, d.nonfinite);
       const uint32_t upd = act & ~bad;  // Eq. masked_update: unchanged off I_t
       sel0 = sel1 = 0;
 #pragma unroll
@@ -860,20 +876,24 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
     // a fresh (cold-restarted) block gets its whole m, v record written: the
     // computed moments of updated rows, zeros for every other row
     if (sel0) {
+      const float4 s4 = my_ss[lane];
+      const float ss0[4] = {s4.x, s4.y, s4.z, s4.w};
       adam_f4(t0, m0, v0, g0, ss0, K, sel0);
       __stcs(pt + f0, t0);
     }
     if (sel0 || fresh) {
-      __stcs(pm + f0, m0);
-      __stcs(pv + f0, v0);
+      __stcs(pt + rf4 + f0, m0);
+      __stcs(pt + 2 * rf4 + f0, v0);
     }
     if (sel1) {
+      const float4 s4 = my_ss[lane + 32];
+      const float ss1[4] = {s4.x, s4.y, s4.z, s4.w};
       adam_f4(t1, m1, v1, g1, ss1, K, sel1);
       __stcs(pt + f1, t1);
     }
     if (sel1 || (fresh && has1)) {
-      __stcs(pm + f1, m1);
-      __stcs(pv + f1, v1);
+      __stcs(pt + rf4 + f1, m1);
+      __stcs(pt + 2 * rf4 + f1, v1);
     }
   }
 }
