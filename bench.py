@@ -242,6 +242,7 @@ def run_reference(args, ws, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": _config_dict(args, wl, ws),
             "cpu_baseline": {"value": value, "unit": "Gaussians/s", "cores": cores,
+                             "host": _host_cpu(),
                              "kind": "oracle",
                              "sample": f"oracle (single-thread C++17) from batch {args.start}, "
                                        f"{len(times)} timed of {total} requested steps "
@@ -314,7 +315,21 @@ def cpu_baseline(args, wl, sc, tr, budget_s):
     o.close()
     return {"value": rows / dt, "unit": "Gaussians/s", "cores": 1, "kind": "oracle",
             "sample": f"first {n} batches from {args.start} of the same workload "
-                      f"({dt:.1f}s single-thread, rows zero-filled, cold start)"}
+                      f"({dt:.1f}s single-thread, rows zero-filled, cold start)",
+            "host": _host_cpu()}
+
+
+def _host_cpu():
+    """CPU model and logical core count of the box the oracle ran on."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
 
 
 def main():
