@@ -30,6 +30,18 @@ import workload as W  # noqa: E402
 
 METRIC = "active Gaussians materialised+updated/sec"
 ROW_BYTES_ADAM = 1652  # read g, m, v, theta (4 x 236 B) + write theta, m, v (3 x 236 B)
+# cold restart (R6): a block's first update after admission reads no m, v (the
+# moments are zero): 708 B per active row (read g, theta; write theta) plus its
+# whole m, v record written (472 B per row of the block)
+ROW_BYTES_ADAM_FRESH = 708
+ROW_BYTES_MV = 472
+
+
+def adam_bytes(rows, fresh_rows, fresh_blocks, B):
+    """Algorithmic HBM bytes of k_adam over `rows` active rows, of which
+    `fresh_rows` belong to the `fresh_blocks` first-updated (cold-restarted) blocks."""
+    return ((rows - fresh_rows) * ROW_BYTES_ADAM + fresh_rows * ROW_BYTES_ADAM_FRESH
+            + fresh_blocks * B * ROW_BYTES_MV)
 
 
 def lr_3dgs():
@@ -409,7 +421,20 @@ def main():
     cnt_host = torch.zeros((8, 8), dtype=torch.int64).pin_memory() if ws > 1 else None
     cnt_dev = torch.zeros((8, 8), dtype=torch.int64, device=dev) if ws > 1 else None
 
+    steplog = os.environ.get("TGS_BENCH_STEPLOG")  # per-step Adam counters (ncu runs only:
+    steplog = open(steplog, "w") if steplog else None  # each line syncs the device)
+
     def step(i, cams=None):
+        _step(i, cams)
+        if steplog:
+            t, st = table.timing(), table.stats()
+            steplog.write(json.dumps({"step": i, "rows": st["n_active_rows"],
+                                      "fresh_rows": t["fresh_active_rows"],
+                                      "fresh_blocks": t["fresh_blocks"],
+                                      "active_blocks": st["n_active_blocks"], "B": sc.B}) + "\n")
+            steplog.flush()
+
+    def _step(i, cams=None):
         act = table.activate(planes[i] if cams is None else cams)
         if fmask is not None:
             table.fine_filter(fmask.data_ptr())
@@ -432,6 +457,7 @@ def main():
     torch.cuda.synchronize()
     table.set_profiling(True)
     st0 = table.stats()
+    tm0 = table.timing()
     ss0 = table.store_stats() if store else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -479,6 +505,9 @@ def main():
                         "cached": ss1["cached"], "cached_dirty": ss1["cached_dirty"]}
     tm = table.timing()
     rows = st1["n_active_rows"] - st0["n_active_rows"]
+    rows_local = rows
+    fresh_rows = tm["fresh_active_rows"] - tm0["fresh_active_rows"]
+    fresh_blocks = tm["fresh_blocks"] - tm0["fresh_blocks"]
     h2d = st1["h2d_bytes"] - st0["h2d_bytes"]
     d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
     stage_in = st1["n_stage_in"] - st0["n_stage_in"]
@@ -525,9 +554,10 @@ def main():
                       "one sync at the end" % n_e}
 
     hbm_peak, peak_kind = peaks()
-    adam_rows = rows if ws == 1 else rows / ws
+    # this rank's k_adam launches: its rows, its fresh rows, its launch time
     adam_ms = tm["adam_ms"] / max(1, tm["adam_launches"])
-    achieved = (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM / (adam_ms / 1e3) / 1e9
+    adam_bpl = adam_bytes(rows_local, fresh_rows, fresh_blocks, sc.B) / max(1, args.steps)
+    achieved = adam_bpl / (adam_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_adam_r01.json")
     if os.path.exists(tp):  # ncu --set full capture of a k_adam launch of this workload
@@ -538,7 +568,11 @@ def main():
     roof = {"bound": "hbm", "kernel": "k_adam", "achieved": achieved, "peak": hbm_peak,
             "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
             "peak_kind": peak_kind,
-            "algorithmic_bytes_per_launch": (adam_rows / max(1, args.steps)) * ROW_BYTES_ADAM,
+            "algorithmic_bytes_per_launch": adam_bpl,
+            "algorithmic_bytes_rule": "1652 B per active row; first update of a cold-restarted "
+                                      "block: 708 B per active row + 472 B per row of the block "
+                                      "(m, v record written, not read)",
+            "fresh_row_share": fresh_rows / max(1, rows_local),
             "avg_launch_ms": adam_ms}
     lp = link_peak(torch, dev) if rank == 0 else None
     if store and store_detail is not None:

@@ -139,6 +139,11 @@ typedef struct {
   uint64_t h2d_bytes, d2h_bytes; /* bytes moved by the timed copy batches        */
   uint64_t kernel_launches;  /* every kernel this library launched              */
   uint64_t copy_calls;       /* cudaMemcpyAsync calls issued (after run merging) */
+  /* cumulative since init (not only while profiling), for the algorithmic bytes
+   * of k_adam under cold restart (R6): a block's first update after admission
+   * reads no m, v and writes its whole m, v record */
+  uint64_t fresh_active_rows; /* active rows of blocks updated for the first time */
+  uint64_t fresh_blocks;      /* blocks updated for the first time since admission */
 } tgs_timing;
 
 /* ---------------------------------------------------------------- lifecycle */

@@ -17,7 +17,9 @@ constexpr uint32_t kMaxBuckets = 2 * 2 * (kMaxAge + 2);  // rank x (in R_t ? 0 :
 enum Stat : int {
   ST_ITER = 0, ST_VISIBLE, ST_RESIDENT, ST_ACTIVE_BLOCKS, ST_STAGE_IN, ST_EVICT, ST_EVICT_DIRTY,
   ST_ACTIVE_ROWS, ST_H2D, ST_D2H, ST_FLUSH_BYTES, ST_FLUSH_BLOCKS, ST_READMIT, ST_COLD_UPD,
-  ST_TOTAL_UPD, ST_STREAK_SUM, ST_STREAK_CNT, ST_N
+  ST_TOTAL_UPD, ST_STREAK_SUM, ST_STREAK_CNT, ST_N,
+  // internal (not in tgs_stats): fresh-update counts for tgs_timing
+  ST_FRESH_ROWS = ST_N, ST_FRESH_BLOCKS, ST_ALL
 };
 
 // per-activate counters written by the cull kernel (zeroed before it)

@@ -526,8 +526,8 @@ __global__ void __launch_bounds__(256) k_readmit(Dev d, int parity, int32_t T) {
 // ------------------------------------------------ a5 prologue (per block)
 __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int parity,
                                                        const uint32_t* __restrict__ mask) {
-  __shared__ unsigned long long acc[3];
-  if (threadIdx.x < 3) acc[threadIdx.x] = 0;
+  __shared__ unsigned long long acc[5];
+  if (threadIdx.x < 5) acc[threadIdx.x] = 0;
   __syncthreads();
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -560,6 +560,10 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
         atomicAdd(&acc[0], 1ull);
         atomicAdd(&acc[1], (unsigned long long)n);
         if (d.cold && before == 0u && d.evicted[l]) atomicAdd(&acc[2], 1ull);
+        if (e.fresh) {
+          atomicAdd(&acc[3], (unsigned long long)n);
+          atomicAdd(&acc[4], 1ull);
+        }
       }
       d.ent[i] = e;
     }
@@ -569,6 +573,8 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
     if (acc[0]) atomicAdd(&d.stats[ST_TOTAL_UPD], acc[0]);
     if (acc[1]) atomicAdd(&d.stats[ST_ACTIVE_ROWS], acc[1]);
     if (acc[2]) atomicAdd(&d.stats[ST_COLD_UPD], acc[2]);
+    if (acc[3]) atomicAdd(&d.stats[ST_FRESH_ROWS], acc[3]);
+    if (acc[4]) atomicAdd(&d.stats[ST_FRESH_BLOCKS], acc[4]);
   }
 }
 

@@ -782,7 +782,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   }
   d.hdr_dev = dalloc_t<PlanHdr>(c, 1, ok);
   d.cnt = dalloc_t<uint32_t>(c, CNT_N, ok);
-  d.stats = dalloc_t<unsigned long long>(c, ST_N, ok);
+  d.stats = dalloc_t<unsigned long long>(c, ST_ALL, ok);
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
   for (int r = 0; r < 3; ++r) {
     c->a3_blk[r] = dalloc_t<uint32_t>(c, Cc, ok);
@@ -838,7 +838,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   CKI(cudaMemsetAsync(d.s2b, 0xff, sizeof(int32_t) * P, s0));
   CKI(cudaMemsetAsync(d.occ, 0, sizeof(uint32_t) * d.PW, s0));
   CKI(cudaMemsetAsync(d.dirty, 0, sizeof(uint32_t) * d.PW, s0));
-  CKI(cudaMemsetAsync(d.stats, 0, sizeof(unsigned long long) * ST_N, s0));
+  CKI(cudaMemsetAsync(d.stats, 0, sizeof(unsigned long long) * ST_ALL, s0));
   CKI(cudaMemsetAsync(d.cnt, 0, sizeof(uint32_t) * CNT_N, s0));  // k_plan re-zeroes it after use
   CKI(cudaMemsetAsync(d.nonfinite, 0xff, sizeof(unsigned long long), s0));
   CKI(cudaMemsetAsync(d.hdr_dev, 0, sizeof(PlanHdr), s0));
@@ -1230,6 +1230,10 @@ tgs_status tgs_get_timing(tgs_ctx* c, tgs_timing* out) {
   st = sync_all(c);
   if (st != TGS_OK) return st;
   *out = c->tm;
+  unsigned long long fr[2] = {0, 0};
+  CK(cudaMemcpy(fr, c->d.stats + ST_FRESH_ROWS, sizeof(fr), cudaMemcpyDeviceToHost));
+  out->fresh_active_rows = fr[0];
+  out->fresh_blocks = fr[1];
   return TGS_OK;
 }
 

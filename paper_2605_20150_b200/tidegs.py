@@ -87,7 +87,8 @@ class Timing(C.Structure):
                 [(n, C.c_uint64) for n in ("adam_launches", "plan_launches", "h2d_batches",
                                            "d2h_batches", "adam_rows", "adam_elems_quads",
                                            "h2d_bytes", "d2h_bytes", "kernel_launches",
-                                           "copy_calls")])
+                                           "copy_calls", "fresh_active_rows",
+                                           "fresh_blocks")])
 
     def as_dict(self):
         return {n: (float(getattr(self, n)) if t is C.c_double else int(getattr(self, n)))
