@@ -34,9 +34,10 @@ for f in names:
 out = [f"# bench.py results, round {tag[1:]} (one B200, fresh gpurun box)", "",
        "Raw JSON lines: `profiles/bench_%s_*.json`. value = active Gaussians updated by Adam per "
        "second of device time (CUDA events on the compute stream); one step = tgs_activate + "
-       "tgs_step_adam (a1-a5). e2e = the same loop through the public API with pinned host camera "
-       "planes in and an async per-step counter readback, wall clock. Adam GB/s = algorithmic 1652 "
-       "B/row / event-timed k_adam launch vs the measured HBM copy peak of MEASURED_PEAKS.json (%.0f GB/s). Link GB/s = "
+       "tgs_step_adam (a1-a5). e2e = the same timed steps through the public API with pinned host "
+       "camera planes in and an async per-step counter readback, wall clock. Adam GB/s = "
+       "algorithmic bytes (1652 B per active row; 708 B per row + the 472 B/row m, v record for "
+       "the first update of a cold-restarted block) / event-timed k_adam launch vs the measured HBM copy peak of MEASURED_PEAKS.json (%.0f GB/s). Link GB/s = "
        "copy-batch bytes / event-timed span on the h2d / d2h streams vs the pinned 1 GiB copy "
        "peak measured in the same run." % (tag, peak), "",
        "| run | workload | G Gaussians/s | ms/step | e2e G/s | active blocks/step | S+ blocks/step | "
