@@ -612,6 +612,7 @@ def main():
                            "plan_ms_per_step": tm["plan_ms"] / args.steps,
                            "fine_ms_per_step": tm["fine_ms"] / args.steps,
                            "adam_prologue_ms_per_step": tm["adam_prologue_ms"] / args.steps,
+                           "evict_pack_ms_per_step": tm["evict_ms"] / args.steps,
                            "h2d_ms_per_step": tm["h2d_ms"] / args.steps,
                            "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
                            "copy_calls_per_step": tm["copy_calls"] / args.steps,

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
 // moments persist) into staging[parity][i] with 128-bit streaming loads and
 // stores, so the slot is free for the next gather as soon as this kernel ends
 // and the copy engine drains the staging ring to the host tier meanwhile.
-__global__ void __launch_bounds__(256) k_pack(Dev d, int parity) {
+__global__ void __launch_bounds__(256, 6) k_pack(Dev d, int parity) {
   const uint32_t i = blockIdx.y;
   if (i >= d.ndirty_dev[parity]) return;
   const uint32_t s = d.dl_slot[i];
@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(256) k_pack(Dev d, int parity) {
   float4* dst = reinterpret_cast<float4*>(d.staging[parity] + (size_t)i * d.n_arr * d.rec_floats);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 1
   for (; e + 3 * stride < n4; e += 4 * stride) {  // 4 independent 16 B loads in flight
     const float4 a = __ldcs(src + e), b = __ldcs(src + e + stride);
     const float4 c = __ldcs(src + e + 2 * stride), f = __ldcs(src + e + 3 * stride);
@@ -502,6 +503,7 @@ __global__ void __launch_bounds__(256) k_pack(Dev d, int parity) {
     __stcs(dst + e + 2 * stride, c);
     __stcs(dst + e + 3 * stride, f);
   }
+#pragma unroll 1
   for (; e < n4; e += stride) __stcs(dst + e, __ldcs(src + e));
 }
 
