@@ -418,3 +418,24 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
         ob = np.stack([pr.orc.bound(k) for k in range(sc.K)])
         np.testing.assert_array_equal(gb.view(np.uint32), ob.view(np.uint32))
     pr.close()
+
+
+def test_fresh_counters_match_oracle_first_updates():
+    """tgs_timing.fresh_active_rows / fresh_blocks (the cold-restart term of k_adam's
+    algorithmic bytes, bench.py roofline) count exactly the blocks of A whose
+    update is their first since admission: oracle step count 1 after the step."""
+    cfg, sc, tr = tiny()
+    pr = _pair(sc, capacity=cfg.capacity, moments=O.COLD_RESTART)
+    seen = 0
+    for t in range(24):
+        act = pr.activate(tr.batch_planes(t, cfg.J))
+        t0 = pr.gpu.timing()
+        assert pr.step(act, t) == O.OK
+        t1 = pr.gpu.timing()
+        fresh = [int(k) for k in pr.orc.list("A") if pr.orc.step_count(int(k)) == 1]
+        rows = sum(min(sc.B, sc.N - k * sc.B) for k in fresh)
+        assert t1["fresh_blocks"] - t0["fresh_blocks"] == len(fresh)
+        assert t1["fresh_active_rows"] - t0["fresh_active_rows"] == rows
+        seen += len(fresh)
+    assert seen > cfg.capacity  # re-admissions happened (cold restarts beyond the first fill)
+    pr.close()
