@@ -49,3 +49,9 @@ def test_our_arm_contract():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["cpu_baseline"]["kind"] == "oracle"
+    # e2e covers the device-timed steps themselves (same rows), through the public API
+    assert d["e2e"]["device_value_same_steps"] == pytest.approx(d["value"], rel=1e-3)
+    det = d["detail"]
+    assert det["step_ms"]["p50"] > 0 and det["step_ms"]["p99"] >= det["step_ms"]["p50"]
+    assert {"evict_per_step", "readmissions_per_step", "cold_restart_ratio"} <= set(det["churn"])
+    assert 0 <= r["fresh_row_share"] <= 1
