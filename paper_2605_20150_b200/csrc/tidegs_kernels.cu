@@ -697,6 +697,7 @@ __global__ void __launch_bounds__(256) k_refresh(Dev d, int parity) {
 // quads, masked rows, non-finite rows (R20).
 constexpr int kAdamNT = 256;
 constexpr uint32_t kAdamQPW = 16;  // quads per warp (short CTA lifetime: the plan gets SMs)
+constexpr uint32_t kAdamMinWaves = 4;  // small launches: fewer quads per warp, >= 4 waves
 #ifndef TGS_ADAM_MINB
 #define TGS_ADAM_MINB 3  // resident CTAs per SM the register budget targets
 #endif
@@ -768,19 +769,19 @@ __device__ __noinline__ uint32_t adam_nonfinite(uint32_t nf0, uint32_t nf1, uint
 
 __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t nA, int parity,
                                                      const uint32_t* __restrict__ mask,
-                                                     AdamHyper hp) {
+                                                     AdamHyper hp, uint32_t qpw) {
   __shared__ float lr[kDim];
   if (threadIdx.x < kDim) lr[threadIdx.x] = hp.lr[threadIdx.x];
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t QB = d.B / 4;
   const uint64_t total = (uint64_t)nA * QB;
-  // non-persistent grid: each warp a contiguous run of kAdamQPW quads, so CTAs
-  // retire continuously and the (high-priority) plan of the next batch can be
-  // scheduled while this Adam is still running
+  // non-persistent grid: each warp a contiguous run of qpw (<= kAdamQPW) quads,
+  // so CTAs retire continuously and the (high-priority) plan of the next batch
+  // can be scheduled while this Adam is still running
   const uint64_t wid = (uint64_t)blockIdx.x * (kAdamNT / 32) + (threadIdx.x >> 5);
-  const uint64_t q0 = wid * kAdamQPW;
-  const uint64_t q1 = q0 + kAdamQPW < total ? q0 + kAdamQPW : total;
+  const uint64_t q0 = wid * qpw;
+  const uint64_t q1 = q0 + qpw < total ? q0 + qpw : total;
   if (q0 >= q1) return;
 
   // loop-invariant per-lane maps: rows of the 4 components of float4 #lane and #lane+32
@@ -812,7 +813,7 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
 
   uint32_t i = (uint32_t)(q0 / QB);
   uint32_t quad = (uint32_t)(q0 - (uint64_t)i * QB);
-  const uint32_t nq = (uint32_t)(q1 - q0);  // <= kAdamQPW
+  const uint32_t nq = (uint32_t)(q1 - q0);  // <= qpw
   for (uint32_t k = 0; k < nq; ++k) {
     if (i != cur) {
       cur = i;
@@ -1163,11 +1164,16 @@ cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const ui
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  (void)grid_ctas;
   const uint64_t quads = (uint64_t)nA * (d.B / 4);
-  const uint64_t per_cta = (uint64_t)(kAdamNT / 32) * kAdamQPW;
-  const unsigned grid = (unsigned)((quads + per_cta - 1) / per_cta);
-  k_adam<<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp);
+  // grid_ctas = resident CTAs of the device: a small launch (the in-memory
+  // configs) gets fewer quads per warp so that it still spans several waves
+  uint32_t qpw = kAdamQPW;
+  auto ctas = [&](uint32_t q) { return (quads + (uint64_t)(kAdamNT / 32) * q - 1) /
+                                       ((uint64_t)(kAdamNT / 32) * q); };
+  while (qpw > 1 && ctas(qpw) < (uint64_t)kAdamMinWaves * (uint64_t)std::max(grid_ctas, 1))
+    qpw /= 2;
+  const unsigned grid = (unsigned)ctas(qpw);
+  k_adam<<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qpw);
   return cudaGetLastError();
 }
 
