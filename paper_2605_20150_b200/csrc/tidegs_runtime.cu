@@ -673,10 +673,14 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   // (TGS_PLAN_PRIO=0: default priority, for A/B measurements)
   const char* pp = getenv("TGS_PLAN_PRIO");
   const int plan_prio = (pp && atoi(pp) == 0) ? prio_lo : prio_hi;
+  // the fix-up stream (k_readmit after the gather) sits on the gather -> Adam
+  // chain; TGS_FIX_PRIO=1 gives it the highest priority (A/B knob)
+  const char* fp = getenv("TGS_FIX_PRIO");
+  const int fix_prio = (fp && atoi(fp) == 1) ? prio_hi : prio_lo;
   if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, plan_prio) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->fix, cudaStreamNonBlocking) != cudaSuccess)
+      cudaStreamCreateWithPriority(&c->fix, cudaStreamNonBlocking, fix_prio) != cudaSuccess)
     return fail(TGS_ECUDA);
   for (cudaEvent_t* e : {&c->ev_plan, &c->ev_gstart, &c->ev_gdone, &c->ev_ready[0],
                          &c->ev_ready[1], &c->ev_evict[0],
