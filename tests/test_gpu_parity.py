@@ -439,3 +439,41 @@ def test_fresh_counters_match_oracle_first_updates():
         seen += len(fresh)
     assert seen > cfg.capacity  # re-admissions happened (cold restarts beyond the first fill)
     pr.close()
+
+
+@pytest.mark.parametrize("name", ["quota_member_by_key_q1", "quota_min_with_camera_size"])
+def test_camera_balanced_topc_golden_on_gpu(name):
+    """The hand-worked CameraBalancedTopC examples (tests/golden/
+    camera_balanced_topc.json) through the C ABI: k_quota /
+    k_plan must give the hand-derived R, S+, S-, Omega and K^(j)."""
+    from paper_2605_20150_b200 import tidegs as T
+    from test_oracle_golden import _scn, line_bounds, slab_planes
+    scn = _scn(name)
+    n = scn["n_blocks"]
+    tab = T.Table(T.make_config(4 * n, 4, scn["capacity"], lam=scn["lambda"], gamma=scn["gamma"],
+                                quota=tuple(scn["beta"])), line_bounds(n),
+                  fill=lambda k: np.zeros((4, 59), np.float32))
+    for b in scn["batches"]:
+        tab.activate(slab_planes(b["slabs"]))
+        for j, kj in enumerate(b.get("K_per_camera", [])):
+            assert tab.percam(j).tolist() == kj
+        for which in ("R", "S+", "S-", "Omega"):
+            if which in b:
+                assert tab.list(which).tolist() == b[which], which
+    tab.close()
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_recency_golden_on_gpu(case):
+    """Recency golden case (gamma^age, age 8 keeps / age 9 evicts) through the
+    GPU's rank LUT."""
+    from paper_2605_20150_b200 import tidegs as T
+    from test_oracle_golden import _scn, line_bounds, run_recency_case
+    scn = _scn("recency_gamma_power_age")
+    c = scn["cases"][case]
+    tab = run_recency_case(lambda: T.Table(
+        T.make_config(12, 4, scn["capacity"], lam=scn["lambda"], gamma=scn["gamma"],
+                      quota=tuple(scn["beta"])), line_bounds(3),
+        fill=lambda k: np.zeros((4, 59), np.float32)), c["empty_batches"])
+    assert tab.list("R").tolist() == c["R_final"]
+    tab.close()

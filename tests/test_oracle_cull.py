@@ -118,12 +118,34 @@ def test_union_examples_spec():
     assert o.list("K").tolist() == [0, 1, 2]
 
 
-def test_nan_distance_is_visible_and_nonfinite_planes_rejected():
-    bounds = np.array([[0, 0, 0, 1]], np.float32)
+def test_overflowing_distance_and_nonfinite_inputs():
+    """R2 edge cases. With finite planes and bounds (non-finite ones are
+    rejected, SPEC.md EINVAL rule) the fmaf chain of R2 can overflow to +-inf but
+    never yield NaN (inf - inf needs an infinite operand, and fma(a, b, +-inf) with
+    finite a*b stays +-inf). So: d = +inf never culls, d = -inf always culls
+    (-inf < -r), and the NaN branch of R2 is unreachable by construction."""
+    big = np.float32(3.0e38)
+    bounds = np.array([[big, 0, 0, 1]], np.float32)
     o = _oracle(4, 4, bounds, C=1)
-    pl = _box_planes(1.0)[None].copy()
-    pl[0, 0, 3] = np.inf
-    assert o.activate(pl) == O.EINVAL
+    # x-plane n=(1,0,0), d0=+3e38: d = fl(3e38 + 3e38) = +inf -> kept; the other
+    # five planes are far away and pass
+    keep = _box_planes(3.4e38)[None].copy()
+    keep[0, 0] = [1, 0, 0, big]
+    assert o.activate(keep) == O.OK
+    assert o.list("K").tolist() == [0]
+    # n=(-1,0,0), d0=-3e38: d = fl(-3e38 - 3e38) = -inf < -1 -> culled
+    cull = _box_planes(3.4e38)[None].copy()
+    cull[0, 1] = [-1, 0, 0, -big]
+    assert o.activate(cull) == O.OK
+    assert o.list("K").tolist() == []
+    # non-finite planes and bounds are refused, state unchanged
+    for bad in (np.inf, -np.inf, np.nan):
+        pl = _box_planes(1.0)[None].copy()
+        pl[0, 2, 1] = bad
+        assert o.activate(pl) == O.EINVAL
+        with pytest.raises(O.OracleError):
+            _oracle(4, 4, np.array([[0, bad, 0, 1]], np.float32), C=1)
+    assert o.list("K").tolist() == []
 
 
 def test_shards_union_equals_single_shard():

@@ -5,6 +5,7 @@ import json
 import os
 
 import numpy as np
+import pytest
 
 import oracle as O
 
@@ -30,9 +31,89 @@ def test_record_and_block_arithmetic():
     assert o.stats()["h2d_bytes"] == p["one_block_B4096_D59"]
 
 
-def test_recency_and_score_examples():
+def slab_planes(slabs):
+    """one camera per (lo, hi): the slab lo <= x <= hi, |y|, |z| <= 5"""
+    out = np.zeros((len(slabs), 6, 4), np.float32)
+    for j, (lo, hi) in enumerate(slabs):
+        out[j] = [[1, 0, 0, -lo], [-1, 0, 0, hi], [0, 1, 0, 5], [0, -1, 0, 5],
+                  [0, 0, 1, 5], [0, 0, -1, 5]]
+    return out
+
+
+def line_bounds(n):
+    """blocks k = 0..n-1: spheres of radius 0.1 at (k, 0, 0)"""
+    xs = np.arange(n, dtype=np.float32)
+    return np.stack([xs, np.zeros(n), np.zeros(n), np.full(n, 0.1)], 1).astype(np.float32)
+
+
+TOPC = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                   "camera_balanced_topc.json")))["scenarios"]
+
+
+def _scn(name):
+    return next(s for s in TOPC if s["name"] == name)
+
+
+def replay_batches(make, scn):
+    """(batch dict, table, planes) for each batch of a golden scenario"""
+    o = make(scn)
+    for b in scn["batches"]:
+        yield b, o, slab_planes(b["slabs"])
+
+
+def _oracle_for(scn):
+    return O.Oracle(O.make_config(4 * scn["n_blocks"], 4, scn["capacity"], lam=scn["lambda"],
+                                  gamma=scn["gamma"], quota=tuple(scn["beta"])),
+                    line_bounds(scn["n_blocks"]), fill=None, track_all=False)
+
+
+@pytest.mark.parametrize("name", ["quota_member_by_key_q1", "quota_min_with_camera_size"])
+def test_camera_balanced_topc_worked_example(name):
+    """CameraBalancedTopC (Alg. 1 l.6) on hand-worked examples
+    (tests/golden/camera_balanced_topc.json, derivation inside): the quota size
+    q_j = min(|K^(j)|, floor(beta C/J)), the quota members chosen by s (not by id)
+    and the fill by s decide R; a q_j+1, by-id, no-quota or high-id-tie oracle
+    gives one of the listed wrong sets instead."""
+    scn = _scn(name)
+    for b, o, pl in replay_batches(_oracle_for, scn):
+        assert o.activate(pl) == O.OK
+        for j, kj in enumerate(b.get("K_per_camera", [])):
+            assert o.percam(j).tolist() == kj
+        assert o.list("R").tolist() == b["R"]
+        assert o.list("S+").tolist() == b["S+"]
+        assert o.list("S-").tolist() == b["S-"]
+        if "Omega" in b:
+            assert o.list("Omega").tolist() == b["Omega"]
+    for wrong in scn["wrong_readings_give"].values():
+        if isinstance(wrong, list) and wrong != scn["batches"][-1]["R"]:
+            assert o.list("R").tolist() != wrong
+
+
+def run_recency_case(make_table, n_empty):
+    """Recency pin (R4/R12): block 0 accessed at t=0, then
+    n_empty empty batches, then a batch seeing {1, 2} with C = 2, lambda = 0.3."""
+    o = make_table()
+    batches = [slab_planes([(-0.5, 0.5)])] + [np.zeros((0, 6, 4), np.float32)] * n_empty
+    for pl in batches + [slab_planes([(0.5, 2.5)])]:
+        r = o.activate(pl)        # the oracle returns a status, the GPU table raises
+        assert not isinstance(r, int) or r == O.OK
+    return o
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_recency_gamma_power_of_age(case):
+    """s(0) = 0.7 * 0.9^age against s = 0.3 for never-accessed visible blocks:
+    age 8 keeps block 0 (0.3013), age 9 evicts it (0.2712) -- pins gamma^age,
+    age = (t-1) - last access and the (1 - lambda) weight (golden file)."""
+    scn = _scn("recency_gamma_power_age")
+    c = scn["cases"][case]
+    o = run_recency_case(lambda: O.Oracle(
+        O.make_config(12, 4, scn["capacity"], lam=scn["lambda"], gamma=scn["gamma"],
+                      quota=tuple(scn["beta"])), line_bounds(3), fill=None, track_all=False),
+        c["empty_batches"])
+    assert o.list("R").tolist() == c["R_final"]
+    # the golden arithmetic the case rests on (SPEC.md:401: gamma^3 = 0.729)
     assert abs(0.9 ** 3 - G["recency_gamma09_age3"]["value"]) < 1e-12
-    assert abs(0.7 * 1 + 0.3 * 0.5 - G["score_lambda07_inK_recency05"]["value"]) < 1e-12
 
 
 def test_churn_table_little_law_consistency():
