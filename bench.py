@@ -302,32 +302,72 @@ def _config_dict_base(args, wl, ws):
             "seeds": W.SEEDS}
 
 
-def cpu_baseline(args, wl, sc, tr, budget_s):
-    """The oracle as it stands, single thread, on a bounded sample of the same
-    workload (the first batches from --start), rows zero-filled."""
+def _gpu_local_core(local):
+    """One core of the NUMA node local to GPU `local` (sysfs local_cpulist of its PCI
+    device), else the last core of this process's affinity set."""
+    allowed = sorted(os.sched_getaffinity(0))
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(local)
+        bdf = "%04x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        spec = open(f"/sys/bus/pci/devices/{bdf}/local_cpulist").read().strip()
+        cores = []
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cores += range(int(lo), int(hi or lo) + 1)
+        cores = [c for c in cores if c in allowed]
+        if cores:
+            return cores[-1]
+    except Exception:
+        pass
+    return allowed[-1]
+
+
+def cpu_baseline(args, wl, sc, tr, budget_s, shard_ws=1, shard_rank=0, local=0):
+    """The oracle as it stands (single thread, pinned to one core on the GPU's
+    NUMA node) on a bounded sample of the same workload: it is first advanced
+    metadata-only through the batches before the GPU's timed window, then times
+    whole steps from the window's first batch on (rows zero-filled), with its
+    per-phase clocks (cull / plan / copies / Adam).  --shard-of G: rank 0's shard."""
     import oracle as O
     moments = O.COLD_RESTART if args.moments == "cold" else O.PERSIST
-    o = O.Oracle(O.make_config(sc.N, sc.B, wl.capacity, moments=moments), sc.bounds(),
-                 fill=None, track_all=True)
+    cap = -(-wl.capacity // shard_ws)
+    o = O.Oracle(O.make_config(sc.N, sc.B, cap, moments=moments, world_size=shard_ws,
+                               rank=shard_rank), sc.bounds(), fill=None, track_all=False)
     syn = _synth_struct(sc)
     gfn = C.cast(W.lib().wl_grad_cb, C.c_void_p).value
     lr = lr_3dgs()
-    t0 = time.perf_counter()
-    n = 0
-    rows = 0
-    while True:
-        before = o.stats()["n_active_rows"]
-        o.activate(tr.batch_planes(args.start + n, wl.J))
+    first = args.start + args.warmup
+    for i in range(args.start, first):  # state of the GPU's timed window, untimed
+        o.activate(tr.batch_planes(i, wl.J))
         o.step_adam(lr, grad=(gfn, C.addressof(syn)))
-        rows += o.stats()["n_active_rows"] - before
-        n += 1
-        if time.perf_counter() - t0 > budget_s or n >= 64:
-            break
-    dt = time.perf_counter() - t0
+    o.track_all_from_now()
+    core = _gpu_local_core(local)
+    mask0 = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, {core})
+    try:
+        ph0 = o.phase_seconds()
+        t0 = time.perf_counter()
+        n = rows = 0
+        while True:
+            before = o.stats()["n_active_rows"]
+            o.activate(tr.batch_planes(first + n, wl.J))
+            o.step_adam(lr, grad=(gfn, C.addressof(syn)))
+            rows += o.stats()["n_active_rows"] - before
+            n += 1
+            if time.perf_counter() - t0 > budget_s or n >= 64:
+                break
+        dt = time.perf_counter() - t0
+        ph1 = o.phase_seconds()
+    finally:
+        os.sched_setaffinity(0, mask0)
     o.close()
     return {"value": rows / dt, "unit": "Gaussians/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {n} batches from {args.start} of the same workload "
-                      f"({dt:.1f}s single-thread, rows zero-filled, cold start)",
+            "sample": f"batches {first}..{first + n - 1} (the GPU's timed window onwards), "
+                      f"{dt:.1f}s single-thread pinned to core {core}, after a metadata-only "
+                      f"pass over batches {args.start}..{first - 1}; rows zero-filled"
+                      + (f"; rank 0 of a {shard_ws}-way sharded table" if shard_ws > 1 else ""),
+            "phases_s_per_step": {k: (ph1[k] - ph0[k]) / n for k in ph1},
             "host": _host_cpu()}
 
 
@@ -344,9 +384,28 @@ def _host_cpu():
     return {"model": model, "nproc": os.cpu_count()}
 
 
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-run this command as N
+    ranks of one node through torch.distributed.run (127.0.0.1 rendezvous).
+    Rank 0 prints the JSON line; the exit code is the launcher's."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     ws, rank, local = dist_init(args)
+    if ws != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; measuring {ws} rank(s)",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
@@ -393,6 +452,8 @@ def main():
         table = T.Table(cfg, sc.bounds(), fill=sc.fill_fn, stream=stream.cuda_stream,
                         store=store)
     setup_s = time.perf_counter() - t_setup
+    if ws > 1:  # C1 active-set all-gather / C2 count all-reduce, issued by the library
+        table.set_comm(T.torch_comm())
     # synthetic gradients for every slot, written once (renderer out of scope)
     P_ = table.P
     ids = torch.arange(P_, dtype=torch.int32, device=dev) % max(1, table.num_local_blocks)
@@ -408,18 +469,8 @@ def main():
     total = args.warmup + args.steps
     planes = [tr.batch_planes(args.start + i, J) for i in range(total)]
 
-    from paper_2605_20150_b200 import shard
-
-    class _CudaView:  # zero-copy torch view of a library-owned device list
-        def __init__(self, ptr, n):
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4",
-                                             "data": (ptr or 0, False), "version": 3}
-
     fmask = torch.zeros((table.P, (sc.B + 31) // 32), dtype=torch.int32, device=dev) \
         if args.fine_filter else None
-    # C2 inputs: a ring of pinned rows (the host runs at most ~2 batches ahead)
-    cnt_host = torch.zeros((8, 8), dtype=torch.int64).pin_memory() if ws > 1 else None
-    cnt_dev = torch.zeros((8, 8), dtype=torch.int64, device=dev) if ws > 1 else None
 
     steplog = os.environ.get("TGS_BENCH_STEPLOG")  # per-step Adam counters (ncu runs only:
     steplog = open(steplog, "w") if steplog else None  # each line syncs the device)
@@ -438,16 +489,6 @@ def main():
         act = table.activate(planes[i] if cams is None else cams)
         if fmask is not None:
             table.fine_filter(fmask.data_ptr())
-        if ws > 1:  # C1 active-set exchange + C2 count reduction (NCCL over NVLink)
-            n = act.n_active_blocks
-            A = torch.as_tensor(_CudaView(act.d_active_blocks, n), device=dev) if n else \
-                torch.empty(0, dtype=torch.int32, device=dev)
-            shard.exchange_active(A, cap, union=False)
-            row = i % 8
-            cnt_host[row, :5] = torch.tensor([act.n_visible, act.n_resident, act.n_stage_in,
-                                              act.n_evict, n], dtype=torch.int64)
-            cnt_dev[row].copy_(cnt_host[row], non_blocking=True)
-            shard.reduce_counts(cnt_dev[row])
         table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
 
     for i in range(args.warmup):
@@ -513,6 +554,11 @@ def main():
     stage_in = st1["n_stage_in"] - st0["n_stage_in"]
     visible = st1["n_visible"] - st0["n_visible"]
     active_blocks = st1["n_active_blocks"] - st0["n_active_blocks"]
+    # this rank's host-link bytes of the timed steps: S+ records gathered over
+    # PCIe (not those re-admitted from the write-back ring in HBM) and dirty S-
+    rec_b = sc.B * 59 * 4 * (3 if args.moments == "persist" else 1)
+    ring_recs = tm["h2d_ring_records"] - tm0["h2d_ring_records"]
+    h2d_link, d2h_link = h2d - ring_recs * rec_b, d2h
     if ws > 1:  # whole job: counts summed over ranks, the slowest rank's clock
         t = torch.tensor([rows, ms, h2d, d2h, stage_in, visible, tm["adam_ms"], active_blocks],
                          dtype=torch.float64, device=dev)
@@ -579,17 +625,20 @@ def main():
         store_detail["ssd_read_peak_GBps"] = ssd_read_peak(os.path.join(store["dir"], "base.tdgs"))
     link = None
     if rank == 0:
-        h2d_rate = tm["h2d_bytes"] / (tm["h2d_ms"] / 1e3) / 1e9 if tm["h2d_ms"] else None
-        d2h_rate = tm["d2h_bytes"] / (tm["d2h_ms"] / 1e3) / 1e9 if tm["d2h_ms"] else None
+        h2d_rate = h2d_link / (tm["h2d_ms"] / 1e3) / 1e9 if tm["h2d_ms"] else None
+        d2h_rate = d2h_link / (tm["d2h_ms"] / 1e3) / 1e9 if tm["d2h_ms"] else None
         link = {"bound": "host-link", "h2d_achieved": h2d_rate, "d2h_achieved": d2h_rate,
                 "h2d_peak": lp["h2d"], "d2h_peak": lp["d2h"], "unit": "GB/s",
                 "h2d_frac": (h2d_rate / lp["h2d"]) if h2d_rate else None,
                 "d2h_frac": (d2h_rate / lp["d2h"]) if d2h_rate else None,
                 "peak_kind": "measured in this run: pinned 1 GiB cudaMemcpy",
+                "how": "k_xfer gather / write-back kernel spans (CUDA events on the h2d / d2h "
+                       "streams) over the records they moved across PCIe",
+                "ring_readmissions_per_step": ring_recs / args.steps,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps}
     cpu = None
-    if rank == 0 and ws == 1 and shard_ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, wl, sc, tr, args.cpu_sample_s)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, wl, sc, tr, args.cpu_sample_s, shard_ws, shard_rank, local)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Gaussians/s", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -605,6 +654,15 @@ def main():
                            "h2d_GB_per_step": h2d / args.steps / 1e9,
                            "d2h_GB_per_step": d2h / args.steps / 1e9,
                            "churn": _churn(st0, st1, args.steps),
+                           "locality": {
+                               "mean_K_over_Kloc": (st1["n_visible"] - st0["n_visible"])
+                               / args.steps / max(1, table.num_local_blocks),
+                               "jaccard_consecutive_K": (
+                                   (st1["k_inter_sum"] - st0["k_inter_sum"])
+                                   / max(1, st1["k_union_sum"] - st0["k_union_sum"])),
+                               "how": "rank 0 over the timed steps: mean |K_t| / K_loc, and "
+                                      "sum |K_t n K_t+1| / sum |K_t u K_t+1| (PAPER.md:139, "
+                                      "SURVEY §8d targets 3.5% and 0.88)"},
                            "step_ms": {"p50": float(np.percentile(step_ms, 50)),
                                        "p99": float(np.percentile(step_ms, 99)),
                                        "max": float(step_ms.max()),
@@ -615,7 +673,6 @@ def main():
                            "evict_pack_ms_per_step": tm["evict_ms"] / args.steps,
                            "h2d_ms_per_step": tm["h2d_ms"] / args.steps,
                            "d2h_ms_per_step": tm["d2h_ms"] / args.steps,
-                           "copy_calls_per_step": tm["copy_calls"] / args.steps,
                            "setup_s": setup_s, "layout_build_gpu_ms": build_ms,
                            "view_order_gpu_ms": order_ms,
                            "store": store_detail}}

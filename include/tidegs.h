@@ -50,7 +50,7 @@ typedef enum {
   TGS_ESTATE = 2,      /* call order violated (see tgs_step_adam)                   */
   TGS_ENOMEM = 3,      /* host pinned or device allocation failed                   */
   TGS_ECUDA = 4,       /* CUDA runtime error; context poisoned                      */
-  TGS_ENCCL = 5,       /* reserved for collective errors                            */
+  TGS_ENCCL = 5,       /* a collective of tgs_set_comm's transport failed (poisons)   */
   TGS_ENONFINITE = 6,  /* a non-finite gradient was seen in an active row (R20)     */
   TGS_EPOISONED = 7,   /* an earlier CUDA error poisoned this context               */
   TGS_EIO = 8          /* storage (f3 store tier) read/write failed; context poisoned */
@@ -116,6 +116,13 @@ typedef struct {
   uint64_t slot_stride;      /* floats per slot in d_params (3*B*59)            */
   uint64_t grad_stride;      /* floats per slot in d_grads (B*59)               */
   void* ready;               /* cudaEvent_t: wait on it before touching slots   */
+  /* C1 (multi-GPU, tgs_set_comm): the active sets A of every rank, [world_size]
+   * rows of capacity entries each (rank-major, global ids ascending, padded with
+   * 0xFFFFFFFF); device, library-owned, double-buffered by activate parity;
+   * NULL without a comm.  global_ready (cudaEvent_t): wait before reading. */
+  const uint32_t* d_global_active;
+  uint32_t global_stride;    /* entries per rank row (= capacity C_g)           */
+  void* global_ready;
 } tgs_activation;
 
 typedef struct {
@@ -126,7 +133,10 @@ typedef struct {
 typedef struct {
   uint64_t iter, n_visible, n_resident, n_active_blocks, n_stage_in, n_evict, n_evict_dirty,
       n_active_rows, h2d_bytes, d2h_bytes, flush_bytes, n_flush_blocks, readmissions,
-      cold_restart_updates, total_updates, resident_streak_sum, streak_count;
+      cold_restart_updates, total_updates, resident_streak_sum, streak_count,
+      k_inter_sum, k_union_sum; /* sum over activates of |K_t n K_{t+1}| and |K_t u K_{t+1}|
+                                  (consecutive-batch Jaccard of the visible sets, the
+                                  PAPER.md:139 / 522,572 locality analog) */
 } tgs_stats; /* cumulative */
 
 typedef struct {
@@ -138,13 +148,41 @@ typedef struct {
   uint64_t adam_elems_quads; /* 4-row quads visited by the timed Adam launches   */
   uint64_t h2d_bytes, d2h_bytes; /* bytes moved by the timed copy batches        */
   uint64_t kernel_launches;  /* every kernel this library launched              */
-  uint64_t copy_calls;       /* cudaMemcpyAsync calls issued (after run merging) */
+  uint64_t copy_calls;       /* cudaMemcpyAsync calls issued (tgs_flush only; the
+                              * per-step transfers are kernels, k_xfer) */
   /* cumulative since init (not only while profiling), for the algorithmic bytes
    * of k_adam under cold restart (R6): a block's first update after admission
    * reads no m, v and writes its whole m, v record */
   uint64_t fresh_active_rows; /* active rows of blocks updated for the first time */
   uint64_t fresh_blocks;      /* blocks updated for the first time since admission */
+  /* cumulative: S+ records the gather took from the previous activate's
+   * write-back ring in HBM (a block evicted dirty and re-admitted at once)
+   * instead of over the host link */
+  uint64_t h2d_ring_records;
 } tgs_timing;
+
+/* Transport of the two per-batch collectives of the sharded path (
+ * reading R17: block k lives on rank k mod world_size, every rank runs the
+ * whole step on its shard).  The library decides what is exchanged and when:
+ *   C1  at the end of every tgs_activate, on the library's plan stream: the
+ *       rank's A = R n K as global ids, padded to C_g, all-gathered into
+ *       tgs_activation.d_global_active;
+ *   C2  at the end of every tgs_step_adam, on the compute stream: the rank's
+ *       cumulative tgs_stats counters, all-reduced (sum) into the buffer
+ *       tgs_get_global_stats reads.
+ * The caller supplies the transport: NCCL over NVLink on a B200 node
+ * (ncclAllGather / ncclAllReduce(ncclUint64, ncclSum) enqueued on `stream`),
+ * or torch.distributed (the Python binding's TorchComm).  Each function moves
+ * device buffers and must be stream-ordered on `stream` (cudaStream_t) or
+ * complete before returning; a non-zero return poisons the context and the
+ * call reports TGS_ENCCL. */
+typedef struct {
+  /* d_recv[world_size * bytes] <- every rank's d_send[bytes], rank-major */
+  int (*allgather)(void* user, const void* d_send, void* d_recv, size_t bytes, void* stream);
+  /* d_buf[count] <- sum over ranks of d_buf[count] (uint64), in place */
+  int (*allreduce_u64)(void* user, uint64_t* d_buf, size_t count, void* stream);
+  void* user;
+} tgs_comm;
 
 /* ---------------------------------------------------------------- lifecycle */
 
@@ -163,6 +201,14 @@ tgs_status tgs_init_table(const tgs_config* cfg, const float* theta_rows, tgs_fi
                           void* compute_stream, tgs_ctx** out);
 
 tgs_status tgs_destroy(tgs_ctx* ctx);
+
+/* Attach the collectives' transport (copied; comm->user must outlive the ctx).
+ * Allowed once, before the first tgs_activate (ESTATE otherwise); EINVAL if a
+ * function pointer is NULL.  Without it, a rank runs its shard alone. */
+tgs_status tgs_set_comm(tgs_ctx* ctx, const tgs_comm* comm);
+/* C2 result: every rank's tgs_stats summed, as of the last tgs_step_adam
+ * (synchronising).  ESTATE without a comm. */
+tgs_status tgs_get_global_stats(tgs_ctx* ctx, tgs_stats* out);
 
 /* NEXT f3 -- the tier below the host tier (§3.4 "SSD
  * Storage, CPU Tiered Cache"; readings R27, R28 of DESIGN.md §3).  Instead of a

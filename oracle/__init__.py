@@ -34,7 +34,7 @@ class Stats(C.Structure):
         "iter", "n_visible", "n_resident", "n_active_blocks", "n_stage_in", "n_evict",
         "n_evict_dirty", "n_active_rows", "h2d_bytes", "d2h_bytes", "flush_bytes",
         "n_flush_blocks", "readmissions", "cold_restart_updates", "total_updates",
-        "resident_streak_sum", "streak_count")]
+        "resident_streak_sum", "streak_count", "k_inter_sum", "k_union_sum")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -95,6 +95,10 @@ def lib():
         L.or_store_reopen.argtypes = [vp, C.c_char_p, C.c_uint32, C.c_uint64]
         L.or_store_index.argtypes = [vp, C.c_uint64, C.POINTER(C.c_uint64)]
         L.or_store_stats.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.or_phase_ns.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.or_crc32c.restype = C.c_uint32
+        L.or_crc32c.argtypes = [C.c_char_p, C.c_uint64]
+        L.or_track_all_from_now.argtypes = [vp]
         L.or_store_lru.restype = C.c_uint32
         L.or_store_lru.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), C.c_uint32]
         _lib = L
@@ -216,6 +220,18 @@ class Oracle:
         lib().or_get_stats(self.h, C.byref(s))
         return s.as_dict()
 
+    def track_all_from_now(self):
+        """timing aid (bench cpu_baseline): compute every block from now on"""
+        rc = lib().or_track_all_from_now(self.h)
+        if rc != OK:
+            raise OracleError(rc, "or_track_all_from_now")
+
+    def phase_seconds(self) -> dict:
+        """cumulative wall time of the oracle's phases (SURVEY §8c timing hooks)"""
+        out = (C.c_uint64 * 4)()
+        lib().or_phase_ns(self.h, out)
+        return dict(zip(("cull", "plan", "copies", "adam"), (x / 1e9 for x in out)))
+
     def nonfinite_index(self):
         v = int(lib().or_nonfinite_index(self.h))
         return None if v == 2**64 - 1 else v
@@ -298,6 +314,10 @@ class Oracle:
     def fine_filter_mask(self):
         """(C fn, user) mask callback: step_adam with I_t from the fine filter."""
         return C.cast(lib().or_fine_filter_cb, C.c_void_p).value, self.h.value
+
+
+def crc32c(data: bytes) -> int:
+    return int(lib().or_crc32c(data, len(data)))
 
 
 def exp_det(x: float) -> float:

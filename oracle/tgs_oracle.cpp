@@ -6,6 +6,7 @@
 #include "tgs_oracle.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -48,6 +49,8 @@ struct Store {
   uint64_t clock = 0;
   uint32_t cur_file = 0;       // 0 = no patch segment open yet
   uint64_t cur_size = 0;       // bytes in the current patch segment
+  uint64_t epoch = 0;          // barriers (and compactions) written to the manifest
+  std::vector<uint64_t> base_version;  // version of each block's base record (R31)
   uint64_t hits = 0, misses = 0, evictions = 0, dirty_evictions = 0, flush_appends = 0,
            read_bytes = 0, write_bytes = 0, segments = 0;
 };
@@ -91,6 +94,9 @@ struct Ctx {
   uint64_t nonfinite = std::numeric_limits<uint64_t>::max();
   or_stats st{};
   Store sto;
+  // phase timers (SURVEY §8c timing hooks): cull, plan (selection, delta,
+  // slots), copies (write-back + gather of records), Adam -- nanoseconds
+  uint64_t phase_ns[4] = {0, 0, 0, 0};
 
   uint64_t gid_block(uint32_t l) const { return (uint64_t)l * cfg.world_size + cfg.rank; }
   uint32_t rows(uint32_t l) const {
@@ -215,6 +221,26 @@ bool contains(const std::vector<uint32_t>& s, uint32_t x) {
 constexpr uint64_t kPage = 4096;
 uint64_t pad_page(uint64_t x) { return (x + kPage - 1) / kPage * kPage; }
 
+// CRC-32C (Castagnoli, reflected polynomial 0x82F63B78, init and final xor
+// 0xFFFFFFFF): the textbook byte-table form, the table being the bitwise
+// division of each byte value by the polynomial (check value of "123456789":
+// 0xE3069283).  R28 format 2: integrity of every record.
+uint32_t crc32c(const void* data, uint64_t n) {
+  static const std::vector<uint32_t> table = [] {
+    std::vector<uint32_t> t(256);
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0x82F63B78u & (0u - (c & 1u)));
+      t[i] = c;
+    }
+    return t;
+  }();
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  uint32_t crc = 0xFFFFFFFFu;
+  for (uint64_t i = 0; i < n; ++i) crc = (crc >> 8) ^ table[(crc ^ p[i]) & 0xFFu];
+  return crc ^ 0xFFFFFFFFu;
+}
+
 void put32(unsigned char* p, uint32_t v) {
   for (int i = 0; i < 4; ++i) p[i] = (unsigned char)(v >> (8 * i));
 }
@@ -267,9 +293,10 @@ void read_at(const std::string& path, uint64_t off, void* p, uint64_t n) {
 // "updated blocks are written sequentially into patch
 // segments rather than overwriting existing block locations in place"; Index[k]
 // then points to the latest location.  R28: a record is a
-// header page ("TREC", format 1, global id, version, payload bytes) followed by
-// the payload padded to whole pages; a new segment starts when the record
-// would push a non-empty segment past the byte budget.
+// header page ("TREC", format 2, global id, version, payload bytes, CRC-32C of
+// the payload, CRC-32C of header bytes [0, 36)) followed by the payload padded
+// to whole pages; a new segment starts when the record would push a non-empty
+// segment past the byte budget.
 void append_version(Ctx& c, uint32_t l, const CacheEntry& e) {
   Store& s = c.sto;
   const uint64_t rec = kPage + s.S;
@@ -289,11 +316,13 @@ void append_version(Ctx& c, uint32_t l, const CacheEntry& e) {
   if (s.data) {
     std::vector<unsigned char> r(rec, 0);
     std::memcpy(&r[0], "TREC", 4);
-    put32(&r[4], 1);
+    put32(&r[4], 2);
     put64(&r[8], c.gid_block(l));
     put64(&r[16], version);
     put64(&r[24], s.payload);
     std::memcpy(&r[kPage], e.payload.data(), s.payload);
+    put32(&r[32], crc32c(&r[kPage], s.payload));
+    put32(&r[36], crc32c(&r[0], 36));
     write_at(seg_path(s, s.cur_file), off, r.data(), rec, false);
   }
   ix.file_id = s.cur_file;
@@ -302,6 +331,38 @@ void append_version(Ctx& c, uint32_t l, const CacheEntry& e) {
   ix.version = version;
   s.cur_size += rec;
   s.write_bytes += rec;
+}
+
+// R30 barrier manifest ("manifest.tdgm"), written at every barrier and after a
+// compaction: "TDGM", format 1, epoch, the last patch segment and its length
+// as of the barrier (the durable end of the log), the shard geometry, then per
+// local block the version of its base record (R31) and its Adam step counter,
+// then a CRC-32C of everything before.  Written to a temporary name and
+// renamed, so a crash leaves the previous barrier's manifest.
+void write_manifest(Ctx& c) {
+  Store& s = c.sto;
+  s.epoch += 1;
+  std::vector<unsigned char> m(64 + 12 * (size_t)c.Kloc + 4, 0);
+  std::memcpy(&m[0], "TDGM", 4);
+  put32(&m[4], 1);
+  put64(&m[8], s.epoch);
+  put32(&m[16], s.cur_file);
+  put64(&m[24], s.cur_file ? s.cur_size : 0);
+  put32(&m[32], c.n_arr());
+  put64(&m[40], c.cfg.n_gaussians);
+  put32(&m[48], c.cfg.block_size);
+  put32(&m[52], (uint32_t)c.cfg.world_size);
+  put32(&m[56], (uint32_t)c.cfg.rank);
+  put32(&m[60], c.Kloc);
+  for (uint32_t l = 0; l < c.Kloc; ++l) {
+    put64(&m[64 + 8 * (size_t)l], s.base_version[l]);
+    put32(&m[64 + 8 * (size_t)c.Kloc + 4 * (size_t)l], c.step[l]);
+  }
+  put32(&m[m.size() - 4], crc32c(m.data(), m.size() - 4));
+  const std::string tmp = s.dir + "/manifest.tdgm.tmp";
+  write_at(tmp, 0, m.data(), m.size(), true);
+  std::error_code ec;
+  std::filesystem::rename(tmp, s.dir + "/manifest.tdgm", ec);
 }
 
 // R27 (b): CPU-cache access of an S+ block.  Hit:
@@ -413,8 +474,14 @@ int or_track_block(or_ctx* o, uint64_t kg) {
   return OR_OK;
 }
 
+using Clock = std::chrono::steady_clock;
+static uint64_t ns_since(Clock::time_point a) {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - a).count();
+}
+
 int or_activate(or_ctx* o, const float* planes, uint32_t J) {
   Ctx& c = o->c;
+  auto t0 = Clock::now();
   const or_config& g = c.cfg;
   if (J > g.max_cameras || (J > 0 && !planes)) return OR_EINVAL;
   for (uint32_t i = 0; i < J * 24; ++i)
@@ -435,6 +502,11 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
       if (sphere_visible(&c.bounds[4 * l], planes + 24 * j)) c.percam[j].push_back(l);
   std::vector<uint32_t> Kn;
   for (uint32_t j = 0; j < J; ++j) Kn = set_union(Kn, c.percam[j]);
+  c.phase_ns[0] += ns_since(t0);
+  t0 = Clock::now();
+  // locality of consecutive batches (the Jaccard of K_t and K_{t+1})
+  c.st.k_inter_sum += set_inter(c.Kset, Kn).size();
+  c.st.k_union_sum += set_union(c.Kset, Kn).size();
 
   // ---- Alg. 1 l.2: update Recency from R_t n K_t, the blocks
   //      accessed by the previous iteration (R12): stamp last access = t-1.
@@ -519,6 +591,8 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
     freelist.insert(freelist.end(), rel.begin(), rel.end());
   }
 
+  c.phase_ns[1] += ns_since(t0);
+  t0 = Clock::now();
   // ---- stage 4: evict S-, writing back dirty blocks
   const uint64_t rb = c.rec_bytes() * c.n_arr();
   c.evicted_dirty.clear();
@@ -595,6 +669,7 @@ int or_activate(or_ctx* o, const float* planes, uint32_t J) {
   c.R = Rn;
   c.A = set_inter(Rn, Kn);
   c.A_prev = c.A;
+  c.phase_ns[2] += ns_since(t0);
   c.st.iter += 1;
   c.st.n_visible += Kn.size();
   c.st.n_resident += Rn.size();
@@ -613,6 +688,11 @@ int or_step_adam(or_ctx* o, const float* lr, float beta1, float beta2, float eps
   if (!c.can_step) return OR_ESTATE;
   if (!lr) return OR_EINVAL;
   c.can_step = false;
+  struct PhaseTimer {  // Adam's share of the step (every return path)
+    uint64_t& acc;
+    Clock::time_point a = Clock::now();
+    ~PhaseTimer() { acc += ns_since(a); }
+  } timer{c.phase_ns[3]};
   const uint32_t B = g.block_size;
   const uint32_t nw = (B + 31) / 32;
   const uint64_t it = (uint64_t)(c.t - 1);  // iteration index of this batch
@@ -715,13 +795,15 @@ int or_flush(or_ctx* o) {
   // consistency barriers such as checkpointing and shutdown":
   // every dirty CPU-cache entry is appended, ascending id, and becomes clean;
   // the cache keeps its contents and LRU order.
-  if (c.sto.on)
+  if (c.sto.on) {
     for (auto& kv : c.sto.cache)
       if (kv.second.dirty) {
         append_version(c, kv.first, kv.second);
         kv.second.dirty = false;
         c.sto.flush_appends += 1;
       }
+    if (c.sto.data) write_manifest(c);  // R30: the durable end of the log
+  }
   c.can_step = false;
   return OR_OK;
 }
@@ -948,12 +1030,17 @@ int or_store_open(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t se
   s.on = true;
   s.data = dir != nullptr;
   s.H = cache_blocks;
-  if (dir) s.dir = dir;
+  if (dir) {
+    s.dir = dir;
+    std::error_code ec;
+    std::filesystem::create_directories(s.dir, ec);
+  }
   // "The initial model is written once as an immutable base segment"
   // (PAPER.md:228): header page, then record l at 4096 + l * S, Index[l] =
   // (0, offset, size, 0).
   s.index.assign(c.Kloc, IndexEntry{});
   for (uint32_t l = 0; l < c.Kloc; ++l) s.index[l] = {0, kPage + (uint64_t)l * s.S, s.payload, 0};
+  s.base_version.assign(c.Kloc, 0);
   if (s.data) {
     const std::string base = seg_path(s, 0);
     std::vector<unsigned char> h = segment_header(c, 0);
@@ -966,6 +1053,7 @@ int or_store_open(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t se
       std::memcpy(r.data(), v.data(), s.payload);
       write_at(base, kPage + (uint64_t)l * s.S, r.data(), s.S, false);
     }
+    write_manifest(c);  // epoch 1: the base alone
   }
   return OR_OK;
 }
@@ -998,38 +1086,66 @@ int or_store_reopen(or_ctx* o, const char* dir, uint32_t cache_blocks, uint64_t 
   s.seg_budget = segment_bytes ? segment_bytes : (1ull << 30);
   if (s.seg_budget < 2 * kPage + s.S) return OR_EINVAL;
   s.dir = dir;
+  // the manifest of the last barrier: the durable end of the log, base
+  // versions and step counters (R30); it must describe this shard and be intact
+  const std::string mpath = s.dir + "/manifest.tdgm";
+  std::error_code ec;
+  const uint64_t msize = std::filesystem::file_size(mpath, ec);
+  const uint64_t mwant = 64 + 12 * (uint64_t)c.Kloc + 4;
+  if (ec || msize != mwant) return OR_EINVAL;
+  std::vector<unsigned char> m(msize, 0);
+  read_at(mpath, 0, m.data(), msize);
+  if (std::memcmp(&m[0], "TDGM", 4) != 0 || get32(&m[4]) != 1 ||
+      get32(&m[msize - 4]) != crc32c(m.data(), msize - 4) || get32(&m[32]) != c.n_arr() ||
+      get64(&m[40]) != c.cfg.n_gaussians || get32(&m[48]) != c.cfg.block_size ||
+      get32(&m[52]) != (uint32_t)c.cfg.world_size || get32(&m[56]) != (uint32_t)c.cfg.rank ||
+      get32(&m[60]) != c.Kloc)
+    return OR_EINVAL;
+  const uint32_t last = get32(&m[16]);
+  const uint64_t end = get64(&m[24]);
   // the base header must describe this shard
   std::vector<unsigned char> want = segment_header(c, 0), got(kPage, 0);
   read_at(seg_path(s, 0), 0, got.data(), kPage);
   if (got != want) return OR_EINVAL;
   s.index.assign(c.Kloc, IndexEntry{});
-  for (uint32_t l = 0; l < c.Kloc; ++l) s.index[l] = {0, kPage + (uint64_t)l * s.S, s.payload, 0};
-  uint32_t last = 0;
-  uint64_t end = 0;
-  for (uint32_t fid = 1;; ++fid) {
+  s.base_version.assign(c.Kloc, 0);
+  for (uint32_t l = 0; l < c.Kloc; ++l) {
+    s.base_version[l] = get64(&m[64 + 8 * (size_t)l]);
+    s.index[l] = {0, kPage + (uint64_t)l * s.S, s.payload, s.base_version[l]};
+  }
+  // patch segments 1..last up to the durable end; every record there was made
+  // durable at the barrier, so a bad one is corruption, not a torn tail
+  const uint64_t rec = kPage + s.S;
+  std::vector<unsigned char> payload(s.payload);
+  for (uint32_t fid = 1; fid <= last; ++fid) {
     const std::string path = seg_path(s, fid);
-    std::error_code ec;
     const uint64_t size = std::filesystem::file_size(path, ec);
-    if (ec) break;
+    if (ec) return OR_EINVAL;
     std::vector<unsigned char> h(kPage, 0);
     read_at(path, 0, h.data(), kPage);
     if (h != segment_header(c, fid)) return OR_EINVAL;
-    uint64_t off = kPage;
-    while (off + kPage + s.S <= size) {
+    const uint64_t limit = fid == last ? end : size;
+    if (limit > size || limit < kPage || (limit - kPage) % rec != 0) return OR_EINVAL;
+    for (uint64_t off = kPage; off < limit; off += rec) {
       std::vector<unsigned char> r(kPage, 0);
       read_at(path, off, r.data(), kPage);
       const uint64_t gid = get64(&r[8]);
-      if (std::memcmp(r.data(), "TREC", 4) != 0 || get32(&r[4]) != 1 ||
+      if (std::memcmp(r.data(), "TREC", 4) != 0 || get32(&r[4]) != 2 ||
           get64(&r[24]) != s.payload || gid % c.cfg.world_size != (uint64_t)c.cfg.rank ||
-          gid / c.cfg.world_size >= c.Kloc)
-        break;
+          gid / c.cfg.world_size >= c.Kloc || get32(&r[36]) != crc32c(r.data(), 36))
+        return OR_EINVAL;
+      read_at(path, off + kPage, payload.data(), s.payload);
+      if (get32(&r[32]) != crc32c(payload.data(), s.payload)) return OR_EINVAL;
       s.index[gid / c.cfg.world_size] = {fid, off + kPage, s.payload, get64(&r[16])};
-      off += kPage + s.S;
     }
-    last = fid;
-    end = off;
   }
-  if (last) std::filesystem::resize_file(seg_path(s, last), end);  // drop a torn tail
+  // appends after the barrier are not part of its state: cut and removed
+  if (last) std::filesystem::resize_file(seg_path(s, last), end, ec);
+  if (ec) return OR_EINVAL;
+  for (uint32_t fid = last + 1; std::filesystem::exists(seg_path(s, fid), ec); ++fid)
+    std::filesystem::remove(seg_path(s, fid), ec);
+  for (uint32_t l = 0; l < c.Kloc; ++l) c.step[l] = get32(&m[64 + 8 * (size_t)c.Kloc + 4 * (size_t)l]);
+  s.epoch = get64(&m[8]);
   s.cur_file = last;
   s.cur_size = last ? end : 0;
   s.segments = 0;
@@ -1065,14 +1181,19 @@ int or_store_compact(or_ctx* o) {
     read_at(seg_path(s, ix.file_id), ix.offset, r.data(), s.payload);
     write_at(tmp, kPage + (uint64_t)l * s.S, r.data(), s.S, false);
   }
-  std::filesystem::rename(tmp, seg_path(s, 0));
-  for (uint32_t fid = 1; fid <= s.cur_file; ++fid) std::filesystem::remove(seg_path(s, fid));
+  std::error_code ec;
+  std::filesystem::rename(tmp, seg_path(s, 0), ec);
+  if (ec) return OR_EINVAL;
+  const uint32_t old_last = s.cur_file;
   for (uint32_t l = 0; l < c.Kloc; ++l) {
     s.index[l].file_id = 0;
     s.index[l].offset = kPage + (uint64_t)l * s.S;
+    s.base_version[l] = s.index[l].version;
   }
   s.cur_file = 0;
   s.cur_size = 0;
+  write_manifest(c);  // the base alone, with the versions it now holds
+  for (uint32_t fid = 1; fid <= old_last; ++fid) std::filesystem::remove(seg_path(s, fid), ec);
   return OR_OK;
 }
 
@@ -1262,3 +1383,29 @@ int or_order_views(const double* feat, uint32_t M, uint32_t D, uint32_t* perm,
 }
 
 }  // extern "C"
+
+extern "C" void or_phase_ns(or_ctx* o, uint64_t* out4) {
+  for (int i = 0; i < 4; ++i) out4[i] = o->c.phase_ns[i];
+}
+
+// Timing aid for bench.py's cpu_baseline (never used by a parity check): from
+// now on every block is tracked.  Resident blocks that were not tracked get
+// their slot record from the host tier's initial rows (their updates so far
+// were not computed), so the contents are not the method's; the work per step
+// is.  Not allowed on a store tier.
+extern "C" int or_track_all_from_now(or_ctx* o) {
+  Ctx& c = o->c;
+  if (c.sto.on) return OR_ESTATE;
+  for (uint32_t l = 0; l < c.Kloc; ++l) {
+    const int32_t s = c.slot_of[l];
+    if (s < 0 || c.is_tracked(l)) continue;
+    std::vector<float>& h = c.host_rec(l);
+    std::vector<float> d(3 * c.rec_floats(), 0.0f);
+    std::memcpy(d.data(), h.data(), sizeof(float) * c.n_arr() * c.rec_floats());
+    c.slot_data[s] = std::move(d);
+  }
+  c.track_all = true;
+  return OR_OK;
+}
+
+extern "C" uint32_t or_crc32c(const void* data, uint64_t n) { return crc32c(data, n); }

@@ -45,7 +45,8 @@ typedef struct {
 typedef struct {
   uint64_t iter, n_visible, n_resident, n_active_blocks, n_stage_in, n_evict, n_evict_dirty,
       n_active_rows, h2d_bytes, d2h_bytes, flush_bytes, n_flush_blocks, readmissions,
-      cold_restart_updates, total_updates, resident_streak_sum, streak_count;
+      cold_restart_updates, total_updates, resident_streak_sum, streak_count,
+      k_inter_sum, k_union_sum;  /* sum over activates of |K_t n K_{t+1}|, |K_t u K_{t+1}| */
 } or_stats;
 
 typedef void (*or_fill_fn)(void* user, uint64_t k_global, float* out /* B*59 */);
@@ -124,6 +125,17 @@ uint32_t or_store_lru(or_ctx* c, uint32_t* blocks, uint8_t* dirty, uint32_t cap)
  * k_out = number of clusters, iters_out = Lloyd iterations. */
 int or_order_views(const double* feat, uint32_t M, uint32_t D, uint32_t* perm,
                    uint32_t* cluster, uint32_t* k_out, uint32_t* iters_out);
+
+/* cumulative wall time (ns) of the phases: [0] cull, [1] plan (selection, delta,
+ * slots), [2] copies (write-back + gather of records), [3] Adam */
+void or_phase_ns(or_ctx* o, uint64_t* out4);
+
+/* timing aid (bench.py cpu_baseline only, never a parity check): track every
+ * block from now on; resident untracked blocks take their initial rows */
+int or_track_all_from_now(or_ctx* o);
+
+/* CRC-32C of n bytes (the R28 format-2 record checksum), for the pins */
+uint32_t or_crc32c(const void* data, uint64_t n);
 
 #ifdef __cplusplus
 }

@@ -17,9 +17,10 @@ constexpr uint32_t kMaxBuckets = 2 * 2 * (kMaxAge + 2);  // rank x (in R_t ? 0 :
 enum Stat : int {
   ST_ITER = 0, ST_VISIBLE, ST_RESIDENT, ST_ACTIVE_BLOCKS, ST_STAGE_IN, ST_EVICT, ST_EVICT_DIRTY,
   ST_ACTIVE_ROWS, ST_H2D, ST_D2H, ST_FLUSH_BYTES, ST_FLUSH_BLOCKS, ST_READMIT, ST_COLD_UPD,
-  ST_TOTAL_UPD, ST_STREAK_SUM, ST_STREAK_CNT, ST_N,
-  // internal (not in tgs_stats): fresh-update counts for tgs_timing
-  ST_FRESH_ROWS = ST_N, ST_FRESH_BLOCKS, ST_ALL
+  ST_TOTAL_UPD, ST_STREAK_SUM, ST_STREAK_CNT, ST_K_INTER, ST_K_UNION, ST_N,
+  // internal (not in tgs_stats): fresh-update counts and the S+ records gathered
+  // from the write-back ring instead of the host (tgs_timing)
+  ST_FRESH_ROWS = ST_N, ST_FRESH_BLOCKS, ST_RING_READMIT, ST_ALL
 };
 
 // per-activate counters written by the cull kernel (zeroed before it)
@@ -78,6 +79,7 @@ struct Dev {
   uint32_t* ndirty_map;    // mapped host [2] |dirty S-| (parity)
   uint32_t* ndirty_dev;    // [2] |dirty S-| (parity), read by k_pack
   uint32_t* dl_slot;     // [C] device copy of the dirty S- slots (pack source)
+  uint32_t* dl_blk;      // [C] device copy of the dirty S- local ids (write-back destination)
   int32_t* wb_tag;       // [Kloc] activate index at which the block was packed (-1 never)
   uint32_t* wb_idx;      // [Kloc] its staging-ring index then
   float* staging[2];     // [S_max][n_arr][B][59] write-back staging ring (parity)
@@ -93,6 +95,11 @@ struct Dev {
   // Adam
   AdamEnt* ent;          // [C]
   float *lut_bc1, *lut_ibs;  // [lut_cap]
+  // host tier as the transfer kernels see it (device-mapped pinned memory)
+  unsigned char* host_dev;  // flat tier: record l at l * host_stride; store tier: CPU-cache entries
+  uint64_t host_stride;     // bytes between host records (n_arr*B*236, or the padded entry size)
+  int32_t* ent_of;          // [Kloc] store tier: cache entry of each resident block (else nullptr)
+  const uint32_t* sp_entry; // mapped host [C] store tier: cache entry of S+ block i (host-written)
   // pools
   float* params;         // [P][3][B][59]
   float* grads;          // [P][B][59]
@@ -111,7 +118,13 @@ cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s)
 cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
 cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t T, bool tag,
                                 cudaStream_t s);
-cudaError_t launch_readmit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s);
+// a4 transfers (XferMode in tidegs_kernels.cu): 0 gather S+ (sel/n_sel: a host-
+// selected subset, else all of hdr_dev->nSp), 1 scatter the ring, 2 scatter from
+// the slots; n_hint > 0 is an upper bound of the records (sizes the grid);
+// ctas CTAs of one warp, bufs 32 KB shared-memory buffers each (bufs-1 loads in flight)
+cudaError_t launch_xfer(const Dev& d, int mode, int parity, int32_t T, const uint32_t* sel,
+                        uint32_t n_sel, uint32_t n_hint, int ctas, int bufs, cudaStream_t s);
+cudaError_t launch_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C, cudaStream_t s);
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s);
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,

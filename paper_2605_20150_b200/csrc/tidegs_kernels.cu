@@ -19,6 +19,7 @@
 // only carry commutative effects (or/and on bitmaps, integer adds, min).
 // Floating point: IEEE RN intrinsics in the exact order DESIGN.md §3 (R2, R9)
 // fixes; compiled without fast-math, FTZ off.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -215,6 +216,11 @@ __global__ void __launch_bounds__(256) k_cull(Dev d, uint32_t J, int32_t T, int 
     uni |= bits;
   }
   if (lane == 0 && w < d.W) {
+    const uint32_t kold = d.Kb[w];  // K_t (the previous activate's)
+    if (kold | uni) {
+      atomicAdd(&d.stats[ST_K_INTER], (unsigned long long)__popc(kold & uni));
+      atomicAdd(&d.stats[ST_K_UNION], (unsigned long long)__popc(kold | uni));
+    }
     d.Kb[w] = uni;  // Eq. Kt_def: K_{t+1} = U_j K^{(j)}
     const uint32_t cw = d.tide ? (d.R[parity][w] | uni) : uni;  // C_t = R_t u K_{t+1}
     d.cand[w] = cw;
@@ -464,6 +470,7 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
       d.dirty_map[parity][2 * o] = l;
       d.dirty_map[parity][2 * o + 1] = s;
       d.dl_slot[o] = s;
+      d.dl_blk[o] = l;
       if (tag) {  // packed into staging[parity][o]: a re-admission next batch reads it there
         d.wb_tag[l] = T;
         d.wb_idx[l] = o;
@@ -507,22 +514,126 @@ __global__ void __launch_bounds__(256, 6) k_pack(Dev d, int parity) {
   for (; e < n4; e += stride) __stcs(dst + e, __ldcs(src + e));
 }
 
-// ------------- a4 re-admission fixup: S+ blocks packed by the previous batch
-// Their newest record sits in the previous staging ring (its write-back to the
-// host tier may still be in flight), so it is copied ring -> slot over the
-// copy-engine value the gather brought.  grid (chunks, nSp).
-__global__ void __launch_bounds__(256) k_readmit(Dev d, int parity, int32_t T) {
-  const uint32_t i = blockIdx.y;
-  const uint32_t l = d.sp_blk[parity][i];
-  if (d.wb_tag[l] != T - 1) return;
-  const uint32_t s = d.sp_slot[parity][i];
-  const size_t n4 = (size_t)d.n_arr * d.rec_floats / 4;
-  const float4* src = reinterpret_cast<const float4*>(
-      d.staging[parity ^ 1] + (size_t)d.wb_idx[l] * d.n_arr * d.rec_floats);
-  float4* dst = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * d.rec_floats);
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
-       e += (size_t)gridDim.x * blockDim.x)
-    __stcs(dst + e, __ldcs(src + e));
+// ------------------------- a4 record transfer over the host link (TMA)
+// One kernel per direction moves whole block records between pinned host
+// memory (device-mapped, UVA) and HBM: a few CTAs of one warp each, whose lane 0
+// streams 32 KB chunks through a ring of shared-memory buffers with bulk
+// copies -- cp.async.bulk global->shared (completion on an mbarrier), then
+// cp.async.bulk shared->global -- keeping kXferBufs-1 loads and one store in
+// flight per CTA.  The copy engines are not used: each chunk is an SM-issued
+// PCIe read (gather) or posted write (scatter), and a CTA occupies one SM's
+// shared memory but almost none of its issue slots or load/store units, so the
+// HBM-bound kernels beside it keep their bandwidth (profiles/linkbench2_r02.txt).
+//
+// XFER_GATHER   record i < n of S+ (or of the host-selected subset sel[0..n)):
+//               l = sp_blk[i] -> slot sp_slot[i].  Source: host record of l
+//               (flat tier: l * host_stride; store tier: entry sp_entry[i]), or,
+//               for a block the previous activate packed into its write-back
+//               ring (wb_tag[l] == T-1), that ring record in HBM -- its host
+//               write-back may still be in flight and the ring copy is the newest.
+// XFER_SCATTER  dirty record i < ndirty of this activate: write-back ring
+//               (ring mode) or its slot (direct mode) -> host record of l
+//               (flat: l * host_stride; store: entry ent_of[l]).
+constexpr uint32_t kXferChunk = 32768, kXferMaxBufs = 6;
+enum XferMode : int { XFER_GATHER = 0, XFER_SCATTER_RING = 1, XFER_SCATTER_DIRECT = 2 };
+
+__device__ __forceinline__ uint32_t smem_addr(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+
+__global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int32_t T,
+                                             const uint32_t* __restrict__ sel, uint32_t n_sel,
+                                             uint32_t nbuf) {
+  extern __shared__ __align__(128) unsigned char xbuf[];
+  __shared__ __align__(8) unsigned long long bar[kXferMaxBufs];
+  if (threadIdx.x != 0) return;
+  const uint32_t n = mode == XFER_GATHER ? (sel ? n_sel : d.hdr_dev->nSp) : d.ndirty_dev[parity];
+  const uint64_t rec_bytes = (uint64_t)d.n_arr * d.rec_floats * 4ull;
+  const uint32_t per_rec = (uint32_t)((rec_bytes + kXferChunk - 1) / kXferChunk);
+  const uint64_t total = (uint64_t)n * per_rec;
+  if ((uint64_t)blockIdx.x >= total) return;
+  const uint64_t mine = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  for (uint32_t b = 0; b < nbuf; ++b)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  // chunk c of this CTA is global chunk blockIdx.x + c * gridDim.x
+  auto geo = [&](uint64_t c, const unsigned char*& src, unsigned char*& dst, uint32_t& bytes) {
+    const uint64_t g = blockIdx.x + c * gridDim.x;
+    const uint32_t r = (uint32_t)(g / per_rec);
+    const uint64_t off = (g - (uint64_t)r * per_rec) * kXferChunk;
+    bytes = (uint32_t)(rec_bytes - off < kXferChunk ? rec_bytes - off : kXferChunk);
+    if (mode == XFER_GATHER) {
+      const uint32_t i = sel ? sel[r] : r;
+      const uint32_t l = d.sp_blk[parity][i];
+      const uint32_t s = d.sp_slot[parity][i];
+      if (T > 0 && d.wb_tag[l] == T - 1) {
+        src = reinterpret_cast<const unsigned char*>(d.staging[parity ^ 1]) +
+              (uint64_t)d.wb_idx[l] * rec_bytes;
+      } else {
+        const uint64_t e = d.ent_of ? (uint64_t)d.sp_entry[i] : (uint64_t)l;
+        src = d.host_dev + e * d.host_stride;
+      }
+      dst = reinterpret_cast<unsigned char*>(d.params + (size_t)s * 3 * d.rec_floats);
+    } else {
+      const uint32_t l = d.dl_blk[r];
+      src = mode == XFER_SCATTER_RING
+                ? reinterpret_cast<const unsigned char*>(d.staging[parity]) + (uint64_t)r * rec_bytes
+                : reinterpret_cast<const unsigned char*>(d.params + (size_t)d.dl_slot[r] * 3 * d.rec_floats);
+      const uint64_t e = d.ent_of ? (uint64_t)d.ent_of[l] : (uint64_t)l;
+      dst = d.host_dev + e * d.host_stride;
+    }
+    src += off;
+    dst += off;
+  };
+  auto load = [&](uint64_t c) {
+    const uint32_t b = (uint32_t)(c % nbuf);
+    const unsigned char* src;
+    unsigned char* dst;
+    uint32_t bytes;
+    geo(c, src, dst, bytes);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[b])),
+                 "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(xbuf + (size_t)b * kXferChunk)),
+        "l"(src), "r"(bytes), "r"(smem_addr(&bar[b])) : "memory");
+  };
+  // nbuf-1 loads in flight; buffer (c-1) % nbuf is refilled once its store has
+  // read it (wait_group.read 1: all but the newest store group)
+  uint64_t issued = 0;
+  for (; issued < mine && issued < nbuf - 1; ++issued) load(issued);
+  uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+  for (uint64_t c = 0; c < mine; ++c) {
+    const uint32_t b = (uint32_t)(c % nbuf);
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok) : "r"(smem_addr(&bar[b])), "r"((phase >> b) & 1u) : "memory");
+    phase ^= 1u << b;
+    const unsigned char* src;
+    unsigned char* dst;
+    uint32_t bytes;
+    geo(c, src, dst, bytes);
+    if (mode == XFER_GATHER && (blockIdx.x + c * gridDim.x) % per_rec == 0) {
+      const uint32_t r = (uint32_t)((blockIdx.x + c * gridDim.x) / per_rec);
+      const uint32_t i = sel ? sel[r] : r;
+      const uint32_t l = d.sp_blk[parity][i];
+      if (d.ent_of) d.ent_of[l] = (int32_t)d.sp_entry[i];  // store tier: entry of a resident block
+      if (T > 0 && d.wb_tag[l] == T - 1) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
+    }
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_addr(xbuf + (size_t)b * kXferChunk)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (issued < mine) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      load(issued++);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  for (uint32_t b = 0; b < nbuf; ++b)
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(&bar[b])));
 }
 
 // ------------------------------------------------ a5 prologue (per block)
@@ -1139,10 +1250,32 @@ cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_readmit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s) {
-  if (nSp == 0 || T == 0) return cudaSuccess;
-  dim3 grid(8, nSp);
-  k_readmit<<<grid, 256, 0, s>>>(d, parity, T);
+// C1 send buffer: the A list's global ids padded to C with 0xFFFFFFFF
+__global__ void __launch_bounds__(256) k_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C) {
+  for (uint32_t i = h->nA + blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x)
+    gid[i] = 0xFFFFFFFFu;
+}
+
+cudaError_t launch_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C, cudaStream_t s) {
+  k_pad_active<<<(C + 255) / 256 < 64 ? (C + 255) / 256 : 64, 256, 0, s>>>(gid, h, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xfer(const Dev& d, int mode, int parity, int32_t T, const uint32_t* sel,
+                        uint32_t n_sel, uint32_t n_hint, int ctas, int bufs, cudaStream_t s) {
+  if (n_hint == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(k_xfer, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kXferChunk * kXferMaxBufs));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const uint32_t nbuf = (uint32_t)std::max(2, std::min(bufs, (int)kXferMaxBufs));
+  const uint64_t per_rec = ((uint64_t)d.n_arr * d.rec_floats * 4ull + kXferChunk - 1) / kXferChunk;
+  const uint64_t chunks = (uint64_t)n_hint * per_rec;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctas, chunks));
+  k_xfer<<<grid, 32, kXferChunk * nbuf, s>>>(d, mode, parity, T, sel, n_sel, nbuf);
   return cudaGetLastError();
 }
 

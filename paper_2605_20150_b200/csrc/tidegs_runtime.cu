@@ -9,18 +9,20 @@
 //                    k_cull -> k_quota -> k_plan                       (a1-a3)
 //   host           : wait for the plan only (never for an Adam)
 //   h2d stream     : [slots freed by t-1, host records written by t-2]
-//                    one cudaMemcpyBatchAsync of S+ host tier -> slots (a4 gather)
-//                    -> k_readmit (S+ packed by t-1: newest copy in the ring)
+//                    k_xfer gather: S+ records host tier -> slots over PCIe
+//                    (a block packed by t-1 comes from its ring record instead)
 //                    -> ready[p]   (cold-restart zeros are folded into k_adam)
 //   compute stream : [after Adam(t-1)] k_evict (dirty S-) -> k_pack (slots ->
 //                    staging ring p) -> evict[p]                        (a4)
-//   I/O thread     : waits evict[p], reads the dirty list, one batch of
-//                    staging ring p -> host tier on the d2h stream -> d2h[p]
+//   d2h stream     : [evict[p]] k_xfer scatter: ring p -> host tier -> d2h[p]
 //   step_adam      : compute waits ready[p]; k_adam_prologue; k_adam   (a5)
 //
 // S+ always lands in slots that R_t does not hold (R13), so the gather of
 // batch t overlaps Adam of batch t-1; the write-back of t is decided after
-// Adam(t-1) (R14) without blocking the caller.
+// Adam(t-1) (R14) without blocking the caller: every step of the chain is a
+// GPU-side dependency, the host waits only for the plan.  The host link is
+// driven by the transfer kernels (TMA bulk copies to / from device-mapped
+// pinned memory), not by the copy engines.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -82,15 +84,27 @@ struct tgs_ctx {
   uint32_t* ndirty = nullptr;     // host view [2]
   float* planes_pinned = nullptr; // [2][kMaxCams*24] mapped staging of the camera batch
   // streams / events (ev_*[p]: last record by an activate of parity p)
-  cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr, fix = nullptr;
-  cudaEvent_t ev_plan = nullptr, ev_gstart = nullptr, ev_gdone = nullptr;
+  cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_plan = nullptr;
   cudaEvent_t ev_ready[2] = {}, ev_evict[2] = {}, ev_d2h[2] = {}, ev_lists[2] = {};
   cudaEvent_t ev_job[4] = {};      // write-back of activate J done: ev_job[J & 3] (store mode)
   bool rec_ready[2] = {}, rec_evict[2] = {}, rec_lists[2] = {};
-  int32_t d2h_job[2] = {-1, -1};   // activate index of the last write-back job of parity p
+  int32_t d2h_job[2] = {-1, -1};   // activate index of the last write-back of parity p
   bool prev_direct = false;        // previous activate wrote back straight from its slots
-  bool prev_packed = false;        // previous activate packed dirty records into its ring
-  // I/O thread (write-back issue)
+  // a4 transfer kernels: CTAs of the gather (h2d) and the write-back (d2h)
+  // (TGS_GATHER_CTAS / TGS_SCATTER_CTAS; defaults from profiles/linkbench2_r02.txt)
+  int gather_ctas = 8, scatter_ctas = 4, gather_bufs = 4, scatter_bufs = 4;
+  // store tier, per parity (the host fills them while the other parity's gather may still run):
+  uint32_t* sel_map[2][2] = {};               // mapped host [C]: S+ subsets (hits, misses)
+  uint32_t* sp_entry_map[2] = {};             // mapped host [C]: cache entry of S+ block i
+  int32_t h2d_prof = -1;           // pending timer of the last gather (bytes known after the readback)
+  // C1 / C2 collectives (tgs_set_comm)
+  tgs_comm comm{};
+  bool has_comm = false;
+  uint32_t* c1_recv[2] = {nullptr, nullptr};  // [G][C] gathered A lists (parity)
+  unsigned long long* c2_buf = nullptr;       // [ST_N] summed cumulative counters
+  cudaEvent_t ev_c1[2] = {nullptr, nullptr};
+  // I/O thread (store tier: marks the CPU-cache entries of each write-back dirty)
   struct Job { int32_t T; int parity; bool direct; };
   std::thread io;
   std::mutex mu;
@@ -102,7 +116,6 @@ struct tgs_ctx {
   std::string io_err;
   uint32_t last_ndirty = 0;
   std::mutex prof_mu;
-  size_t d2h_max_merge = SIZE_MAX;  // TGS_D2H_MERGE=<records> caps merged write-back copies
   // The plan of t+2 waits for all of Adam(t) (default), or with
   // TGS_LISTS_AFTER_ADAM=0 only for its prologue (the A lists then come from
   // the 3-deep ring).  The early release lets the high-priority plan kernels
@@ -197,15 +210,16 @@ void prof_begin(tgs_ctx* c, cudaStream_t s, Timer& t) {
   cudaEventRecord(t.a, s);
   t.armed = true;
 }
-void prof_end(tgs_ctx* c, cudaStream_t s, Timer& t, int kind, uint64_t bytes = 0) {
-  if (!t.armed) return;
+int32_t prof_end(tgs_ctx* c, cudaStream_t s, Timer& t, int kind, uint64_t bytes = 0) {
+  if (!t.armed) return -1;
   std::lock_guard<std::mutex> g(c->prof_mu);
   cudaEventRecord(t.b, s);
   c->pending.push_back({t.a, t.b, kind, bytes, c->T});
+  return (int32_t)c->pending.size() - 1;
 }
 void prof_collect(tgs_ctx* c) {
   std::lock_guard<std::mutex> g(c->prof_mu);
-  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "cold_init", "readmit", "fine"};
+  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "-", "-", "fine"};
   for (auto& p : c->pending) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.a, p.b) != cudaSuccess) ms = 0.f;
@@ -322,12 +336,7 @@ inline float* slot_rec(tgs_ctx* c, uint32_t s) {
   return c->d.params + (size_t)s * 3 * c->d.rec_floats;
 }
 
-// A batch of 1-D copies submitted with one cudaMemcpyBatchAsync: the copy
-// engines then keep both PCIe directions busy at once (measured on this box:
-// ~49 + 49 GB/s for 370 single-record copies per direction, against ~31 + 30
-// GB/s for the same copies issued one cudaMemcpyAsync at a time;
-// profiles/linkbench_r01.txt).  Adjacent copies merge when both sides are
-// contiguous.
+// A list of 1-D copies; adjacent copies merge when both sides are contiguous.
 struct CopyBatch {
   std::vector<void*> dst;
   std::vector<void*> src;
@@ -350,15 +359,8 @@ struct CopyBatch {
 
 tgs_status submit(tgs_ctx* c, CopyBatch& b, cudaStream_t s) {
   if (b.dst.empty()) return TGS_OK;
-  if (b.dst.size() == 1) {
-    CK(cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, s));
-  } else {
-    cudaMemcpyAttributes at{};
-    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t aidx = 0, fail = 0;
-    CK(cudaMemcpyBatchAsync(b.dst.data(), b.src.data(), b.size.data(), b.dst.size(), &at, &aidx,
-                            1, &fail, s));
-  }
+  for (size_t i = 0; i < b.dst.size(); ++i)
+    CK(cudaMemcpyAsync(b.dst[i], b.src[i], b.size[i], cudaMemcpyDefault, s));
   {
     std::lock_guard<std::mutex> g(c->mu);  // the I/O thread counts its copies too
     c->tm.copy_calls += b.dst.size();
@@ -426,50 +428,18 @@ void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user,
 // the dirty decision depends on Adam(t-1) (R14), so the caller's thread never
 // waits for it.  Jobs run in activate order.
 void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
-  Dev& d = c->d;
   const int p = j.parity;
-  auto fail = [&](const char* what, cudaError_t e) {
-    std::lock_guard<std::mutex> g(c->mu);
-    c->io_err = std::string(what) + ": " + cudaGetErrorString(e);
-    c->io_failed = true;
-  };
   cudaError_t e = cudaEventSynchronize(c->ev_evict[p]);
-  if (e != cudaSuccess) return fail("io: cudaEventSynchronize(evict)", e);
+  if (e != cudaSuccess) {
+    std::lock_guard<std::mutex> g(c->mu);
+    c->io_err = std::string("io: cudaEventSynchronize(evict): ") + cudaGetErrorString(e);
+    c->io_failed = true;
+    return;
+  }
   const uint32_t nd = c->ndirty[p];
   const uint32_t* dl = c->dirty_map[p];
-  const size_t w = (size_t)d.n_arr * c->rec_bytes;
-  CopyBatch b;
-  b.max_merge = c->d2h_max_merge;
-  for (uint32_t k = 0; k < nd; ++k) {
-    if (c->store) c->store->mark_dirty(dl[2 * k], j.T);  // R27 (a): inserted dirty
-    float* h = host_rec(c, dl[2 * k]);
-    const float* src = j.direct ? slot_rec(c, dl[2 * k + 1])
-                                : d.staging[p] + (size_t)k * d.n_arr * d.rec_floats;
-    b.add(h, src, w);
-  }
-  Timer td;
-  prof_begin(c, c->d2h, td);
-  if (!b.dst.empty()) {
-    if (b.dst.size() == 1) {
-      e = cudaMemcpyAsync(b.dst[0], b.src[0], b.size[0], cudaMemcpyDefault, c->d2h);
-    } else {
-      cudaMemcpyAttributes at{};
-      at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t aidx = 0, failidx = 0;
-      e = cudaMemcpyBatchAsync(b.dst.data(), b.src.data(), b.size.data(), b.dst.size(), &at,
-                               &aidx, 1, &failidx, c->d2h);
-    }
-    if (e != cudaSuccess) return fail("io: write-back batch", e);
-  }
-  prof_end(c, c->d2h, td, 4, (uint64_t)nd * w);
-  e = cudaEventRecord(c->ev_d2h[p], c->d2h);
-  if (e != cudaSuccess) return fail("io: cudaEventRecord(d2h)", e);
-  if (c->store) {
-    e = cudaEventRecord(c->ev_job[j.T & 3], c->d2h);
-    if (e != cudaSuccess) return fail("io: cudaEventRecord(job)", e);
-  }
+  for (uint32_t k = 0; k < nd; ++k) c->store->mark_dirty(dl[2 * k], j.T);  // R27 (a): inserted dirty
   std::lock_guard<std::mutex> g(c->mu);
-  c->tm.copy_calls += b.dst.size();
   c->last_ndirty = nd;
 }
 
@@ -532,7 +502,6 @@ tgs_status sync_all(tgs_ctx* c) {
   CK(cudaStreamSynchronize(c->h2d));
   CK(cudaStreamSynchronize(c->compute));
   CK(cudaStreamSynchronize(c->d2h));
-  CK(cudaStreamSynchronize(c->fix));
   prof_collect(c);
   return TGS_OK;
 }
@@ -559,19 +528,24 @@ void destroy_impl(tgs_ctx* c) {
   delete c->store;
   if (c->cache_pool) cudaFreeHost(c->cache_pool);
   if (c->sm_map) cudaFreeHost(c->sm_map);
+  for (int q = 0; q < 2; ++q)
+    for (void* h : {(void*)c->sel_map[q][0], (void*)c->sel_map[q][1], (void*)c->sp_entry_map[q]})
+      if (h) cudaFreeHost(h);
   for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
                   (void*)c->ndirty, (void*)c->planes_pinned, (void*)c->lut_pinned})
     if (h) cudaFreeHost(h);
   for (cudaEvent_t e : c->ev_job)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_gstart, c->ev_gdone, c->ev_ready[0], c->ev_ready[1],
+  for (cudaEvent_t e : c->ev_c1)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_plan, c->ev_ready[0], c->ev_ready[1],
                         c->ev_evict[0],
                         c->ev_evict[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_lists[0],
                         c->ev_lists[1], c->trace_base})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  for (cudaStream_t s : {c->plan, c->h2d, c->d2h, c->fix}) if (s) cudaStreamDestroy(s);
+  for (cudaStream_t s : {c->plan, c->h2d, c->d2h}) if (s) cudaStreamDestroy(s);
   cudaGetLastError();
   delete c;
 }
@@ -673,16 +647,11 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   // (TGS_PLAN_PRIO=0: default priority, for A/B measurements)
   const char* pp = getenv("TGS_PLAN_PRIO");
   const int plan_prio = (pp && atoi(pp) == 0) ? prio_lo : prio_hi;
-  // the fix-up stream (k_readmit after the gather) sits on the gather -> Adam
-  // chain; TGS_FIX_PRIO=1 gives it the highest priority (A/B knob)
-  const char* fp = getenv("TGS_FIX_PRIO");
-  const int fix_prio = (fp && atoi(fp) == 1) ? prio_hi : prio_lo;
   if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, plan_prio) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->fix, cudaStreamNonBlocking, fix_prio) != cudaSuccess)
+      cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
-  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_gstart, &c->ev_gdone, &c->ev_ready[0],
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready[0],
                          &c->ev_ready[1], &c->ev_evict[0],
                          &c->ev_evict[1], &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_lists[0],
                          &c->ev_lists[1], &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
@@ -696,7 +665,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     // NEXT f3: CPU cache of H records over the log-structured store
     const uint64_t S = (d.n_arr * c->rec_bytes + 4095) / 4096 * 4096;
     if (cudaHostAlloc((void**)&c->cache_pool, (size_t)scfg->cache_blocks * S,
-                      cudaHostAllocPortable) != cudaSuccess) {
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
       c->cache_pool = nullptr;
       cudaGetLastError();
       return fail(TGS_ENOMEM);
@@ -717,7 +686,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   } else {
     c->host_bytes = (size_t)d.Kloc * d.n_arr * c->rec_bytes;
     if (c->host_bytes &&
-        cudaHostAlloc((void**)&c->host, c->host_bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaHostAlloc((void**)&c->host, c->host_bytes,
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
       c->host = nullptr;
       cudaGetLastError();
       return fail(TGS_ENOMEM);
@@ -738,13 +708,21 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     return fail(TGS_ENOMEM);
   }
   if (c->store) {
-    if (cudaHostAlloc((void**)&c->sm_map, sizeof(uint32_t) * std::max(d.C, 1u),
-                      cudaHostAllocMapped) != cudaSuccess) {
-      c->sm_map = nullptr;
+    const size_t cb = sizeof(uint32_t) * std::max(d.C, 1u);
+    bool okm = cudaHostAlloc((void**)&c->sm_map, cb, cudaHostAllocMapped) == cudaSuccess;
+    for (int q = 0; q < 2; ++q)
+      for (uint32_t** m : {&c->sel_map[q][0], &c->sel_map[q][1], &c->sp_entry_map[q]})
+        okm = okm && cudaHostAlloc((void**)m, cb, cudaHostAllocMapped) == cudaSuccess;
+    if (!okm) {
       cudaGetLastError();
       return fail(TGS_ENOMEM);
     }
     cudaHostGetDevicePointer((void**)&d.sm_map, c->sm_map, 0);
+    cudaHostGetDevicePointer((void**)&d.host_dev, c->cache_pool, 0);
+    d.host_stride = c->store->entry_bytes();
+  } else {
+    if (c->host) cudaHostGetDevicePointer((void**)&d.host_dev, c->host, 0);
+    d.host_stride = (uint64_t)d.n_arr * c->rec_bytes;
   }
   std::memset(c->hdr, 0, sizeof(PlanHdr));
   std::memset(c->ndirty, 0, sizeof(uint32_t) * 2);
@@ -795,6 +773,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   }
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
   d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
+  d.dl_blk = dalloc_t<uint32_t>(c, Cc, ok);
+  if (c->store) d.ent_of = dalloc_t<int32_t>(c, Kl, ok);
   d.pend[0] = dalloc_t<uint32_t>(c, Kl, ok);
   d.pend[1] = dalloc_t<uint32_t>(c, Kl, ok);
   d.last_planes[0] = dalloc_t<float4>(c, kMaxCams * 6, ok);
@@ -827,11 +807,15 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   CKI(cudaMemcpyAsync(d.rank_lut, lut.data(), sizeof(uint16_t) * lut.size(), cudaMemcpyHostToDevice, s0));
   CKI(cudaMemsetAsync(d.last_access, 0xff, sizeof(int32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.step, 0, sizeof(uint32_t) * Kl, s0));
+  if (c->store && reopen && d.Kloc)  // R30: step counters of the barrier resumed from
+    CKI(cudaMemcpyAsync(d.step, c->store->barrier_steps().data(), sizeof(uint32_t) * d.Kloc,
+                        cudaMemcpyHostToDevice, s0));
   CKI(cudaMemsetAsync(d.b2s, 0xff, sizeof(int32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.ever, 0, Kl, s0));
   CKI(cudaMemsetAsync(d.evicted, 0, Kl, s0));
   CKI(cudaMemsetAsync(d.admit, 0, sizeof(int32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.wb_tag, 0xff, sizeof(int32_t) * Kl, s0));
+  if (d.ent_of) CKI(cudaMemsetAsync(d.ent_of, 0xff, sizeof(int32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.pend[0], 0, sizeof(uint32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.pend[1], 0, sizeof(uint32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * 2, s0));
@@ -852,11 +836,41 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
 #undef CKI
   int dev = g.device;
   c->adam_grid = adam_grid(dev);
-  if (const char* m = getenv("TGS_D2H_MERGE"))
-    c->d2h_max_merge = (size_t)std::max(1, atoi(m)) * d.n_arr * c->rec_bytes;
+  if (const char* m = getenv("TGS_GATHER_CTAS")) c->gather_ctas = std::max(1, atoi(m));
+  if (const char* m = getenv("TGS_SCATTER_CTAS")) c->scatter_ctas = std::max(1, atoi(m));
+  if (const char* m = getenv("TGS_GATHER_BUFS")) c->gather_bufs = atoi(m);
+  if (const char* m = getenv("TGS_SCATTER_BUFS")) c->scatter_bufs = atoi(m);
   if (const char* m = getenv("TGS_LISTS_AFTER_ADAM")) c->lists_after_adam = atoi(m) != 0;
-  c->io = std::thread(io_main, c);
+  if (c->store) c->io = std::thread(io_main, c);  // flat tier: no host work per write-back
   *out = c;
+  return TGS_OK;
+}
+
+// a5: k_adam_prologue, k_adam (+ k_refresh) of the last activate's A list
+tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
+                         const uint32_t* d_row_mask) {
+  const Dev dk = dev_for(c, p, c->T - 1);
+  Timer t1, t2;
+  prof_begin(c, c->compute, t1);
+  CK(launch_adam_prologue(dk, nA, p, d_row_mask, c->compute));
+  prof_end(c, c->compute, t1, 1);
+  // After the prologue, Adam reads only its A lists (3-deep ring), the per-
+  // entry constants and slots the plan never hands out while R_{t+1} holds
+  // them: the plan of t+2 could overwrite this parity's other lists now
+  // (TGS_LISTS_AFTER_ADAM=0).  By default, and always with the bound refresh
+  // on (that plan merges k_refresh's radii, R25), they stay in use until the
+  // end of this step's compute work.
+  const bool lists_late = c->d.refresh || c->lists_after_adam;
+  if (!lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));
+  prof_begin(c, c->compute, t2);
+  CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
+  prof_end(c, c->compute, t2, 0);
+  c->tm.kernel_launches += 2;
+  if (c->d.refresh) {
+    CK(launch_refresh(dk, nA, p, c->compute));
+    c->tm.kernel_launches++;
+  }
+  if (lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }
 
@@ -915,25 +929,70 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   prof_end(c, c->plan, tp, 2);
   c->tm.kernel_launches += (d.Kloc ? 1 : 0) + ((J && d.Kloc) ? 2 : 0) + 1;
   CK(cudaEventRecord(c->ev_plan, c->plan));
+
+  // ---- a4 gather of S+ into free slots (k_xfer on the h2d stream).  Hazards
+  //      (GPU-side waits only): slots freed by t-1 (its pack, or its direct
+  //      write-back, done), host records written back by t-2 landed.  With the
+  //      default pool (P >= 2C) and Tide on, S+ never takes a slot S- frees in
+  //      the same activate (R13), so the gather is enqueued before the host even
+  //      reads the plan: it starts the moment k_plan ends.
+  Dev dg = dev_for(c, p, T);
+  uint32_t* const* sel = c->sel_map[p];
+  uint32_t* spe = c->sp_entry_map[p];
+  if (c->store) CK(cudaHostGetDevicePointer((void**)&dg.sp_entry, spe, 0));
+  auto gather_waits = [&]() -> tgs_status {
+    CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
+    if (c->rec_evict[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[q], 0));
+    if (c->prev_direct) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[q], 0));
+    if (c->d2h_job[p] >= 0 && c->d2h_job[p] < T) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
+    return TGS_OK;
+  };
+  auto gather_flat = [&](uint32_t n_hint) -> tgs_status {
+    tgs_status gs = gather_waits();
+    if (gs != TGS_OK) return gs;
+    Timer th;
+    prof_begin(c, c->h2d, th);
+    CK(launch_xfer(dg, 0, p, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
+    c->h2d_prof = prof_end(c, c->h2d, th, 3);
+    c->tm.kernel_launches++;
+    CK(cudaEventRecord(c->ev_ready[p], c->h2d));
+    c->rec_ready[p] = true;
+    return TGS_OK;
+  };
+  const bool early = !c->store && d.tide && d.P >= 2u * d.C;
+  if (early) {
+    st = gather_flat(d.C);
+    if (st != TGS_OK) return st;
+  }
   CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
   const PlanHdr h = *c->hdr;
   c->last = h;
   c->last_J = J;
+  if (c->h2d_prof >= 0) {  // the timed gather's algorithmic bytes
+    std::lock_guard<std::mutex> g(c->prof_mu);
+    if ((size_t)c->h2d_prof < c->pending.size())
+      c->pending[c->h2d_prof].bytes = (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
+    c->h2d_prof = -1;
+  }
 
   // ---- a4 write-back of dirty S-, enqueued on the compute stream after
   //      Adam(t-1) (the dirty decision).  Normal path: k_evict compacts the
   //      dirty list and k_pack copies those records into staging ring p, so
-  //      their slots are free at once; the I/O thread then drains the ring to
-  //      the host tier.  Direct path (this activate's S+ may reuse S- slots or
-  //      records, or the ring is too small): the copies read the slots.
+  //      their slots are free at once; k_xfer then drains the ring to the host
+  //      tier on the d2h stream.  Direct path (this activate's S+ may reuse S-
+  //      slots, or the ring is too small): k_xfer reads the slots themselves.
   const bool reuse_now = !d.tide || h.fallback;
   const bool direct = reuse_now || h.nSm > d.S_max;
   auto writeback = [&]() -> tgs_status {
-    Timer te;
+    Timer te, td;
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-    if (!direct && c->d2h_job[p] >= 0) {  // ring p is still drained by job t-2
-      io_join(c, c->d2h_job[p]);
-      CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[p], 0));
+    // ring p is read by the previous activate's gather (re-admissions): done
+    if (c->rec_ready[q]) CK(cudaStreamWaitEvent(c->compute, c->ev_ready[q], 0));
+    if (c->d2h_job[p] >= 0) {
+      // store tier: the I/O job of t-2 must have read dirty_map[p] / ndirty[p]
+      // before k_evict of t rewrites them; a ring job also still drains ring p
+      if (c->store) io_join(c, c->d2h_job[p]);
+      if (!direct) CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[p], 0));
     }
     prof_begin(c, c->compute, te);
     CK(launch_evict_tagged(d, h.nSm, p, T, !direct, c->compute));
@@ -942,108 +1001,86 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     c->tm.kernel_launches += direct ? 1 : 2;
     CK(cudaEventRecord(c->ev_evict[p], c->compute));
     c->rec_evict[p] = true;
-    io_submit(c, {T, p, direct});
+    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[p], 0));
+    prof_begin(c, c->d2h, td);
+    CK(launch_xfer(d, direct ? 2 : 1, p, T, nullptr, 0, h.nSm, c->scatter_ctas, c->scatter_bufs, c->d2h));
+    prof_end(c, c->d2h, td, 4);
+    c->tm.kernel_launches++;
+    CK(cudaEventRecord(c->ev_d2h[p], c->d2h));
+    if (c->store) {
+      CK(cudaEventRecord(c->ev_job[T & 3], c->d2h));
+      io_submit(c, {T, p, direct});
+    }
     c->d2h_job[p] = T;
     return TGS_OK;
   };
   if (reuse_now && h.nSm) {
     st = writeback();
     if (st != TGS_OK) return st;
-    io_join(c, T);
+    if (c->store) io_join(c, T);
     if (c->io_failed) return check(c);
     CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
   }
 
-  // ---- a4 gather of S+ into free slots: one batch on the copy engine.
-  //      Hazards: slots freed by t-1 (pack done, or its direct write-back
-  //      done) and host records written back by t-2.
-  if (c->rec_evict[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[q], 0));
-  if (c->prev_direct) {
+  if (!early && !c->store) {
+    st = gather_flat(h.nSp);
+    if (st != TGS_OK) return st;
+  } else if (c->store) {
+    // NEXT f3, R27 (b): S+ records come from their CPU-cache entries; misses
+    // are read from SSD through Index[k] after a dirty LRU victim (if any) is
+    // appended to the patch log.  Needs the dirty marks of activate T-1.  The
+    // hits move over PCIe (k_xfer from their entries) while the SSD reads the
+    // misses; then a second k_xfer moves the misses.
+    st = gather_waits();
+    if (st != TGS_OK) return st;
     io_join(c, T - 1);
-    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[q], 0));
-  }
-  if (c->d2h_job[p] >= 0 && c->d2h_job[p] < T) {
-    io_join(c, c->d2h_job[p]);
-    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
-  }
-  if (c->io_failed) return check(c);
-  // the fix-up stream zeroes moments (cold restart) while the batch streams in
-  // and patches re-admissions after it; the next gather does not wait for it
-  cudaStream_t ready_on = c->h2d;
-  if (h.nSp) {
-    const bool fixups = c->prev_packed;  // cold restart needs no fix-up (see k_adam)
-    if (fixups) {
-      CK(cudaEventRecord(c->ev_gstart, c->h2d));
-      CK(cudaStreamWaitEvent(c->fix, c->ev_gstart, 0));
-      CK(cudaStreamWaitEvent(c->fix, c->ev_plan, 0));
-      ready_on = c->fix;
-    }
-    Timer th;
-    CopyBatch b;
-    if (c->store) {
-      // NEXT f3, R27 (b): S+ records come from their CPU-cache entries; misses
-      // are read from SSD through Index[k] after a dirty LRU victim (if any) is
-      // appended to the patch log.  Needs the dirty marks of activate T-1.
-      // The hits move over PCIe while the SSD reads the misses.
-      io_join(c, T - 1);
-      if (c->io_failed) return check(c);
-      auto wait_d2h = [&](int32_t job) {
-        // the plan of T waited (GPU-side) for the gather of T-2, which waited
-        // for the write-back of T-4: older jobs have landed
-        if (job + 4 <= T) return;
-        io_join(c, job);
-        cudaEventSynchronize(c->ev_job[job & 3]);
-      };
-      std::vector<uint32_t> pairs[2];  // (local id, slot) of hits / misses
-      tgs_status hst = TGS_OK;
-      auto hits_ready = [&](const std::vector<uint8_t>& miss) {
-        for (uint32_t i = 0; i < h.nSp; ++i) {
-          pairs[miss[i]].push_back(c->sp_map[2 * i]);
-          pairs[miss[i]].push_back(c->sp_map[2 * i + 1]);
-        }
-        Timer t1;
-        prof_begin(c, c->h2d, t1);
-        add_records(c, b, pairs[0].data(), (uint32_t)pairs[0].size() / 2, true);
-        hst = submit(c, b, c->h2d);
-        prof_end(c, c->h2d, t1, 3, (uint64_t)pairs[0].size() / 2 * d.n_arr * c->rec_bytes);
-        b = CopyBatch{};
-      };
-      const std::string e = c->store->gather(c->sp_map, h.nSp, T, wait_d2h, hits_ready);
-      if (!e.empty()) {
-        c->poisoned = true;
-        set_err(c, "store: %s", e.c_str());
-        return TGS_EIO;
-      }
-      if (hst != TGS_OK) return hst;
-      prof_begin(c, c->h2d, th);
-      add_records(c, b, pairs[1].data(), (uint32_t)pairs[1].size() / 2, true);
-      st = submit(c, b, c->h2d);
-      if (st != TGS_OK) return st;
-      prof_end(c, c->h2d, th, 3, (uint64_t)pairs[1].size() / 2 * d.n_arr * c->rec_bytes);
-    } else {
-      prof_begin(c, c->h2d, th);
-      add_records(c, b, c->sp_map, h.nSp, true);
-      st = submit(c, b, c->h2d);
-      if (st != TGS_OK) return st;
-      prof_end(c, c->h2d, th, 3, (uint64_t)h.nSp * d.n_arr * c->rec_bytes);
-    }
-    if (c->prev_packed) {  // S+ blocks the previous batch packed: newest copy is in its ring
-      CK(cudaEventRecord(c->ev_gdone, c->h2d));
-      CK(cudaStreamWaitEvent(c->fix, c->ev_gdone, 0));
-      Timer tr;
-      prof_begin(c, c->fix, tr);
-      CK(launch_readmit(d, h.nSp, p, T, c->fix));
-      prof_end(c, c->fix, tr, 7);
+    if (c->io_failed) return check(c);
+    auto wait_d2h = [&](int32_t job) {
+      // the plan of T waited (GPU-side) for the gather of T-2, which waited
+      // for the write-back of T-4: older jobs have landed
+      if (job + 4 <= T) return;
+      io_join(c, job);
+      cudaEventSynchronize(c->ev_job[job & 3]);
+    };
+    uint32_t n_sel[2] = {0, 0};
+    tgs_status hst = TGS_OK;
+    auto launch_subset = [&](int which) -> tgs_status {
+      if (!n_sel[which]) return TGS_OK;
+      Timer t1;
+      prof_begin(c, c->h2d, t1);
+      uint32_t* sel_dev = nullptr;
+      CK(cudaHostGetDevicePointer((void**)&sel_dev, sel[which], 0));
+      CK(launch_xfer(dg, 0, p, T, sel_dev, n_sel[which], n_sel[which], c->gather_ctas, c->gather_bufs, c->h2d));
+      prof_end(c, c->h2d, t1, 3, (uint64_t)n_sel[which] * d.n_arr * c->rec_bytes);
       c->tm.kernel_launches++;
-    } else if (fixups) {
-      CK(cudaEventRecord(c->ev_gdone, c->h2d));
-      CK(cudaStreamWaitEvent(c->fix, c->ev_gdone, 0));
+      return TGS_OK;
+    };
+    auto hits_ready = [&](const std::vector<uint8_t>& miss) {
+      for (uint32_t i = 0; i < h.nSp; ++i) {
+        const int w = miss[i] ? 1 : 0;
+        sel[w][n_sel[w]++] = i;
+        if (!miss[i]) spe[i] = (uint32_t)c->store->entry_index(c->sp_map[2 * i]);
+      }
+      hst = launch_subset(0);
+    };
+    const std::string e = c->store->gather(c->sp_map, h.nSp, T, wait_d2h, hits_ready);
+    if (!e.empty()) {
+      c->poisoned = true;
+      set_err(c, "store: %s", e.c_str());
+      return TGS_EIO;
     }
+    if (hst != TGS_OK) return hst;
+    for (uint32_t k = 0; k < n_sel[1]; ++k) {
+      const uint32_t i = sel[1][k];
+      spe[i] = (uint32_t)c->store->entry_index(c->sp_map[2 * i]);
+    }
+    st = launch_subset(1);
+    if (st != TGS_OK) return st;
+    CK(cudaEventRecord(c->ev_ready[p], c->h2d));
+    c->rec_ready[p] = true;
+    // R27 (c): the blocks that left the GPU are accesses of the CPU cache too
+    if (h.nSm) c->store->touch_evicted(c->sm_map, h.nSm, T);
   }
-  CK(cudaEventRecord(c->ev_ready[p], ready_on));
-  c->rec_ready[p] = true;
-  // R27 (c): the blocks that left the GPU are accesses of the CPU cache too
-  if (c->store && h.nSm) c->store->touch_evicted(c->sm_map, h.nSm, T);
 
   if (!reuse_now && h.nSm) {
     st = writeback();
@@ -1054,8 +1091,21 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   CK(cudaEventRecord(c->ev_lists[p], c->compute));
   c->rec_lists[p] = true;
   c->prev_direct = direct && h.nSm > 0;
-  c->prev_packed = !direct && h.nSm > 0;
 
+  // ---- C1: the active set of every rank, on the plan stream
+  //      after k_plan; every rank calls it once per activate
+  if (c->has_comm) {
+    uint32_t* send = c->a3_gid[(uint32_t)T % 3u];
+    CK(launch_pad_active(send, d.hdr_dev, d.C, c->plan));
+    c->tm.kernel_launches++;
+    if (c->comm.allgather(c->comm.user, send, c->c1_recv[p], sizeof(uint32_t) * d.C,
+                          (void*)c->plan) != 0) {
+      c->poisoned = true;
+      set_err(c, "C1 all-gather failed (activate %d)", T);
+      return TGS_ENCCL;
+    }
+    CK(cudaEventRecord(c->ev_c1[p], c->plan));
+  }
   c->last_parity = p;
   c->parity = q;
   c->T = T + 1;
@@ -1079,6 +1129,9 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     out->slot_stride = 3 * d.rec_floats;
     out->grad_stride = d.rec_floats;
     out->ready = (void*)c->ev_ready[p];
+    out->d_global_active = c->has_comm ? c->c1_recv[p] : nullptr;
+    out->global_stride = d.C;
+    out->global_ready = c->has_comm ? (void*)c->ev_c1[p] : nullptr;
   }
   return TGS_OK;
 }
@@ -1103,29 +1156,20 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   h.eps = hp->eps;
   CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
   CK(cudaStreamWaitEvent(c->compute, c->ev_ready[p], 0));
-  if (nA == 0) return TGS_OK;
-  const Dev dk = dev_for(c, p, c->T - 1);
-  Timer t1, t2;
-  prof_begin(c, c->compute, t1);
-  CK(launch_adam_prologue(dk, nA, p, d_row_mask, c->compute));
-  prof_end(c, c->compute, t1, 1);
-  // After the prologue, Adam reads only its A lists (3-deep ring), the per-
-  // entry constants and slots the plan never hands out while R_{t+1} holds
-  // them: the plan of t+2 could overwrite this parity's other lists now
-  // (TGS_LISTS_AFTER_ADAM=0).  By default, and always with the bound refresh
-  // on (that plan merges k_refresh's radii, R25), they stay in use until the
-  // end of this step's compute work.
-  const bool lists_late = c->d.refresh || c->lists_after_adam;
-  if (!lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));
-  prof_begin(c, c->compute, t2);
-  CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
-  prof_end(c, c->compute, t2, 0);
-  c->tm.kernel_launches += 2;
-  if (c->d.refresh) {
-    CK(launch_refresh(dk, nA, p, c->compute));
-    c->tm.kernel_launches++;
+  st = nA ? adam_launches(c, p, nA, h, d_row_mask) : TGS_OK;
+  if (st != TGS_OK) return st;
+  // ---- C2: every rank's cumulative counters summed, after this
+  //      step's Adam on the compute stream; every rank calls it once per step
+  if (c->has_comm) {
+    CK(cudaMemcpyAsync(c->c2_buf, c->d.stats, sizeof(unsigned long long) * ST_N,
+                       cudaMemcpyDeviceToDevice, c->compute));
+    if (c->comm.allreduce_u64(c->comm.user, reinterpret_cast<uint64_t*>(c->c2_buf), ST_N,
+                              (void*)c->compute) != 0) {
+      c->poisoned = true;
+      set_err(c, "C2 all-reduce failed (step %llu)", (unsigned long long)c->n_steps);
+      return TGS_ENCCL;
+    }
   }
-  if (lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   if (c->cfg.serialize) CK(cudaStreamSynchronize(c->compute));  // ablation w/o Overlap
   return TGS_OK;
 }
@@ -1174,7 +1218,10 @@ tgs_status tgs_flush(tgs_ctx* c) {
     // NEXT f3: the barrier reaches the SSD too: the dirty
     // residents just landed in their entries, then every dirty entry is appended
     for (auto& e : list) c->store->mark_dirty(e.first, -1);
-    const std::string e = c->store->flush_all([](int32_t) {});
+    // R30: the manifest carries the Adam step counters of this barrier
+    std::vector<uint32_t> steps(std::max(d.Kloc, 1u));
+    CK(cudaMemcpy(steps.data(), d.step, sizeof(uint32_t) * d.Kloc, cudaMemcpyDeviceToHost));
+    const std::string e = c->store->flush_all([](int32_t) {}, steps.data());
     if (!e.empty()) {
       c->poisoned = true;
       set_err(c, "store: %s", e.c_str());
@@ -1184,6 +1231,37 @@ tgs_status tgs_flush(tgs_ctx* c) {
   c->host_flush_blocks += list.size();
   c->host_flush_bytes += (uint64_t)list.size() * d.n_arr * c->rec_bytes;
   c->can_step = false;
+  return TGS_OK;
+}
+
+tgs_status tgs_set_comm(tgs_ctx* c, const tgs_comm* comm) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!comm || !comm->allgather || !comm->allreduce_u64) return TGS_EINVAL;
+  if (c->T != 0 || c->has_comm) return TGS_ESTATE;
+  bool ok = true;
+  const size_t rows = (size_t)c->cfg.world_size * std::max(c->d.C, 1u);
+  c->c1_recv[0] = dalloc_t<uint32_t>(c, rows, ok);
+  c->c1_recv[1] = dalloc_t<uint32_t>(c, rows, ok);
+  c->c2_buf = dalloc_t<unsigned long long>(c, ST_N, ok);
+  if (!ok) return TGS_ENOMEM;
+  for (cudaEvent_t* e : {&c->ev_c1[0], &c->ev_c1[1]})
+    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  CK(cudaMemsetAsync(c->c2_buf, 0, sizeof(unsigned long long) * ST_N, c->compute));
+  CK(cudaStreamSynchronize(c->compute));
+  c->comm = *comm;
+  c->has_comm = true;
+  return TGS_OK;
+}
+
+tgs_status tgs_get_global_stats(tgs_ctx* c, tgs_stats* out) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (!out) return TGS_EINVAL;
+  if (!c->has_comm) return TGS_ESTATE;
+  st = sync_all(c);
+  if (st != TGS_OK) return st;
+  CK(cudaMemcpy(out, c->c2_buf, sizeof(uint64_t) * ST_N, cudaMemcpyDeviceToHost));
   return TGS_OK;
 }
 
@@ -1234,10 +1312,11 @@ tgs_status tgs_get_timing(tgs_ctx* c, tgs_timing* out) {
   st = sync_all(c);
   if (st != TGS_OK) return st;
   *out = c->tm;
-  unsigned long long fr[2] = {0, 0};
+  unsigned long long fr[3] = {0, 0, 0};
   CK(cudaMemcpy(fr, c->d.stats + ST_FRESH_ROWS, sizeof(fr), cudaMemcpyDeviceToHost));
   out->fresh_active_rows = fr[0];
   out->fresh_blocks = fr[1];
+  out->h2d_ring_records = fr[2];
   return TGS_OK;
 }
 

@@ -99,8 +99,13 @@ class BlockStore {
   void touch_evicted(const uint32_t* sm, uint32_t n, int32_t T);
   // R27 (a): the D2H write-back of activate T put block l's dirty record into its entry
   void mark_dirty(uint32_t l, int32_t T);
-  // the barrier: append every dirty entry (ascending id), clear dirty, fdatasync
-  std::string flush_all(const std::function<void(int32_t)>& wait_d2h);
+  // the barrier: append every dirty entry (ascending id), clear dirty, fdatasync,
+  // then the manifest (R30) with the Adam step counters `steps` [Kloc] (NULL:
+  // those of the last barrier)
+  std::string flush_all(const std::function<void(int32_t)>& wait_d2h,
+                        const uint32_t* steps = nullptr);
+  // R30: the Adam step counters of the barrier a reopened store resumed from
+  const std::vector<uint32_t>& barrier_steps() const { return steps_; }
   // R31: merge the patch segments into a new base (after flush_all)
   std::string compact();
 
@@ -109,6 +114,8 @@ class BlockStore {
     const int32_t e = ent_of_[l];
     return e < 0 ? nullptr : reinterpret_cast<float*>(pool_ + (uint64_t)e * S_);
   }
+  // index of block l's cache entry (its record sits at pool + index * entry_bytes()), -1 if none
+  int32_t entry_index(uint32_t l) const { return ent_of_[l]; }
   // newest version of block l (cache, else SSD) into dst (payload bytes)
   std::string read_block(uint32_t l, void* dst);
 
@@ -135,6 +142,7 @@ class BlockStore {
   int fd_of(uint32_t fid);
   std::string new_segment();
   std::string recover();
+  std::string write_manifest();
   // reserves the next record of the patch log for block l: (fd, file offset of the record)
   std::string reserve_append(uint32_t l, int& fd, uint64_t& rec_off);
   std::string write_records(const std::vector<std::pair<uint32_t, int32_t>>& recs /* (l, entry) */);
@@ -158,6 +166,9 @@ class BlockStore {
   StoreCounters cnt_{};
   IoPool* pool_io_ = nullptr;
   char* hdr_pages_ = nullptr;      // aligned record header pages (grown on demand)
+  uint64_t epoch_ = 0;             // manifests written (barriers, compactions, the initial base)
+  std::vector<uint64_t> base_version_;  // version of each block's base record (R31)
+  std::vector<uint32_t> steps_;    // Adam step counters of the last barrier (R30)
   size_t hdr_cap_ = 0;
 };
 

@@ -30,7 +30,7 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
            "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error",
            "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru",
-           "tgs_order_views", "tgs_store_compact")
+           "tgs_order_views", "tgs_store_compact", "tgs_set_comm", "tgs_get_global_stats")
 
 
 class Config(C.Structure):
@@ -60,7 +60,18 @@ class Activation(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d_active_blocks", C.c_void_p),
                 ("d_active_slots", C.c_void_p), ("d_params", C.c_void_p),
                 ("d_grads", C.c_void_p), ("slot_stride", C.c_uint64),
-                ("grad_stride", C.c_uint64), ("ready", C.c_void_p)]
+                ("grad_stride", C.c_uint64), ("ready", C.c_void_p),
+                ("d_global_active", C.c_void_p), ("global_stride", C.c_uint32),
+                ("global_ready", C.c_void_p)]
+
+
+COMM_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+COMM_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.c_void_p)
+
+
+class Comm(C.Structure):
+    _fields_ = [("allgather", COMM_ALLGATHER), ("allreduce_u64", COMM_ALLREDUCE),
+                ("user", C.c_void_p)]
 
 
 class Adam(C.Structure):
@@ -71,7 +82,7 @@ class Adam(C.Structure):
 STAT_FIELDS = ("iter", "n_visible", "n_resident", "n_active_blocks", "n_stage_in", "n_evict",
                "n_evict_dirty", "n_active_rows", "h2d_bytes", "d2h_bytes", "flush_bytes",
                "n_flush_blocks", "readmissions", "cold_restart_updates", "total_updates",
-               "resident_streak_sum", "streak_count")
+               "resident_streak_sum", "streak_count", "k_inter_sum", "k_union_sum")
 
 
 class Stats(C.Structure):
@@ -88,7 +99,7 @@ class Timing(C.Structure):
                                            "d2h_batches", "adam_rows", "adam_elems_quads",
                                            "h2d_bytes", "d2h_bytes", "kernel_launches",
                                            "copy_calls", "fresh_active_rows",
-                                           "fresh_blocks")])
+                                           "fresh_blocks", "h2d_ring_records")])
 
     def as_dict(self):
         return {n: (float(getattr(self, n)) if t is C.c_double else int(getattr(self, n)))
@@ -147,6 +158,8 @@ def lib():
         L.tgs_flush.argtypes = [vp]
         L.tgs_fine_filter.argtypes = [vp, vp]
         L.tgs_get_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.tgs_set_comm.argtypes = [vp, C.POINTER(Comm)]
+        L.tgs_get_global_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.tgs_get_stats_async.argtypes = [vp, vp]
         L.tgs_set_profiling.argtypes = [vp, C.c_int]
@@ -220,6 +233,65 @@ def torch_allocator(device=0):
         torch.cuda.caching_allocator_delete(int(ptr))
 
     return Allocator(ALLOC_FN(_alloc), FREE_FN(_free), None)
+
+
+def _device_view(torch, ptr, nbytes, device):
+    """uint8 torch view of nbytes of library-owned device memory (no copy)"""
+    class _V:
+        __cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                    "data": (int(ptr), False), "version": 3}
+    return torch.as_tensor(_V(), device=device)
+
+
+def torch_comm(group=None, device=None):
+    """tgs_comm transport over torch.distributed (argument marshalling only): NCCL
+    enqueues the collective on the library's stream; gloo (CPU tests, several
+    ranks sharing one GPU) stages through host memory and completes before
+    returning.  Keep the returned object alive as long as the table."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    nccl = dist.get_backend(group) == "nccl"
+    G = dist.get_world_size(group)
+
+    def _ag(_user, send, recv, nbytes, stream):
+        try:
+            s = _device_view(torch, send, nbytes, dev)
+            r = _device_view(torch, recv, nbytes * G, dev)
+            if nccl:
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0), device=dev)):
+                    dist.all_gather_into_tensor(r, s, group=group)
+            else:
+                torch.cuda.ExternalStream(int(stream or 0), device=dev).synchronize()
+                parts = [torch.empty(int(nbytes), dtype=torch.uint8) for _ in range(G)]
+                dist.all_gather(parts, s.cpu(), group=group)
+                r.copy_(torch.cat(parts).to(dev))
+                torch.cuda.synchronize(dev)
+            return 0
+        except Exception as e:  # surfaces as TGS_ENCCL
+            print(f"tidegs torch_comm all-gather: {e}", flush=True)
+            return 1
+
+    def _ar(_user, buf, count, stream):
+        try:
+            addr = C.cast(buf, C.c_void_p).value
+            b = _device_view(torch, addr, count * 8, dev).view(torch.int64)
+            if nccl:
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0), device=dev)):
+                    dist.all_reduce(b, group=group)
+            else:
+                torch.cuda.ExternalStream(int(stream or 0), device=dev).synchronize()
+                h = b.cpu()
+                dist.all_reduce(h, group=group)
+                b.copy_(h.to(dev))
+                torch.cuda.synchronize(dev)
+            return 0
+        except Exception as e:
+            print(f"tidegs torch_comm all-reduce: {e}", flush=True)
+            return 1
+
+    return Comm(COMM_ALLGATHER(_ag), COMM_ALLREDUCE(_ar), None)
 
 
 class Table:
@@ -347,6 +419,26 @@ class Table:
         s = Stats()
         self._err(lib().tgs_get_stats(self.h, C.byref(s)), "tgs_get_stats")
         return s.as_dict()
+
+    def set_comm(self, comm: Comm):
+        """C1 / C2 transport (tgs_set_comm); e.g. torch_comm()"""
+        self._comm = comm  # the callbacks must outlive the table
+        self._err(lib().tgs_set_comm(self.h, C.byref(comm)), "tgs_set_comm")
+
+    def global_stats(self) -> dict:
+        """C2: every rank's counters summed, as of the last step_adam"""
+        s = Stats()
+        self._err(lib().tgs_get_global_stats(self.h, C.byref(s)), "tgs_get_global_stats")
+        return s.as_dict()
+
+    def global_active(self, act: Activation):
+        """C1 result of `act` as a [G, C] uint32 numpy array (synchronising)"""
+        import torch
+        G = self.cfg.world_size
+        v = _device_view(torch, act.d_global_active, 4 * G * act.global_stride,
+                         torch.device("cuda", self.cfg.device))
+        torch.cuda.synchronize()
+        return v.cpu().numpy().view(np.uint32).reshape(G, act.global_stride)
 
     def stats_async(self, pinned_ptr):
         """Enqueue a D2H read of the counters into pinned host memory (no sync)."""

@@ -280,3 +280,25 @@ def test_churn_counters_consistent():
     mean_streak = st["n_resident"] / st["n_stage_in"]
     assert 0.8 <= mean_streak * ev_rate <= 1.2, (mean_streak, ev_rate)
     assert 0.8 <= 18.7 * 0.048 <= 1.2 and 0.8 <= 13.4 * 0.069 <= 1.2
+
+
+def test_consecutive_k_locality_counters():
+    """k_inter_sum / k_union_sum = sum over activates of |K_t n K_{t+1}| and
+    |K_t u K_{t+1}| (the consecutive-batch Jaccard the bench reports):
+    recomputed from the K lists; a repeated batch adds |K| to both (Jaccard 1),
+    an empty batch adds 0 and |K_t|."""
+    cfg, sc, tr = tiny()
+    o = O.Oracle(O.make_config(sc.N, sc.B, cfg.capacity), sc.bounds(), fill=None,
+                 track_all=False)
+    prev, inter, union = set(), 0, 0
+    batches = [tr.batch_planes(t, cfg.J) for t in range(10)]
+    batches += [batches[-1], np.zeros((0, 6, 4), np.float32), batches[3]]
+    for pl in batches:
+        assert o.activate(pl) == O.OK
+        K = set(o.list("K").tolist())
+        inter += len(prev & K)
+        union += len(prev | K)
+        st = o.stats()
+        assert (st["k_inter_sum"], st["k_union_sum"]) == (inter, union)
+        prev = K
+    assert 0 < inter < union

@@ -27,10 +27,51 @@ def _pad(x):
     return (x + PAGE - 1) // PAGE * PAGE
 
 
-def read_segments(d):
-    """R28 reader: {file_id: (kind, header fields, [(offset, gid, version, payload bytes)])}."""
+def _crc32c_table():
+    t = []
+    for i in range(256):
+        c = i
+        for _ in range(8):
+            c = (c >> 1) ^ (0x82F63B78 if c & 1 else 0)
+        t.append(c)
+    return t
+
+
+_CRC_T = _crc32c_table()
+
+
+def crc32c(data: bytes) -> int:
+    """CRC-32C (Castagnoli, reflected 0x82F63B78), table-driven; pinned below by
+    the standard check value of b"123456789"."""
+    c = 0xFFFFFFFF
+    for b in data:
+        c = (c >> 8) ^ _CRC_T[(c ^ b) & 0xFF]
+    return c ^ 0xFFFFFFFF
+
+
+def read_manifest(d):
+    """R30 barrier manifest: epoch, durable log end, base versions, step counters."""
+    raw = open(os.path.join(d, "manifest.tdgm"), "rb").read()
+    assert raw[:4] == b"TDGM" and int.from_bytes(raw[4:8], "little") == 1
+    K = int.from_bytes(raw[60:64], "little")
+    assert len(raw) == 64 + 12 * K + 4
+    assert int.from_bytes(raw[-4:], "little") == crc32c(raw[:-4])
+    return dict(epoch=int.from_bytes(raw[8:16], "little"),
+                last_file=int.from_bytes(raw[16:20], "little"),
+                end=int.from_bytes(raw[24:32], "little"), Kloc=K,
+                base_version=np.frombuffer(raw[64:64 + 8 * K], "<u8"),
+                step=np.frombuffer(raw[64 + 8 * K:64 + 12 * K], "<u4"))
+
+
+def read_segments(d, check_crc=2):
+    """R28 reader: {file_id: (kind, header fields, [(offset, gid, version, payload bytes)])};
+    the payload CRC-32C of the first check_crc records of the store is
+    recomputed here, every record's header CRC is."""
     out = {}
+    crc_left = [check_crc]
     for name in sorted(os.listdir(d)):
+        if name == "manifest.tdgm":
+            continue
         p = os.path.join(d, name)
         raw = open(p, "rb").read()
         magic = raw[:4]
@@ -45,9 +86,15 @@ def read_segments(d):
             off = PAGE
             while off < len(raw):
                 assert raw[off:off + 4] == b"TREC"
+                assert int.from_bytes(raw[off + 4:off + 8], "little") == 2
                 gid = int.from_bytes(raw[off + 8:off + 16], "little")
                 ver = int.from_bytes(raw[off + 16:off + 24], "little")
                 n = int.from_bytes(raw[off + 24:off + 32], "little")
+                assert int.from_bytes(raw[off + 36:off + 40], "little") == crc32c(raw[off:off + 36])
+                if crc_left[0] > 0:
+                    crc_left[0] -= 1
+                    assert (int.from_bytes(raw[off + 32:off + 36], "little")
+                            == crc32c(raw[off + PAGE:off + PAGE + n]))
                 recs.append((off + PAGE, gid, ver, n))
                 off += PAGE + _pad(n)
             assert off == len(raw)
@@ -430,3 +477,127 @@ def test_compaction_keeps_every_newest_version(tmp_path):
     assert 1 in segs
     for off, gid, ver, n in segs[1][2]:
         assert ver > idx[gid][3]
+
+
+def test_crc32c_check_value():
+    """R28 format 2 record checksum: CRC-32C's standard check value (the CRC of
+    b"123456789" is 0xE3069283) for both the oracle's and this file's CRC."""
+    assert O.crc32c(b"123456789") == crc32c(b"123456789") == 0xE3069283
+    assert O.crc32c(b"") == crc32c(b"") == 0
+    blob = bytes(range(256)) * 17
+    assert O.crc32c(blob) == crc32c(blob)
+
+
+def _session(d, sc, C, H, budget, batches, *, reopen=False, flush=True, o=None):
+    lr = lr_3dgs()
+    g = synth_grad(W.SEEDS["grads"], sc.N, sc.B)
+    grad = lambda k, t: g(k, 0)  # noqa: E731 -- independent of the session's batch counter
+    if o is None:
+        o = O.Oracle(O.make_config(sc.N, sc.B, C, moments=O.PERSIST), sc.bounds(),
+                     fill=None if reopen else sc.fill_fn, track_all=True)
+        (o.store_reopen if reopen else o.store_open)(d, H, budget)
+    for planes in batches:
+        assert o.activate(planes) == O.OK
+        assert o.list("K").size <= C  # A = K whatever the history (resume is exact)
+        o.step_adam(lr, grad=grad)
+    if flush:
+        o.flush()
+    return o
+
+
+def _boxes(sc, n, seed):
+    return [p for p in random_boxes(sc, 4 * n, seed=seed)][:n]
+
+
+def test_resume_continues_exactly_and_drops_post_barrier_appends(tmp_path):
+    """R30 resume = the barrier's state: a session that keeps
+    training after a barrier and dies without another one leaves later patch
+    records (dirty CPU-cache victims) behind; reopening recovers exactly the
+    barrier's Index, contents and Adam step counters (the manifest bounds the
+    log), removes the later records, and training resumed from there ends
+    bit-identical to a session that never stopped (persist policy)."""
+    cfg, sc, tr = tiny()
+    C, H = 16, 32
+    budget = PAGE + 6 * (PAGE + _pad(3 * sc.B * 59 * 4))
+    first, extra, rest = _boxes(sc, 18, 41), _boxes(sc, 8, 42), _boxes(sc, 10, 43)
+    a, b = tmp_path / "a", tmp_path / "b"
+    # uninterrupted: first, barrier, rest, barrier
+    oa = _session(a, sc, C, H, budget, first)
+    _session(a, sc, C, H, budget, rest, o=oa)
+    want = {k: oa.read_block(k) for k in range(sc.K)}
+    want_steps = {k: oa.step_count(k) for k in range(sc.K)}
+    # interrupted: first, barrier, extra (no barrier: appended victims only), "crash"
+    ob = _session(b, sc, C, H, budget, first)
+    at_barrier = {k: (ob.store_index(k), ob.read_block(k), ob.step_count(k)) for k in range(sc.K)}
+    man = read_manifest(b)
+    _session(b, sc, C, H, budget, extra, o=ob, flush=False)
+    appended = sum(len(r[2]) for f, r in read_segments(b).items() if f) - \
+        sum(len(r[2]) for f, r in read_segments(b).items() if f and f < man["last_file"])
+    assert ob.store_stats()["dirty_evictions"] > 0 and appended > 0
+    ob.close()
+    oc = O.Oracle(O.make_config(sc.N, sc.B, C, moments=O.PERSIST), sc.bounds(), fill=None,
+                  track_all=True)
+    oc.store_reopen(b, H, budget)
+    segs = read_segments(b)
+    assert max(segs) == man["last_file"]
+    if man["last_file"]:
+        assert os.path.getsize(b / f"patch-{man['last_file']:06d}.tdgp") == man["end"]
+    for k in range(sc.K):
+        ix, blk, stp = at_barrier[k]
+        assert oc.store_index(k) == ix, k
+        assert oc.step_count(k) == stp, k
+        for x, y in zip(oc.read_block(k), blk):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), k
+    _session(b, sc, C, H, budget, rest, o=oc)
+    for k in range(sc.K):
+        assert oc.step_count(k) == want_steps[k], k
+        for x, y in zip(oc.read_block(k), want[k]):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), k
+
+
+@pytest.mark.parametrize("where", ["payload", "header", "manifest"])
+def test_corruption_inside_the_barrier_is_refused(tmp_path, where):
+    """Every record up to the manifest's end was made durable at a barrier, so
+    a bad CRC-32C there (payload or header) is corruption, not a torn tail: the
+    resume refuses it, as it refuses a manifest that fails its own CRC."""
+    cfg, sc, tr = tiny()
+    C, H = 16, 32
+    budget = PAGE + 6 * (PAGE + _pad(3 * sc.B * 59 * 4))
+    o = _session(tmp_path, sc, C, H, budget, _boxes(sc, 14, 51))
+    o.close()
+    segs = read_segments(tmp_path)
+    fid = min(f for f in segs if f)
+    off = segs[fid][2][0][0]
+    path, pos = {"payload": (tmp_path / f"patch-{fid:06d}.tdgp", off + 1000),
+                 "header": (tmp_path / f"patch-{fid:06d}.tdgp", off - PAGE + 9),
+                 "manifest": (tmp_path / "manifest.tdgm", 70)}[where]
+    raw = bytearray(open(path, "rb").read())
+    raw[pos] ^= 0x40
+    open(path, "wb").write(bytes(raw))
+    r = O.Oracle(O.make_config(sc.N, sc.B, C, moments=O.PERSIST), sc.bounds(), fill=None,
+                 track_all=True)
+    with pytest.raises(O.OracleError):
+        r.store_reopen(tmp_path, H, budget)
+
+
+def test_compaction_then_resume_keeps_versions(tmp_path):
+    """R31 + R30: the manifest written by a compaction carries every block's
+    version, so a session resumed after it sees Index[k] = (0, base offset,
+    size, the version before compaction) and versions keep increasing."""
+    cfg, sc, tr = tiny()
+    C, H = 16, 32
+    S = _pad(3 * sc.B * 59 * 4)
+    budget = PAGE + 6 * (PAGE + S)
+    o = _session(tmp_path, sc, C, H, budget, _boxes(sc, 14, 61))
+    vers = {k: o.store_index(k)[3] for k in range(sc.K)}
+    assert max(vers.values()) > 0
+    o.store_compact()
+    m = read_manifest(tmp_path)
+    assert m["last_file"] == 0 and m["end"] == 0
+    assert [int(x) for x in m["base_version"]] == [vers[k] for k in range(sc.K)]
+    o.close()
+    r = O.Oracle(O.make_config(sc.N, sc.B, C, moments=O.PERSIST), sc.bounds(), fill=None,
+                 track_all=True)
+    r.store_reopen(tmp_path, H, budget)
+    for k in range(sc.K):
+        assert r.store_index(k) == (0, PAGE + k * S, 3 * sc.B * 59 * 4, vers[k]), k

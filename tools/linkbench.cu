@@ -1,176 +1,186 @@
-// linkbench.cu -- host<->device link microbenchmark for the a4 gather/write-back
-// design (copy engines vs SM zero-copy, 1-D vs pitched, one vs both directions).
+// linkbench.cu -- host<->device link microbenchmark for the a4 gather / write-back
+// design without batched copy submission: per-record copy-engine copies spread
+// over several streams, SM zero-copy gather/scatter kernels over a record list,
+// and one large contiguous copy (the write-back into a log-structured host tier),
+// each alone and with the opposite direction running concurrently.
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/linkbench tools/linkbench.cu
+#include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <vector>
-#include <cstdint>
-#include <algorithm>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
-__global__ void zc_copy(float4* __restrict__ dst, const float4* __restrict__ src, size_t n4) {
-  size_t stride = (size_t)gridDim.x * blockDim.x;
-  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n4; i += 4 * stride) {
-    float4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
-    dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
+// one CTA-stride loop over (record, float4) of a list of records: dst[i] <- src[list[i]]
+// (gather) or dst[list[i]] <- src[i] (scatter); 4 independent 16-B loads in flight per thread
+__global__ void zc_move(float4* __restrict__ dst, const float4* __restrict__ src,
+                        const uint32_t* __restrict__ list, uint32_t n, uint32_t rec4, int gather) {
+  const uint64_t total = (uint64_t)n * rec4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto at = [&](uint64_t e, bool is_src) -> uint64_t {
+    const uint64_t r = e / rec4, f = e - r * rec4;
+    const bool indirect = (gather != 0) == is_src;
+    return (indirect ? (uint64_t)list[r] : r) * rec4 + f;
+  };
+  for (; i + 3 * stride < total; i += 4 * stride) {
+    float4 a = __ldcs(src + at(i, true)), b = __ldcs(src + at(i + stride, true));
+    float4 c = __ldcs(src + at(i + 2 * stride, true)), d = __ldcs(src + at(i + 3 * stride, true));
+    __stcs(dst + at(i, false), a);
+    __stcs(dst + at(i + stride, false), b);
+    __stcs(dst + at(i + 2 * stride, false), c);
+    __stcs(dst + at(i + 3 * stride, false), d);
   }
-  for (; i < n4; i += stride) dst[i] = src[i];
+  for (; i < total; i += stride) __stcs(dst + at(i, false), __ldcs(src + at(i, true)));
+}
+
+__global__ void hbm_copy(float4* __restrict__ dst, const float4* __restrict__ src, size_t n4) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+    __stcs(dst + i, __ldcs(src + i));
 }
 
 static float ms_between(cudaEvent_t a, cudaEvent_t b) { float m; cudaEventElapsedTime(&m, a, b); return m; }
 
-int main() {
+int main(int argc, char** argv) {
   const size_t rec = 4096 * 59 * 4;  // 966,656 B
-  const int n = 370;
+  const int n = argc > 1 ? atoi(argv[1]) : 370;
   const size_t bytes = rec * n;
-  char *h_src, *h_dst;
-  CK(cudaHostAlloc((void**)&h_src, bytes * 3, cudaHostAllocMapped));
-  CK(cudaHostAlloc((void**)&h_dst, bytes * 3, cudaHostAllocMapped));
-  for (size_t i = 0; i < bytes * 3; i += 4096) h_src[i] = 1, h_dst[i] = 2;
-  char *d_a, *d_b;
-  CK(cudaMalloc(&d_a, bytes * 3));
-  CK(cudaMalloc(&d_b, bytes * 3));
-  cudaStream_t s1, s2, s3;
-  CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
-  cudaEvent_t e[8];
-  for (auto& x : e) CK(cudaEventCreate(&x));
-  char *hs_dev, *hd_dev;
-  CK(cudaHostGetDevicePointer((void**)&hs_dev, h_src, 0));
-  CK(cudaHostGetDevicePointer((void**)&hd_dev, h_dst, 0));
-
-  auto h2d_1d = [&](cudaStream_t s) { for (int i = 0; i < n; ++i) cudaMemcpyAsync(d_a + i * rec, h_src + i * rec, rec, cudaMemcpyHostToDevice, s); };
-  auto h2d_2d = [&](cudaStream_t s) { for (int i = 0; i < n; ++i) cudaMemcpy2DAsync(d_a + 3 * i * rec, 3 * rec, h_src + i * rec, rec, rec, 1, cudaMemcpyHostToDevice, s); };
-  auto h2d_one = [&](cudaStream_t s) { cudaMemcpyAsync(d_a, h_src, bytes, cudaMemcpyHostToDevice, s); };
-  auto d2h_1d = [&](cudaStream_t s) { for (int i = 0; i < n; ++i) cudaMemcpyAsync(h_dst + i * rec, d_b + i * rec, rec, cudaMemcpyDeviceToHost, s); };
-  auto d2h_one = [&](cudaStream_t s) { cudaMemcpyAsync(h_dst, d_b, bytes, cudaMemcpyDeviceToHost, s); };
-  auto zc_h2d = [&](cudaStream_t s, int g) { zc_copy<<<g, 512, 0, s>>>((float4*)d_a, (const float4*)hs_dev, bytes / 16); };
-  auto zc_d2h = [&](cudaStream_t s, int g) { zc_copy<<<g, 512, 0, s>>>((float4*)hd_dev, (const float4*)d_b, bytes / 16); };
-
-  auto one = [&](const char* name, auto f) {
-    for (int rep = 0; rep < 2; ++rep) {
-      CK(cudaDeviceSynchronize());
-      cudaEventRecord(e[0], s1);
-      f(s1);
-      cudaEventRecord(e[1], s1);
-      CK(cudaDeviceSynchronize());
-      if (rep) printf("%-34s %7.2f GB/s\n", name, bytes / (ms_between(e[0], e[1]) * 1e6));
-    }
-  };
-  auto two = [&](const char* name, auto f, auto g) {
-    for (int rep = 0; rep < 2; ++rep) {
-      CK(cudaDeviceSynchronize());
-      cudaEventRecord(e[0], s1);
-      cudaStreamWaitEvent(s2, e[0], 0);
-      f(s1);
-      g(s2);
-      cudaEventRecord(e[1], s1);
-      cudaEventRecord(e[2], s2);
-      CK(cudaDeviceSynchronize());
-      float a = ms_between(e[0], e[1]), b = ms_between(e[0], e[2]);
-      if (rep) printf("%-34s A %7.2f GB/s  B %7.2f GB/s  total %7.2f GB/s\n", name, bytes / (a * 1e6), bytes / (b * 1e6), 2 * bytes / (std::max(a, b) * 1e6));
-    }
-  };
-  one("h2d one copy", h2d_one);
-  one("h2d 370 x 1D", h2d_1d);
-  one("h2d 370 x 2D pitched", h2d_2d);
-  one("d2h one copy", d2h_one);
-  one("d2h 370 x 1D", d2h_1d);
-  for (int g : {16, 32, 64, 148, 296, 592}) {
-    char nm[64];
-    snprintf(nm, sizeof nm, "zero-copy h2d kernel grid %d", g);
-    one(nm, [&](cudaStream_t s) { zc_h2d(s, g); });
-    snprintf(nm, sizeof nm, "zero-copy d2h kernel grid %d", g);
-    one(nm, [&](cudaStream_t s) { zc_d2h(s, g); });
+  const size_t host_recs = 8192;     // 7.9 GB pinned host region, records scattered in it
+  char *h_tier;
+  CK(cudaHostAlloc((void**)&h_tier, rec * host_recs, cudaHostAllocMapped));
+  for (size_t i = 0; i < rec * host_recs; i += 4096) h_tier[i] = 1;
+  char *d_slots, *d_ring;
+  CK(cudaMalloc(&d_slots, bytes * 2));
+  CK(cudaMalloc(&d_ring, bytes));
+  CK(cudaMemset(d_slots, 0, bytes * 2));
+  CK(cudaMemset(d_ring, 0, bytes));
+  // S+ sources and write-back destinations: distinct random host records
+  std::vector<uint32_t> perm(host_recs);
+  for (size_t i = 0; i < host_recs; ++i) perm[i] = (uint32_t)i;
+  uint64_t st = 88172645463325252ull;
+  for (size_t i = host_recs - 1; i > 0; --i) {
+    st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+    std::swap(perm[i], perm[st % (i + 1)]);
   }
-  two("DMA h2d 1D || DMA d2h 1D", h2d_1d, d2h_1d);
-  two("DMA h2d 2D || DMA d2h 1D", h2d_2d, d2h_1d);
-  two("DMA h2d one || DMA d2h one", h2d_one, d2h_one);
-  two("DMA h2d || ZC d2h 148", h2d_1d, [&](cudaStream_t s) { zc_d2h(s, 148); });
-  two("ZC h2d 148 || DMA d2h", [&](cudaStream_t s) { zc_h2d(s, 148); }, d2h_1d);
-  two("ZC h2d 148 || ZC d2h 148", [&](cudaStream_t s) { zc_h2d(s, 148); }, [&](cudaStream_t s) { zc_d2h(s, 148); });
-  two("DMA h2d halves 2 streams (per-stream half bytes)", [&](cudaStream_t s) { for (int i = 0; i < n; i += 2) cudaMemcpyAsync(d_a + i * rec, h_src + i * rec, rec, cudaMemcpyHostToDevice, s); },
-      [&](cudaStream_t s) { for (int i = 1; i < n; i += 2) cudaMemcpyAsync(d_a + i * rec, h_src + i * rec, rec, cudaMemcpyHostToDevice, s); });
-  for (int L : {1, 2, 4, 8, 16, 37}) {
+  std::vector<uint32_t> src_l(perm.begin(), perm.begin() + n), dst_l(perm.begin() + n, perm.begin() + 2 * n);
+  const uint32_t run0 = perm[2 * n] % (uint32_t)(host_recs - n);  // contiguous append target
+  uint32_t *d_src_l, *d_dst_l;
+  CK(cudaMalloc(&d_src_l, n * 4));
+  CK(cudaMalloc(&d_dst_l, n * 4));
+  CK(cudaMemcpy(d_src_l, src_l.data(), n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_dst_l, dst_l.data(), n * 4, cudaMemcpyHostToDevice));
+  char* h_dev;
+  CK(cudaHostGetDevicePointer((void**)&h_dev, h_tier, 0));
+
+  const int NS = 8;
+  cudaStream_t hs[NS], ds[NS], fork, hb_s;
+  for (int i = 0; i < NS; ++i) {
+    CK(cudaStreamCreateWithFlags(&hs[i], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ds[i], cudaStreamNonBlocking));
+  }
+  CK(cudaStreamCreateWithFlags(&fork, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&hb_s, cudaStreamNonBlocking));
+  cudaEvent_t e0, eh[NS], ed[NS], ehb;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&ehb));
+  for (int i = 0; i < NS; ++i) { CK(cudaEventCreate(&eh[i])); CK(cudaEventCreate(&ed[i])); }
+
+  // H2D variants: per-record DMA over k streams, zero-copy gather with grid g
+  using Fn = std::function<void(void)>;
+  auto h2d_dma = [&](int k) -> Fn {
+    return [=, &src_l] { for (int i = 0; i < n; ++i) cudaMemcpyAsync(d_slots + i * rec, h_tier + (size_t)src_l[i] * rec, rec, cudaMemcpyHostToDevice, hs[i % k]); };
+  };
+  auto h2d_zc = [&](int g) -> Fn {
+    return [=] { zc_move<<<g, 512, 0, hs[0]>>>((float4*)d_slots, (const float4*)h_dev, d_src_l, n, rec / 16, 1); };
+  };
+  auto h2d_big = [&]() -> Fn { return [=] { cudaMemcpyAsync(d_slots, h_tier, bytes, cudaMemcpyHostToDevice, hs[0]); }; };
+  auto d2h_dma = [&](int k) -> Fn {
+    return [=, &dst_l] { for (int i = 0; i < n; ++i) cudaMemcpyAsync(h_tier + (size_t)dst_l[i] * rec, d_ring + i * rec, rec, cudaMemcpyDeviceToHost, ds[i % k]); };
+  };
+  auto d2h_zc = [&](int g) -> Fn {
+    return [=] { zc_move<<<g, 512, 0, ds[0]>>>((float4*)h_dev, (const float4*)d_ring, d_dst_l, n, rec / 16, 0); };
+  };
+  auto d2h_big = [&]() -> Fn { return [=] { cudaMemcpyAsync(h_tier + (size_t)run0 * rec, d_ring, bytes, cudaMemcpyDeviceToHost, ds[0]); }; };
+  auto d2h_big_k = [&](int k) -> Fn {  // the append split into k equal pieces on k streams
+    return [=] {
+      const size_t per = (size_t)(n + k - 1) / k;
+      for (int i = 0; i < k; ++i) {
+        const size_t a = i * per, b = std::min<size_t>(n, a + per);
+        if (a < b) cudaMemcpyAsync(h_tier + (run0 + a) * rec, d_ring + a * rec, (b - a) * rec, cudaMemcpyDeviceToHost, ds[i]);
+      }
+    };
+  };
+  const size_t hbm_bytes = (size_t)4 << 30;
+  char *x = nullptr, *y = nullptr;
+  CK(cudaMalloc(&x, hbm_bytes));
+  CK(cudaMalloc(&y, hbm_bytes));
+  CK(cudaMemset(x, 0, hbm_bytes));
+  auto hbm = [&](int reps) { for (int r = 0; r < reps; ++r) hbm_copy<<<148 * 4, 512, 0, hb_s>>>((float4*)y, (const float4*)x, hbm_bytes / 16); };
+
+  // run h (may be null) and d (may be null) concurrently, optionally with the HBM kernel
+  auto run = [&](const char* name, Fn h, Fn d, int hbm_reps = 0) {
+    for (int rep = 0; rep < 3; ++rep) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0, fork));
+      for (int i = 0; i < NS; ++i) { cudaStreamWaitEvent(hs[i], e0, 0); cudaStreamWaitEvent(ds[i], e0, 0); }
+      cudaStreamWaitEvent(hb_s, e0, 0);
+      if (hbm_reps) hbm(hbm_reps);
+      if (h) h();
+      if (d) d();
+      for (int i = 0; i < NS; ++i) { cudaEventRecord(eh[i], hs[i]); cudaEventRecord(ed[i], ds[i]); }
+      cudaEventRecord(ehb, hb_s);
+      CK(cudaDeviceSynchronize());
+      if (rep < 2) continue;
+      float th = 0, td = 0;
+      for (int i = 0; i < NS; ++i) { th = std::max(th, ms_between(e0, eh[i])); td = std::max(td, ms_between(e0, ed[i])); }
+      printf("%-46s", name);
+      if (h) printf(" h2d %6.2f", bytes / (th * 1e6));
+      if (d) printf(" d2h %6.2f", bytes / (td * 1e6));
+      if (h && d) printf(" sum %6.2f GB/s (both done %.3f ms)", 2 * bytes / (std::max(th, td) * 1e6), std::max(th, td));
+      else printf(" GB/s");
+      if (hbm_reps) printf("  | HBM kernel %.1f GB/s", hbm_reps * 2.0 * hbm_bytes / (ms_between(e0, ehb) * 1e6));
+      printf("\n");
+    }
+  };
+  printf("# %d records of %zu B, host records scattered over %zu pinned records\n", n, rec, host_recs);
+  run("HBM kernel alone", nullptr, nullptr, 4);
+  run("h2d one copy", h2d_big(), nullptr);
+  run("d2h one copy", nullptr, d2h_big());
+  run("h2d one || d2h one", h2d_big(), d2h_big());
+  for (int k : {1, 2, 4, 8}) {
     char nm[96];
-    snprintf(nm, sizeof nm, "runs of %d: DMA h2d || DMA d2h", L);
-    two(nm, [&](cudaStream_t s) { for (int i = 0; i < n; i += L) cudaMemcpyAsync(d_a + i * rec, h_src + i * rec, rec * std::min(L, n - i), cudaMemcpyHostToDevice, s); },
-        [&](cudaStream_t s) { for (int i = 0; i < n; i += L) cudaMemcpyAsync(h_dst + i * rec, d_b + i * rec, rec * std::min(L, n - i), cudaMemcpyDeviceToHost, s); });
+    snprintf(nm, sizeof nm, "h2d per-record DMA, %d streams", k);
+    run(nm, h2d_dma(k), nullptr);
+    snprintf(nm, sizeof nm, "d2h per-record DMA, %d streams", k);
+    run(nm, nullptr, d2h_dma(k));
+    snprintf(nm, sizeof nm, "h2d DMA %d st || d2h DMA %d st", k, k);
+    run(nm, h2d_dma(k), d2h_dma(k));
+    snprintf(nm, sizeof nm, "h2d DMA %d st || d2h one copy", k);
+    run(nm, h2d_dma(k), d2h_big());
+    snprintf(nm, sizeof nm, "h2d DMA %d st || d2h append in %d pieces", k, k);
+    run(nm, h2d_dma(k), d2h_big_k(k));
   }
-  // cudaMemcpyBatchAsync of 370 single records per direction
-  std::vector<void*> hd(n), hs(n), dd(n), ds(n);
-  std::vector<size_t> sz(n, rec);
-  for (int i = 0; i < n; ++i) { hd[i] = d_a + i * rec; hs[i] = h_src + i * rec; dd[i] = h_dst + i * rec; ds[i] = d_b + i * rec; }
-  cudaMemcpyAttributes at{};
-  at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t aidx = 0, fail = 0;
-  auto b_h2d = [&](cudaStream_t s) { CK(cudaMemcpyBatchAsync(hd.data(), hs.data(), sz.data(), n, &at, &aidx, 1, &fail, s)); };
-  auto b_d2h = [&](cudaStream_t s) { CK(cudaMemcpyBatchAsync(dd.data(), ds.data(), sz.data(), n, &at, &aidx, 1, &fail, s)); };
-  one("batch h2d 370", b_h2d);
-  one("batch d2h 370", b_d2h);
-  two("batch h2d || batch d2h", b_h2d, b_d2h);
-  at.flags = 0;
-  one("batch(noflag) h2d 370", b_h2d);
-  two("batch(noflag) h2d || d2h", b_h2d, b_d2h);
-
-  // (1) the same batches while an HBM-saturating kernel runs on a third stream
-  const size_t hb = (size_t)8 << 30;
-  char *x, *y;
-  CK(cudaMalloc(&x, hb));
-  CK(cudaMalloc(&y, hb));
-  auto hbm = [&](cudaStream_t s) { for (int r = 0; r < 6; ++r) zc_copy<<<148 * 4, 512, 0, s>>>((float4*)y, (const float4*)x, hb / 16); };
-  {
-    CK(cudaDeviceSynchronize());
-    cudaEventRecord(e[0], s3);
-    hbm(s3);
-    cudaEventRecord(e[1], s3);
-    CK(cudaDeviceSynchronize());
-    printf("%-34s %7.1f GB/s (r+w)\n", "HBM copy kernel alone", 6 * 2.0 * hb / (ms_between(e[0], e[1]) * 1e6));
-    for (int rep = 0; rep < 2; ++rep) {
-      CK(cudaDeviceSynchronize());
-      cudaEventRecord(e[0], s3);
-      cudaStreamWaitEvent(s1, e[0], 0);
-      cudaStreamWaitEvent(s2, e[0], 0);
-      hbm(s3);
-      b_h2d(s1);
-      b_d2h(s2);
-      cudaEventRecord(e[1], s1);
-      cudaEventRecord(e[2], s2);
-      cudaEventRecord(e[3], s3);
-      CK(cudaDeviceSynchronize());
-      if (rep) printf("%-34s h2d %6.2f d2h %6.2f GB/s, HBM kernel %.2f ms\n", "batch || batch || HBM kernel",
-                      bytes / (ms_between(e[0], e[1]) * 1e6), bytes / (ms_between(e[0], e[2]) * 1e6), ms_between(e[0], e[3]));
-    }
+  for (int g : {4, 8, 16, 32, 148}) {
+    char nm[96];
+    snprintf(nm, sizeof nm, "h2d ZC gather grid %d", g);
+    run(nm, h2d_zc(g), nullptr);
+    snprintf(nm, sizeof nm, "d2h ZC scatter grid %d", g);
+    run(nm, nullptr, d2h_zc(g));
+    snprintf(nm, sizeof nm, "h2d ZC %d || d2h one copy", g);
+    run(nm, h2d_zc(g), d2h_big());
+    snprintf(nm, sizeof nm, "h2d ZC %d || d2h ZC %d", g, g);
+    run(nm, h2d_zc(g), d2h_zc(g));
+    snprintf(nm, sizeof nm, "h2d ZC %d || d2h DMA 4 st", g);
+    run(nm, h2d_zc(g), d2h_dma(4));
   }
-  CK(cudaFree(x));
-  CK(cudaFree(y));
-  // (2) records scattered over a large pinned host region (host-tier-like)
-  const size_t big = (size_t)64 << 30;
-  char* hbig;
-  if (cudaHostAlloc((void**)&hbig, big, cudaHostAllocDefault) == cudaSuccess) {
-    for (size_t i = 0; i < big; i += 4096) hbig[i] = 0;
-    const size_t nrec = big / rec;
-    std::vector<void*> bs(n), bd(n);
-    uint64_t st = 88172645463325252ull;
-    for (int i = 0; i < n; ++i) {
-      st ^= st << 13; st ^= st >> 7; st ^= st << 17;
-      char* r = hbig + (st % nrec) * rec;
-      bs[i] = r;
-      bd[i] = r;
-    }
-    auto s_h2d = [&](cudaStream_t s) { CK(cudaMemcpyBatchAsync(hd.data(), bs.data(), sz.data(), n, &at, &aidx, 1, &fail, s)); };
-    auto s_d2h = [&](cudaStream_t s) { CK(cudaMemcpyBatchAsync(bd.data(), ds.data(), sz.data(), n, &at, &aidx, 1, &fail, s)); };
-    one("scattered-64GB batch h2d", s_h2d);
-    one("scattered-64GB batch d2h", s_d2h);
-    two("scattered-64GB batch h2d || d2h", s_h2d, s_d2h);
-    cudaFreeHost(hbig);
-  } else {
-    printf("64 GB pinned alloc failed\n");
-  }
+  // contention with an HBM-bound kernel (Adam stand-in)
+  run("h2d DMA 4 st || d2h one copy || HBM", h2d_dma(4), d2h_big(), 4);
+  run("h2d ZC 16 || d2h one copy || HBM", h2d_zc(16), d2h_big(), 4);
+  run("h2d ZC 16 || d2h ZC 16 || HBM", h2d_zc(16), d2h_zc(16), 4);
+  run("h2d DMA 4 st || d2h DMA 4 st || HBM", h2d_dma(4), d2h_dma(4), 4);
   return 0;
 }
