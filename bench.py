@@ -84,6 +84,8 @@ def parse():
                     help="override the config's capacity C (blocks, world size 1; C_g = ceil(C/G))")
     ap.add_argument("--pool-slots", type=int, default=0,
                     help="device slot pool P per GPU (0 -> 2 C_g, R13)")
+    ap.add_argument("--no-persist-detail", action="store_true",
+                    help="skip the 100m persist measurement the default run adds (detail.persist)")
     ap.add_argument("--io-threads", type=int, default=0,
                     help="parallel SSD requests of the --store tier (0 -> library default)")
     return ap.parse_args()
@@ -410,13 +412,47 @@ def main():
         run_reference(args, ws, rank)
         return
     import torch
-    import paper_2605_20150_b200 as P
-    from paper_2605_20150_b200 import tidegs as T
-
     if os.environ.get("TGS_BENCH_BACKEND") == "gloo":
         local = 0  # every rank on cuda:0 (functional multi-rank run on one GPU)
     torch.cuda.set_device(local)
+    line = measure(args, ws, rank, local)
+    if persist_detail_wanted(args, ws):
+        # the north-star persist policy (moments gathered and scattered with theta)
+        # on the largest config whose persist host tier fits this box: 100m
+        import copy
+        a2 = copy.copy(args)
+        a2.config, a2.moments, a2.no_cpu_baseline, a2.capacity = "100m", "persist", True, 0
+        l2 = measure(a2, ws, rank, local)
+        if rank == 0:
+            line["detail"]["persist"] = {
+                k: l2[k] for k in ("value", "unit", "ms_per_step", "config", "e2e", "roofline",
+                                   "link_roofline", "gpu_launches", "clocks")}
+            line["detail"]["persist"]["detail"] = {
+                k: l2["detail"][k] for k in ("active_blocks_per_step", "stage_in_blocks_per_step",
+                                             "h2d_GB_per_step", "d2h_GB_per_step", "churn",
+                                             "locality", "step_ms")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def persist_detail_wanted(args, ws):
+    """the default invocation (300m cold, N = 1) also measures 100m persist"""
+    return (ws == 1 and args.config == "300m" and args.moments == "cold" and not args.shard_of
+            and not args.store and not args.capacity and not args.no_persist_detail
+            and not (args.no_tide or args.no_overlap or args.fine_filter or args.refresh_bounds))
+
+
+def measure(args, ws, rank, local):
+    """One table of args.config through the timed window; rank 0 gets the JSON
+    line (dict), the other ranks None.  Frees the table before returning."""
+    import torch
+    import paper_2605_20150_b200 as P  # noqa: F401
+    from paper_2605_20150_b200 import tidegs as T
+
     dev = torch.device("cuda", local)
+    line = None
     wl = _workload(args)
     sc = wl.scene()
     tr = wl.trajectory(sc)
@@ -432,7 +468,8 @@ def main():
     cfg = T.make_config(sc.N, sc.B, cap, pool_slots=args.pool_slots, moments=moments, world_size=shard_ws, rank=shard_rank,
                         device=local, tide=0 if args.no_tide else 1,
                         serialize=1 if args.no_overlap else 0,
-                        refresh_bounds=1 if args.refresh_bounds else 0)
+                        refresh_bounds=1 if args.refresh_bounds else 0,
+                        level2=1 if args.fine_filter else 0)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
     build_ms = None
@@ -676,13 +713,14 @@ def main():
                            "setup_s": setup_s, "layout_build_gpu_ms": build_ms,
                            "view_order_gpu_ms": order_ms,
                            "store": store_detail}}
-        print(json.dumps(line), flush=True)
     table.close()
+    del table
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     if store and os.environ.get("TGS_KEEP_STORE") != "1":
         import shutil
         shutil.rmtree(store["dir"], ignore_errors=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
+    return line
 
 
 if __name__ == "__main__":

@@ -81,6 +81,11 @@ typedef struct {
                              Gaussian of the block; the cull of batch t+2 sees it  */
   int32_t serialize;      /* ablation "w/o Overlap": activate returns
                              after its gather and write-back, step_adam after Adam  */
+  int32_t level2;         /* NEXT f1: keep a 16-B extent sphere per resident row
+                             (derived by the gather, updated by k_adam) so that
+                             tgs_fine_filter reads 16 B per row instead of theta;
+                             implied by refresh_bounds (whose per-row radius k_adam
+                             then computes in its epilogue)                      */
 } tgs_config;
 
 /* Optional device allocator hooks (PyTorch's caching allocator from Python).

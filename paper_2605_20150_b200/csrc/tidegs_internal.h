@@ -8,6 +8,7 @@
 namespace tgs {
 
 constexpr uint32_t kDim = 59;
+constexpr int kRings = 3;                  // write-back ring slots (activate T uses T % 3)
 constexpr uint32_t kMaxCams = 256;
 constexpr uint32_t kMaxAge = 1023;
 constexpr uint32_t kMaxBuckets = 2 * 2 * (kMaxAge + 2);  // rank x (in R_t ? 0 : 1)
@@ -75,14 +76,16 @@ struct Dev {
   PlanHdr* hdr_map;      // device alias of the mapped host header
   uint32_t* sp_map;      // mapped host [C][2] (local id, slot) of S+
   uint32_t* sm_map;      // mapped host [C] S- local ids (store mode only, else nullptr)
-  uint32_t* dirty_map[2];  // mapped host [C][2] (local id, slot) of dirty S- (parity)
-  uint32_t* ndirty_map;    // mapped host [2] |dirty S-| (parity)
-  uint32_t* ndirty_dev;    // [2] |dirty S-| (parity), read by k_pack
-  uint32_t* dl_slot;     // [C] device copy of the dirty S- slots (pack source)
-  uint32_t* dl_blk;      // [C] device copy of the dirty S- local ids (write-back destination)
+  // write-back state of activate T lives in ring slot T % kRings: the scatter of
+  // T may still read it while the next two activates write theirs
+  uint32_t* dirty_map[3];  // mapped host [C][2] (local id, slot) of dirty S- (ring slot)
+  uint32_t* ndirty_map;    // mapped host [3] |dirty S-| (ring slot)
+  uint32_t* ndirty_dev;    // [3] |dirty S-| (ring slot), read by k_pack and k_xfer
+  uint32_t* dl_slot[3];  // [C] dirty S- slots (pack / direct write-back source)
+  uint32_t* dl_blk[3];   // [C] dirty S- local ids (write-back destination)
   int32_t* wb_tag;       // [Kloc] activate index at which the block was packed (-1 never)
   uint32_t* wb_idx;      // [Kloc] its staging-ring index then
-  float* staging[2];     // [S_max][n_arr][B][59] write-back staging ring (parity)
+  float* staging[3];     // [S_max][n_arr][B][59] write-back staging rings (ring slot)
   uint32_t S_max;        // staging capacity in records
   float4* last_planes[2];  // [kMaxCams*6] camera batch of the activate of that parity
   const float4* planes_map[2];  // mapped pinned host staging of the camera batch (parity)
@@ -100,6 +103,11 @@ struct Dev {
   uint64_t host_stride;     // bytes between host records (n_arr*B*236, or the padded entry size)
   int32_t* ent_of;          // [Kloc] store tier: cache entry of each resident block (else nullptr)
   const uint32_t* sp_entry; // mapped host [C] store tier: cache entry of S+ block i (host-written)
+  // f1 / f2 (cfg.level2 or cfg.refresh_bounds): per slot row, the extent sphere
+  // (mu, 3 exp(max log-scale)) of its current theta -- written by the gather
+  // for admitted rows and by k_adam for updated rows; read by k_fine and by the
+  // bound refresh folded into k_adam (R24, R25).  nullptr when off.
+  float4* sphere;        // [P][B]
   // pools
   float* params;         // [P][3][B][59]
   float* grads;          // [P][B][59]
@@ -114,16 +122,16 @@ struct AdamHyper {
 cudaError_t launch_cull(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s);
 cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s);
-cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
-cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s);
-cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t T, bool tag,
-                                cudaStream_t s);
+cudaError_t launch_pack(const Dev& d, uint32_t nSm, int ring, cudaStream_t s);
+cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int ring, int32_t T,
+                                bool tag, cudaStream_t s);
 // a4 transfers (XferMode in tidegs_kernels.cu): 0 gather S+ (sel/n_sel: a host-
 // selected subset, else all of hdr_dev->nSp), 1 scatter the ring, 2 scatter from
 // the slots; n_hint > 0 is an upper bound of the records (sizes the grid);
 // ctas CTAs of one warp, bufs 32 KB shared-memory buffers each (bufs-1 loads in flight)
-cudaError_t launch_xfer(const Dev& d, int mode, int parity, int32_t T, const uint32_t* sel,
-                        uint32_t n_sel, uint32_t n_hint, int ctas, int bufs, cudaStream_t s);
+cudaError_t launch_xfer(const Dev& d, int mode, int parity, int ring, int32_t T,
+                        const uint32_t* sel, uint32_t n_sel, uint32_t n_hint, int ctas, int bufs,
+                        cudaStream_t s);
 cudaError_t launch_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C, cudaStream_t s);
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s);
@@ -131,7 +139,6 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s);
 cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
                         cudaStream_t s);
-cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s);
 int adam_grid(int device);
 
 // NEXT f2b: Morton sort + blocking

@@ -231,26 +231,28 @@ __global__ void __launch_bounds__(256) k_cull(Dev d, uint32_t J, int32_t T, int 
 }
 
 // ------------------------------------------------------ a3 camera quota (R10)
-constexpr int kQuotaNT = 512;
-__global__ void __launch_bounds__(kQuotaNT) k_quota(Dev d, uint32_t J, int32_t T, int parity) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_quota(Dev d, uint32_t J, int32_t T, int parity) {
   __shared__ uint32_t hist[kMaxBuckets];
   __shared__ uint32_t sh[40];
   if (d.cnt[CNT_CAND] <= d.C) return;  // #C_t <= C: nothing to select
   const uint32_t j = blockIdx.x;
   const uint32_t* pc = d.percam[parity] + (size_t)j * d.W;
   uint32_t mine = 0;
-  for (uint32_t w = threadIdx.x; w < d.W; w += kQuotaNT) mine += __popc(pc[w]);
-  const uint32_t nj = block_sum<kQuotaNT>(mine, sh);
+  for (uint32_t w = threadIdx.x; w < d.W; w += NT) mine += __popc(pc[w]);
+  const uint32_t nj = block_sum<NT>(mine, sh);
   const uint64_t q = ((uint64_t)d.C * d.quota_num) / ((uint64_t)d.quota_den * J);
   const uint32_t qj = (uint32_t)(nj < q ? nj : q);
-  select_top<kQuotaNT>(
+  select_top<NT>(
       d, qj, d.W, T, hist, sh, [&](uint32_t w) { return pc[w]; }, d.R[parity], true,
       [&](uint32_t w, uint32_t bits) { atomicOr(&d.Q[w], bits); });
 }
 
 // ------------------------------------- a2 + a3 fill, delta, slots, A list
-constexpr int kPlanNT = 1024;
-__global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) {
+// NT = 256 for bitsets of <= 1024 words (fits beside a running k_adam, whose
+// CTAs leave too few registers for a 1024-thread CTA), 1024 above
+template <int NT>
+__global__ void __launch_bounds__(NT) k_plan(Dev d, int32_t T, int parity) {
   __shared__ uint32_t hist[kMaxBuckets];
   __shared__ uint32_t sh[40];
   __shared__ unsigned long long acc[4];
@@ -263,17 +265,17 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
 
   // ---- Alg. 1 l.6: R_{t+1} = CameraBalancedTopC(...)
   if (n_cand <= d.C) {
-    for (uint32_t w = tid; w < W; w += kPlanNT) Rn[w] = d.cand[w];
+    for (uint32_t w = tid; w < W; w += NT) Rn[w] = d.cand[w];
   } else {
     uint32_t mine = 0;
-    for (uint32_t w = tid; w < W; w += kPlanNT) {
+    for (uint32_t w = tid; w < W; w += NT) {
       const uint32_t q = d.Q[w];
       Rn[w] = q;
       mine += __popc(q);
     }
-    const uint32_t nQ = block_sum<kPlanNT>(mine, sh);
+    const uint32_t nQ = block_sum<NT>(mine, sh);
     const uint32_t nfill = d.C - nQ;
-    select_top<kPlanNT>(
+    select_top<NT>(
         d, nfill, W, T, hist, sh, [&](uint32_t w) { return d.cand[w] & ~d.Q[w]; }, R, false,
         [&](uint32_t w, uint32_t bits) { Rn[w] |= bits; });
   }
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
 
   // ---- Alg. 1 l.7-8: Omega, S+, S-; A = R_{t+1} n K_{t+1}
   uint32_t nR_mine = 0, nOm_mine = 0;
-  for (uint32_t w = tid; w < W; w += kPlanNT) {
+  for (uint32_t w = tid; w < W; w += NT) {
     const uint32_t r = R[w], rn = Rn[w];
     const uint32_t sp = d.tide ? (rn & ~r) : rn;
     const uint32_t sm = d.tide ? (r & ~rn) : r;
@@ -293,8 +295,8 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
     nR_mine += __popc(rn);
     nOm_mine += __popc(om);
   }
-  const uint32_t nR = block_sum<kPlanNT>(nR_mine, sh);
-  const uint32_t nOm = block_sum<kPlanNT>(nOm_mine, sh);
+  const uint32_t nR = block_sum<NT>(nR_mine, sh);
+  const uint32_t nOm = block_sum<NT>(nOm_mine, sh);
 
   // ---- compaction of S+ and S- (ascending ids) by prefix sums
   uint32_t* smb = d.sm_blk[parity];
@@ -302,12 +304,12 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
   uint32_t* spb = d.sp_blk[parity];
   uint32_t* sps = d.sp_slot[parity];
   uint32_t cSp = 0, cSm = 0;
-  for (uint32_t base = 0; base < W; base += kPlanNT) {
+  for (uint32_t base = 0; base < W; base += NT) {
     const uint32_t w = base + tid;
     uint32_t sp = w < W ? d.Sp[w] : 0u, sm = w < W ? d.Sm[w] : 0u;
     uint32_t tp, tm;
-    uint32_t op = cSp + block_scan<kPlanNT>(__popc(sp), tp, sh);
-    uint32_t om = cSm + block_scan<kPlanNT>(__popc(sm), tm, sh);
+    uint32_t op = cSp + block_scan<NT>(__popc(sp), tp, sh);
+    uint32_t om = cSm + block_scan<NT>(__popc(sm), tm, sh);
     while (sp) {
       const int b = __ffs(sp) - 1;
       sp &= sp - 1;
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
   // ---- slot allocation (R13): the i-th S+ block takes the i-th lowest slot not
   //      held by R_t; if short, the slots S- releases, ascending.
   uint32_t nfree = 0;
-  for (uint32_t base = 0; base < d.PW; base += kPlanNT) {
+  for (uint32_t base = 0; base < d.PW; base += NT) {
     const uint32_t w = base + tid;
     uint32_t fr = 0;
     if (w < d.PW) {
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
       fr = ~d.occ[w] & valid;
     }
     uint32_t tot;
-    uint32_t r = nfree + block_scan<kPlanNT>(__popc(fr), tot, sh);
+    uint32_t r = nfree + block_scan<NT>(__popc(fr), tot, sh);
     while (fr && r < nSp) {
       const int b = __ffs(fr) - 1;
       fr &= fr - 1;
@@ -348,16 +350,16 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
   }
   const uint32_t fallback = nfree < nSp ? 1u : 0u;
   if (fallback) {
-    for (uint32_t w = tid; w < d.PW; w += kPlanNT) d.rel[w] = 0u;
+    for (uint32_t w = tid; w < d.PW; w += NT) d.rel[w] = 0u;
     __syncthreads();
-    for (uint32_t i = tid; i < nSm; i += kPlanNT) atomicOr(&d.rel[sms[i] >> 5], 1u << (sms[i] & 31));
+    for (uint32_t i = tid; i < nSm; i += NT) atomicOr(&d.rel[sms[i] >> 5], 1u << (sms[i] & 31));
     __syncthreads();
     uint32_t c = 0;
-    for (uint32_t base = 0; base < d.PW; base += kPlanNT) {
+    for (uint32_t base = 0; base < d.PW; base += NT) {
       const uint32_t w = base + tid;
       uint32_t fr = w < d.PW ? d.rel[w] : 0u;
       uint32_t tot;
-      uint32_t r = nfree + c + block_scan<kPlanNT>(__popc(fr), tot, sh);
+      uint32_t r = nfree + c + block_scan<NT>(__popc(fr), tot, sh);
       while (fr && r < nSp) {
         const int b = __ffs(fr) - 1;
         fr &= fr - 1;
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
 
   // ---- eviction bookkeeping (stage 4; dirty write-back decided after Adam(t))
   unsigned long long streak = 0;
-  for (uint32_t i = tid; i < nSm; i += kPlanNT) {
+  for (uint32_t i = tid; i < nSm; i += NT) {
     const uint32_t l = smb[i], s = sms[i];
     if (d.sm_map) d.sm_map[i] = l;  // f3: the host touches the CPU-cache entries of S-
     d.b2s[l] = -1;
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
   __syncthreads();
   // ---- admission bookkeeping (stage 2); cold restart resets the step
   unsigned long long readmit = 0;
-  for (uint32_t i = tid; i < nSp; i += kPlanNT) {
+  for (uint32_t i = tid; i < nSp; i += NT) {
     const uint32_t l = spb[i], s = sps[i];
     d.b2s[l] = (int32_t)s;
     d.s2b[s] = (int32_t)l;
@@ -402,11 +404,11 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
   uint32_t* as = d.a_slot[parity];
   uint32_t* ag = d.a_gid[parity];
   uint32_t cA = 0;
-  for (uint32_t base = 0; base < W; base += kPlanNT) {
+  for (uint32_t base = 0; base < W; base += NT) {
     const uint32_t w = base + tid;
     uint32_t a = w < W ? d.Ab[w] : 0u;
     uint32_t tot;
-    uint32_t o = cA + block_scan<kPlanNT>(__popc(a), tot, sh);
+    uint32_t o = cA + block_scan<NT>(__popc(a), tot, sh);
     while (a) {
       const int b = __ffs(a) - 1;
       a &= a - 1;
@@ -448,14 +450,14 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(Dev d, int32_t T, int parity) 
 }
 
 // ---------------------------------------- a4 dirty S- -> write-back list
-constexpr int kEvictNT = 1024;
-__global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int parity, int32_t T,
-                                                    int tag) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_evict(Dev d, uint32_t nSm, int parity, int ring,
+                                              int32_t T, int tag) {
   __shared__ uint32_t sh[40];
   const uint32_t* smb = d.sm_blk[parity];
   const uint32_t* sms = d.sm_slot[parity];
   uint32_t c = 0;
-  for (uint32_t base = 0; base < nSm; base += kEvictNT) {
+  for (uint32_t base = 0; base < nSm; base += NT) {
     const uint32_t i = base + threadIdx.x;
     uint32_t dirty = 0, l = 0, s = 0;
     if (i < nSm) {
@@ -465,13 +467,13 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
       dirty = (d.dirty[s >> 5] >> (s & 31)) & 1u;  // dirty only if updated
     }
     uint32_t tot;
-    const uint32_t o = c + block_scan<kEvictNT>(dirty, tot, sh);
+    const uint32_t o = c + block_scan<NT>(dirty, tot, sh);
     if (dirty) {
-      d.dirty_map[parity][2 * o] = l;
-      d.dirty_map[parity][2 * o + 1] = s;
-      d.dl_slot[o] = s;
-      d.dl_blk[o] = l;
-      if (tag) {  // packed into staging[parity][o]: a re-admission next batch reads it there
+      d.dirty_map[ring][2 * o] = l;
+      d.dirty_map[ring][2 * o + 1] = s;
+      d.dl_slot[ring][o] = s;
+      d.dl_blk[ring][o] = l;
+      if (tag) {  // packed into staging[ring][o]: a re-admission within two batches reads it there
         d.wb_tag[l] = T;
         d.wb_idx[l] = o;
       }
@@ -480,38 +482,78 @@ __global__ void __launch_bounds__(kEvictNT) k_evict(Dev d, uint32_t nSm, int par
     c += tot;
   }
   if (threadIdx.x == 0) {
-    d.ndirty_map[parity] = c;
-    d.ndirty_dev[parity] = c;
+    d.ndirty_map[ring] = c;
+    d.ndirty_dev[ring] = c;
     atomicAdd(&d.stats[ST_EVICT_DIRTY], (unsigned long long)c);
     atomicAdd(&d.stats[ST_D2H], (unsigned long long)c * d.rec_floats * 4ull * d.n_arr);
   }
 }
 
 // ------------------- a4 pack: dirty S- records -> write-back staging ring
-// grid (chunks, nSm); entry i < n_dirty copies its slot's theta (| m | v when
-// moments persist) into staging[parity][i] with 128-bit streaming loads and
-// stores, so the slot is free for the next gather as soon as this kernel ends
-// and the copy engine drains the staging ring to the host tier meanwhile.
-__global__ void __launch_bounds__(256, 6) k_pack(Dev d, int parity) {
-  const uint32_t i = blockIdx.y;
-  if (i >= d.ndirty_dev[parity]) return;
-  const uint32_t s = d.dl_slot[i];
+// grid (chunks, min(n_dirty, 65535)); entry i < n_dirty copies its slot's theta
+// (| m | v when moments persist) into staging[ring][i] with 128-bit streaming
+// loads and stores, so the slot is free for the next gather as soon as this
+// kernel ends while k_xfer drains the ring to the host tier.
+__global__ void __launch_bounds__(256, 6) k_pack(Dev d, int ring) {
+  const uint32_t nd = d.ndirty_dev[ring];
   const size_t n4 = (size_t)d.n_arr * d.rec_floats / 4;
-  const float4* src = reinterpret_cast<const float4*>(d.params + (size_t)s * 3 * d.rec_floats);
-  float4* dst = reinterpret_cast<float4*>(d.staging[parity] + (size_t)i * d.n_arr * d.rec_floats);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t i = blockIdx.y; i < nd; i += gridDim.y) {  // grid.y is capped at 65535
+    const uint32_t s = d.dl_slot[ring][i];
+    const float4* src = reinterpret_cast<const float4*>(d.params + (size_t)s * 3 * d.rec_floats);
+    float4* dst = reinterpret_cast<float4*>(d.staging[ring] + (size_t)i * d.n_arr * d.rec_floats);
+    size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
 #pragma unroll 1
-  for (; e + 3 * stride < n4; e += 4 * stride) {  // 4 independent 16 B loads in flight
-    const float4 a = __ldcs(src + e), b = __ldcs(src + e + stride);
-    const float4 c = __ldcs(src + e + 2 * stride), f = __ldcs(src + e + 3 * stride);
-    __stcs(dst + e, a);
-    __stcs(dst + e + stride, b);
-    __stcs(dst + e + 2 * stride, c);
-    __stcs(dst + e + 3 * stride, f);
+    for (; e + 3 * stride < n4; e += 4 * stride) {  // 4 independent 16 B loads in flight
+      const float4 a = __ldcs(src + e), b = __ldcs(src + e + stride);
+      const float4 c = __ldcs(src + e + 2 * stride), f = __ldcs(src + e + 3 * stride);
+      __stcs(dst + e, a);
+      __stcs(dst + e + stride, b);
+      __stcs(dst + e + 2 * stride, c);
+      __stcs(dst + e + 3 * stride, f);
+    }
+#pragma unroll 1
+    for (; e < n4; e += stride) __stcs(dst + e, __ldcs(src + e));
   }
-#pragma unroll 1
-  for (; e < n4; e += stride) __stcs(dst + e, __ldcs(src + e));
+}
+
+// R24 deterministic exp: k = rint(x log2 e) by the 1.5*2^23 trick, two-step
+// Cody-Waite reduction, degree-7 Taylor polynomial by fma Horner, exact 2^k.
+__device__ __forceinline__ float exp_det(float x) {
+  if (x > 80.0f) x = 80.0f;
+  if (x < -80.0f) x = -80.0f;
+  const float t = __fmaf_rn(x, 1.44269504088896341f, 12582912.0f);
+  const float kf = __fsub_rn(t, 12582912.0f);
+  float r = __fmaf_rn(kf, -0.693145751953125f, x);
+  r = __fmaf_rn(kf, -1.428606765330187045e-06f, r);
+  float p = 1.98412698412698413e-04f;
+  p = __fmaf_rn(p, r, 1.38888888888888889e-03f);
+  p = __fmaf_rn(p, r, 8.33333333333333333e-03f);
+  p = __fmaf_rn(p, r, 4.16666666666666667e-02f);
+  p = __fmaf_rn(p, r, 1.66666666666666667e-01f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  const int k = (int)kf;
+  return __fmul_rn(p, __int_as_float((k + 127) << 23));
+}
+
+
+// f1 / f2 per-row extent sphere (R24, R25): centre mu = attrs 0..2, extent
+// 3 (x) exp_det(max of the log-scales 52..54), in the order both filters use
+__device__ __forceinline__ float4 row_sphere(float x, float y, float z, float s0, float s1,
+                                             float s2) {
+  float sc = s0;
+  if (s1 > sc) sc = s1;
+  if (s2 > sc) sc = s2;
+  return make_float4(x, y, z, __fmul_rn(3.0f, exp_det(sc)));
+}
+
+// R25 refreshed radius of a row around the fixed centre c_k, as fp32 bits
+__device__ __forceinline__ uint32_t refresh_bits(const float4& sp, const float4& c) {
+  const float dx = __fsub_rn(sp.x, c.x), dy = __fsub_rn(sp.y, c.y), dz = __fsub_rn(sp.z, c.z);
+  const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+  return __float_as_uint(__fmul_rn(__fadd_rn(__fsqrt_rn(d2), sp.w), 1.0000019073486328f));
 }
 
 // ------------------------- a4 record transfer over the host link (TMA)
@@ -534,52 +576,68 @@ __global__ void __launch_bounds__(256, 6) k_pack(Dev d, int parity) {
 // XFER_SCATTER  dirty record i < ndirty of this activate: write-back ring
 //               (ring mode) or its slot (direct mode) -> host record of l
 //               (flat: l * host_stride; store: entry ent_of[l]).
-constexpr uint32_t kXferChunk = 32768, kXferMaxBufs = 6;
+// A chunk is 128 whole rows (30,208 B = 32 x 944 B): a gather chunk of theta
+// rows is complete in shared memory when its mbarrier fires, so with the f1/f2
+// sphere array on (d.sphere) the CTA's 32 lanes derive each admitted row's
+// extent sphere from it there (R24) -- 16 B per row written, nothing re-read.
+constexpr uint32_t kXferChunk = 128 * kDim * 4, kXferMaxBufs = 7;
 enum XferMode : int { XFER_GATHER = 0, XFER_SCATTER_RING = 1, XFER_SCATTER_DIRECT = 2 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* ptr) {
   return (uint32_t)__cvta_generic_to_shared(ptr);
 }
 
-__global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int32_t T,
+__global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ring, int32_t T,
                                              const uint32_t* __restrict__ sel, uint32_t n_sel,
                                              uint32_t nbuf) {
   extern __shared__ __align__(128) unsigned char xbuf[];
   __shared__ __align__(8) unsigned long long bar[kXferMaxBufs];
-  if (threadIdx.x != 0) return;
-  const uint32_t n = mode == XFER_GATHER ? (sel ? n_sel : d.hdr_dev->nSp) : d.ndirty_dev[parity];
+  const bool leader = threadIdx.x == 0;
+  const uint32_t n = mode == XFER_GATHER ? (sel ? n_sel : d.hdr_dev->nSp) : d.ndirty_dev[ring];
   const uint64_t rec_bytes = (uint64_t)d.n_arr * d.rec_floats * 4ull;
+  const uint64_t theta_bytes = d.rec_floats * 4ull;
   const uint32_t per_rec = (uint32_t)((rec_bytes + kXferChunk - 1) / kXferChunk);
   const uint64_t total = (uint64_t)n * per_rec;
   if ((uint64_t)blockIdx.x >= total) return;
   const uint64_t mine = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  for (uint32_t b = 0; b < nbuf; ++b)
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const bool spheres = mode == XFER_GATHER && d.sphere != nullptr;
+  if (leader) {
+    for (uint32_t b = 0; b < nbuf; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
 
   // chunk c of this CTA is global chunk blockIdx.x + c * gridDim.x
-  auto geo = [&](uint64_t c, const unsigned char*& src, unsigned char*& dst, uint32_t& bytes) {
+  auto geo = [&](uint64_t c, const unsigned char*& src, unsigned char*& dst, uint32_t& bytes,
+                 uint32_t& slot, uint64_t& off) {
     const uint64_t g = blockIdx.x + c * gridDim.x;
     const uint32_t r = (uint32_t)(g / per_rec);
-    const uint64_t off = (g - (uint64_t)r * per_rec) * kXferChunk;
+    off = (g - (uint64_t)r * per_rec) * kXferChunk;
     bytes = (uint32_t)(rec_bytes - off < kXferChunk ? rec_bytes - off : kXferChunk);
     if (mode == XFER_GATHER) {
       const uint32_t i = sel ? sel[r] : r;
       const uint32_t l = d.sp_blk[parity][i];
-      const uint32_t s = d.sp_slot[parity][i];
-      if (T > 0 && d.wb_tag[l] == T - 1) {
-        src = reinterpret_cast<const unsigned char*>(d.staging[parity ^ 1]) +
+      slot = d.sp_slot[parity][i];
+      const int32_t tg = d.wb_tag[l];
+      if (tg >= 0 && tg >= T - 2) {  // packed by one of the last two activates
+        src = reinterpret_cast<const unsigned char*>(d.staging[tg % kRings]) +
               (uint64_t)d.wb_idx[l] * rec_bytes;
       } else {
         const uint64_t e = d.ent_of ? (uint64_t)d.sp_entry[i] : (uint64_t)l;
         src = d.host_dev + e * d.host_stride;
       }
-      dst = reinterpret_cast<unsigned char*>(d.params + (size_t)s * 3 * d.rec_floats);
+      dst = reinterpret_cast<unsigned char*>(d.params + (size_t)slot * 3 * d.rec_floats);
+      if (leader && off == 0) {
+        if (d.ent_of) d.ent_of[l] = (int32_t)d.sp_entry[i];  // store tier: entry of a resident block
+        if (tg >= 0 && tg >= T - 2) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
+      }
     } else {
-      const uint32_t l = d.dl_blk[r];
+      const uint32_t l = d.dl_blk[ring][r];
+      slot = d.dl_slot[ring][r];
       src = mode == XFER_SCATTER_RING
-                ? reinterpret_cast<const unsigned char*>(d.staging[parity]) + (uint64_t)r * rec_bytes
-                : reinterpret_cast<const unsigned char*>(d.params + (size_t)d.dl_slot[r] * 3 * d.rec_floats);
+                ? reinterpret_cast<const unsigned char*>(d.staging[ring]) + (uint64_t)r * rec_bytes
+                : reinterpret_cast<const unsigned char*>(d.params + (size_t)slot * 3 * d.rec_floats);
       const uint64_t e = d.ent_of ? (uint64_t)d.ent_of[l] : (uint64_t)l;
       dst = d.host_dev + e * d.host_stride;
     }
@@ -590,8 +648,9 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int32_
     const uint32_t b = (uint32_t)(c % nbuf);
     const unsigned char* src;
     unsigned char* dst;
-    uint32_t bytes;
-    geo(c, src, dst, bytes);
+    uint32_t bytes, slot;
+    uint64_t off;
+    geo(c, src, dst, bytes, slot, off);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[b])),
                  "r"(bytes) : "memory");
     asm volatile(
@@ -602,38 +661,50 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int32_
   // nbuf-1 loads in flight; buffer (c-1) % nbuf is refilled once its store has
   // read it (wait_group.read 1: all but the newest store group)
   uint64_t issued = 0;
-  for (; issued < mine && issued < nbuf - 1; ++issued) load(issued);
+  if (leader)
+    for (; issued < mine && issued < nbuf - 1; ++issued) load(issued);
   uint32_t phase = 0;  // bit b: parity of buffer b's next completion
   for (uint64_t c = 0; c < mine; ++c) {
     const uint32_t b = (uint32_t)(c % nbuf);
-    uint32_t ok = 0;
-    while (!ok)
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-          : "=r"(ok) : "r"(smem_addr(&bar[b])), "r"((phase >> b) & 1u) : "memory");
+    if (leader || spheres) {
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok) : "r"(smem_addr(&bar[b])), "r"((phase >> b) & 1u) : "memory");
+    }
     phase ^= 1u << b;
     const unsigned char* src;
     unsigned char* dst;
-    uint32_t bytes;
-    geo(c, src, dst, bytes);
-    if (mode == XFER_GATHER && (blockIdx.x + c * gridDim.x) % per_rec == 0) {
-      const uint32_t r = (uint32_t)((blockIdx.x + c * gridDim.x) / per_rec);
-      const uint32_t i = sel ? sel[r] : r;
-      const uint32_t l = d.sp_blk[parity][i];
-      if (d.ent_of) d.ent_of[l] = (int32_t)d.sp_entry[i];  // store tier: entry of a resident block
-      if (T > 0 && d.wb_tag[l] == T - 1) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
+    uint32_t bytes, slot;
+    uint64_t off;
+    if (leader || spheres) geo(c, src, dst, bytes, slot, off);
+    if (leader) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"(smem_addr(xbuf + (size_t)b * kXferChunk)), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                 "r"(smem_addr(xbuf + (size_t)b * kXferChunk)), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (issued < mine) {
+    if (spheres && off < theta_bytes) {  // theta rows of an admitted block (R24 extent)
+      const uint32_t row0 = (uint32_t)(off / (kDim * 4));
+      const uint32_t nrow = d.B - row0 < 128u ? d.B - row0 : 128u;
+      const float* rows = reinterpret_cast<const float*>(xbuf + (size_t)b * kXferChunk);
+      float4* out = d.sphere + (size_t)slot * d.B + row0;
+      for (uint32_t j = threadIdx.x; j < nrow; j += 32) {
+        const float* rw = rows + (size_t)j * kDim;
+        out[j] = row_sphere(rw[0], rw[1], rw[2], rw[52], rw[53], rw[54]);
+      }
+    }
+    __syncwarp();  // every lane is done reading buffer b before it can be refilled
+    if (leader && issued < mine) {
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       load(issued++);
     }
   }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  for (uint32_t b = 0; b < nbuf; ++b)
-    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(&bar[b])));
+  if (leader) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    for (uint32_t b = 0; b < nbuf; ++b)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(&bar[b])));
+  }
 }
 
 // ------------------------------------------------ a5 prologue (per block)
@@ -692,110 +763,66 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
 }
 
 // ------------------------------------------- f1 Level-2 fine filter -> I_t
-// R24 deterministic exp: k = rint(x log2 e) by the 1.5*2^23 trick, two-step
-// Cody-Waite reduction, degree-7 Taylor polynomial by fma Horner, exact 2^k.
-__device__ __forceinline__ float exp_det(float x) {
-  if (x > 80.0f) x = 80.0f;
-  if (x < -80.0f) x = -80.0f;
-  const float t = __fmaf_rn(x, 1.44269504088896341f, 12582912.0f);
-  const float kf = __fsub_rn(t, 12582912.0f);
-  float r = __fmaf_rn(kf, -0.693145751953125f, x);
-  r = __fmaf_rn(kf, -1.428606765330187045e-06f, r);
-  float p = 1.98412698412698413e-04f;
-  p = __fmaf_rn(p, r, 1.38888888888888889e-03f);
-  p = __fmaf_rn(p, r, 8.33333333333333333e-03f);
-  p = __fmaf_rn(p, r, 4.16666666666666667e-02f);
-  p = __fmaf_rn(p, r, 1.66666666666666667e-01f);
-  p = __fmaf_rn(p, r, 0.5f);
-  p = __fmaf_rn(p, r, 1.0f);
-  p = __fmaf_rn(p, r, 1.0f);
-  const int k = (int)kf;
-  return __fmul_rn(p, __int_as_float((k + 127) << 23));
-}
-
 // grid (ceil(B/256), nA): one thread per row of an A block.  The row's
 // extent sphere (mu, 3 exp(max log-scale)) against every camera that sees the
 // block at Level 1, with the Level-1 rule; a ballot per 32
 // rows writes the I_t mask word of the slot.
-__global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t J, int parity,
+__global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, int parity,
                                               uint32_t* __restrict__ mask) {
   __shared__ float4 pl[kMaxCams * 6];
   __shared__ uint32_t cams[kMaxCams];
   __shared__ uint32_t wcount[8];
-  const uint32_t i = blockIdx.y;
-  const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
-  // cameras whose Level-1 set K^(j) holds block l (R24): camera j renders only
-  // its own visible blocks; compacted in camera order by warp ballots
-  const uint32_t j0 = threadIdx.x;  // blockDim 256 >= kMaxCams
-  const bool has = j0 < J && ((d.percam[parity][(size_t)j0 * d.W + (l >> 5)] >> (l & 31)) & 1u);
-  const uint32_t bal = __ballot_sync(kFull, has);
-  if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
-  __syncthreads();
-  uint32_t base = 0, ncam = 0;
-  for (uint32_t w = 0; w < 8; ++w) {
-    if (w < (threadIdx.x >> 5)) base += wcount[w];
-    ncam += wcount[w];
-  }
-  if (has) {
-    const uint32_t pos = base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-    cams[pos] = j0;
-  }
-  __syncthreads();
-  for (uint32_t k = threadIdx.x; k < ncam * 6; k += blockDim.x)
-    pl[k] = d.last_planes[parity][cams[k / 6] * 6 + k % 6];
-  __syncthreads();
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nw = (d.B + 31) / 32;
-  if (r >= nw * 32) return;  // whole warps only
-  bool vis = false;
-  if (r < block_rows(d, l)) {
-    const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
-    const float x = row[0], y = row[1], z = row[2];
-    float sc = row[52];
-    if (row[53] > sc) sc = row[53];
-    if (row[54] > sc) sc = row[54];
-    const float nr = -__fmul_rn(3.0f, exp_det(sc));
-    for (uint32_t j = 0; j < ncam && !vis; ++j) {
-      bool in = true;
-#pragma unroll
-      for (int p = 0; p < 6; ++p) {
-        const float4 n = pl[j * 6 + p];
-        const float dist = __fmaf_rn(n.z, z, __fmaf_rn(n.y, y, __fmaf_rn(n.x, x, n.w)));
-        if (dist < nr) in = false;
-      }
-      vis = in;
-    }
-  }
-  const uint32_t bits = __ballot_sync(kFull, vis);
-  if ((threadIdx.x & 31) == 0) mask[(size_t)s * nw + (r >> 5)] = bits;
-}
-
-// -------------------------------- f2 conservative bound refresh (R25)
-// grid (ceil(B/256), nA), after k_adam: every row of an updated block gives
-// (|mu - c_k| + 3 exp(max log-scale)) * (1 + 2^-19) in fp32 RN; the block max
-// (on the bit pattern: radii are >= 0) goes to pend[parity][l], which the cull
-// of batch t+2 merges into r_k.
-__global__ void __launch_bounds__(256) k_refresh(Dev d, int parity) {
-  const uint32_t i = blockIdx.y;
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d.ent[i].step == 0u) return;  // block not updated this step (uniform per CTA)
-  const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
-  uint32_t bits = 0u;
-  if (r < block_rows(d, l)) {
-    const float4 c = d.bounds[l];
-    const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
-    const float dx = __fsub_rn(row[0], c.x), dy = __fsub_rn(row[1], c.y);
-    const float dz = __fsub_rn(row[2], c.z);
-    const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-    const float dist = __fsqrt_rn(d2);
-    float sc = row[52];
-    if (row[53] > sc) sc = row[53];
-    if (row[54] > sc) sc = row[54];
-    const float ext = __fmul_rn(3.0f, exp_det(sc));
-    bits = __float_as_uint(__fmul_rn(__fadd_rn(dist, ext), 1.0000019073486328f));
+  for (uint32_t i = blockIdx.y; i < nA; i += gridDim.y) {  // grid.y is capped at 65535
+    const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+    // cameras whose Level-1 set K^(j) holds block l (R24): camera j renders only
+    // its own visible blocks; compacted in camera order by warp ballots
+    const uint32_t j0 = threadIdx.x;  // blockDim 256 >= kMaxCams
+    const bool has = j0 < J && ((d.percam[parity][(size_t)j0 * d.W + (l >> 5)] >> (l & 31)) & 1u);
+    const uint32_t bal = __ballot_sync(kFull, has);
+    if ((threadIdx.x & 31) == 0) wcount[threadIdx.x >> 5] = __popc(bal);
+    __syncthreads();
+    uint32_t base = 0, ncam = 0;
+    for (uint32_t w = 0; w < 8; ++w) {
+      if (w < (threadIdx.x >> 5)) base += wcount[w];
+      ncam += wcount[w];
+    }
+    if (has) {
+      const uint32_t pos = base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+      cams[pos] = j0;
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < ncam * 6; k += blockDim.x)
+      pl[k] = d.last_planes[parity][cams[k / 6] * 6 + k % 6];
+    __syncthreads();
+    if (r < nw * 32) {  // whole warps only
+      bool vis = false;
+      if (r < block_rows(d, l)) {
+        float4 sp;
+        if (d.sphere) {  // 16 B per row, kept current by the gather and k_adam
+          sp = d.sphere[(size_t)s * d.B + r];
+        } else {
+          const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
+          sp = row_sphere(row[0], row[1], row[2], row[52], row[53], row[54]);
+        }
+        const float nr = -sp.w;
+        for (uint32_t j = 0; j < ncam && !vis; ++j) {
+          bool in = true;
+#pragma unroll
+          for (int p = 0; p < 6; ++p) {
+            const float4 n = pl[j * 6 + p];
+            const float dist = __fmaf_rn(n.z, sp.z, __fmaf_rn(n.y, sp.y, __fmaf_rn(n.x, sp.x, n.w)));
+            if (dist < nr) in = false;
+          }
+          vis = in;
+        }
+      }
+      const uint32_t bits = __ballot_sync(kFull, vis);
+      if ((threadIdx.x & 31) == 0) mask[(size_t)s * nw + (r >> 5)] = bits;
+    }
+    __syncthreads();  // the next block's cameras overwrite the shared lists
   }
-  bits = __reduce_max_sync(kFull, bits);
-  if ((threadIdx.x & 31) == 0 && bits) atomicMax(&d.pend[parity][l], bits);
 }
 
 // ------------------------------------------------------- a5 masked Adam
@@ -878,6 +905,36 @@ __device__ __noinline__ uint32_t adam_nonfinite(uint32_t nf0, uint32_t nf1, uint
   return bad;
 }
 
+// f1 / f2 epilogue of a quad (warp-collective; only with the sphere array on):
+// the updated theta float4s go through a per-warp shared scratch so that lane q
+// (< 4) sees row q's centre and log-scales, writes the row's new extent sphere
+// (R24) and -- refresh on -- returns its R25 radius bits around c_k; a valid row
+// that was not updated (masked, non-finite) keeps its stored sphere, which the
+// refresh reads instead.  Out of line: the plain fast path keeps its registers.
+__device__ __noinline__ uint32_t adam_quad_spheres(float4* scratch, float4* sph, const float4 t0,
+                                                   const float4 t1, uint32_t sel0, uint32_t sel1,
+                                                   uint32_t upd, uint32_t valid, float4 ck,
+                                                   int refresh, uint32_t lane) {
+  if (sel0) scratch[lane] = t0;
+  if (sel1) scratch[lane + 32] = t1;
+  __syncwarp();
+  uint32_t bits = 0;
+  if (lane < 4 && ((valid >> lane) & 1u)) {
+    float4 sp;
+    if ((upd >> lane) & 1u) {
+      const float* row = reinterpret_cast<const float*>(scratch) + 59 * lane;
+      sp = row_sphere(row[0], row[1], row[2], row[52], row[53], row[54]);
+      sph[lane] = sp;
+    } else {
+      sp = sph[lane];
+    }
+    if (refresh) bits = refresh_bits(sp, ck);
+  }
+  __syncwarp();
+  return __reduce_max_sync(kFull, bits);
+}
+
+template <bool kSph>
 __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t nA, int parity,
                                                      const uint32_t* __restrict__ mask,
                                                      AdamHyper hp, uint32_t qpw) {
@@ -910,6 +967,15 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
 
   uint32_t cur = 0xffffffffu;
   uint32_t step = 0, rows = 0, fresh = 0;
+  // f1 / f2 (kSph): per-warp scratch of one quad, the block's centre and the
+  // running max of the refreshed radii of the current block (R25)
+  __shared__ float4 quad_tab[kSph ? kAdamNT / 32 : 1][kSph ? 64 : 1];
+  float4 ck = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t rad = 0;
+  auto flush_rad = [&]() {
+    if (kSph && rad) atomicMax(&d.pend[parity][d.a_blk[parity][cur]], rad);
+    rad = 0;
+  };
   // per-lane step sizes ss_a = lr[a] / (1 - beta1^s) of float4 #lane and
   // #lane+32, kept in shared memory (each lane reads back only what it wrote):
   // in registers they pushed the loop past the 80-register budget into spills
@@ -927,8 +993,10 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   const uint32_t nq = (uint32_t)(q1 - q0);  // <= qpw
   for (uint32_t k = 0; k < nq; ++k) {
     if (i != cur) {
+      if (kSph) flush_rad();
       cur = i;
       const AdamEnt ent = d.ent[i];
+      if (kSph && d.refresh && ent.step) ck = d.bounds[d.a_blk[parity][i]];
       step = ent.step;
       rows = ent.rows;
       fresh = ent.fresh;
@@ -951,9 +1019,18 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       ++i;
     }
     if (step == 0u) continue;  // no active row in this block: untouched
-    uint32_t act = r0 >= rows ? 0u : (rows - r0) >= 4u ? 0xFu : ((1u << (rows - r0)) - 1u);
+    const uint32_t valid = r0 >= rows ? 0u : (rows - r0) >= 4u ? 0xFu : ((1u << (rows - r0)) - 1u);
+    uint32_t act = valid;
     if (pmask) act &= (pmask[r0 >> 5] >> (r0 & 31)) & 0xFu;
-    if (act == 0u && !fresh) continue;  // warp-uniform
+    if (act == 0u && !fresh) {  // warp-uniform
+      if (kSph && d.refresh && valid)  // R25: every row of an updated block, stored spheres
+        rad = max(rad, adam_quad_spheres(quad_tab[threadIdx.x >> 5],
+                                         d.sphere + (size_t)d.a_slot[parity][cur] * d.B + r0,
+                                         make_float4(0.f, 0.f, 0.f, 0.f),
+                                         make_float4(0.f, 0.f, 0.f, 0.f), 0u, 0u, 0u, valid, ck,
+                                         1, lane));
+      continue;
+    }
     const size_t f0 = (size_t)(r0 / 4) * 59 + lane, f1 = f0 + 32;
     // components of float4 #lane / #lane+32 whose row is active: lanes whose
     // float4s hold only inactive rows skip their loads and stores (masked I_t)
@@ -982,10 +1059,11 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       }
     }
     const uint32_t nf0 = nonfinite4(g0) & sel0, nf1 = nonfinite4(g1) & sel1;
+    uint32_t upd = act;  // rows updated by this quad
     if (__any_sync(kFull, (nf0 | nf1) != 0u)) {  // R20: rows with a non-finite g are skipped
       const uint32_t bad = adam_nonfinite(nf0, nf1, rowsel0, rowsel1, lane,
                                           (uint64_t)d.a_gid[parity][cur] * d.B + r0, d.nonfinite);
-      const uint32_t upd = act & ~bad;  // Eq. masked_update: unchanged off I_t
+      upd = act & ~bad;  // Eq. masked_update: unchanged off I_t
       sel0 = sel1 = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1015,7 +1093,12 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       __stcs(pt + rf4 + f1, m1);
       __stcs(pt + 2 * rf4 + f1, v1);
     }
+    if (kSph)
+      rad = max(rad, adam_quad_spheres(quad_tab[threadIdx.x >> 5],
+                                       d.sphere + (size_t)d.a_slot[parity][cur] * d.B + r0, t0,
+                                       t1, sel0, sel1, upd, valid, ck, d.refresh, lane));
   }
+  if (kSph) flush_rad();
 }
 
 
@@ -1230,23 +1313,27 @@ cudaError_t launch_cull(const Dev& d, uint32_t J, int32_t T, int parity, cudaStr
 
 cudaError_t launch_quota(const Dev& d, uint32_t J, int32_t T, int parity, cudaStream_t s) {
   if (J == 0 || d.Kloc == 0) return cudaSuccess;
-  k_quota<<<J, kQuotaNT, 0, s>>>(d, J, T, parity);
+  if (d.W <= 1024)
+    k_quota<256><<<J, 256, 0, s>>>(d, J, T, parity);
+  else
+    k_quota<512><<<J, 512, 0, s>>>(d, J, T, parity);
   return cudaGetLastError();
 }
 
 cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s) {
-  k_plan<<<1, kPlanNT, 0, s>>>(d, T, parity);
+  if (d.W <= 1024 && d.PW <= 1024)
+    k_plan<256><<<1, 256, 0, s>>>(d, T, parity);
+  else
+    k_plan<1024><<<1, 1024, 0, s>>>(d, T, parity);
   return cudaGetLastError();
 }
 
-cudaError_t launch_evict(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) {
-  k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity, 0, 0);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int32_t T, bool tag,
-                                cudaStream_t s) {
-  k_evict<<<1, kEvictNT, 0, s>>>(d, nSm, parity, T, tag ? 1 : 0);
+cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int ring, int32_t T,
+                                bool tag, cudaStream_t s) {
+  if (nSm <= 1024)
+    k_evict<256><<<1, 256, 0, s>>>(d, nSm, parity, ring, T, tag ? 1 : 0);
+  else
+    k_evict<1024><<<1, 1024, 0, s>>>(d, nSm, parity, ring, T, tag ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -1261,8 +1348,9 @@ cudaError_t launch_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t launch_xfer(const Dev& d, int mode, int parity, int32_t T, const uint32_t* sel,
-                        uint32_t n_sel, uint32_t n_hint, int ctas, int bufs, cudaStream_t s) {
+cudaError_t launch_xfer(const Dev& d, int mode, int parity, int ring, int32_t T,
+                        const uint32_t* sel, uint32_t n_sel, uint32_t n_hint, int ctas, int bufs,
+                        cudaStream_t s) {
   if (n_hint == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -1275,14 +1363,14 @@ cudaError_t launch_xfer(const Dev& d, int mode, int parity, int32_t T, const uin
   const uint64_t per_rec = ((uint64_t)d.n_arr * d.rec_floats * 4ull + kXferChunk - 1) / kXferChunk;
   const uint64_t chunks = (uint64_t)n_hint * per_rec;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctas, chunks));
-  k_xfer<<<grid, 32, kXferChunk * nbuf, s>>>(d, mode, parity, T, sel, n_sel, nbuf);
+  k_xfer<<<grid, 32, kXferChunk * nbuf, s>>>(d, mode, parity, ring, T, sel, n_sel, nbuf);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack(const Dev& d, uint32_t nSm, int parity, cudaStream_t s) {
+cudaError_t launch_pack(const Dev& d, uint32_t nSm, int ring, cudaStream_t s) {
   if (nSm == 0) return cudaSuccess;
-  dim3 grid(16, nSm);
-  k_pack<<<grid, 256, 0, s>>>(d, parity);
+  dim3 grid(16, nSm < 65535u ? nSm : 65535u);
+  k_pack<<<grid, 256, 0, s>>>(d, ring);
   return cudaGetLastError();
 }
 
@@ -1306,24 +1394,21 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
   while (qpw > 1 && ctas(qpw) < (uint64_t)kAdamMinWaves * (uint64_t)std::max(grid_ctas, 1))
     qpw /= 2;
   const unsigned grid = (unsigned)ctas(qpw);
-  k_adam<<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qpw);
+  if (d.sphere)
+    k_adam<true><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qpw);
+  else
+    k_adam<false><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qpw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
                         cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  dim3 grid(((d.B + 31) / 32 * 32 + 255) / 256, nA);
-  k_fine<<<grid, 256, 0, s>>>(d, J, parity, mask);
+  dim3 grid(((d.B + 31) / 32 * 32 + 255) / 256, nA < 65535u ? nA : 65535u);
+  k_fine<<<grid, 256, 0, s>>>(d, nA, J, parity, mask);
   return cudaGetLastError();
 }
 
-cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s) {
-  if (nA == 0) return cudaSuccess;
-  dim3 grid((d.B + 255) / 256, nA);
-  k_refresh<<<grid, 256, 0, s>>>(d, parity);
-  return cudaGetLastError();
-}
 
 uint32_t layout_ntile(uint64_t n) { return (uint32_t)((n + kRsTile - 1) / kRsTile); }
 uint64_t layout_scan_len(uint64_t n) { return 256ull * layout_ntile(n); }
@@ -1376,7 +1461,7 @@ cudaError_t layout_run(const LayoutBufs& b, uint64_t n, uint32_t B, cudaStream_t
 int adam_grid(int device) {
   int sms = 148, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adam, kAdamNT, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adam<false>, kAdamNT, 0);
   if (per < 1) per = 1;
   return sms * per;
 }

@@ -80,17 +80,18 @@ struct tgs_ctx {
   // mapped pinned
   PlanHdr* hdr = nullptr;         // host view
   uint32_t* sp_map = nullptr;     // host view
-  uint32_t* dirty_map[2] = {nullptr, nullptr};  // host views (parity)
-  uint32_t* ndirty = nullptr;     // host view [2]
+  uint32_t* dirty_map[kRings] = {};  // host views (ring slot T % 3)
+  uint32_t* ndirty = nullptr;     // host view [kRings]
   float* planes_pinned = nullptr; // [2][kMaxCams*24] mapped staging of the camera batch
   // streams / events (ev_*[p]: last record by an activate of parity p)
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_plan = nullptr;
-  cudaEvent_t ev_ready[2] = {}, ev_evict[2] = {}, ev_d2h[2] = {}, ev_lists[2] = {};
+  cudaEvent_t ev_ready[2] = {}, ev_lists[2] = {};
+  cudaEvent_t ev_evict[kRings] = {}, ev_d2h[kRings] = {};  // by ring slot T % 3
   cudaEvent_t ev_job[4] = {};      // write-back of activate J done: ev_job[J & 3] (store mode)
-  bool rec_ready[2] = {}, rec_evict[2] = {}, rec_lists[2] = {};
-  int32_t d2h_job[2] = {-1, -1};   // activate index of the last write-back of parity p
-  bool prev_direct = false;        // previous activate wrote back straight from its slots
+  bool rec_ready[2] = {}, rec_lists[2] = {}, rec_evict[kRings] = {};
+  int32_t d2h_job[kRings] = {-1, -1, -1};  // activate whose write-back last used ring slot k
+  bool ring_direct[kRings] = {};   // ... and whether it wrote back straight from its slots
   // a4 transfer kernels: CTAs of the gather (h2d) and the write-back (d2h)
   // (TGS_GATHER_CTAS / TGS_SCATTER_CTAS; defaults from profiles/linkbench2_r02.txt)
   int gather_ctas = 8, scatter_ctas = 4, gather_bufs = 4, scatter_bufs = 4;
@@ -428,7 +429,7 @@ void fill_host_tier(tgs_ctx* c, const float* rows, tgs_fill_fn fill, void* user,
 // the dirty decision depends on Adam(t-1) (R14), so the caller's thread never
 // waits for it.  Jobs run in activate order.
 void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
-  const int p = j.parity;
+  const int p = j.parity;  // the job's ring slot
   cudaError_t e = cudaEventSynchronize(c->ev_evict[p]);
   if (e != cudaSuccess) {
     std::lock_guard<std::mutex> g(c->mu);
@@ -532,15 +533,16 @@ void destroy_impl(tgs_ctx* c) {
     for (void* h : {(void*)c->sel_map[q][0], (void*)c->sel_map[q][1], (void*)c->sp_entry_map[q]})
       if (h) cudaFreeHost(h);
   for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
-                  (void*)c->ndirty, (void*)c->planes_pinned, (void*)c->lut_pinned})
+                  (void*)c->dirty_map[2], (void*)c->ndirty, (void*)c->planes_pinned,
+                  (void*)c->lut_pinned})
     if (h) cudaFreeHost(h);
   for (cudaEvent_t e : c->ev_job)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_c1)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_ready[0], c->ev_ready[1],
-                        c->ev_evict[0],
-                        c->ev_evict[1], c->ev_d2h[0], c->ev_d2h[1], c->ev_lists[0],
+  for (cudaEvent_t e : {c->ev_plan, c->ev_ready[0], c->ev_ready[1], c->ev_evict[0],
+                        c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
+                        c->ev_d2h[2], c->ev_lists[0],
                         c->ev_lists[1], c->trace_base})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
@@ -652,8 +654,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
   for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready[0],
-                         &c->ev_ready[1], &c->ev_evict[0],
-                         &c->ev_evict[1], &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_lists[0],
+                         &c->ev_ready[1], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
+                         &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_d2h[2], &c->ev_lists[0],
                          &c->ev_lists[1], &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
                          &c->ev_job[3]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
@@ -701,7 +703,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaHostAlloc((void**)&c->sp_map, list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[0], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[1], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * 2, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->dirty_map[2], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * kRings, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 2 * kMaxCams * 24,
                     cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
@@ -725,11 +728,11 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     d.host_stride = (uint64_t)d.n_arr * c->rec_bytes;
   }
   std::memset(c->hdr, 0, sizeof(PlanHdr));
-  std::memset(c->ndirty, 0, sizeof(uint32_t) * 2);
+  std::memset(c->ndirty, 0, sizeof(uint32_t) * kRings);
   cudaHostGetDevicePointer((void**)&d.hdr_map, c->hdr, 0);
   cudaHostGetDevicePointer((void**)&d.sp_map, c->sp_map, 0);
-  cudaHostGetDevicePointer((void**)&d.dirty_map[0], c->dirty_map[0], 0);
-  cudaHostGetDevicePointer((void**)&d.dirty_map[1], c->dirty_map[1], 0);
+  for (int k = 0; k < kRings; ++k)
+    cudaHostGetDevicePointer((void**)&d.dirty_map[k], c->dirty_map[k], 0);
   cudaHostGetDevicePointer((void**)&d.ndirty_map, c->ndirty, 0);
   for (int p = 0; p < 2; ++p) {
     float* dp = nullptr;
@@ -772,19 +775,21 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     c->a3_gid[r] = dalloc_t<uint32_t>(c, Cc, ok);
   }
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
-  d.dl_slot = dalloc_t<uint32_t>(c, Cc, ok);
-  d.dl_blk = dalloc_t<uint32_t>(c, Cc, ok);
+  for (int k = 0; k < kRings; ++k) {
+    d.dl_slot[k] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.dl_blk[k] = dalloc_t<uint32_t>(c, Cc, ok);
+  }
   if (c->store) d.ent_of = dalloc_t<int32_t>(c, Kl, ok);
   d.pend[0] = dalloc_t<uint32_t>(c, Kl, ok);
   d.pend[1] = dalloc_t<uint32_t>(c, Kl, ok);
   d.last_planes[0] = dalloc_t<float4>(c, kMaxCams * 6, ok);
   d.last_planes[1] = dalloc_t<float4>(c, kMaxCams * 6, ok);
-  d.ndirty_dev = dalloc_t<uint32_t>(c, 2, ok);
+  d.ndirty_dev = dalloc_t<uint32_t>(c, kRings, ok);
   d.wb_tag = dalloc_t<int32_t>(c, Kl, ok);
   d.wb_idx = dalloc_t<uint32_t>(c, Kl, ok);
   d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C / 4);
-  for (int p = 0; p < 2; ++p)
-    d.staging[p] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
+  for (int k = 0; k < kRings; ++k)
+    d.staging[k] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
   std::vector<uint16_t> lut;
   uint32_t n_ranks = 0;
   build_rank_lut(g, lut, n_ranks);
@@ -792,6 +797,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   d.rank_lut = dalloc_t<uint16_t>(c, lut.size(), ok);
   const size_t pool_floats = (size_t)P * 3 * d.rec_floats, grad_floats = (size_t)P * d.rec_floats;
   d.params = dalloc_t<float>(c, pool_floats, ok);
+  if (g.level2 || g.refresh_bounds) d.sphere = dalloc_t<float4>(c, (size_t)P * d.B, ok);
   d.grads = dalloc_t<float>(c, grad_floats, ok);
   if (!ok) return fail(TGS_ENOMEM);
 
@@ -818,7 +824,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (d.ent_of) CKI(cudaMemsetAsync(d.ent_of, 0xff, sizeof(int32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.pend[0], 0, sizeof(uint32_t) * Kl, s0));
   CKI(cudaMemsetAsync(d.pend[1], 0, sizeof(uint32_t) * Kl, s0));
-  CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * 2, s0));
+  CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * kRings, s0));
   for (uint32_t* p : {d.Kb, d.cand, d.Q, d.Sp, d.Sm, d.Om, d.Ab, d.R[0], d.R[1]})
     CKI(cudaMemsetAsync(p, 0, sizeof(uint32_t) * Wd, s0));
   for (int p = 0; p < 2; ++p)
@@ -832,6 +838,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   CKI(cudaMemsetAsync(d.hdr_dev, 0, sizeof(PlanHdr), s0));
   CKI(cudaMemsetAsync(d.params, 0, sizeof(float) * pool_floats, s0));
   CKI(cudaMemsetAsync(d.grads, 0, sizeof(float) * grad_floats, s0));
+  if (d.sphere) CKI(cudaMemsetAsync(d.sphere, 0, sizeof(float4) * (size_t)P * d.B, s0));
   CKI(cudaStreamSynchronize(s0));
 #undef CKI
   int dev = g.device;
@@ -846,7 +853,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   return TGS_OK;
 }
 
-// a5: k_adam_prologue, k_adam (+ k_refresh) of the last activate's A list
+// a5: k_adam_prologue, k_adam (its epilogue: f1 spheres, f2 refresh) of the last activate's A list
 tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
                          const uint32_t* d_row_mask) {
   const Dev dk = dev_for(c, p, c->T - 1);
@@ -858,18 +865,14 @@ tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
   // entry constants and slots the plan never hands out while R_{t+1} holds
   // them: the plan of t+2 could overwrite this parity's other lists now
   // (TGS_LISTS_AFTER_ADAM=0).  By default, and always with the bound refresh
-  // on (that plan merges k_refresh's radii, R25), they stay in use until the
+  // on (that plan merges the refreshed radii, R25), they stay in use until the
   // end of this step's compute work.
   const bool lists_late = c->d.refresh || c->lists_after_adam;
   if (!lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));
   prof_begin(c, c->compute, t2);
   CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
-  c->tm.kernel_launches += 2;
-  if (c->d.refresh) {
-    CK(launch_refresh(dk, nA, p, c->compute));
-    c->tm.kernel_launches++;
-  }
+  c->tm.kernel_launches += 2;  // the R25 refresh (if on) is k_adam's epilogue
   if (lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }
@@ -940,11 +943,18 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   uint32_t* const* sel = c->sel_map[p];
   uint32_t* spe = c->sp_entry_map[p];
   if (c->store) CK(cudaHostGetDevicePointer((void**)&dg.sp_entry, spe, 0));
+  //      Write-back state: activate T uses ring slot T % 3.  A block packed by
+  //      T-1 or T-2 is re-admitted from its ring record (the host write-back may
+  //      still be in flight); one written back by T-3 or earlier from the host,
+  //      whose write-back (serial on the d2h stream) is waited for here.
+  const int k = (int)(((uint32_t)T) % kRings);
+  const int k1 = (int)(((uint32_t)T + 2) % kRings), k2 = (int)(((uint32_t)T + 1) % kRings);
   auto gather_waits = [&]() -> tgs_status {
     CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
-    if (c->rec_evict[q]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[q], 0));
-    if (c->prev_direct) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[q], 0));
-    if (c->d2h_job[p] >= 0 && c->d2h_job[p] < T) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
+    if (c->rec_evict[k1]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[k1], 0));  // slots of T-1 free
+    for (int r : {k1, k2})  // a direct write-back (T-1, T-2) has no ring copy: wait for it
+      if (c->d2h_job[r] >= 0 && c->ring_direct[r]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[r], 0));
+    if (c->d2h_job[k] >= 0 && c->d2h_job[k] <= T - 3) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
     return TGS_OK;
   };
   auto gather_flat = [&](uint32_t n_hint) -> tgs_status {
@@ -952,7 +962,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     if (gs != TGS_OK) return gs;
     Timer th;
     prof_begin(c, c->h2d, th);
-    CK(launch_xfer(dg, 0, p, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
+    CK(launch_xfer(dg, 0, p, k, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
     c->h2d_prof = prof_end(c, c->h2d, th, 3);
     c->tm.kernel_launches++;
     CK(cudaEventRecord(c->ev_ready[p], c->h2d));
@@ -986,32 +996,35 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   auto writeback = [&]() -> tgs_status {
     Timer te, td;
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-    // ring p is read by the previous activate's gather (re-admissions): done
+    // ring slot k held T-3's records, which the previous activate's gather may
+    // re-admit from: it must be done
     if (c->rec_ready[q]) CK(cudaStreamWaitEvent(c->compute, c->ev_ready[q], 0));
-    if (c->d2h_job[p] >= 0) {
-      // store tier: the I/O job of t-2 must have read dirty_map[p] / ndirty[p]
-      // before k_evict of t rewrites them; a ring job also still drains ring p
-      if (c->store) io_join(c, c->d2h_job[p]);
-      if (!direct) CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[p], 0));
+    if (c->d2h_job[k] >= 0) {
+      // the write-back of T-3 must be done with ring slot k (its ring, dirty
+      // lists; store tier: the I/O job's read of dirty_map[k] / ndirty[k])
+      if (c->store) io_join(c, c->d2h_job[k]);
+      CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[k], 0));
     }
     prof_begin(c, c->compute, te);
-    CK(launch_evict_tagged(d, h.nSm, p, T, !direct, c->compute));
-    if (!direct) CK(launch_pack(d, h.nSm, p, c->compute));
+    CK(launch_evict_tagged(d, h.nSm, p, k, T, !direct, c->compute));
+    if (!direct) CK(launch_pack(d, h.nSm, k, c->compute));
     prof_end(c, c->compute, te, 5);
     c->tm.kernel_launches += direct ? 1 : 2;
-    CK(cudaEventRecord(c->ev_evict[p], c->compute));
-    c->rec_evict[p] = true;
-    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[p], 0));
+    CK(cudaEventRecord(c->ev_evict[k], c->compute));
+    c->rec_evict[k] = true;
+    CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[k], 0));
     prof_begin(c, c->d2h, td);
-    CK(launch_xfer(d, direct ? 2 : 1, p, T, nullptr, 0, h.nSm, c->scatter_ctas, c->scatter_bufs, c->d2h));
+    CK(launch_xfer(d, direct ? 2 : 1, p, k, T, nullptr, 0, h.nSm, c->scatter_ctas,
+                   c->scatter_bufs, c->d2h));
     prof_end(c, c->d2h, td, 4);
     c->tm.kernel_launches++;
-    CK(cudaEventRecord(c->ev_d2h[p], c->d2h));
+    CK(cudaEventRecord(c->ev_d2h[k], c->d2h));
     if (c->store) {
       CK(cudaEventRecord(c->ev_job[T & 3], c->d2h));
-      io_submit(c, {T, p, direct});
+      io_submit(c, {T, k, direct});
     }
-    c->d2h_job[p] = T;
+    c->d2h_job[k] = T;
+    c->ring_direct[k] = direct;
     return TGS_OK;
   };
   if (reuse_now && h.nSm) {
@@ -1019,7 +1032,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     if (st != TGS_OK) return st;
     if (c->store) io_join(c, T);
     if (c->io_failed) return check(c);
-    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[p], 0));
+    CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
   }
 
   if (!early && !c->store) {
@@ -1050,7 +1063,8 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
       prof_begin(c, c->h2d, t1);
       uint32_t* sel_dev = nullptr;
       CK(cudaHostGetDevicePointer((void**)&sel_dev, sel[which], 0));
-      CK(launch_xfer(dg, 0, p, T, sel_dev, n_sel[which], n_sel[which], c->gather_ctas, c->gather_bufs, c->h2d));
+      CK(launch_xfer(dg, 0, p, k, T, sel_dev, n_sel[which], n_sel[which], c->gather_ctas,
+                     c->gather_bufs, c->h2d));
       prof_end(c, c->h2d, t1, 3, (uint64_t)n_sel[which] * d.n_arr * c->rec_bytes);
       c->tm.kernel_launches++;
       return TGS_OK;
@@ -1090,7 +1104,6 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   // its Adam, which re-records this event) are done
   CK(cudaEventRecord(c->ev_lists[p], c->compute));
   c->rec_lists[p] = true;
-  c->prev_direct = direct && h.nSm > 0;
 
   // ---- C1: the active set of every rank, on the plan stream
   //      after k_plan; every rank calls it once per activate
@@ -1378,10 +1391,10 @@ uint32_t tgs_get_percam(tgs_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap) 
 uint32_t tgs_get_evicted_dirty(tgs_ctx* c, uint32_t* blocks, uint32_t cap) {
   if (check(c) != TGS_OK) return 0;
   if (sync_all(c) != TGS_OK) return 0;
-  const int p = c->last_parity;
-  const uint32_t n = (c->T > 0 && c->last.nSm) ? c->ndirty[p] : 0;
+  const int k = c->T > 0 ? (int)(((uint32_t)c->T - 1) % kRings) : 0;  // the last activate's slot
+  const uint32_t n = (c->T > 0 && c->last.nSm) ? c->ndirty[k] : 0;
   for (uint32_t i = 0; i < n && i < cap; ++i)
-    if (blocks) blocks[i] = c->dirty_map[p][2 * i] * c->cfg.world_size + c->cfg.rank;
+    if (blocks) blocks[i] = c->dirty_map[k][2 * i] * c->cfg.world_size + c->cfg.rank;
   return n;
 }
 

@@ -55,3 +55,28 @@ def test_our_arm_contract():
     assert det["step_ms"]["p50"] > 0 and det["step_ms"]["p99"] >= det["step_ms"]["p50"]
     assert {"evict_per_step", "readmissions_per_step", "cold_restart_ratio"} <= set(det["churn"])
     assert 0 <= r["fresh_row_share"] <= 1
+    assert 0 < det["locality"]["mean_K_over_Kloc"] <= 1
+    assert 0 <= det["locality"]["jaccard_consecutive_K"] <= 1
+
+
+def test_gpus_n_self_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (127.0.0.1
+    rendezvous); rank 0 alone prints the line (reference arm: CPU only)."""
+    d = _run(["--impl", "reference", "--gpus", "2", "--config", "tiny", "--steps", "2",
+              "--warmup", "3"])
+    assert d["impl"] == "reference" and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_our_arm_two_ranks_on_one_gpu():
+    """TGS_BENCH_BACKEND=gloo bench.py --gpus 2: two libtidegs ranks share the
+    GPU, the library issues C1 / C2 through torch_comm; one n_gpus = 2 line."""
+    env = dict(os.environ, TGS_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config",
+                        "tiny", "--steps", "4", "--warmup", "3", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["world_size"] == 2

@@ -235,12 +235,18 @@ def test_full_size_index_parity_and_sampled_rows(name):
     pr.close()
 
 
+@pytest.mark.parametrize("level2", [0, 1])
 @pytest.mark.parametrize("J", [2, 5])
-def test_fine_filter_parity(J):
+def test_fine_filter_parity(J, level2):
     """NEXT f1: the Level-2 I_t mask is bit-exact with the oracle on every A
-    block of every batch, and masked Adam driven by it matches (0 ULP)."""
+    block of every batch, and masked Adam driven by it matches (0 ULP) -- from
+    theta rows (level2 = 0) and from the 16-B extent spheres the gather derives
+    and k_adam keeps current (level2 = 1), here under training that moves the
+    centres and scales."""
     cfg, sc, tr = tiny()
-    pr = _pair(sc, capacity=cfg.capacity)
+    pr = _pair(sc, capacity=cfg.capacity, level2=level2)
+    pr.lr[0:3] = 0.5
+    pr.lr[52:55] = 0.05
     total = 0
     for t in range(16):
         act = pr.activate(tr.batch_planes(t, J))
@@ -366,7 +372,8 @@ def test_edge_configs(N, B, C, J, kw):
 
 
 @pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct",
-                                  "plain_early_lists", "fine_early_lists"])
+                                  "plain_early_lists", "fine_early_lists", "fine_level2",
+                                  "fine_level2_masked_refresh"])
 def test_pipelined_run_matches_oracle(mode, monkeypatch):
     """The GPU runs ahead exactly as in bench.py -- no inspection call (hence no
     host sync) between batches -- so every cross-batch hazard (plan of t+1 vs
@@ -382,6 +389,7 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
         mode = mode[: -len("_early_lists")]
     kw = {"plain": {}, "fine": {}, "fine_refresh_cold": {"refresh_bounds": 1,
                                                           "moments": O.COLD_RESTART},
+          "fine_level2": {"level2": 1}, "fine_level2_masked_refresh": {"level2": 1, "refresh_bounds": 1},
           "mask_direct": {"staging_blocks": 1, "mask_p": 0.5}}[mode]
     pr = _pair(sc, capacity=cfg.capacity, **kw)
     if "refresh" in mode:

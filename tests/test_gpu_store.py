@@ -177,7 +177,7 @@ def test_store_compaction(tmp_path):
     pr.gpu.store_compact()
     pr.orc.flush()
     pr.orc.store_compact()
-    assert _compare_files(g, o) == 1
+    assert _compare_files(g, o) == 2  # base.tdgs + its manifest (R30, R31)
     pr.compare_store(range(sc.K))
     for t, planes in enumerate(boxes[28:], 28):
         act = pr.activate(planes)

@@ -12,6 +12,10 @@ out = {"value_G/s": round(d["value"] / 1e9, 4), "ms/step": round(d["ms_per_step"
        "d2h_GB": det.get("d2h_GB_per_step"),
        "p50/p99_ms": [round(det["step_ms"]["p50"], 3), round(det["step_ms"]["p99"], 3)]
        if det.get("step_ms") else None}
+L = d.get("link_roofline") or {}
+if L.get("h2d_achieved"):
+    out.update({"h2d_GBps": round(L["h2d_achieved"], 1), "d2h_GBps": round(L["d2h_achieved"] or 0, 1),
+                "adam_ms": round(d["roofline"]["avg_launch_ms"], 3)})
 st = det.get("store")
 if st:
     out.update({"hit_rate": round(st["hit_rate"], 3), "ssd_read_GBps": st["ssd_read_GBps_in_reads"],
