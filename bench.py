@@ -86,6 +86,9 @@ def parse():
                     help="device slot pool P per GPU (0 -> 2 C_g, R13)")
     ap.add_argument("--no-persist-detail", action="store_true",
                     help="skip the 100m persist measurement the default run adds (detail.persist)")
+    ap.add_argument("--prefetch", type=int, default=-1, metavar="BLOCKS",
+                    help="--store read-ahead buffers (tgs_prefetch of the next batch every step; "
+                         "-1 -> C, 0 -> off)")
     ap.add_argument("--io-threads", type=int, default=0,
                     help="parallel SSD requests of the --store tier (0 -> library default)")
     return ap.parse_args()
@@ -479,7 +482,8 @@ def measure(args, ws, rank, local):
             args.cache_blocks = 3 * cap
         store = dict(dir=os.path.join(args.store, f"rank{shard_rank:03d}"),
                      cache_blocks=args.cache_blocks, direct_io=0 if args.store_buffered else 1,
-                     io_threads=args.io_threads)
+                     io_threads=args.io_threads,
+                     prefetch_blocks=cap if args.prefetch < 0 else args.prefetch)
         os.makedirs(args.store, exist_ok=True)
     if wl.build:  # f2b: Morton-sort + block the unsorted scene on the GPU
         perm, bounds, build_ms = T.build_layout(sc.table_cs(), sc.B, local)
@@ -527,6 +531,8 @@ def measure(args, ws, rank, local):
         if fmask is not None:
             table.fine_filter(fmask.data_ptr())
         table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
+        if store and store["prefetch_blocks"] and i + 1 < total:
+            table.prefetch(planes[i + 1])  # f3 read-ahead of the next batch, during this step
 
     for i in range(args.warmup):
         step(i)
@@ -656,7 +662,10 @@ def measure(args, ws, rank, local):
                                       "block: 708 B per active row + 472 B per row of the block "
                                       "(m, v record written, not read)",
             "fresh_row_share": fresh_rows / max(1, rows_local),
-            "avg_launch_ms": adam_ms}
+            "avg_launch_ms": adam_ms,
+            "note": "k_adam is the dominant device-memory kernel; the longest-running kernel is "
+                    "k_xfer, the TMA transfer over PCIe, whose roofline is the host link "
+                    "(link_roofline)"}
     lp = link_peak(torch, dev) if rank == 0 else None
     if store and store_detail is not None:
         store_detail["ssd_read_peak_GBps"] = ssd_read_peak(os.path.join(store["dir"], "base.tdgs"))
@@ -697,9 +706,13 @@ def measure(args, ws, rank, local):
                                "jaccard_consecutive_K": (
                                    (st1["k_inter_sum"] - st0["k_inter_sum"])
                                    / max(1, st1["k_union_sum"] - st0["k_union_sum"])),
-                               "how": "rank 0 over the timed steps: mean |K_t| / K_loc, and "
-                                      "sum |K_t n K_t+1| / sum |K_t u K_t+1| (PAPER.md:139, "
-                                      "SURVEY §8d targets 3.5% and 0.88)"},
+                               "stage_in_over_visible": (st1["n_stage_in"] - st0["n_stage_in"])
+                               / max(1, st1["n_visible"] - st0["n_visible"]),
+                               "how": "rank 0 over the timed steps: mean |K_t| / K_loc (paper "
+                                      "~3.5%, PAPER.md:139), the consecutive-batch Jaccard "
+                                      "sum |K_t n K_t+1| / sum |K_t u K_t+1|, and sum |S+| / "
+                                      "sum |K_t|: the Tide / w/o-Tide traffic ratio (paper "
+                                      "0.10 / 0.85 GB = 0.12, PAPER.md:522, 572)"},
                            "step_ms": {"p50": float(np.percentile(step_ms, 50)),
                                        "p99": float(np.percentile(step_ms, 99)),
                                        "max": float(step_ms.max()),

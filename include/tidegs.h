@@ -237,13 +237,18 @@ typedef struct {
   uint64_t segment_bytes;  /* patch segment rollover budget; 0 -> 1 GiB             */
   int32_t direct_io;       /* 1: O_DIRECT reads/writes (page cache bypassed)        */
   int32_t io_threads;      /* parallel SSD requests; 0 -> 8                         */
-  int32_t reopen;          /* 1: resume over the segments an earlier session left at its
-                              barrier (checkpoint/resume, reading R30): no base is
-                              written (theta_rows and fill may both be NULL), Index is
-                              recovered by scanning the segments (later records win, a
-                              torn trailing record is cut off), the cache starts empty and
-                              Adam step counters / recency start at zero; TGS_EIO if the
-                              base header does not describe this shard               */
+  int32_t reopen;          /* 1: resume the state of the last barrier an earlier session
+                              left (checkpoint/resume, reading R30): no base is written
+                              (theta_rows and fill may both be NULL); the barrier
+                              manifest bounds the log, Index is recovered from the base
+                              and the patch records up to it (later records win; every
+                              record's CRC-32C checked), records appended after the
+                              barrier are dropped, the Adam step counters come back from
+                              the manifest; the cache starts empty, recency at zero;
+                              TGS_EIO if the manifest or base does not describe this
+                              shard or a durable record is corrupt                  */
+  uint32_t prefetch_blocks; /* read-ahead buffers for tgs_prefetch (0: off); the pinned
+                              pool then holds cache_blocks + prefetch_blocks records */
 } tgs_store_config;
 
 /* As tgs_init_table, with the store tier.  TGS_EIO: the store could not be
@@ -265,9 +270,23 @@ typedef struct {
   double read_ms, write_ms;     /* host wall time spent in SSD reads / appends             */
   uint64_t read_calls;          /* vector reads issued (runs of neighbouring records)      */
   double read_busy_ms;          /* summed over the I/O threads: time inside the reads      */
+  uint64_t prefetch_reads;      /* records read ahead (tgs_prefetch)                       */
+  uint64_t prefetch_hits;       /* misses served from a read-ahead record (no SSD read then) */
+  uint64_t prefetch_wasted;     /* read-ahead records recycled unused                      */
 } tgs_store_stats;
 /* ESTATE without a store.  Synchronising. */
 tgs_status tgs_get_store_stats(tgs_ctx* ctx, tgs_store_stats* out);
+/* NEXT f3 read-ahead ("Prefetch needed blocks into the CPU cache",
+ * 253-259): announce the camera batch of the NEXT tgs_activate (the trajectory
+ * is known ahead).  Its Level-1 visible set is culled on the GPU (k_probe, R1/R2
+ * rule, no state changed), and the store's read-ahead threads read the newest
+ * version of every such block that is not cached into free read-ahead buffers
+ * while the current step runs.  The CPU cache (R27) is not changed: the next
+ * gather, for a miss whose read-ahead record is still the newest version, swaps
+ * that buffer into the miss's entry instead of reading the SSD.  Returns once the
+ * reads are queued.  No-op (TGS_OK) without a store or with prefetch_blocks = 0;
+ * EINVAL on J > J_max or non-finite planes. */
+tgs_status tgs_prefetch(tgs_ctx* ctx, const tgs_camera* cams, uint32_t J);
 /* Index[k] of global block k: out4 = (file_id, payload offset, payload bytes, version) */
 tgs_status tgs_store_index(tgs_ctx* ctx, uint64_t k_global, uint64_t* out4);
 /* Compaction ("Optional compaction can merge patch segments into a

@@ -103,11 +103,11 @@ struct Dev {
   uint64_t host_stride;     // bytes between host records (n_arr*B*236, or the padded entry size)
   int32_t* ent_of;          // [Kloc] store tier: cache entry of each resident block (else nullptr)
   const uint32_t* sp_entry; // mapped host [C] store tier: cache entry of S+ block i (host-written)
-  // f1 / f2 (cfg.level2 or cfg.refresh_bounds): per slot row, the extent sphere
-  // (mu, 3 exp(max log-scale)) of its current theta -- written by the gather
-  // for admitted rows and by k_adam for updated rows; read by k_fine and by the
-  // bound refresh folded into k_adam (R24, R25).  nullptr when off.
-  float4* sphere;        // [P][B]
+  // f1 / f2 (cfg.level2 or cfg.refresh_bounds): per slot row, the 6 theta
+  // attributes the Level-2 test and the bound refresh read -- centre (0..2) and
+  // log-scales (52..54) -- packed as 24 B: written by the gather for admitted rows
+  // and by k_adam for updated rows (R24, R25).  nullptr when off.
+  float* geo6;           // [P][B][6]
   // pools
   float* params;         // [P][3][B][59]
   float* grads;          // [P][B][59]
@@ -132,6 +132,9 @@ cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int ring
 cudaError_t launch_xfer(const Dev& d, int mode, int parity, int ring, int32_t T,
                         const uint32_t* sel, uint32_t n_sel, uint32_t n_hint, int ctas, int bufs,
                         cudaStream_t s);
+cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s);
+cudaError_t launch_probe(const Dev& d, const float4* planes, uint32_t J, uint32_t* out,
+                         cudaStream_t s);
 cudaError_t launch_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C, cudaStream_t s);
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s);

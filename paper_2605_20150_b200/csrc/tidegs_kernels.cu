@@ -578,8 +578,8 @@ __device__ __forceinline__ uint32_t refresh_bits(const float4& sp, const float4&
 //               (flat: l * host_stride; store: entry ent_of[l]).
 // A chunk is 128 whole rows (30,208 B = 32 x 944 B): a gather chunk of theta
 // rows is complete in shared memory when its mbarrier fires, so with the f1/f2
-// sphere array on (d.sphere) the CTA's 32 lanes derive each admitted row's
-// extent sphere from it there (R24) -- 16 B per row written, nothing re-read.
+// array on (d.geo6) the CTA's 32 lanes copy each admitted row's centre and
+// log-scales from it there -- 24 B per row written, nothing re-read.
 constexpr uint32_t kXferChunk = 128 * kDim * 4, kXferMaxBufs = 7;
 enum XferMode : int { XFER_GATHER = 0, XFER_SCATTER_RING = 1, XFER_SCATTER_DIRECT = 2 };
 
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ri
   const uint64_t total = (uint64_t)n * per_rec;
   if ((uint64_t)blockIdx.x >= total) return;
   const uint64_t mine = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const bool spheres = mode == XFER_GATHER && d.sphere != nullptr;
+  const bool spheres = mode == XFER_GATHER && d.geo6 != nullptr;
   if (leader) {
     for (uint32_t b = 0; b < nbuf; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])));
@@ -684,14 +684,14 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ri
                    "r"(smem_addr(xbuf + (size_t)b * kXferChunk)), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    if (spheres && off < theta_bytes) {  // theta rows of an admitted block (R24 extent)
+    if (spheres && off < theta_bytes) {  // theta rows of an admitted block (R24, R25 inputs)
       const uint32_t row0 = (uint32_t)(off / (kDim * 4));
       const uint32_t nrow = d.B - row0 < 128u ? d.B - row0 : 128u;
       const float* rows = reinterpret_cast<const float*>(xbuf + (size_t)b * kXferChunk);
-      float4* out = d.sphere + (size_t)slot * d.B + row0;
-      for (uint32_t j = threadIdx.x; j < nrow; j += 32) {
-        const float* rw = rows + (size_t)j * kDim;
-        out[j] = row_sphere(rw[0], rw[1], rw[2], rw[52], rw[53], rw[54]);
+      float* out = d.geo6 + ((size_t)slot * d.B + row0) * 6;
+      for (uint32_t e = threadIdx.x; e < 6 * nrow; e += 32) {  // coalesced 24-B rows
+        const uint32_t j = e / 6, f = e - 6 * j;
+        out[e] = rows[(size_t)j * kDim + (f < 3 ? f : f + 49)];
       }
     }
     __syncwarp();  // every lane is done reading buffer b before it can be refilled
@@ -800,8 +800,9 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
       bool vis = false;
       if (r < block_rows(d, l)) {
         float4 sp;
-        if (d.sphere) {  // 16 B per row, kept current by the gather and k_adam
-          sp = d.sphere[(size_t)s * d.B + r];
+        if (d.geo6) {  // 24 B per row, kept current by the gather and k_adam
+          const float* g6 = d.geo6 + ((size_t)s * d.B + r) * 6;
+          sp = row_sphere(g6[0], g6[1], g6[2], g6[3], g6[4], g6[5]);
         } else {
           const float* row = d.params + (size_t)s * 3 * d.rec_floats + (size_t)r * kDim;
           sp = row_sphere(row[0], row[1], row[2], row[52], row[53], row[54]);
@@ -822,6 +823,27 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
       if ((threadIdx.x & 31) == 0) mask[(size_t)s * nw + (r >> 5)] = bits;
     }
     __syncthreads();  // the next block's cameras overwrite the shared lists
+  }
+}
+
+// -------------------------------- f2 conservative bound refresh (R25)
+// grid (ceil(B/256), min(nA, 65535)), after k_adam: every row of an updated
+// block gives (|mu - c_k| + 3 exp(max log-scale)) * (1 + 2^-19) in fp32 RN from
+// its packed centre / log-scales (24 B, written by the gather and k_adam); the
+// block max (on the bit pattern: radii are >= 0) goes to pend[parity][l], which
+// the cull of batch t+2 merges into r_k.
+__global__ void __launch_bounds__(256) k_refresh(Dev d, uint32_t nA, int parity) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t i = blockIdx.y; i < nA; i += gridDim.y) {
+    if (d.ent[i].step == 0u) continue;  // block not updated this step (uniform per CTA)
+    const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+    uint32_t bits = 0u;
+    if (r < block_rows(d, l)) {
+      const float* g6 = d.geo6 + ((size_t)s * d.B + r) * 6;
+      bits = refresh_bits(row_sphere(g6[0], g6[1], g6[2], g6[3], g6[4], g6[5]), d.bounds[l]);
+    }
+    bits = __reduce_max_sync(kFull, bits);
+    if ((threadIdx.x & 31) == 0 && bits) atomicMax(&d.pend[parity][l], bits);
   }
 }
 
@@ -905,35 +927,6 @@ __device__ __noinline__ uint32_t adam_nonfinite(uint32_t nf0, uint32_t nf1, uint
   return bad;
 }
 
-// f1 / f2 epilogue of a quad (warp-collective; only with the sphere array on):
-// the updated theta float4s go through a per-warp shared scratch so that lane q
-// (< 4) sees row q's centre and log-scales, writes the row's new extent sphere
-// (R24) and -- refresh on -- returns its R25 radius bits around c_k; a valid row
-// that was not updated (masked, non-finite) keeps its stored sphere, which the
-// refresh reads instead.  Out of line: the plain fast path keeps its registers.
-__device__ __noinline__ uint32_t adam_quad_spheres(float4* scratch, float4* sph, const float4 t0,
-                                                   const float4 t1, uint32_t sel0, uint32_t sel1,
-                                                   uint32_t upd, uint32_t valid, float4 ck,
-                                                   int refresh, uint32_t lane) {
-  if (sel0) scratch[lane] = t0;
-  if (sel1) scratch[lane + 32] = t1;
-  __syncwarp();
-  uint32_t bits = 0;
-  if (lane < 4 && ((valid >> lane) & 1u)) {
-    float4 sp;
-    if ((upd >> lane) & 1u) {
-      const float* row = reinterpret_cast<const float*>(scratch) + 59 * lane;
-      sp = row_sphere(row[0], row[1], row[2], row[52], row[53], row[54]);
-      sph[lane] = sp;
-    } else {
-      sp = sph[lane];
-    }
-    if (refresh) bits = refresh_bits(sp, ck);
-  }
-  __syncwarp();
-  return __reduce_max_sync(kFull, bits);
-}
-
 template <bool kSph>
 __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t nA, int parity,
                                                      const uint32_t* __restrict__ mask,
@@ -967,15 +960,16 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
 
   uint32_t cur = 0xffffffffu;
   uint32_t step = 0, rows = 0, fresh = 0;
-  // f1 / f2 (kSph): per-warp scratch of one quad, the block's centre and the
-  // running max of the refreshed radii of the current block (R25)
-  __shared__ float4 quad_tab[kSph ? kAdamNT / 32 : 1][kSph ? 64 : 1];
-  float4 ck = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint32_t rad = 0;
-  auto flush_rad = [&]() {
-    if (kSph && rad) atomicMax(&d.pend[parity][d.a_blk[parity][cur]], rad);
-    rad = 0;
+  // f1 / f2 (kSph, d.geo6 on): a lane whose float4 holds the centre (attrs
+  // 0..2) or a log-scale (52..54) of an updated row also stores that component,
+  // post-update, into the row's packed 24-B record: 6 predicated scalar stores
+  // per quad, no extra loop state
+  auto g6idx = [](uint32_t e) -> uint32_t {  // e in [0, 236) of a quad: row*6 + field, or 0xFF
+    const uint32_t a = e % 59;
+    const uint32_t f = a < 3 ? a : (a >= 52 && a <= 54) ? a - 49 : 0xFFu;
+    return f == 0xFFu ? 0xFFu : (e / 59) * 6 + f;
   };
+  float* pg6 = nullptr;
   // per-lane step sizes ss_a = lr[a] / (1 - beta1^s) of float4 #lane and
   // #lane+32, kept in shared memory (each lane reads back only what it wrote):
   // in registers they pushed the loop past the 80-register budget into spills
@@ -993,10 +987,8 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   const uint32_t nq = (uint32_t)(q1 - q0);  // <= qpw
   for (uint32_t k = 0; k < nq; ++k) {
     if (i != cur) {
-      if (kSph) flush_rad();
       cur = i;
       const AdamEnt ent = d.ent[i];
-      if (kSph && d.refresh && ent.step) ck = d.bounds[d.a_blk[parity][i]];
       step = ent.step;
       rows = ent.rows;
       fresh = ent.fresh;
@@ -1005,6 +997,7 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       pt = reinterpret_cast<float4*>(d.params + (size_t)s * 3 * rf);
       pg = reinterpret_cast<const float4*>(d.grads + (size_t)s * rf);
       pmask = mask ? mask + (size_t)s * nw : nullptr;
+      if (kSph) pg6 = d.geo6 + (size_t)s * d.B * 6;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // ss_a = lr[a] / (1 - beta1^s)  (R9)
         const uint32_t e0 = 4 * lane + q, e1 = 4 * (lane + 32) + q;
@@ -1022,15 +1015,7 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
     const uint32_t valid = r0 >= rows ? 0u : (rows - r0) >= 4u ? 0xFu : ((1u << (rows - r0)) - 1u);
     uint32_t act = valid;
     if (pmask) act &= (pmask[r0 >> 5] >> (r0 & 31)) & 0xFu;
-    if (act == 0u && !fresh) {  // warp-uniform
-      if (kSph && d.refresh && valid)  // R25: every row of an updated block, stored spheres
-        rad = max(rad, adam_quad_spheres(quad_tab[threadIdx.x >> 5],
-                                         d.sphere + (size_t)d.a_slot[parity][cur] * d.B + r0,
-                                         make_float4(0.f, 0.f, 0.f, 0.f),
-                                         make_float4(0.f, 0.f, 0.f, 0.f), 0u, 0u, 0u, valid, ck,
-                                         1, lane));
-      continue;
-    }
+    if (act == 0u && !fresh) continue;  // warp-uniform
     const size_t f0 = (size_t)(r0 / 4) * 59 + lane, f1 = f0 + 32;
     // components of float4 #lane / #lane+32 whose row is active: lanes whose
     // float4s hold only inactive rows skip their loads and stores (masked I_t)
@@ -1060,6 +1045,7 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
     }
     const uint32_t nf0 = nonfinite4(g0) & sel0, nf1 = nonfinite4(g1) & sel1;
     uint32_t upd = act;  // rows updated by this quad
+    (void)upd;
     if (__any_sync(kFull, (nf0 | nf1) != 0u)) {  // R20: rows with a non-finite g are skipped
       const uint32_t bad = adam_nonfinite(nf0, nf1, rowsel0, rowsel1, lane,
                                           (uint64_t)d.a_gid[parity][cur] * d.B + r0, d.nonfinite);
@@ -1093,12 +1079,20 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
       __stcs(pt + rf4 + f1, m1);
       __stcs(pt + 2 * rf4 + f1, v1);
     }
-    if (kSph)
-      rad = max(rad, adam_quad_spheres(quad_tab[threadIdx.x >> 5],
-                                       d.sphere + (size_t)d.a_slot[parity][cur] * d.B + r0, t0,
-                                       t1, sel0, sel1, upd, valid, ck, d.refresh, lane));
+    if (kSph) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((sel0 >> q) & 1u) {
+          const uint32_t c0 = g6idx(4 * lane + q);
+          if (c0 != 0xFFu) pg6[(size_t)r0 * 6 + c0] = reinterpret_cast<const float*>(&t0)[q];
+        }
+        if ((sel1 >> q) & 1u) {
+          const uint32_t c1 = g6idx(4 * (lane + 32) + q);
+          if (c1 != 0xFFu) pg6[(size_t)r0 * 6 + c1] = reinterpret_cast<const float*>(&t1)[q];
+        }
+      }
+    }
   }
-  if (kSph) flush_rad();
 }
 
 
@@ -1343,6 +1337,44 @@ __global__ void __launch_bounds__(256) k_pad_active(uint32_t* gid, const PlanHdr
     gid[i] = 0xFFFFFFFFu;
 }
 
+// f3 read-ahead: the Level-1 union of an announced camera batch (the R2 rule of
+// k_cull), written to mapped host memory; nothing else is touched
+__global__ void __launch_bounds__(256) k_probe(Dev d, const float4* __restrict__ planes, uint32_t J,
+                                               uint32_t* __restrict__ out) {
+  __shared__ float4 pl[kMaxCams * 6];
+  for (uint32_t i = threadIdx.x; i < J * 6; i += blockDim.x) pl[i] = planes[i];
+  __syncthreads();
+  const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = l < d.Kloc;
+  const float4 c = in ? d.bounds[l] : make_float4(0.f, 0.f, 0.f, 0.f);
+  bool any = false;
+  for (uint32_t j = 0; j < J && in; ++j) {
+    bool vis = true;
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const float4 n = pl[j * 6 + p];
+      const float dist = __fmaf_rn(n.z, c.z, __fmaf_rn(n.y, c.y, __fmaf_rn(n.x, c.x, n.w)));
+      if (dist < -c.w) vis = false;
+    }
+    any = any || vis;
+  }
+  const uint32_t bits = __ballot_sync(kFull, any);
+  if ((threadIdx.x & 31) == 0 && (l >> 5) < d.W) out[l >> 5] = bits;
+}
+
+cudaError_t launch_probe(const Dev& d, const float4* planes, uint32_t J, uint32_t* out,
+                         cudaStream_t s) {
+  k_probe<<<(d.Kloc + 255) / 256, 256, 0, s>>>(d, planes, J, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s) {
+  if (nA == 0) return cudaSuccess;
+  dim3 grid((d.B + 255) / 256, nA < 65535u ? nA : 65535u);
+  k_refresh<<<grid, 256, 0, s>>>(d, nA, parity);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pad_active(uint32_t* gid, const PlanHdr* h, uint32_t C, cudaStream_t s) {
   k_pad_active<<<(C + 255) / 256 < 64 ? (C + 255) / 256 : 64, 256, 0, s>>>(gid, h, C);
   return cudaGetLastError();
@@ -1394,7 +1426,7 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
   while (qpw > 1 && ctas(qpw) < (uint64_t)kAdamMinWaves * (uint64_t)std::max(grid_ctas, 1))
     qpw /= 2;
   const unsigned grid = (unsigned)ctas(qpw);
-  if (d.sphere)
+  if (d.geo6)
     k_adam<true><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qpw);
   else
     k_adam<false><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qpw);

@@ -82,7 +82,9 @@ struct tgs_ctx {
   uint32_t* sp_map = nullptr;     // host view
   uint32_t* dirty_map[kRings] = {};  // host views (ring slot T % 3)
   uint32_t* ndirty = nullptr;     // host view [kRings]
-  float* planes_pinned = nullptr; // [2][kMaxCams*24] mapped staging of the camera batch
+  float* planes_pinned = nullptr; // [3][kMaxCams*24] mapped staging: camera batches (parity), prefetch
+  uint32_t* probe_map = nullptr;  // mapped host [W] Level-1 union of an announced batch (prefetch)
+  cudaEvent_t ev_probe = nullptr;
   // streams / events (ev_*[p]: last record by an activate of parity p)
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_plan = nullptr;
@@ -534,13 +536,13 @@ void destroy_impl(tgs_ctx* c) {
       if (h) cudaFreeHost(h);
   for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
                   (void*)c->dirty_map[2], (void*)c->ndirty, (void*)c->planes_pinned,
-                  (void*)c->lut_pinned})
+                  (void*)c->lut_pinned, (void*)c->probe_map})
     if (h) cudaFreeHost(h);
   for (cudaEvent_t e : c->ev_job)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_c1)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_ready[0], c->ev_ready[1], c->ev_evict[0],
+  for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_evict[0],
                         c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
                         c->ev_d2h[2], c->ev_lists[0],
                         c->ev_lists[1], c->trace_base})
@@ -653,7 +655,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
-  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_ready[0],
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_probe, &c->ev_ready[0],
                          &c->ev_ready[1], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
                          &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_d2h[2], &c->ev_lists[0],
                          &c->ev_lists[1], &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
@@ -666,7 +668,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (scfg) {
     // NEXT f3: CPU cache of H records over the log-structured store
     const uint64_t S = (d.n_arr * c->rec_bytes + 4095) / 4096 * 4096;
-    if (cudaHostAlloc((void**)&c->cache_pool, (size_t)scfg->cache_blocks * S,
+    if (cudaHostAlloc((void**)&c->cache_pool, ((size_t)scfg->cache_blocks + scfg->prefetch_blocks) * S,
                       cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
       c->cache_pool = nullptr;
       cudaGetLastError();
@@ -685,6 +687,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       fprintf(stderr, "tidegs: store: %s\n", e.c_str());  // the context is gone on return
       return fail(TGS_EIO);
     }
+    c->store->start_prefetch(scfg->prefetch_blocks, io_threads);
   } else {
     c->host_bytes = (size_t)d.Kloc * d.n_arr * c->rec_bytes;
     if (c->host_bytes &&
@@ -705,7 +708,9 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaHostAlloc((void**)&c->dirty_map[1], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[2], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * kRings, cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 2 * kMaxCams * 24,
+      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 3 * kMaxCams * 24,
+                    cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->probe_map, sizeof(uint32_t) * std::max(d.W, 1u),
                     cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     return fail(TGS_ENOMEM);
@@ -797,7 +802,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   d.rank_lut = dalloc_t<uint16_t>(c, lut.size(), ok);
   const size_t pool_floats = (size_t)P * 3 * d.rec_floats, grad_floats = (size_t)P * d.rec_floats;
   d.params = dalloc_t<float>(c, pool_floats, ok);
-  if (g.level2 || g.refresh_bounds) d.sphere = dalloc_t<float4>(c, (size_t)P * d.B, ok);
+  if (g.level2 || g.refresh_bounds) d.geo6 = dalloc_t<float>(c, (size_t)P * d.B * 6, ok);
   d.grads = dalloc_t<float>(c, grad_floats, ok);
   if (!ok) return fail(TGS_ENOMEM);
 
@@ -838,7 +843,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   CKI(cudaMemsetAsync(d.hdr_dev, 0, sizeof(PlanHdr), s0));
   CKI(cudaMemsetAsync(d.params, 0, sizeof(float) * pool_floats, s0));
   CKI(cudaMemsetAsync(d.grads, 0, sizeof(float) * grad_floats, s0));
-  if (d.sphere) CKI(cudaMemsetAsync(d.sphere, 0, sizeof(float4) * (size_t)P * d.B, s0));
+  if (d.geo6) CKI(cudaMemsetAsync(d.geo6, 0, sizeof(float) * (size_t)P * d.B * 6, s0));
   CKI(cudaStreamSynchronize(s0));
 #undef CKI
   int dev = g.device;
@@ -853,7 +858,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   return TGS_OK;
 }
 
-// a5: k_adam_prologue, k_adam (its epilogue: f1 spheres, f2 refresh) of the last activate's A list
+// a5: k_adam_prologue, k_adam (+ k_refresh, f2) of the last activate's A list
 tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
                          const uint32_t* d_row_mask) {
   const Dev dk = dev_for(c, p, c->T - 1);
@@ -872,7 +877,11 @@ tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
   prof_begin(c, c->compute, t2);
   CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
-  c->tm.kernel_launches += 2;  // the R25 refresh (if on) is k_adam's epilogue
+  c->tm.kernel_launches += 2;
+  if (c->d.refresh) {  // R25 from the packed centre / log-scales k_adam just wrote
+    CK(launch_refresh(dk, nA, p, c->compute));
+    c->tm.kernel_launches++;
+  }
   if (lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
   return TGS_OK;
 }
@@ -1587,6 +1596,35 @@ tgs_status tgs_frustum_planes(const double w2c[16], double fx, double fy, double
 }
 
 // ---- NEXT f3 inspection
+tgs_status tgs_prefetch(tgs_ctx* c, const tgs_camera* cams, uint32_t J) {
+  tgs_status st = check(c);
+  if (st != TGS_OK) return st;
+  if (J > c->d.J_max || (J > 0 && !cams)) return TGS_EINVAL;
+  for (uint32_t j = 0; j < J; ++j)
+    for (int p = 0; p < 6; ++p)
+      for (int i = 0; i < 4; ++i)
+        if (!std::isfinite(cams[j].plane[p][i])) return TGS_EINVAL;
+  if (!c->store || J == 0 || c->d.Kloc == 0) return TGS_OK;
+  // the third staging buffer: k_probe reads it on the plan stream, and the host
+  // waits for that before returning, so the next prefetch may reuse it
+  float* pl = c->planes_pinned + (size_t)2 * kMaxCams * 24;
+  std::memcpy(pl, cams, sizeof(float) * 24 * J);
+  float* pl_dev = nullptr;
+  uint32_t* out_dev = nullptr;
+  CK(cudaHostGetDevicePointer((void**)&pl_dev, pl, 0));
+  CK(cudaHostGetDevicePointer((void**)&out_dev, c->probe_map, 0));
+  CK(launch_probe(c->d, reinterpret_cast<const float4*>(pl_dev), J, out_dev, c->plan));
+  c->tm.kernel_launches++;
+  CK(cudaEventRecord(c->ev_probe, c->plan));
+  CK(cudaEventSynchronize(c->ev_probe));
+  std::vector<uint32_t> blocks;
+  for (uint32_t w = 0; w < c->d.W; ++w)
+    for (uint32_t bits = c->probe_map[w]; bits; bits &= bits - 1)
+      blocks.push_back(32u * w + (uint32_t)__builtin_ctz(bits));
+  c->store->prefetch(blocks);
+  return TGS_OK;
+}
+
 tgs_status tgs_get_store_stats(tgs_ctx* c, tgs_store_stats* out) {
   tgs_status st = check(c);
   if (st != TGS_OK) return st;
@@ -1594,6 +1632,7 @@ tgs_status tgs_get_store_stats(tgs_ctx* c, tgs_store_stats* out) {
   if (!c->store) return TGS_ESTATE;
   st = sync_all(c);
   if (st != TGS_OK) return st;
+  c->store->settle();  // no read-ahead batch in flight
   const tgs::StoreCounters& k = c->store->counters();
   out->hits = k.hits;
   out->misses = k.misses;
@@ -1609,6 +1648,9 @@ tgs_status tgs_get_store_stats(tgs_ctx* c, tgs_store_stats* out) {
   out->write_ms = k.write_ms;
   out->read_calls = k.read_calls;
   out->read_busy_ms = k.read_busy_ms;
+  out->prefetch_reads = k.prefetch_reads;
+  out->prefetch_hits = k.prefetch_hits;
+  out->prefetch_wasted = k.prefetch_wasted;
   return TGS_OK;
 }
 

@@ -166,6 +166,15 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 
 // ---------------------------------------------------------------- BlockStore
 BlockStore::~BlockStore() {
+  if (pf_thread_.joinable()) {
+    {
+      std::lock_guard<std::mutex> g(pf_mu_);
+      pf_stop_ = true;
+    }
+    pf_cv_.notify_all();
+    pf_thread_.join();
+  }
+  delete pf_pool_;
   delete pool_io_;
   for (int fd : fds_)
     if (fd >= 0) ::close(fd);
@@ -217,6 +226,7 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
     ents_.assign(H, Ent{});
     free_.clear();
     for (uint32_t e = H; e-- > 0;) free_.push_back((int32_t)e);
+    init_buffers();
     return "";
   }
   if (::mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST) return errno_str("mkdir");
@@ -274,7 +284,106 @@ std::string BlockStore::open(const std::string& dir, const Geometry& g, uint32_t
   ents_.assign(H, Ent{});
   free_.clear();
   for (uint32_t e = H; e-- > 0;) free_.push_back((int32_t)e);
+  init_buffers();
   return "";
+}
+
+// entry e's record sits in physical buffer buf_of_[e]; buffers H .. H+X-1 start
+// as the read-ahead pool (X = prefetch_blocks)
+void BlockStore::init_buffers() {
+  buf_of_.resize(H_);
+  for (uint32_t e = 0; e < H_; ++e) buf_of_[e] = e;
+  ra_free_.clear();
+  for (uint32_t b = H_ + X_; b-- > H_;) ra_free_.push_back(b);
+  ra_buf_.assign(g_.Kloc, -1);
+  ra_ver_.assign(g_.Kloc, 0);
+  ra_fifo_.clear();
+}
+
+// ------------------------------------------------------ read-ahead (prefetch)
+// PAPER.md:150 "Prefetch needed blocks into the CPU cache", 253-259 (SSD reads
+// overlapped with compute).  The caller announces the blocks the next batch
+// may need; those not cached get their newest version read into free
+// read-ahead buffers by the prefetch thread.  The cache itself (R27: which
+// blocks are cached, the LRU order, dirty bits, Index) is not touched: the next
+// gather, for a miss whose read-ahead record still holds the newest version,
+// swaps that buffer into the miss's entry instead of reading the SSD.
+void BlockStore::prefetch(const std::vector<uint32_t>& blocks) {
+  if (!X_) return;
+  pf_join();
+  std::vector<PfItem> batch;
+  for (uint32_t l : blocks) {
+    if (ent_of_[l] >= 0 || ra_buf_[l] >= 0) continue;  // cached, or already read ahead
+    if (ra_free_.empty()) {  // recycle the oldest read-ahead record
+      while (!ra_fifo_.empty() && ra_buf_[ra_fifo_.front()] < 0) ra_fifo_.pop_front();
+      if (ra_fifo_.empty()) break;
+      const uint32_t o = ra_fifo_.front();
+      ra_fifo_.pop_front();
+      ra_free_.push_back((uint32_t)ra_buf_[o]);
+      ra_buf_[o] = -1;
+      cnt_.prefetch_wasted += 1;
+    }
+    const uint32_t b = ra_free_.back();
+    ra_free_.pop_back();
+    ra_buf_[l] = (int32_t)b;
+    ra_ver_[l] = index_[l].version;
+    ra_fifo_.push_back(l);
+    // the file and offset are taken here, on the caller's thread (segments are
+    // opened and Index changes only there)
+    batch.push_back({b, fd_of(index_[l].file_id), index_[l].offset});
+  }
+  if (batch.empty()) return;
+  {
+    std::lock_guard<std::mutex> g(pf_mu_);
+    pf_batch_ = std::move(batch);
+    pf_busy_ = true;
+  }
+  pf_cv_.notify_all();
+}
+
+void BlockStore::pf_main() {
+  for (;;) {
+    std::vector<PfItem> batch;
+    {
+      std::unique_lock<std::mutex> g(pf_mu_);
+      pf_cv_.wait(g, [&] { return pf_stop_ || pf_busy_; });
+      if (pf_stop_) return;
+      batch = pf_batch_;
+    }
+    std::atomic<bool> bad{false};
+    pf_pool_->parallel_for((uint32_t)batch.size(), [&](uint32_t i) {
+      const PfItem& it = batch[i];
+      if (it.fd < 0 || !pread_all(it.fd, pool_ + (uint64_t)it.buf * S_, S_, it.off)) bad = true;
+    });
+    {
+      std::lock_guard<std::mutex> g(pf_mu_);
+      pf_bad_ = pf_bad_ || bad;
+      cnt_.prefetch_reads += batch.size();
+      pf_busy_ = false;
+    }
+    pf_cv_.notify_all();
+  }
+}
+
+void BlockStore::pf_join() {
+  if (!X_) return;
+  std::unique_lock<std::mutex> g(pf_mu_);
+  pf_cv_.wait(g, [&] { return !pf_busy_; });
+  if (pf_bad_) {  // a failed read-ahead is dropped; the gather reads those blocks itself
+    for (uint32_t l = 0; l < g_.Kloc; ++l)
+      if (ra_buf_[l] >= 0) {
+        ra_free_.push_back((uint32_t)ra_buf_[l]);
+        ra_buf_[l] = -1;
+      }
+    pf_bad_ = false;
+  }
+}
+
+void BlockStore::start_prefetch(uint32_t X, int threads) {
+  X_ = X;
+  if (!X_) return;
+  pf_pool_ = new IoPool(std::max(1, threads));
+  pf_thread_ = std::thread([this] { pf_main(); });
 }
 
 // R30 barrier manifest (manifest.tdgm): "TDGM", format 1, epoch, the last patch
@@ -406,6 +515,7 @@ std::string BlockStore::recover() {
 // in parallel), which is made durable and renamed over the base; the patch
 // segments are removed and Index points into the base again.
 std::string BlockStore::compact() {
+  pf_join();
   for (const Ent& e : ents_)
     if (e.blk >= 0 && ent_of_[e.blk] >= 0 && e.dirty) return "compact: dirty entries (barrier first)";
   const std::string tmp = dir_ + "/base.tdgs.tmp";
@@ -569,7 +679,7 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
     const size_t b = runs[r].first, e = runs[r].second;
     for (size_t i = b; i < e; ++i) {  // R28 format 2 integrity
       unsigned char* h = reinterpret_cast<unsigned char*>(hdr_pages_ + i * kPage);
-      put32(h + 32, crc32c(pool_ + (uint64_t)recs[i].second * S_, payload_));
+      put32(h + 32, crc32c(pool_ + (uint64_t)buf_of_[recs[i].second] * S_, payload_));
       put32(h + 36, crc32c(h, 36));
     }
     iovec iov[2 * kMaxRec];
@@ -577,7 +687,7 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
     for (size_t i = b; i < e; ++i) {
       iov[n].iov_base = hdr_pages_ + i * kPage;
       iov[n++].iov_len = kPage;
-      iov[n].iov_base = pool_ + (uint64_t)recs[i].second * S_;
+      iov[n].iov_base = pool_ + (uint64_t)buf_of_[recs[i].second] * S_;
       iov[n++].iov_len = S_;
     }
     const uint64_t total = (uint64_t)(e - b) * (kPage + S_);
@@ -588,7 +698,7 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
     if (w == (ssize_t)total) return;
     for (size_t i = b; i < e; ++i)  // short or failed vector write: record by record
       if (!pwrite_all(fd[i], hdr_pages_ + i * kPage, kPage, off[i]) ||
-          !pwrite_all(fd[i], pool_ + (uint64_t)recs[i].second * S_, S_, off[i] + kPage))
+          !pwrite_all(fd[i], pool_ + (uint64_t)buf_of_[recs[i].second] * S_, S_, off[i] + kPage))
         bad = true;
   });
   return bad ? errno_str("append patch record") : "";
@@ -597,6 +707,7 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
 std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
                                const std::function<void(int32_t)>& wait_d2h,
                                const std::function<void(const std::vector<uint8_t>&)>& hits_ready) {
+  pf_join();  // the read-ahead records of the announced batch have landed
   // every S+ block is in R_{t+1}: its entry (if cached) is not evictable (R27)
   for (uint32_t i = 0; i < n; ++i) {
     const int32_t e = ent_of_[sp[2 * i]];
@@ -653,11 +764,27 @@ std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
     cnt_.write_ms += ms_since(t0);
   }
   if (!misses.empty()) {  // fetched through Index[k]
-    const auto t0 = std::chrono::steady_clock::now();
-    std::string err = read_records(misses);
-    if (!err.empty()) return err;
     cnt_.read_bytes += misses.size() * S_;
-    cnt_.read_ms += ms_since(t0);
+    // a miss read ahead at its newest version takes that buffer (the victims
+    // written above no longer need the entry's old one); the rest is read now
+    std::vector<std::pair<uint32_t, int32_t>> rest;
+    for (auto& m : misses) {
+      const int32_t b = ra_buf_[m.first];
+      if (b >= 0 && ra_ver_[m.first] == index_[m.first].version) {
+        ra_free_.push_back(buf_of_[m.second]);
+        buf_of_[m.second] = (uint32_t)b;
+        ra_buf_[m.first] = -1;
+        cnt_.prefetch_hits += 1;
+      } else {
+        rest.push_back(m);
+      }
+    }
+    if (!rest.empty()) {
+      const auto t0 = std::chrono::steady_clock::now();
+      std::string err = read_records(rest);
+      if (!err.empty()) return err;
+      cnt_.read_ms += ms_since(t0);
+    }
   }
   return "";
 }
@@ -718,7 +845,7 @@ std::string BlockStore::read_records(const std::vector<std::pair<uint32_t, int32
         iov[n++].iov_len = kPage;
         total += kPage;
       }
-      iov[n].iov_base = pool_ + (uint64_t)it[i].e * S_;
+      iov[n].iov_base = pool_ + (uint64_t)buf_of_[it[i].e] * S_;
       iov[n++].iov_len = S_;
       total += S_;
       pos = it[i].off + S_;
@@ -734,7 +861,7 @@ std::string BlockStore::read_records(const std::vector<std::pair<uint32_t, int32
     }
     if (got == (ssize_t)total) return;
     for (size_t i = b; i < e; ++i)  // short or failed vector read: record by record
-      if (!pread_all(fd, pool_ + (uint64_t)it[i].e * S_, S_, it[i].off)) bad = true;
+      if (!pread_all(fd, pool_ + (uint64_t)buf_of_[it[i].e] * S_, S_, it[i].off)) bad = true;
   });
   cnt_.read_busy_ms += busy;
   return bad ? errno_str("read block record") : "";
@@ -762,6 +889,7 @@ void BlockStore::mark_dirty(uint32_t l, int32_t T) {
 
 std::string BlockStore::flush_all(const std::function<void(int32_t)>& wait_d2h,
                                   const uint32_t* steps) {
+  pf_join();  // no read-ahead in flight while segments change
   std::vector<std::pair<uint32_t, int32_t>> recs;
   for (uint32_t l = 0; l < g_.Kloc; ++l) {
     const int32_t e = ent_of_[l];

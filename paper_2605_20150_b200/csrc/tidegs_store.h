@@ -19,6 +19,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <deque>
 #include <functional>
 #include <mutex>
 #include <string>
@@ -61,6 +62,7 @@ struct StoreCounters {
   double read_ms = 0.0, write_ms = 0.0;  // wall time of the SSD phases
   uint64_t read_calls = 0;               // vector reads issued (runs of neighbouring records)
   double read_busy_ms = 0.0;             // sum over threads of time inside preadv
+  uint64_t prefetch_reads = 0, prefetch_hits = 0, prefetch_wasted = 0;  // read-ahead records
 };
 
 class BlockStore {
@@ -112,10 +114,17 @@ class BlockStore {
   // host address of block l's cached record, nullptr if not cached
   float* entry_of(uint32_t l) const {
     const int32_t e = ent_of_[l];
-    return e < 0 ? nullptr : reinterpret_cast<float*>(pool_ + (uint64_t)e * S_);
+    return e < 0 ? nullptr : reinterpret_cast<float*>(pool_ + (uint64_t)buf_of_[e] * S_);
   }
-  // index of block l's cache entry (its record sits at pool + index * entry_bytes()), -1 if none
-  int32_t entry_index(uint32_t l) const { return ent_of_[l]; }
+  // physical buffer of block l's cache entry (its record sits at pool + index *
+  // entry_bytes()), -1 if not cached
+  int32_t entry_index(uint32_t l) const { return ent_of_[l] < 0 ? -1 : (int32_t)buf_of_[ent_of_[l]]; }
+  // read-ahead (prefetch): X extra pool buffers (pool holds H + X) and threads
+  void start_prefetch(uint32_t X, int threads);
+  // the blocks the next activate may need (its Level-1 visible set); returns at once
+  void prefetch(const std::vector<uint32_t>& blocks);
+  // waits for the read-ahead batch in flight (counters are then settled)
+  void settle() { pf_join(); }
   // newest version of block l (cache, else SSD) into dst (payload bytes)
   std::string read_block(uint32_t l, void* dst);
 
@@ -143,6 +152,9 @@ class BlockStore {
   std::string new_segment();
   std::string recover();
   std::string write_manifest();
+  void init_buffers();
+  void pf_main();
+  void pf_join();
   // reserves the next record of the patch log for block l: (fd, file offset of the record)
   std::string reserve_append(uint32_t l, int& fd, uint64_t& rec_off);
   std::string write_records(const std::vector<std::pair<uint32_t, int32_t>>& recs /* (l, entry) */);
@@ -169,6 +181,20 @@ class BlockStore {
   uint64_t epoch_ = 0;             // manifests written (barriers, compactions, the initial base)
   std::vector<uint64_t> base_version_;  // version of each block's base record (R31)
   std::vector<uint32_t> steps_;    // Adam step counters of the last barrier (R30)
+  // physical buffers: entry e's record is buffer buf_of_[e]; read-ahead buffers
+  std::vector<uint32_t> buf_of_;
+  uint32_t X_ = 0;                 // read-ahead buffers (0: no prefetch)
+  std::vector<uint32_t> ra_free_;
+  std::vector<int32_t> ra_buf_;    // [Kloc] read-ahead buffer of block l, -1 none
+  std::vector<uint64_t> ra_ver_;   // [Kloc] Index version it was read at
+  std::deque<uint32_t> ra_fifo_;   // blocks in read-ahead, oldest first
+  IoPool* pf_pool_ = nullptr;
+  std::thread pf_thread_;
+  std::mutex pf_mu_;
+  std::condition_variable pf_cv_;
+  struct PfItem { uint32_t buf; int fd; uint64_t off; };
+  std::vector<PfItem> pf_batch_;
+  bool pf_busy_ = false, pf_stop_ = false, pf_bad_ = false;
   size_t hdr_cap_ = 0;
 };
 

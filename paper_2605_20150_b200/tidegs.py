@@ -30,7 +30,8 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_nonfinite_index", "tgs_read_block", "tgs_step_count", "tgs_num_local_blocks",
            "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error",
            "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru",
-           "tgs_order_views", "tgs_store_compact", "tgs_set_comm", "tgs_get_global_stats")
+           "tgs_order_views", "tgs_store_compact", "tgs_set_comm", "tgs_get_global_stats",
+           "tgs_prefetch")
 
 
 class Config(C.Structure):
@@ -109,7 +110,8 @@ class Timing(C.Structure):
 
 class StoreConfig(C.Structure):
     _fields_ = [("dir", C.c_char_p), ("cache_blocks", C.c_uint32), ("segment_bytes", C.c_uint64),
-                ("direct_io", C.c_int32), ("io_threads", C.c_int32), ("reopen", C.c_int32)]
+                ("direct_io", C.c_int32), ("io_threads", C.c_int32), ("reopen", C.c_int32),
+                ("prefetch_blocks", C.c_uint32)]
 
 
 STORE_FIELDS = ("hits", "misses", "evictions", "dirty_evictions", "flush_appends", "read_bytes",
@@ -120,7 +122,10 @@ class StoreStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in STORE_FIELDS] + [("read_ms", C.c_double),
                                                           ("write_ms", C.c_double),
                                                           ("read_calls", C.c_uint64),
-                                                          ("read_busy_ms", C.c_double)]
+                                                          ("read_busy_ms", C.c_double),
+                                                          ("prefetch_reads", C.c_uint64),
+                                                          ("prefetch_hits", C.c_uint64),
+                                                          ("prefetch_wasted", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -160,6 +165,7 @@ def lib():
         L.tgs_fine_filter.argtypes = [vp, vp]
         L.tgs_get_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_set_comm.argtypes = [vp, C.POINTER(Comm)]
+        L.tgs_prefetch.argtypes = [vp, C.c_void_p, u32]
         L.tgs_get_global_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.tgs_get_stats_async.argtypes = [vp, vp]
@@ -337,7 +343,7 @@ class Table:
             self._store_cfg = StoreConfig(os.fsencode(str(store["dir"])), store["cache_blocks"],
                                           store.get("segment_bytes", 0),
                                           store.get("direct_io", 1), store.get("io_threads", 0),
-                                          store.get("reopen", 0))
+                                          store.get("reopen", 0), store.get("prefetch_blocks", 0))
             rc = lib().tgs_init_table_store(C.byref(cfg), C.byref(self._store_cfg), rows_p,
                                             fill_p, fill_u, _fp(self._bounds), alloc,
                                             self.stream or None, C.byref(h))
@@ -363,6 +369,12 @@ class Table:
             raise TgsError(rc, what, lib().tgs_last_error(self.h).decode(errors="replace"))
 
     # ---- the hot path
+    def prefetch(self, planes: np.ndarray):
+        """announce the next activate's camera batch (store tier read-ahead, f3)"""
+        p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)
+        self._err(lib().tgs_prefetch(self.h, p.ctypes.data if p.shape[0] else None, p.shape[0]),
+                  "tgs_prefetch")
+
     def activate(self, planes: np.ndarray, *, check=True) -> Activation:
         p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)
         out = Activation()

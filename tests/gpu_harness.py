@@ -50,7 +50,8 @@ class Pair:
         if store is not None:
             gstore = dict(dir=store["gpu_dir"], cache_blocks=store["cache_blocks"],
                           segment_bytes=store.get("segment_bytes", 0),
-                          direct_io=store.get("direct_io", 0), reopen=store.get("reopen", 0))
+                          direct_io=store.get("direct_io", 0), reopen=store.get("reopen", 0),
+                          prefetch_blocks=store.get("prefetch_blocks", 0))
         self.gpu = T.Table(T.make_config(scene.N, scene.B, capacity, staging_blocks=staging_blocks,
                                          refresh_bounds=refresh_bounds, level2=level2, **kw),
                            bounds,

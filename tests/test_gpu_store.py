@@ -19,11 +19,12 @@ from helpers import random_boxes, tiny
 pytestmark = pytest.mark.gpu
 
 
-def _pair(sc, tmp_path, H, seg=0, direct=0, **kw):
+def _pair(sc, tmp_path, H, seg=0, direct=0, prefetch=0, **kw):
     from gpu_harness import Pair
     g, o = tmp_path / "gpu", tmp_path / "orc"
     o.mkdir()
-    st = dict(gpu_dir=str(g), orc_dir=str(o), cache_blocks=H, segment_bytes=seg, direct_io=direct)
+    st = dict(gpu_dir=str(g), orc_dir=str(o), cache_blocks=H, segment_bytes=seg, direct_io=direct,
+              prefetch_blocks=prefetch)
     return Pair(sc, store=st, **kw), g, o
 
 
@@ -199,7 +200,8 @@ def test_store_conservation_without_updates(tmp_path):
         pr.t = t
         assert pr.step(act, t) == O.OK
     s, n_files = _finish(pr, sc, g, o)
-    assert s["write_bytes"] == 0 and n_files == 1 and s["evictions"] > 0
+    # only the base segment and its barrier manifest (R30): no patch segment
+    assert s["write_bytes"] == 0 and n_files == 2 and s["evictions"] > 0
     for k in range(sc.K):
         th, m, v = pr.gpu.read_block(k)
         assert np.array_equal(th, sc.block_theta(k)) and not m.any() and not v.any()
@@ -236,3 +238,31 @@ def test_store_full_size_100m_index_parity(tmp_path):
     pr.compare_store(sorted(touched))
     pr.close()
     shutil.rmtree(d, ignore_errors=True)  # 23.6 GB: do not leave it to pytest's tmp retention
+
+
+@pytest.mark.parametrize("moments,prefetch", [(O.PERSIST, 8), (O.COLD_RESTART, 24)])
+def test_store_prefetch_is_transparent(tmp_path, moments, prefetch):
+    """f3 read-ahead (tgs_prefetch): announcing each next
+    batch lets the GPU side read the misses ahead into read-ahead buffers, with
+    a pool smaller and larger than a batch's misses.  The CPU cache is untouched,
+    so every list, cache counter, LRU order, Index and file still matches the
+    oracle (which has no read-ahead) bit-exactly, while misses are served from
+    read-ahead records."""
+    cfg, sc, tr = tiny()
+    pr, g, o = _pair(sc, tmp_path, 16, 6 << 20, 1, prefetch=prefetch, capacity=8,
+                     moments=moments)
+    boxes = random_boxes(sc, 36, seed=27)
+    pr.gpu.prefetch(boxes[0])
+    for t, planes in enumerate(boxes):
+        act = pr.activate(planes)
+        pr.t = t
+        pr.compare_plan(1)
+        pr.compare_evicted_dirty()
+        pr.compare_store(pr.orc.list("S+"))
+        assert pr.step(act, t) == O.OK
+        if t + 1 < len(boxes):
+            pr.gpu.prefetch(boxes[t + 1])
+    s, n_files = _finish(pr, sc, g, o)
+    full = pr.gpu.store_stats()
+    assert s["misses"] > 0 and full["prefetch_hits"] > 0 and full["prefetch_reads"] > 0
+    pr.close()
