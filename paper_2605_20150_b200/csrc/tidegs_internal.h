@@ -72,7 +72,8 @@ struct Dev {
   uint32_t *sp_blk[2], *sp_slot[2];    // [C] S+ ascending and its slots (parity)
   uint32_t *sm_blk[2], *sm_slot[2];    // [C] S- ascending and its slots (parity)
   uint32_t *a_blk[2], *a_slot[2], *a_gid[2];  // [C] A = R n K (parity)
-  PlanHdr* hdr_dev;      // device copy of the header
+  PlanHdr* hdr_dev[2];   // device copy of the header (parity: the gather of T reads it
+                         // while the plan of T+1 may already run)
   PlanHdr* hdr_map;      // device alias of the mapped host header
   uint32_t* sp_map;      // mapped host [C][2] (local id, slot) of S+
   uint32_t* sm_map;      // mapped host [C] S- local ids (store mode only, else nullptr)

@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(NT) k_plan(Dev d, int32_t T, int parity) {
     h.nfree = nfree;
     h.fallback = fallback;
     h.n_dirty = 0;
-    *d.hdr_dev = h;
+    *d.hdr_dev[parity] = h;
     *d.hdr_map = h;
     d.cnt[CNT_CAND] = 0u;  // ready for the next activate's cull
     d.cnt[CNT_K] = 0u;
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ri
   extern __shared__ __align__(128) unsigned char xbuf[];
   __shared__ __align__(8) unsigned long long bar[kXferMaxBufs];
   const bool leader = threadIdx.x == 0;
-  const uint32_t n = mode == XFER_GATHER ? (sel ? n_sel : d.hdr_dev->nSp) : d.ndirty_dev[ring];
+  const uint32_t n = mode == XFER_GATHER ? (sel ? n_sel : d.hdr_dev[parity]->nSp) : d.ndirty_dev[ring];
   const uint64_t rec_bytes = (uint64_t)d.n_arr * d.rec_floats * 4ull;
   const uint64_t theta_bytes = d.rec_floats * 4ull;
   const uint32_t per_rec = (uint32_t)((rec_bytes + kXferChunk - 1) / kXferChunk);
@@ -773,8 +773,7 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
   __shared__ uint32_t cams[kMaxCams];
   __shared__ uint32_t wcount[8];
   const uint32_t nw = (d.B + 31) / 32;
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint32_t i = blockIdx.y; i < nA; i += gridDim.y) {  // grid.y is capped at 65535
+  for (uint32_t i = blockIdx.x; i < nA; i += gridDim.x) {  // one CTA per A block
     const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
     // cameras whose Level-1 set K^(j) holds block l (R24): camera j renders only
     // its own visible blocks; compacted in camera order by warp ballots
@@ -796,7 +795,7 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
     for (uint32_t k = threadIdx.x; k < ncam * 6; k += blockDim.x)
       pl[k] = d.last_planes[parity][cams[k / 6] * 6 + k % 6];
     __syncthreads();
-    if (r < nw * 32) {  // whole warps only
+    for (uint32_t r = threadIdx.x; r < nw * 32; r += blockDim.x) {  // whole warps only
       bool vis = false;
       if (r < block_rows(d, l)) {
         float4 sp;
@@ -833,14 +832,16 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
 // block max (on the bit pattern: radii are >= 0) goes to pend[parity][l], which
 // the cull of batch t+2 merges into r_k.
 __global__ void __launch_bounds__(256) k_refresh(Dev d, uint32_t nA, int parity) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint32_t i = blockIdx.y; i < nA; i += gridDim.y) {
+  for (uint32_t i = blockIdx.x; i < nA; i += gridDim.x) {  // one CTA per A block
     if (d.ent[i].step == 0u) continue;  // block not updated this step (uniform per CTA)
     const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
+    const uint32_t rows = block_rows(d, l);
+    const float4 ck = d.bounds[l];
     uint32_t bits = 0u;
-    if (r < block_rows(d, l)) {
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
       const float* g6 = d.geo6 + ((size_t)s * d.B + r) * 6;
-      bits = refresh_bits(row_sphere(g6[0], g6[1], g6[2], g6[3], g6[4], g6[5]), d.bounds[l]);
+      const uint32_t b = refresh_bits(row_sphere(g6[0], g6[1], g6[2], g6[3], g6[4], g6[5]), ck);
+      bits = b > bits ? b : bits;
     }
     bits = __reduce_max_sync(kFull, bits);
     if ((threadIdx.x & 31) == 0 && bits) atomicMax(&d.pend[parity][l], bits);
@@ -1370,7 +1371,7 @@ cudaError_t launch_probe(const Dev& d, const float4* planes, uint32_t J, uint32_
 
 cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  dim3 grid((d.B + 255) / 256, nA < 65535u ? nA : 65535u);
+  const uint32_t grid = nA < 148u * 64u ? nA : 148u * 64u;  // one CTA per block (grid-stride)
   k_refresh<<<grid, 256, 0, s>>>(d, nA, parity);
   return cudaGetLastError();
 }
@@ -1436,7 +1437,7 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
 cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
                         cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  dim3 grid(((d.B + 31) / 32 * 32 + 255) / 256, nA < 65535u ? nA : 65535u);
+  const uint32_t grid = nA < 148u * 64u ? nA : 148u * 64u;  // one CTA per block (grid-stride)
   k_fine<<<grid, 256, 0, s>>>(d, nA, J, parity, mask);
   return cudaGetLastError();
 }

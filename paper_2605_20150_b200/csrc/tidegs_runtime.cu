@@ -119,12 +119,12 @@ struct tgs_ctx {
   std::string io_err;
   uint32_t last_ndirty = 0;
   std::mutex prof_mu;
-  // The plan of t+2 waits for all of Adam(t) (default), or with
-  // TGS_LISTS_AFTER_ADAM=0 only for its prologue (the A lists then come from
-  // the 3-deep ring).  The early release lets the high-priority plan kernels
-  // run inside Adam, which costs Adam ~5% of its HBM rate and gains the
-  // link-bound step nothing (profiles/ab_lists_r01.md): off by default.
-  bool lists_after_adam = true;
+  // The plan of t+2 waits only for Adam(t)'s prologue (default; the A lists
+  // then come from the 3-deep ring), or with TGS_LISTS_AFTER_ADAM=1 for all of
+  // Adam(t).  With 256-thread plan CTAs the early release costs k_adam < 1% and
+  // takes the plan off the chain of the small configs (100m persist 0.96 ->
+  // 0.88 ms/step, 11m 0.199 -> 0.189; profiles/bench_r02.md).
+  bool lists_after_adam = false;
   // Adam LUT (bias corrections, R9)
   std::vector<float> lut_bc1_h, lut_ibs_h;
   float* lut_pinned = nullptr;     // [2][lut_cap]
@@ -770,7 +770,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     d.sm_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
     d.a_blk[p] = d.a_slot[p] = d.a_gid[p] = nullptr;  // per launch, from the ring below
   }
-  d.hdr_dev = dalloc_t<PlanHdr>(c, 1, ok);
+  d.hdr_dev[0] = dalloc_t<PlanHdr>(c, 1, ok);
+  d.hdr_dev[1] = dalloc_t<PlanHdr>(c, 1, ok);
   d.cnt = dalloc_t<uint32_t>(c, CNT_N, ok);
   d.stats = dalloc_t<unsigned long long>(c, ST_ALL, ok);
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
@@ -840,7 +841,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   CKI(cudaMemsetAsync(d.stats, 0, sizeof(unsigned long long) * ST_ALL, s0));
   CKI(cudaMemsetAsync(d.cnt, 0, sizeof(uint32_t) * CNT_N, s0));  // k_plan re-zeroes it after use
   CKI(cudaMemsetAsync(d.nonfinite, 0xff, sizeof(unsigned long long), s0));
-  CKI(cudaMemsetAsync(d.hdr_dev, 0, sizeof(PlanHdr), s0));
+  CKI(cudaMemsetAsync(d.hdr_dev[0], 0, sizeof(PlanHdr), s0));
+  CKI(cudaMemsetAsync(d.hdr_dev[1], 0, sizeof(PlanHdr), s0));
   CKI(cudaMemsetAsync(d.params, 0, sizeof(float) * pool_floats, s0));
   CKI(cudaMemsetAsync(d.grads, 0, sizeof(float) * grad_floats, s0));
   if (d.geo6) CKI(cudaMemsetAsync(d.geo6, 0, sizeof(float) * (size_t)P * d.B * 6, s0));
@@ -1118,7 +1120,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   //      after k_plan; every rank calls it once per activate
   if (c->has_comm) {
     uint32_t* send = c->a3_gid[(uint32_t)T % 3u];
-    CK(launch_pad_active(send, d.hdr_dev, d.C, c->plan));
+    CK(launch_pad_active(send, d.hdr_dev[p], d.C, c->plan));
     c->tm.kernel_launches++;
     if (c->comm.allgather(c->comm.user, send, c->c1_recv[p], sizeof(uint32_t) * d.C,
                           (void*)c->plan) != 0) {

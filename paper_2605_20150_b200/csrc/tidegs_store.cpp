@@ -381,6 +381,8 @@ void BlockStore::pf_join() {
 
 void BlockStore::start_prefetch(uint32_t X, int threads) {
   X_ = X;
+  ra_free_.clear();  // buffers H .. H+X-1 of the pool
+  for (uint32_t b = H_ + X_; b-- > H_;) ra_free_.push_back(b);
   if (!X_) return;
   pf_pool_ = new IoPool(std::max(1, threads));
   pf_thread_ = std::thread([this] { pf_main(); });

@@ -373,7 +373,7 @@ def test_edge_configs(N, B, C, J, kw):
 
 @pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct",
                                   "plain_early_lists", "fine_early_lists", "fine_level2",
-                                  "fine_level2_masked_refresh"])
+                                  "fine_level2_masked_refresh", "plain_late_lists"])
 def test_pipelined_run_matches_oracle(mode, monkeypatch):
     """The GPU runs ahead exactly as in bench.py -- no inspection call (hence no
     host sync) between batches -- so every cross-batch hazard (plan of t+1 vs
@@ -384,9 +384,12 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
     import torch
     from gpu_harness import GRAD_SEED, Synth, _cfn
     cfg, sc, tr = tiny()
-    if mode.endswith("_early_lists"):  # plan of t+2 released after Adam(t)'s prologue
+    if mode.endswith("_early_lists"):  # plan of t+2 released after Adam(t)'s prologue (default)
         monkeypatch.setenv("TGS_LISTS_AFTER_ADAM", "0")
         mode = mode[: -len("_early_lists")]
+    if mode.endswith("_late_lists"):  # plan of t+2 waits for all of Adam(t)
+        monkeypatch.setenv("TGS_LISTS_AFTER_ADAM", "1")
+        mode = mode[: -len("_late_lists")]
     kw = {"plain": {}, "fine": {}, "fine_refresh_cold": {"refresh_bounds": 1,
                                                           "moments": O.COLD_RESTART},
           "fine_level2": {"level2": 1}, "fine_level2_masked_refresh": {"level2": 1, "refresh_bounds": 1},
@@ -485,3 +488,39 @@ def test_recency_golden_on_gpu(case):
         fill=lambda k: np.zeros((4, 59), np.float32)), c["empty_batches"])
     assert tab.list("R").tolist() == c["R_final"]
     tab.close()
+
+
+@pytest.mark.parametrize("ctas", ["1,1,2,2", "3,2,3,5", "16,8,7,4"])
+def test_transfer_grid_shapes_give_identical_results(ctas, monkeypatch):
+    """Determinism across launch shapes: the k_xfer gather / write-back with 1..16
+    CTAs and 2..7 shared-memory buffers each (TGS_GATHER_CTAS / _SCATTER_CTAS /
+    _GATHER_BUFS / _SCATTER_BUFS), on a pipelined run with no host sync between
+    batches, in the smallest-ring configuration (staging of 2 records: many
+    direct write-backs) and both policies; the end state must equal the
+    oracle's bit for bit whatever the interleaving."""
+    g, s_, gb, sb = ctas.split(",")
+    monkeypatch.setenv("TGS_GATHER_CTAS", g)
+    monkeypatch.setenv("TGS_SCATTER_CTAS", s_)
+    monkeypatch.setenv("TGS_GATHER_BUFS", gb)
+    monkeypatch.setenv("TGS_SCATTER_BUFS", sb)
+    import ctypes as C
+    from gpu_harness import _cfn
+    cfg, sc, tr = tiny()
+    for moments, staging in ((O.PERSIST, 2), (O.COLD_RESTART, 0)):
+        pr = _pair(sc, capacity=cfg.capacity, moments=moments, staging_blocks=staging)
+        n = 30
+        for t in range(n):
+            act = pr.gpu.activate(tr.batch_planes(t, cfg.J))
+            pr.grads_gpu_only(act, t)
+            pr.gpu.step_adam(pr.lr)
+        gfn = (_cfn("wl_grad_cb"), C.addressof(pr.gsyn))
+        for t in range(n):
+            assert pr.orc.activate(tr.batch_planes(t, cfg.J)) == O.OK
+            assert pr.orc.step_adam(pr.lr, grad=gfn) == O.OK
+        pr.t = n
+        pr.compare_plan(cfg.J)
+        pr.compare_stats()
+        pr.gpu.flush()
+        pr.orc.flush()
+        assert pr.compare_blocks(range(sc.K)) == 0
+        pr.close()
