@@ -531,8 +531,8 @@ def measure(args, ws, rank, local):
         if fmask is not None:
             table.fine_filter(fmask.data_ptr())
         table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
-        if store and store["prefetch_blocks"] and i + 1 < total:
-            table.prefetch(planes[i + 1])  # f3 read-ahead of the next batch, during this step
+        if store and store["prefetch_blocks"] and i + 2 < total:
+            table.prefetch(planes[i + 2], 2)  # f3 read-ahead, two batches ahead
 
     for i in range(args.warmup):
         step(i)

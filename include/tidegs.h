@@ -277,16 +277,18 @@ typedef struct {
 /* ESTATE without a store.  Synchronising. */
 tgs_status tgs_get_store_stats(tgs_ctx* ctx, tgs_store_stats* out);
 /* NEXT f3 read-ahead ("Prefetch needed blocks into the CPU cache",
- * 253-259): announce the camera batch of the NEXT tgs_activate (the trajectory
- * is known ahead).  Its Level-1 visible set is culled on the GPU (k_probe, R1/R2
+ * 253-259): announce the camera batch of the tgs_activate `ahead` calls from now
+ * (1 = the next one; the trajectory is known ahead, and 2 lets the reads overlap
+ * a whole step).  Its Level-1 visible set is culled on the GPU (k_probe, R1/R2
  * rule, no state changed), and the store's read-ahead threads read the newest
  * version of every such block that is not cached into free read-ahead buffers
- * while the current step runs.  The CPU cache (R27) is not changed: the next
- * gather, for a miss whose read-ahead record is still the newest version, swaps
- * that buffer into the miss's entry instead of reading the SSD.  Returns once the
- * reads are queued.  No-op (TGS_OK) without a store or with prefetch_blocks = 0;
+ * while the steps before it run.  The CPU cache (R27) is not changed: that
+ * activate's gather waits for the batches announced for it (or earlier) and, for a
+ * miss whose read-ahead record is still the newest version, swaps that buffer into
+ * the miss's entry instead of reading the SSD.  Returns once the reads are queued.
+ * EINVAL also for ahead == 0.  No-op (TGS_OK) without a store or with prefetch_blocks = 0;
  * EINVAL on J > J_max or non-finite planes. */
-tgs_status tgs_prefetch(tgs_ctx* ctx, const tgs_camera* cams, uint32_t J);
+tgs_status tgs_prefetch(tgs_ctx* ctx, const tgs_camera* cams, uint32_t J, uint32_t ahead);
 /* Index[k] of global block k: out4 = (file_id, payload offset, payload bytes, version) */
 tgs_status tgs_store_index(tgs_ctx* ctx, uint64_t k_global, uint64_t* out4);
 /* Compaction ("Optional compaction can merge patch segments into a

@@ -390,8 +390,7 @@ __global__ void __launch_bounds__(NT) k_plan(Dev d, int32_t T, int parity) {
     atomicOr(&d.occ[s >> 5], 1u << (s & 31));
     if (d.ever[l]) ++readmit;
     d.ever[l] = 1;
-    d.admit[l] = T;
-    if (d.cold) d.step[l] = 0u;
+    d.admit[l] = T;  // (cold restart resets step[l] in the gather: after the last Adam on l)
     d.sp_map[2 * i] = l;
     d.sp_map[2 * i + 1] = s;
   }
@@ -629,6 +628,10 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ri
       }
       dst = reinterpret_cast<unsigned char*>(d.params + (size_t)slot * 3 * d.rec_floats);
       if (leader && off == 0) {
+        // cold restart: the moments start over at step 0.  Done
+        // here, not in the plan: the plan may run while an earlier Adam still
+        // counts this block's last updates; the gather waits for that Adam
+        if (d.cold) d.step[l] = 0u;
         if (d.ent_of) d.ent_of[l] = (int32_t)d.sp_entry[i];  // store tier: entry of a resident block
         if (tg >= 0 && tg >= T - 2) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
       }

@@ -88,12 +88,22 @@ struct tgs_ctx {
   // streams / events (ev_*[p]: last record by an activate of parity p)
   cudaStream_t compute = nullptr, plan = nullptr, h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_plan = nullptr;
-  cudaEvent_t ev_ready[2] = {}, ev_lists[2] = {};
+  // lists of activate T (S+, S-, K^(j), header, camera batch, A) live in list slot
+  // T % 3: the plan of T+3 reuses them once their consumers of T are done
+  cudaEvent_t ev_ready[3] = {}, ev_lists[3] = {};
+  cudaEvent_t ev_refresh[2] = {};  // R25: the refresh of the step of that parity done
+  bool rec_refresh[2] = {};
+  uint32_t *l3_percam[3] = {}, *l3_sp_blk[3] = {}, *l3_sp_slot[3] = {}, *l3_sm_blk[3] = {},
+           *l3_sm_slot[3] = {};
+  PlanHdr* l3_hdr[3] = {};
+  float4* l3_planes[3] = {};
+  const float4* l3_planes_map[3] = {};
   cudaEvent_t ev_evict[kRings] = {}, ev_d2h[kRings] = {};  // by ring slot T % 3
   cudaEvent_t ev_job[4] = {};      // write-back of activate J done: ev_job[J & 3] (store mode)
-  bool rec_ready[2] = {}, rec_lists[2] = {}, rec_evict[kRings] = {};
+  bool rec_ready[3] = {}, rec_lists[3] = {}, rec_evict[kRings] = {};
   int32_t d2h_job[kRings] = {-1, -1, -1};  // activate whose write-back last used ring slot k
   bool ring_direct[kRings] = {};   // ... and whether it wrote back straight from its slots
+  int last_evict_ring = -1;        // ring slot of the most recent write-back kernels
   // a4 transfer kernels: CTAs of the gather (h2d) and the write-back (d2h)
   // (TGS_GATHER_CTAS / TGS_SCATTER_CTAS; defaults from profiles/linkbench2_r02.txt)
   int gather_ctas = 8, scatter_ctas = 4, gather_bufs = 4, scatter_bufs = 4;
@@ -104,9 +114,9 @@ struct tgs_ctx {
   // C1 / C2 collectives (tgs_set_comm)
   tgs_comm comm{};
   bool has_comm = false;
-  uint32_t* c1_recv[2] = {nullptr, nullptr};  // [G][C] gathered A lists (parity)
+  uint32_t* c1_recv[3] = {};  // [G][C] gathered A lists (list slot)
   unsigned long long* c2_buf = nullptr;       // [ST_N] summed cumulative counters
-  cudaEvent_t ev_c1[2] = {nullptr, nullptr};
+  cudaEvent_t ev_c1[3] = {};
   // I/O thread (store tier: marks the CPU-cache entries of each write-back dirty)
   struct Job { int32_t T; int parity; bool direct; };
   std::thread io;
@@ -320,14 +330,23 @@ tgs_status ensure_lut(tgs_ctx* c, float b1, float b2, uint32_t need) {
   return TGS_OK;
 }
 
-// the device state as the kernels of activate T (parity p) see it: its A lists
-// come from the 3-deep ring
+// the device state as the kernels of activate T (parity p) see it: its lists
+// (the kernels index them by parity) come from list slot T % 3; R and the
+// pending refresh radii stay parity-indexed
 inline Dev dev_for(const tgs_ctx* c, int p, int32_t T) {
   Dev x = c->d;
   const int r = (int)(((uint32_t)T) % 3u);
   x.a_blk[p] = c->a3_blk[r];
   x.a_slot[p] = c->a3_slot[r];
   x.a_gid[p] = c->a3_gid[r];
+  x.percam[p] = c->l3_percam[r];
+  x.sp_blk[p] = c->l3_sp_blk[r];
+  x.sp_slot[p] = c->l3_sp_slot[r];
+  x.sm_blk[p] = c->l3_sm_blk[r];
+  x.sm_slot[p] = c->l3_sm_slot[r];
+  x.hdr_dev[p] = c->l3_hdr[r];
+  x.last_planes[p] = c->l3_planes[r];
+  x.planes_map[p] = c->l3_planes_map[r];
   return x;
 }
 
@@ -542,10 +561,10 @@ void destroy_impl(tgs_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_c1)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_evict[0],
-                        c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
-                        c->ev_d2h[2], c->ev_lists[0],
-                        c->ev_lists[1], c->trace_base})
+  for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_ready[2],
+                        c->ev_evict[0], c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
+                        c->ev_d2h[2], c->ev_lists[0], c->ev_lists[1], c->ev_lists[2],
+                        c->ev_refresh[0], c->ev_refresh[1], c->trace_base})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -655,10 +674,11 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
-  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_probe, &c->ev_ready[0],
-                         &c->ev_ready[1], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
+  for (cudaEvent_t* e : {&c->ev_plan, &c->ev_probe, &c->ev_ready[0], &c->ev_ready[1],
+                         &c->ev_ready[2], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
                          &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_d2h[2], &c->ev_lists[0],
-                         &c->ev_lists[1], &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
+                         &c->ev_lists[1], &c->ev_lists[2], &c->ev_refresh[0], &c->ev_refresh[1],
+                         &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
                          &c->ev_job[3]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
 
@@ -708,7 +728,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaHostAlloc((void**)&c->dirty_map[1], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[2], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * kRings, cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 3 * kMaxCams * 24,
+      cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 4 * kMaxCams * 24,
                     cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->probe_map, sizeof(uint32_t) * std::max(d.W, 1u),
                     cudaHostAllocMapped) != cudaSuccess) {
@@ -739,10 +759,10 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   for (int k = 0; k < kRings; ++k)
     cudaHostGetDevicePointer((void**)&d.dirty_map[k], c->dirty_map[k], 0);
   cudaHostGetDevicePointer((void**)&d.ndirty_map, c->ndirty, 0);
-  for (int p = 0; p < 2; ++p) {
+  for (int r = 0; r < 3; ++r) {
     float* dp = nullptr;
-    cudaHostGetDevicePointer((void**)&dp, c->planes_pinned + (size_t)p * kMaxCams * 24, 0);
-    d.planes_map[p] = reinterpret_cast<const float4*>(dp);
+    cudaHostGetDevicePointer((void**)&dp, c->planes_pinned + (size_t)r * kMaxCams * 24, 0);
+    c->l3_planes_map[r] = reinterpret_cast<const float4*>(dp);
   }
 
   // ---- device state
@@ -755,23 +775,28 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   d.ever = dalloc_t<uint8_t>(c, Kl, ok);
   d.evicted = dalloc_t<uint8_t>(c, Kl, ok);
   d.admit = dalloc_t<int32_t>(c, Kl, ok);
-  d.percam[0] = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
-  d.percam[1] = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
+  for (int r = 0; r < 3; ++r) c->l3_percam[r] = dalloc_t<uint32_t>(c, (size_t)d.J_max * Wd, ok);
   for (uint32_t** p : {&d.Kb, &d.cand, &d.Q, &d.Sp, &d.Sm, &d.Om, &d.Ab, &d.R[0], &d.R[1]})
     *p = dalloc_t<uint32_t>(c, Wd, ok);
   d.s2b = dalloc_t<int32_t>(c, P, ok);
   d.occ = dalloc_t<uint32_t>(c, d.PW, ok);
   d.dirty = dalloc_t<uint32_t>(c, d.PW, ok);
   d.rel = dalloc_t<uint32_t>(c, d.PW, ok);
+  for (int r = 0; r < 3; ++r) {
+    c->l3_sp_blk[r] = dalloc_t<uint32_t>(c, Cc, ok);
+    c->l3_sp_slot[r] = dalloc_t<uint32_t>(c, Cc, ok);
+    c->l3_sm_blk[r] = dalloc_t<uint32_t>(c, Cc, ok);
+    c->l3_sm_slot[r] = dalloc_t<uint32_t>(c, Cc, ok);
+    c->l3_hdr[r] = dalloc_t<PlanHdr>(c, 1, ok);
+    c->l3_planes[r] = dalloc_t<float4>(c, kMaxCams * 6, ok);
+  }
   for (int p = 0; p < 2; ++p) {
-    d.sp_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
-    d.sp_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
-    d.sm_blk[p] = dalloc_t<uint32_t>(c, Cc, ok);
-    d.sm_slot[p] = dalloc_t<uint32_t>(c, Cc, ok);
+    d.percam[p] = d.sp_blk[p] = d.sp_slot[p] = d.sm_blk[p] = d.sm_slot[p] = nullptr;  // per launch
+    d.hdr_dev[p] = nullptr;
+    d.last_planes[p] = nullptr;
+    d.planes_map[p] = nullptr;
     d.a_blk[p] = d.a_slot[p] = d.a_gid[p] = nullptr;  // per launch, from the ring below
   }
-  d.hdr_dev[0] = dalloc_t<PlanHdr>(c, 1, ok);
-  d.hdr_dev[1] = dalloc_t<PlanHdr>(c, 1, ok);
   d.cnt = dalloc_t<uint32_t>(c, CNT_N, ok);
   d.stats = dalloc_t<unsigned long long>(c, ST_ALL, ok);
   d.nonfinite = dalloc_t<unsigned long long>(c, 1, ok);
@@ -788,8 +813,6 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (c->store) d.ent_of = dalloc_t<int32_t>(c, Kl, ok);
   d.pend[0] = dalloc_t<uint32_t>(c, Kl, ok);
   d.pend[1] = dalloc_t<uint32_t>(c, Kl, ok);
-  d.last_planes[0] = dalloc_t<float4>(c, kMaxCams * 6, ok);
-  d.last_planes[1] = dalloc_t<float4>(c, kMaxCams * 6, ok);
   d.ndirty_dev = dalloc_t<uint32_t>(c, kRings, ok);
   d.wb_tag = dalloc_t<int32_t>(c, Kl, ok);
   d.wb_idx = dalloc_t<uint32_t>(c, Kl, ok);
@@ -833,16 +856,16 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   CKI(cudaMemsetAsync(d.ndirty_dev, 0, sizeof(uint32_t) * kRings, s0));
   for (uint32_t* p : {d.Kb, d.cand, d.Q, d.Sp, d.Sm, d.Om, d.Ab, d.R[0], d.R[1]})
     CKI(cudaMemsetAsync(p, 0, sizeof(uint32_t) * Wd, s0));
-  for (int p = 0; p < 2; ++p)
-    CKI(cudaMemsetAsync(d.percam[p], 0, sizeof(uint32_t) * (size_t)d.J_max * Wd, s0));
+  for (int r = 0; r < 3; ++r) {
+    CKI(cudaMemsetAsync(c->l3_percam[r], 0, sizeof(uint32_t) * (size_t)d.J_max * Wd, s0));
+    CKI(cudaMemsetAsync(c->l3_hdr[r], 0, sizeof(PlanHdr), s0));
+  }
   CKI(cudaMemsetAsync(d.s2b, 0xff, sizeof(int32_t) * P, s0));
   CKI(cudaMemsetAsync(d.occ, 0, sizeof(uint32_t) * d.PW, s0));
   CKI(cudaMemsetAsync(d.dirty, 0, sizeof(uint32_t) * d.PW, s0));
   CKI(cudaMemsetAsync(d.stats, 0, sizeof(unsigned long long) * ST_ALL, s0));
   CKI(cudaMemsetAsync(d.cnt, 0, sizeof(uint32_t) * CNT_N, s0));  // k_plan re-zeroes it after use
   CKI(cudaMemsetAsync(d.nonfinite, 0xff, sizeof(unsigned long long), s0));
-  CKI(cudaMemsetAsync(d.hdr_dev[0], 0, sizeof(PlanHdr), s0));
-  CKI(cudaMemsetAsync(d.hdr_dev[1], 0, sizeof(PlanHdr), s0));
   CKI(cudaMemsetAsync(d.params, 0, sizeof(float) * pool_floats, s0));
   CKI(cudaMemsetAsync(d.grads, 0, sizeof(float) * grad_floats, s0));
   if (d.geo6) CKI(cudaMemsetAsync(d.geo6, 0, sizeof(float) * (size_t)P * d.B * 6, s0));
@@ -875,7 +898,8 @@ tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
   // on (that plan merges the refreshed radii, R25), they stay in use until the
   // end of this step's compute work.
   const bool lists_late = c->d.refresh || c->lists_after_adam;
-  if (!lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));
+  const int m = (int)(((uint32_t)c->T + 2) % 3u);  // list slot of the last activate
+  if (!lists_late) CK(cudaEventRecord(c->ev_lists[m], c->compute));
   prof_begin(c, c->compute, t2);
   CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
@@ -884,7 +908,11 @@ tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
     CK(launch_refresh(dk, nA, p, c->compute));
     c->tm.kernel_launches++;
   }
-  if (lists_late) CK(cudaEventRecord(c->ev_lists[p], c->compute));  // lists of p in use until here
+  if (lists_late) CK(cudaEventRecord(c->ev_lists[m], c->compute));  // lists in use until here
+  if (c->d.refresh) {  // the cull two batches later merges these radii (R25)
+    CK(cudaEventRecord(c->ev_refresh[p], c->compute));
+    c->rec_refresh[p] = true;
+  }
   return TGS_OK;
 }
 
@@ -921,20 +949,24 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
       for (int i = 0; i < 4; ++i)
         if (!std::isfinite(cams[j].plane[p][i])) return TGS_EINVAL;
   Dev& d = c->d;
-  const int p = c->parity;  // parity of R_t; lists of this activate go to slot p
-  const int q = p ^ 1;      // parity of the previous activate
+  const int p = c->parity;  // parity of R_t (R and the pending refresh radii)
   const int32_t T = c->T;
+  const int m = (int)(((uint32_t)T) % 3u), mq = (int)(((uint32_t)T + 2) % 3u);  // list slots T, T-1
 
   // ---- plan stream: a1 cull, a3 quota + fill, a2 delta, slots, A list.
-  //      The lists of parity p are free once activate t-2's Adam, write-back
-  //      kernels and gather are done (GPU-side waits only).  The camera batch is
+  //      List slot m is free once activate T-3's consumers are done (Adam or its
+  //      prologue, the Level-2 filter, the write-back kernels, the gather):
+  //      GPU-side waits only, so the plan may run up to two batches ahead of
+  //      Adam.  With the bound refresh on, the cull merges the radii of the step
+  //      two batches back (R25): it waits for that refresh.  The camera batch is
   //      read from mapped pinned memory by k_planes: nothing here queues behind
   //      a copy engine.
-  if (c->rec_lists[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_lists[p], 0));
-  if (c->rec_ready[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_ready[p], 0));
+  if (c->rec_lists[m]) CK(cudaStreamWaitEvent(c->plan, c->ev_lists[m], 0));
+  if (c->rec_ready[m]) CK(cudaStreamWaitEvent(c->plan, c->ev_ready[m], 0));
+  if (d.refresh && c->rec_refresh[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_refresh[p], 0));
   Timer tp;
-  // the batch of t-2 (same staging buffer) was consumed before that plan's readback
-  if (J) std::memcpy(c->planes_pinned + (size_t)p * kMaxCams * 24, cams, sizeof(float) * 24 * J);
+  // the batch of T-3 (same staging buffer) was consumed before that plan's readback
+  if (J) std::memcpy(c->planes_pinned + (size_t)m * kMaxCams * 24, cams, sizeof(float) * 24 * J);
   prof_begin(c, c->plan, tp);
   const Dev dk = dev_for(c, p, T);
   CK(launch_cull(dk, J, T, p, c->plan));
@@ -962,7 +994,9 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   const int k1 = (int)(((uint32_t)T + 2) % kRings), k2 = (int)(((uint32_t)T + 1) % kRings);
   auto gather_waits = [&]() -> tgs_status {
     CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
-    if (c->rec_evict[k1]) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[k1], 0));  // slots of T-1 free
+    // every slot this gather may fill was freed by an earlier write-back, whose
+    // k_evict / k_pack ran after the last Adam on it: wait for the newest one
+    if (c->last_evict_ring >= 0) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[c->last_evict_ring], 0));
     for (int r : {k1, k2})  // a direct write-back (T-1, T-2) has no ring copy: wait for it
       if (c->d2h_job[r] >= 0 && c->ring_direct[r]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[r], 0));
     if (c->d2h_job[k] >= 0 && c->d2h_job[k] <= T - 3) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
@@ -976,8 +1010,8 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     CK(launch_xfer(dg, 0, p, k, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
     c->h2d_prof = prof_end(c, c->h2d, th, 3);
     c->tm.kernel_launches++;
-    CK(cudaEventRecord(c->ev_ready[p], c->h2d));
-    c->rec_ready[p] = true;
+    CK(cudaEventRecord(c->ev_ready[m], c->h2d));
+    c->rec_ready[m] = true;
     return TGS_OK;
   };
   const bool early = !c->store && d.tide && d.P >= 2u * d.C;
@@ -1009,7 +1043,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
     // ring slot k held T-3's records, which the previous activate's gather may
     // re-admit from: it must be done
-    if (c->rec_ready[q]) CK(cudaStreamWaitEvent(c->compute, c->ev_ready[q], 0));
+    if (c->rec_ready[mq]) CK(cudaStreamWaitEvent(c->compute, c->ev_ready[mq], 0));
     if (c->d2h_job[k] >= 0) {
       // the write-back of T-3 must be done with ring slot k (its ring, dirty
       // lists; store tier: the I/O job's read of dirty_map[k] / ndirty[k])
@@ -1017,15 +1051,16 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
       CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[k], 0));
     }
     prof_begin(c, c->compute, te);
-    CK(launch_evict_tagged(d, h.nSm, p, k, T, !direct, c->compute));
-    if (!direct) CK(launch_pack(d, h.nSm, k, c->compute));
+    CK(launch_evict_tagged(dg, h.nSm, p, k, T, !direct, c->compute));
+    if (!direct) CK(launch_pack(dg, h.nSm, k, c->compute));
     prof_end(c, c->compute, te, 5);
     c->tm.kernel_launches += direct ? 1 : 2;
     CK(cudaEventRecord(c->ev_evict[k], c->compute));
     c->rec_evict[k] = true;
+    c->last_evict_ring = k;
     CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[k], 0));
     prof_begin(c, c->d2h, td);
-    CK(launch_xfer(d, direct ? 2 : 1, p, k, T, nullptr, 0, h.nSm, c->scatter_ctas,
+    CK(launch_xfer(dg, direct ? 2 : 1, p, k, T, nullptr, 0, h.nSm, c->scatter_ctas,
                    c->scatter_bufs, c->d2h));
     prof_end(c, c->d2h, td, 4);
     c->tm.kernel_launches++;
@@ -1101,8 +1136,8 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     }
     st = launch_subset(1);
     if (st != TGS_OK) return st;
-    CK(cudaEventRecord(c->ev_ready[p], c->h2d));
-    c->rec_ready[p] = true;
+    CK(cudaEventRecord(c->ev_ready[m], c->h2d));
+    c->rec_ready[m] = true;
     // R27 (c): the blocks that left the GPU are accesses of the CPU cache too
     if (h.nSm) c->store->touch_evicted(c->sm_map, h.nSm, T);
   }
@@ -1113,25 +1148,25 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   }
   // lists of parity p stay in use until this batch's write-back kernels (and
   // its Adam, which re-records this event) are done
-  CK(cudaEventRecord(c->ev_lists[p], c->compute));
-  c->rec_lists[p] = true;
+  CK(cudaEventRecord(c->ev_lists[m], c->compute));
+  c->rec_lists[m] = true;
 
   // ---- C1: the active set of every rank, on the plan stream
   //      after k_plan; every rank calls it once per activate
   if (c->has_comm) {
     uint32_t* send = c->a3_gid[(uint32_t)T % 3u];
-    CK(launch_pad_active(send, d.hdr_dev[p], d.C, c->plan));
+    CK(launch_pad_active(send, dk.hdr_dev[p], d.C, c->plan));
     c->tm.kernel_launches++;
-    if (c->comm.allgather(c->comm.user, send, c->c1_recv[p], sizeof(uint32_t) * d.C,
+    if (c->comm.allgather(c->comm.user, send, c->c1_recv[m], sizeof(uint32_t) * d.C,
                           (void*)c->plan) != 0) {
       c->poisoned = true;
       set_err(c, "C1 all-gather failed (activate %d)", T);
       return TGS_ENCCL;
     }
-    CK(cudaEventRecord(c->ev_c1[p], c->plan));
+    CK(cudaEventRecord(c->ev_c1[m], c->plan));
   }
   c->last_parity = p;
-  c->parity = q;
+  c->parity = p ^ 1;
   c->T = T + 1;
   c->can_step = true;
   if (c->cfg.serialize) {  // ablation w/o Overlap: I/O completes before compute starts
@@ -1152,10 +1187,10 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     out->d_grads = d.grads;
     out->slot_stride = 3 * d.rec_floats;
     out->grad_stride = d.rec_floats;
-    out->ready = (void*)c->ev_ready[p];
-    out->d_global_active = c->has_comm ? c->c1_recv[p] : nullptr;
+    out->ready = (void*)c->ev_ready[m];
+    out->d_global_active = c->has_comm ? c->c1_recv[m] : nullptr;
     out->global_stride = d.C;
-    out->global_ready = c->has_comm ? (void*)c->ev_c1[p] : nullptr;
+    out->global_ready = c->has_comm ? (void*)c->ev_c1[m] : nullptr;
   }
   return TGS_OK;
 }
@@ -1179,7 +1214,7 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   h.omb2 = 1.0f - hp->beta2;
   h.eps = hp->eps;
   CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-  CK(cudaStreamWaitEvent(c->compute, c->ev_ready[p], 0));
+  CK(cudaStreamWaitEvent(c->compute, c->ev_ready[((uint32_t)c->T + 2) % 3u], 0));
   st = nA ? adam_launches(c, p, nA, h, d_row_mask) : TGS_OK;
   if (st != TGS_OK) return st;
   // ---- C2: every rank's cumulative counters summed, after this
@@ -1206,14 +1241,15 @@ tgs_status tgs_fine_filter(tgs_ctx* c, uint32_t* d_row_mask) {
   const int p = c->last_parity;
   // reads theta of every A slot: after the plan and the gather of this batch
   CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-  CK(cudaStreamWaitEvent(c->compute, c->ev_ready[p], 0));
+  const int m = (int)(((uint32_t)c->T + 2) % 3u);  // list slot of the last activate
+  CK(cudaStreamWaitEvent(c->compute, c->ev_ready[m], 0));
   if (c->last.nA == 0 || c->d.Kloc == 0) return TGS_OK;
   Timer tf;
   prof_begin(c, c->compute, tf);
   CK(launch_fine(dev_for(c, p, c->T - 1), c->last.nA, c->last_J, p, d_row_mask, c->compute));
   prof_end(c, c->compute, tf, 8);
   c->tm.kernel_launches++;
-  CK(cudaEventRecord(c->ev_lists[p], c->compute));  // k_fine reads this parity's K^(j)
+  CK(cudaEventRecord(c->ev_lists[m], c->compute));  // k_fine reads this slot's K^(j)
   return TGS_OK;
 }
 
@@ -1265,11 +1301,10 @@ tgs_status tgs_set_comm(tgs_ctx* c, const tgs_comm* comm) {
   if (c->T != 0 || c->has_comm) return TGS_ESTATE;
   bool ok = true;
   const size_t rows = (size_t)c->cfg.world_size * std::max(c->d.C, 1u);
-  c->c1_recv[0] = dalloc_t<uint32_t>(c, rows, ok);
-  c->c1_recv[1] = dalloc_t<uint32_t>(c, rows, ok);
+  for (int r = 0; r < 3; ++r) c->c1_recv[r] = dalloc_t<uint32_t>(c, rows, ok);
   c->c2_buf = dalloc_t<unsigned long long>(c, ST_N, ok);
   if (!ok) return TGS_ENOMEM;
-  for (cudaEvent_t* e : {&c->ev_c1[0], &c->ev_c1[1]})
+  for (cudaEvent_t* e : {&c->ev_c1[0], &c->ev_c1[1], &c->ev_c1[2]})
     CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   CK(cudaMemsetAsync(c->c2_buf, 0, sizeof(unsigned long long) * ST_N, c->compute));
   CK(cudaStreamSynchronize(c->compute));
@@ -1387,7 +1422,8 @@ uint32_t tgs_get_percam(tgs_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap) 
   if (sync_all(c) != TGS_OK) return 0;
   Dev& d = c->d;
   std::vector<uint32_t> bits(std::max(d.W, 1u));
-  if (cudaMemcpy(bits.data(), d.percam[c->last_parity] + (size_t)j * d.W, sizeof(uint32_t) * d.W,
+  if (cudaMemcpy(bits.data(), c->l3_percam[((uint32_t)c->T - 1) % 3u] + (size_t)j * d.W,
+                 sizeof(uint32_t) * d.W,
                  cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
   uint32_t n = 0;
@@ -1598,10 +1634,10 @@ tgs_status tgs_frustum_planes(const double w2c[16], double fx, double fy, double
 }
 
 // ---- NEXT f3 inspection
-tgs_status tgs_prefetch(tgs_ctx* c, const tgs_camera* cams, uint32_t J) {
+tgs_status tgs_prefetch(tgs_ctx* c, const tgs_camera* cams, uint32_t J, uint32_t ahead) {
   tgs_status st = check(c);
   if (st != TGS_OK) return st;
-  if (J > c->d.J_max || (J > 0 && !cams)) return TGS_EINVAL;
+  if (J > c->d.J_max || (J > 0 && !cams) || ahead == 0) return TGS_EINVAL;
   for (uint32_t j = 0; j < J; ++j)
     for (int p = 0; p < 6; ++p)
       for (int i = 0; i < 4; ++i)
@@ -1609,7 +1645,7 @@ tgs_status tgs_prefetch(tgs_ctx* c, const tgs_camera* cams, uint32_t J) {
   if (!c->store || J == 0 || c->d.Kloc == 0) return TGS_OK;
   // the third staging buffer: k_probe reads it on the plan stream, and the host
   // waits for that before returning, so the next prefetch may reuse it
-  float* pl = c->planes_pinned + (size_t)2 * kMaxCams * 24;
+  float* pl = c->planes_pinned + (size_t)3 * kMaxCams * 24;
   std::memcpy(pl, cams, sizeof(float) * 24 * J);
   float* pl_dev = nullptr;
   uint32_t* out_dev = nullptr;
@@ -1623,7 +1659,7 @@ tgs_status tgs_prefetch(tgs_ctx* c, const tgs_camera* cams, uint32_t J) {
   for (uint32_t w = 0; w < c->d.W; ++w)
     for (uint32_t bits = c->probe_map[w]; bits; bits &= bits - 1)
       blocks.push_back(32u * w + (uint32_t)__builtin_ctz(bits));
-  c->store->prefetch(blocks);
+  c->store->prefetch(blocks, c->T + (int32_t)ahead - 1);
   return TGS_OK;
 }
 

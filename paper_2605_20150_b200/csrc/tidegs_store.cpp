@@ -297,6 +297,7 @@ void BlockStore::init_buffers() {
   for (uint32_t b = H_ + X_; b-- > H_;) ra_free_.push_back(b);
   ra_buf_.assign(g_.Kloc, -1);
   ra_ver_.assign(g_.Kloc, 0);
+  ra_seq_.assign(g_.Kloc, 0);
   ra_fifo_.clear();
 }
 
@@ -308,15 +309,20 @@ void BlockStore::init_buffers() {
 // blocks are cached, the LRU order, dirty bits, Index) is not touched: the next
 // gather, for a miss whose read-ahead record still holds the newest version,
 // swaps that buffer into the miss's entry instead of reading the SSD.
-void BlockStore::prefetch(const std::vector<uint32_t>& blocks) {
+void BlockStore::prefetch(const std::vector<uint32_t>& blocks, int32_t target) {
   if (!X_) return;
-  pf_join();
+  uint64_t done;
+  {
+    std::lock_guard<std::mutex> g(pf_mu_);
+    done = pf_done_;
+  }
+  const uint64_t seq = pf_issued_ + 1;
   std::vector<PfItem> batch;
   for (uint32_t l : blocks) {
     if (ent_of_[l] >= 0 || ra_buf_[l] >= 0) continue;  // cached, or already read ahead
-    if (ra_free_.empty()) {  // recycle the oldest read-ahead record
+    if (ra_free_.empty()) {  // recycle the oldest completed read-ahead record
       while (!ra_fifo_.empty() && ra_buf_[ra_fifo_.front()] < 0) ra_fifo_.pop_front();
-      if (ra_fifo_.empty()) break;
+      if (ra_fifo_.empty() || ra_seq_[ra_fifo_.front()] > done) break;  // all still in flight
       const uint32_t o = ra_fifo_.front();
       ra_fifo_.pop_front();
       ra_free_.push_back((uint32_t)ra_buf_[o]);
@@ -327,62 +333,67 @@ void BlockStore::prefetch(const std::vector<uint32_t>& blocks) {
     ra_free_.pop_back();
     ra_buf_[l] = (int32_t)b;
     ra_ver_[l] = index_[l].version;
+    ra_seq_[l] = seq;
     ra_fifo_.push_back(l);
     // the file and offset are taken here, on the caller's thread (segments are
     // opened and Index changes only there)
     batch.push_back({b, fd_of(index_[l].file_id), index_[l].offset});
   }
   if (batch.empty()) return;
+  pf_issued_ = seq;
+  pf_target_.push_back({seq, target});
   {
     std::lock_guard<std::mutex> g(pf_mu_);
-    pf_batch_ = std::move(batch);
-    pf_busy_ = true;
+    pf_q_.push_back({seq, std::move(batch)});
   }
   pf_cv_.notify_all();
 }
 
+// batches are read in order; pf_done_ = the last batch read completely
 void BlockStore::pf_main() {
   for (;;) {
+    uint64_t seq;
     std::vector<PfItem> batch;
     {
       std::unique_lock<std::mutex> g(pf_mu_);
-      pf_cv_.wait(g, [&] { return pf_stop_ || pf_busy_; });
+      pf_cv_.wait(g, [&] { return pf_stop_ || !pf_q_.empty(); });
       if (pf_stop_) return;
-      batch = pf_batch_;
+      seq = pf_q_.front().first;
+      batch = pf_q_.front().second;
     }
-    std::atomic<bool> bad{false};
+    std::vector<uint8_t> bad(batch.size(), 0);
     pf_pool_->parallel_for((uint32_t)batch.size(), [&](uint32_t i) {
       const PfItem& it = batch[i];
-      if (it.fd < 0 || !pread_all(it.fd, pool_ + (uint64_t)it.buf * S_, S_, it.off)) bad = true;
+      if (it.fd < 0 || !pread_all(it.fd, pool_ + (uint64_t)it.buf * S_, S_, it.off)) bad[i] = 1;
     });
     {
       std::lock_guard<std::mutex> g(pf_mu_);
-      pf_bad_ = pf_bad_ || bad;
+      for (size_t i = 0; i < batch.size(); ++i)
+        if (bad[i]) pf_badbuf_[batch[i].buf] = 1;  // dropped at use; the gather reads itself
       cnt_.prefetch_reads += batch.size();
-      pf_busy_ = false;
+      pf_q_.pop_front();
+      pf_done_ = seq;
     }
     pf_cv_.notify_all();
   }
 }
 
-void BlockStore::pf_join() {
-  if (!X_) return;
+// waits until every read-ahead batch up to `upto` has been read; returns the
+// last completed batch
+uint64_t BlockStore::pf_wait(uint64_t upto) {
+  if (!X_) return 0;
   std::unique_lock<std::mutex> g(pf_mu_);
-  pf_cv_.wait(g, [&] { return !pf_busy_; });
-  if (pf_bad_) {  // a failed read-ahead is dropped; the gather reads those blocks itself
-    for (uint32_t l = 0; l < g_.Kloc; ++l)
-      if (ra_buf_[l] >= 0) {
-        ra_free_.push_back((uint32_t)ra_buf_[l]);
-        ra_buf_[l] = -1;
-      }
-    pf_bad_ = false;
-  }
+  pf_cv_.wait(g, [&] { return pf_done_ >= upto; });
+  return pf_done_;
 }
+
+void BlockStore::pf_join() { pf_wait(pf_issued_); }
 
 void BlockStore::start_prefetch(uint32_t X, int threads) {
   X_ = X;
   ra_free_.clear();  // buffers H .. H+X-1 of the pool
   for (uint32_t b = H_ + X_; b-- > H_;) ra_free_.push_back(b);
+  pf_badbuf_.assign((size_t)H_ + X_, 0);
   if (!X_) return;
   pf_pool_ = new IoPool(std::max(1, threads));
   pf_thread_ = std::thread([this] { pf_main(); });
@@ -709,7 +720,14 @@ std::string BlockStore::write_records(const std::vector<std::pair<uint32_t, int3
 std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
                                const std::function<void(int32_t)>& wait_d2h,
                                const std::function<void(const std::vector<uint8_t>&)>& hits_ready) {
-  pf_join();  // the read-ahead records of the announced batch have landed
+  // the read-ahead batches announced for this activate or earlier have landed
+  // (batches for later activates may still be reading)
+  uint64_t upto = 0;
+  while (!pf_target_.empty() && pf_target_.front().second <= T) {
+    upto = pf_target_.front().first;
+    pf_target_.pop_front();
+  }
+  const uint64_t pf_done = pf_wait(upto);
   // every S+ block is in R_{t+1}: its entry (if cached) is not evictable (R27)
   for (uint32_t i = 0; i < n; ++i) {
     const int32_t e = ent_of_[sp[2 * i]];
@@ -772,12 +790,24 @@ std::string BlockStore::gather(const uint32_t* sp, uint32_t n, int32_t T,
     std::vector<std::pair<uint32_t, int32_t>> rest;
     for (auto& m : misses) {
       const int32_t b = ra_buf_[m.first];
-      if (b >= 0 && ra_ver_[m.first] == index_[m.first].version) {
+      const bool complete = b >= 0 && ra_seq_[m.first] <= pf_done;
+      bool bad = false;
+      if (complete) {
+        std::lock_guard<std::mutex> g(pf_mu_);
+        bad = pf_badbuf_[b] != 0;
+        pf_badbuf_[b] = 0;
+      }
+      if (complete && !bad && ra_ver_[m.first] == index_[m.first].version) {
         ra_free_.push_back(buf_of_[m.second]);
         buf_of_[m.second] = (uint32_t)b;
         ra_buf_[m.first] = -1;
         cnt_.prefetch_hits += 1;
       } else {
+        if (complete) {  // stale or failed: released; an in-flight one finishes first
+          ra_free_.push_back((uint32_t)b);
+          ra_buf_[m.first] = -1;
+          cnt_.prefetch_wasted += 1;
+        }
         rest.push_back(m);
       }
     }

@@ -121,8 +121,8 @@ class BlockStore {
   int32_t entry_index(uint32_t l) const { return ent_of_[l] < 0 ? -1 : (int32_t)buf_of_[ent_of_[l]]; }
   // read-ahead (prefetch): X extra pool buffers (pool holds H + X) and threads
   void start_prefetch(uint32_t X, int threads);
-  // the blocks the next activate may need (its Level-1 visible set); returns at once
-  void prefetch(const std::vector<uint32_t>& blocks);
+  // the blocks activate `target` may need (its Level-1 visible set); returns at once
+  void prefetch(const std::vector<uint32_t>& blocks, int32_t target);
   // waits for the read-ahead batch in flight (counters are then settled)
   void settle() { pf_join(); }
   // newest version of block l (cache, else SSD) into dst (payload bytes)
@@ -154,6 +154,7 @@ class BlockStore {
   std::string write_manifest();
   void init_buffers();
   void pf_main();
+  uint64_t pf_wait(uint64_t upto);
   void pf_join();
   // reserves the next record of the patch log for block l: (fd, file offset of the record)
   std::string reserve_append(uint32_t l, int& fd, uint64_t& rec_off);
@@ -187,14 +188,18 @@ class BlockStore {
   std::vector<uint32_t> ra_free_;
   std::vector<int32_t> ra_buf_;    // [Kloc] read-ahead buffer of block l, -1 none
   std::vector<uint64_t> ra_ver_;   // [Kloc] Index version it was read at
+  std::vector<uint64_t> ra_seq_;   // [Kloc] read-ahead batch it belongs to
   std::deque<uint32_t> ra_fifo_;   // blocks in read-ahead, oldest first
   IoPool* pf_pool_ = nullptr;
   std::thread pf_thread_;
   std::mutex pf_mu_;
   std::condition_variable pf_cv_;
   struct PfItem { uint32_t buf; int fd; uint64_t off; };
-  std::vector<PfItem> pf_batch_;
-  bool pf_busy_ = false, pf_stop_ = false, pf_bad_ = false;
+  std::deque<std::pair<uint64_t, std::vector<PfItem>>> pf_q_;  // batches waiting / in flight
+  uint64_t pf_issued_ = 0, pf_done_ = 0;  // batches announced / read completely
+  std::deque<std::pair<uint64_t, int32_t>> pf_target_;  // (batch, activate it targets)
+  std::vector<uint8_t> pf_badbuf_;        // [H + X] a read-ahead read into it failed
+  bool pf_stop_ = false;
   size_t hdr_cap_ = 0;
 };
 

@@ -165,7 +165,7 @@ def lib():
         L.tgs_fine_filter.argtypes = [vp, vp]
         L.tgs_get_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_set_comm.argtypes = [vp, C.POINTER(Comm)]
-        L.tgs_prefetch.argtypes = [vp, C.c_void_p, u32]
+        L.tgs_prefetch.argtypes = [vp, C.c_void_p, u32, u32]
         L.tgs_get_global_stats.argtypes = [vp, C.POINTER(Stats)]
         L.tgs_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.tgs_get_stats_async.argtypes = [vp, vp]
@@ -369,11 +369,11 @@ class Table:
             raise TgsError(rc, what, lib().tgs_last_error(self.h).decode(errors="replace"))
 
     # ---- the hot path
-    def prefetch(self, planes: np.ndarray):
-        """announce the next activate's camera batch (store tier read-ahead, f3)"""
+    def prefetch(self, planes: np.ndarray, ahead: int = 1):
+        """announce the camera batch of the activate `ahead` calls from now (f3 read-ahead)"""
         p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)
-        self._err(lib().tgs_prefetch(self.h, p.ctypes.data if p.shape[0] else None, p.shape[0]),
-                  "tgs_prefetch")
+        self._err(lib().tgs_prefetch(self.h, p.ctypes.data if p.shape[0] else None, p.shape[0],
+                                     ahead), "tgs_prefetch")
 
     def activate(self, planes: np.ndarray, *, check=True) -> Activation:
         p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)

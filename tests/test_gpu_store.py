@@ -32,7 +32,10 @@ def _compare_files(g, o):
     gf, of = sorted(os.listdir(g)), sorted(os.listdir(o))
     assert gf == of, (gf, of)
     for name in gf:
-        assert filecmp.cmp(g / name, o / name, shallow=False), name
+        if not filecmp.cmp(g / name, o / name, shallow=False):
+            a, b = (g / name).read_bytes(), (o / name).read_bytes()
+            first = next((i for i in range(min(len(a), len(b))) if a[i] != b[i]), None)
+            raise AssertionError(f"{name}: sizes {len(a)} / {len(b)}, first difference at {first}")
     return len(gf)
 
 
@@ -240,8 +243,9 @@ def test_store_full_size_100m_index_parity(tmp_path):
     shutil.rmtree(d, ignore_errors=True)  # 23.6 GB: do not leave it to pytest's tmp retention
 
 
-@pytest.mark.parametrize("moments,prefetch", [(O.PERSIST, 8), (O.COLD_RESTART, 24)])
-def test_store_prefetch_is_transparent(tmp_path, moments, prefetch):
+@pytest.mark.parametrize("moments,prefetch,ahead", [(O.PERSIST, 8, 1), (O.COLD_RESTART, 24, 1),
+                                                    (O.PERSIST, 24, 2), (O.COLD_RESTART, 5, 2)])
+def test_store_prefetch_is_transparent(tmp_path, moments, prefetch, ahead):
     """f3 read-ahead (tgs_prefetch): announcing each next
     batch lets the GPU side read the misses ahead into read-ahead buffers, with
     a pool smaller and larger than a batch's misses.  The CPU cache is untouched,
@@ -252,7 +256,8 @@ def test_store_prefetch_is_transparent(tmp_path, moments, prefetch):
     pr, g, o = _pair(sc, tmp_path, 16, 6 << 20, 1, prefetch=prefetch, capacity=8,
                      moments=moments)
     boxes = random_boxes(sc, 36, seed=27)
-    pr.gpu.prefetch(boxes[0])
+    for a in range(ahead):
+        pr.gpu.prefetch(boxes[a], a + 1)
     for t, planes in enumerate(boxes):
         act = pr.activate(planes)
         pr.t = t
@@ -260,8 +265,8 @@ def test_store_prefetch_is_transparent(tmp_path, moments, prefetch):
         pr.compare_evicted_dirty()
         pr.compare_store(pr.orc.list("S+"))
         assert pr.step(act, t) == O.OK
-        if t + 1 < len(boxes):
-            pr.gpu.prefetch(boxes[t + 1])
+        if t + ahead < len(boxes):
+            pr.gpu.prefetch(boxes[t + ahead], ahead)
     s, n_files = _finish(pr, sc, g, o)
     full = pr.gpu.store_stats()
     assert s["misses"] > 0 and full["prefetch_hits"] > 0 and full["prefetch_reads"] > 0
