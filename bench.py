@@ -84,6 +84,8 @@ def parse():
                     help="override the config's capacity C (blocks, world size 1; C_g = ceil(C/G))")
     ap.add_argument("--pool-slots", type=int, default=0,
                     help="device slot pool P per GPU (0 -> 2 C_g, R13)")
+    ap.add_argument("--sync-activate", action="store_true",
+                    help="tgs_activate (plan readback every step) instead of tgs_activate_async")
     ap.add_argument("--no-persist-detail", action="store_true",
                     help="skip the 100m persist measurement the default run adds (detail.persist)")
     ap.add_argument("--prefetch", type=int, default=-1, metavar="BLOCKS",
@@ -294,6 +296,9 @@ def _config_dict_base(args, wl, ws):
             "capacity_blocks_per_gpu": -(-wl.capacity // ws), "moments": args.moments,
             **({"pool_slots_per_gpu": args.pool_slots} if getattr(args, "pool_slots", 0) else {}),
             "policy": "restage-all (w/o Tide)" if getattr(args, "no_tide", False) else "tide",
+            "activate": ("tgs_activate (plan readback)" if (getattr(args, "sync_activate", False)
+                         or getattr(args, "store", None) or getattr(args, "no_tide", False)
+                         or getattr(args, "pool_slots", 0)) else "tgs_activate_async"),
             "overlap": not getattr(args, "no_overlap", False),
             "bound_refresh": bool(getattr(args, "refresh_bounds", False)),
             "world_size": ws,
@@ -526,8 +531,11 @@ def measure(args, ws, rank, local):
                                       "active_blocks": st["n_active_blocks"], "B": sc.B}) + "\n")
             steplog.flush()
 
+    use_async = not (args.sync_activate or args.store or args.no_tide or args.pool_slots)
+
     def _step(i, cams=None):
-        act = table.activate(planes[i] if cams is None else cams)
+        pl = planes[i] if cams is None else cams
+        act = table.activate_async(pl) if use_async else table.activate(pl)
         if fmask is not None:
             table.fine_filter(fmask.data_ptr())
         table.step_adam(lr, mask_ptr=fmask.data_ptr() if fmask is not None else None)
@@ -648,7 +656,7 @@ def measure(args, ws, rank, local):
     adam_bpl = adam_bytes(rows_local, fresh_rows, fresh_blocks, sc.B) / max(1, args.steps)
     achieved = adam_bpl / (adam_ms / 1e3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_adam_r01.json")
+    tp = os.path.join(ROOT, "profiles", "ncu_adam_r02.json")
     if os.path.exists(tp):  # ncu --set full capture of a k_adam launch of this workload
         tj = json.load(open(tp))
         traffic = {"dram_bytes_per_launch": tj["traffic_bytes"],

@@ -74,9 +74,9 @@ typedef struct {
   int32_t world_size, rank; /* block k owned by rank k % world_size (R17)           */
   int32_t device;        /* CUDA device ordinal                                     */
   int32_t init_threads;  /* host threads used to build the host tier (0 -> auto)    */
-  uint32_t staging_blocks; /* write-back staging ring, records per parity (0 -> C/4);
-                              an activate evicting more dirty records than this
-                              writes them back straight from the slots instead  */
+  uint32_t staging_blocks; /* write-back staging ring, records per ring slot (3 slots;
+                              0 -> C); an activate evicting more dirty records than
+                              this writes them back straight from the slots instead */
   int32_t refresh_bounds; /* NEXT f2 (R25): after each update grow r_k to hold every
                              Gaussian of the block; the cull of batch t+2 sees it  */
   int32_t serialize;      /* ablation "w/o Overlap": activate returns
@@ -128,6 +128,9 @@ typedef struct {
   const uint32_t* d_global_active;
   uint32_t global_stride;    /* entries per rank row (= capacity C_g)           */
   void* global_ready;
+  const uint32_t* d_n_active; /* device: |R n K| of this activate (valid in stream
+                                 order after `ready`; the only count
+                                 tgs_activate_async provides)                  */
 } tgs_activation;
 
 typedef struct {
@@ -314,6 +317,19 @@ uint32_t tgs_store_lru(tgs_ctx* ctx, uint32_t* blocks, uint8_t* dirty, uint32_t 
  * init, after step_adam, after flush, and after another activate (R19). */
 tgs_status tgs_activate(tgs_ctx* ctx, const tgs_camera* cams, uint32_t n_cams,
                         tgs_activation* out);
+
+/* tgs_activate without the plan readback: the same a1-a4 work, enqueued and
+ * returned at once, every count (|S+|, |S-|, |A|) read by the kernels from the
+ * plan's device header -- the caller thread never waits for the GPU, so the
+ * host runs ahead and small (latency-bound) steps are not bound by it.  Needs
+ * the flat host tier, Tide on, pool_slots >= 2C (S+ never reuses an S- slot,
+ * R13) and staging_blocks >= C (every S- fits the ring); otherwise it behaves as
+ * tgs_activate.  out (may be NULL): the host counts are 0xFFFFFFFF (unknown),
+ * the device pointers are valid, |A| is at d_n_active; tgs_get_stats /
+ * tgs_get_stats_async give the counters, tgs_get_list the lists.  Errors as
+ * tgs_activate. */
+tgs_status tgs_activate_async(tgs_ctx* ctx, const tgs_camera* cams, uint32_t J,
+                              tgs_activation* out);
 
 /* Masked Adam (a5) over the rows of R n K of the last activate, on the compute
  * stream, after the activation's ready event.  d_row_mask: device

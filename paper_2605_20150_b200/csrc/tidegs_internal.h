@@ -9,6 +9,7 @@ namespace tgs {
 
 constexpr uint32_t kDim = 59;
 constexpr int kRings = 3;                  // write-back ring slots (activate T uses T % 3)
+constexpr uint32_t kFromHdr = 0xFFFFFFFFu; // count argument: read it from the device plan header
 constexpr uint32_t kMaxCams = 256;
 constexpr uint32_t kMaxAge = 1023;
 constexpr uint32_t kMaxBuckets = 2 * 2 * (kMaxAge + 2);  // rank x (in R_t ? 0 : 1)
@@ -98,6 +99,7 @@ struct Dev {
   unsigned long long* nonfinite;  // lowest gid*59+attr
   // Adam
   AdamEnt* ent;          // [C]
+  uint32_t* adam_ctr;    // [1] dynamic quad-chunk counter of k_adam (count from the header)
   float *lut_bc1, *lut_ibs;  // [lut_cap]
   // host tier as the transfer kernels see it (device-mapped pinned memory)
   unsigned char* host_dev;  // flat tier: record l at l * host_stride; store tier: CPU-cache entries

@@ -33,6 +33,13 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// a count argument equal to kFromHdr is read from the activate's device plan
+// header (tgs_activate_async: the host never reads the plan back)
+__device__ __forceinline__ uint32_t count_or_hdr(uint32_t n, const PlanHdr* h, int which) {
+  if (n != kFromHdr) return n;
+  return which == 0 ? h->nA : h->nSm;
+}
+
 __device__ __forceinline__ uint32_t block_rows(const Dev& d, uint32_t l) {
   const uint64_t lo = ((uint64_t)l * d.G + d.rank) * d.B;
   if (lo >= d.N) return 0u;
@@ -456,6 +463,7 @@ __global__ void __launch_bounds__(NT) k_evict(Dev d, uint32_t nSm, int parity, i
   const uint32_t* smb = d.sm_blk[parity];
   const uint32_t* sms = d.sm_slot[parity];
   uint32_t c = 0;
+  nSm = count_or_hdr(nSm, d.hdr_dev[parity], 1);
   for (uint32_t base = 0; base < nSm; base += NT) {
     const uint32_t i = base + threadIdx.x;
     uint32_t dirty = 0, l = 0, s = 0;
@@ -718,6 +726,8 @@ __global__ void __launch_bounds__(256) k_adam_prologue(Dev d, uint32_t nA, int p
   __syncthreads();
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  nA = count_or_hdr(nA, d.hdr_dev[parity], 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d.adam_ctr = 0u;  // k_adam's dynamic chunk counter
   if (i < nA) {
     const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
     const uint32_t rows = block_rows(d, l);
@@ -776,6 +786,7 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
   __shared__ uint32_t cams[kMaxCams];
   __shared__ uint32_t wcount[8];
   const uint32_t nw = (d.B + 31) / 32;
+  nA = count_or_hdr(nA, d.hdr_dev[parity], 0);
   for (uint32_t i = blockIdx.x; i < nA; i += gridDim.x) {  // one CTA per A block
     const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
     // cameras whose Level-1 set K^(j) holds block l (R24): camera j renders only
@@ -835,6 +846,7 @@ __global__ void __launch_bounds__(256) k_fine(Dev d, uint32_t nA, uint32_t J, in
 // block max (on the bit pattern: radii are >= 0) goes to pend[parity][l], which
 // the cull of batch t+2 merges into r_k.
 __global__ void __launch_bounds__(256) k_refresh(Dev d, uint32_t nA, int parity) {
+  nA = count_or_hdr(nA, d.hdr_dev[parity], 0);
   for (uint32_t i = blockIdx.x; i < nA; i += gridDim.x) {  // one CTA per A block
     if (d.ent[i].step == 0u) continue;  // block not updated this step (uniform per CTA)
     const uint32_t l = d.a_blk[parity][i], s = d.a_slot[parity][i];
@@ -940,14 +952,18 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t QB = d.B / 4;
+  // host-known count: a non-persistent grid, each warp a contiguous run of qpw
+  // (<= kAdamQPW) quads, so CTAs retire continuously and the (high-priority)
+  // plan of the next batch can be scheduled while this Adam is still running.
+  // Count from the device header (tgs_activate_async): a resident grid whose
+  // warps take qpw-quad chunks from a counter the prologue zeroed.
+  const bool dynamic = nA == kFromHdr;
+  if (dynamic) nA = d.hdr_dev[parity]->nA;
   const uint64_t total = (uint64_t)nA * QB;
-  // non-persistent grid: each warp a contiguous run of qpw (<= kAdamQPW) quads,
-  // so CTAs retire continuously and the (high-priority) plan of the next batch
-  // can be scheduled while this Adam is still running
   const uint64_t wid = (uint64_t)blockIdx.x * (kAdamNT / 32) + (threadIdx.x >> 5);
-  const uint64_t q0 = wid * qpw;
-  const uint64_t q1 = q0 + qpw < total ? q0 + qpw : total;
-  if (q0 >= q1) return;
+  uint64_t q0 = wid * qpw;
+  uint64_t q1 = q0 + qpw < total ? q0 + qpw : total;
+  if (!dynamic && q0 >= q1) return;
 
   // loop-invariant per-lane maps: rows of the 4 components of float4 #lane and #lane+32
   const bool has1 = lane + 32 < 59;
@@ -986,6 +1002,15 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   const uint32_t* pmask = nullptr;
   const size_t rf4 = rf / 4;
 
+  for (;;) {
+  if (dynamic) {
+    uint32_t ch = 0;
+    if (lane == 0) ch = atomicAdd(d.adam_ctr, 1u);
+    ch = __shfl_sync(kFull, ch, 0);
+    q0 = (uint64_t)ch * qpw;
+    if (q0 >= total) break;
+    q1 = q0 + qpw < total ? q0 + qpw : total;
+  }
   uint32_t i = (uint32_t)(q0 / QB);
   uint32_t quad = (uint32_t)(q0 - (uint64_t)i * QB);
   const uint32_t nq = (uint32_t)(q1 - q0);  // <= qpw
@@ -1096,6 +1121,8 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
         }
       }
     }
+  }
+  if (!dynamic) break;
   }
 }
 
@@ -1328,11 +1355,17 @@ cudaError_t launch_plan(const Dev& d, int32_t T, int parity, cudaStream_t s) {
 
 cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int ring, int32_t T,
                                 bool tag, cudaStream_t s) {
-  if (nSm <= 1024)
+  if (nSm <= 1024)  // (kFromHdr > 1024: the count comes from the header)
     k_evict<256><<<1, 256, 0, s>>>(d, nSm, parity, ring, T, tag ? 1 : 0);
   else
     k_evict<1024><<<1, 1024, 0, s>>>(d, nSm, parity, ring, T, tag ? 1 : 0);
   return cudaGetLastError();
+}
+
+// grid for a per-A-block kernel: one CTA per block, or a resident-sized
+// grid-stride grid when the count is read from the device header
+static uint32_t per_block_grid(uint32_t nA) {
+  return nA == kFromHdr ? 148u * 4u : (nA < 148u * 64u ? nA : 148u * 64u);
 }
 
 // C1 send buffer: the A list's global ids padded to C with 0xFFFFFFFF
@@ -1374,8 +1407,7 @@ cudaError_t launch_probe(const Dev& d, const float4* planes, uint32_t J, uint32_
 
 cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  const uint32_t grid = nA < 148u * 64u ? nA : 148u * 64u;  // one CTA per block (grid-stride)
-  k_refresh<<<grid, 256, 0, s>>>(d, nA, parity);
+  k_refresh<<<per_block_grid(nA), 256, 0, s>>>(d, nA, parity);
   return cudaGetLastError();
 }
 
@@ -1405,7 +1437,8 @@ cudaError_t launch_xfer(const Dev& d, int mode, int parity, int ring, int32_t T,
 
 cudaError_t launch_pack(const Dev& d, uint32_t nSm, int ring, cudaStream_t s) {
   if (nSm == 0) return cudaSuccess;
-  dim3 grid(16, nSm < 65535u ? nSm : 65535u);
+  // grid-stride over the dirty records (count from the header: 64 rows of CTAs)
+  dim3 grid(16, nSm == kFromHdr ? 64u : (nSm < 4096u ? nSm : 4096u));
   k_pack<<<grid, 256, 0, s>>>(d, ring);
   return cudaGetLastError();
 }
@@ -1413,7 +1446,7 @@ cudaError_t launch_pack(const Dev& d, uint32_t nSm, int ring, cudaStream_t s) {
 cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                                  cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  const uint32_t grid = (nA + 7) / 8;
+  const uint32_t grid = ((nA == kFromHdr ? d.C : nA) + 7) / 8;
   k_adam_prologue<<<grid, 256, 0, s>>>(d, nA, parity, mask);
   return cudaGetLastError();
 }
@@ -1421,6 +1454,14 @@ cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const ui
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
+  if (nA == kFromHdr) {  // count on the device: resident grid, dynamic chunks of 16 quads
+    const unsigned grid = (unsigned)std::max(grid_ctas, 1);
+    if (d.geo6)
+      k_adam<true><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, kAdamQPW);
+    else
+      k_adam<false><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, kAdamQPW);
+    return cudaGetLastError();
+  }
   const uint64_t quads = (uint64_t)nA * (d.B / 4);
   // grid_ctas = resident CTAs of the device: a small launch (the in-memory
   // configs) gets fewer quads per warp so that it still spans several waves
@@ -1440,8 +1481,7 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
 cudaError_t launch_fine(const Dev& d, uint32_t nA, uint32_t J, int parity, uint32_t* mask,
                         cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  const uint32_t grid = nA < 148u * 64u ? nA : 148u * 64u;  // one CTA per block (grid-stride)
-  k_fine<<<grid, 256, 0, s>>>(d, nA, J, parity, mask);
+  k_fine<<<per_block_grid(nA), 256, 0, s>>>(d, nA, J, parity, mask);
   return cudaGetLastError();
 }
 

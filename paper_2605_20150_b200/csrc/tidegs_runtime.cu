@@ -147,7 +147,8 @@ struct tgs_ctx {
   int last_parity = 0;            // parity the last activate wrote lists into
   bool can_step = false;
   bool poisoned = false;
-  PlanHdr last{};                 // header of the last activate
+  PlanHdr last{};                 // header of the last activate (when last_known)
+  bool last_known = false;        // false after tgs_activate_async: counts are on the device
   uint32_t last_J = 0;            // batch size of the last activate
   uint64_t n_steps = 0;
   uint64_t host_flush_bytes = 0, host_flush_blocks = 0;
@@ -806,6 +807,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     c->a3_gid[r] = dalloc_t<uint32_t>(c, Cc, ok);
   }
   d.ent = dalloc_t<AdamEnt>(c, Cc, ok);
+  d.adam_ctr = dalloc_t<uint32_t>(c, 1, ok);
   for (int k = 0; k < kRings; ++k) {
     d.dl_slot[k] = dalloc_t<uint32_t>(c, Cc, ok);
     d.dl_blk[k] = dalloc_t<uint32_t>(c, Cc, ok);
@@ -816,7 +818,9 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   d.ndirty_dev = dalloc_t<uint32_t>(c, kRings, ok);
   d.wb_tag = dalloc_t<int32_t>(c, Kl, ok);
   d.wb_idx = dalloc_t<uint32_t>(c, Kl, ok);
-  d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C / 4);
+  // default ring = C records: any S- fits, so no write-back ever has to come
+  // straight from the slots (and tgs_activate_async needs no plan readback)
+  d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C);
   for (int k = 0; k < kRings; ++k)
     d.staging[k] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
   std::vector<uint16_t> lut;
@@ -940,7 +944,20 @@ tgs_status tgs_destroy(tgs_ctx* c) {
   return TGS_OK;
 }
 
+static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
+                                tgs_activation* out, bool want_async);
+
 tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_activation* out) {
+  return activate_impl(c, cams, J, out, false);
+}
+
+tgs_status tgs_activate_async(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
+                              tgs_activation* out) {
+  return activate_impl(c, cams, J, out, true);
+}
+
+static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
+                                tgs_activation* out, bool want_async) {
   tgs_status st = check(c);
   if (st != TGS_OK) return st;
   if (J > c->d.J_max || (J > 0 && !cams)) return TGS_EINVAL;
@@ -1015,15 +1032,26 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     return TGS_OK;
   };
   const bool early = !c->store && d.tide && d.P >= 2u * d.C;
+  // asynchronous activate: no host decision needs the plan -- S+ never reuses an
+  // S- slot (P >= 2C) and the ring holds any S- (S_max >= C), so every count is
+  // read from the device header by the kernels themselves
+  const bool async = want_async && early && d.S_max >= d.C;
   if (early) {
     st = gather_flat(d.C);
     if (st != TGS_OK) return st;
   }
-  CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
-  const PlanHdr h = *c->hdr;
-  c->last = h;
+  PlanHdr h{};
+  if (async) {
+    h.nSm = kFromHdr;
+    c->last_known = false;
+  } else {
+    CK(cudaEventSynchronize(c->ev_plan));  // the one plan readback (R14)
+    h = *c->hdr;
+    c->last = h;
+    c->last_known = true;
+  }
   c->last_J = J;
-  if (c->h2d_prof >= 0) {  // the timed gather's algorithmic bytes
+  if (c->h2d_prof >= 0 && !async) {  // the timed gather's algorithmic bytes
     std::lock_guard<std::mutex> g(c->prof_mu);
     if ((size_t)c->h2d_prof < c->pending.size())
       c->pending[c->h2d_prof].bytes = (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
@@ -1036,8 +1064,8 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
   //      their slots are free at once; k_xfer then drains the ring to the host
   //      tier on the d2h stream.  Direct path (this activate's S+ may reuse S-
   //      slots, or the ring is too small): k_xfer reads the slots themselves.
-  const bool reuse_now = !d.tide || h.fallback;
-  const bool direct = reuse_now || h.nSm > d.S_max;
+  const bool reuse_now = !async && (!d.tide || h.fallback);
+  const bool direct = !async && (reuse_now || h.nSm > d.S_max);
   auto writeback = [&]() -> tgs_status {
     Timer te, td;
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
@@ -1060,7 +1088,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     c->last_evict_ring = k;
     CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[k], 0));
     prof_begin(c, c->d2h, td);
-    CK(launch_xfer(dg, direct ? 2 : 1, p, k, T, nullptr, 0, h.nSm, c->scatter_ctas,
+    CK(launch_xfer(dg, direct ? 2 : 1, p, k, T, nullptr, 0, async ? d.C : h.nSm, c->scatter_ctas,
                    c->scatter_bufs, c->d2h));
     prof_end(c, c->d2h, td, 4);
     c->tm.kernel_launches++;
@@ -1142,7 +1170,7 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     if (h.nSm) c->store->touch_evicted(c->sm_map, h.nSm, T);
   }
 
-  if (!reuse_now && h.nSm) {
+  if (!reuse_now && h.nSm) {  // (async: always; the kernels read |S-| themselves)
     st = writeback();
     if (st != TGS_OK) return st;
   }
@@ -1174,13 +1202,15 @@ tgs_status tgs_activate(tgs_ctx* c, const tgs_camera* cams, uint32_t J, tgs_acti
     if (st != TGS_OK) return st;
   }
   if (out) {
-    out->n_visible = h.nK;
-    out->n_resident = h.nR;
-    out->n_active_blocks = h.nA;
-    out->n_stage_in = h.nSp;
-    out->n_evict = h.nSm;
+    const uint32_t unknown = 0xFFFFFFFFu;
+    out->n_visible = async ? unknown : h.nK;
+    out->n_resident = async ? unknown : h.nR;
+    out->n_active_blocks = async ? unknown : h.nA;
+    out->n_stage_in = async ? unknown : h.nSp;
+    out->n_evict = async ? unknown : h.nSm;
     out->n_evict_dirty = 0;  // decided after the previous Adam; see tgs_get_stats
-    out->h2d_bytes = (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
+    out->h2d_bytes = async ? ~0ull : (uint64_t)h.nSp * d.n_arr * c->rec_bytes;
+    out->d_n_active = &dev_for(c, p, T).hdr_dev[p]->nA;
     out->d_active_blocks = c->a3_gid[(uint32_t)T % 3u];
     out->d_active_slots = c->a3_slot[(uint32_t)T % 3u];
     out->d_params = d.params;
@@ -1202,7 +1232,7 @@ tgs_status tgs_step_adam(tgs_ctx* c, const tgs_adam* hp, const uint32_t* d_row_m
   if (!hp || !hp->lr) return TGS_EINVAL;
   c->can_step = false;
   const int p = c->last_parity;
-  const uint32_t nA = c->last.nA;
+  const uint32_t nA = c->last_known ? c->last.nA : kFromHdr;  // async: read on the device
   st = ensure_lut(c, hp->beta1, hp->beta2, (uint32_t)std::min<uint64_t>(c->n_steps + 2, 0xffffffffu));
   if (st != TGS_OK) return st;
   c->n_steps++;
@@ -1243,10 +1273,11 @@ tgs_status tgs_fine_filter(tgs_ctx* c, uint32_t* d_row_mask) {
   CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
   const int m = (int)(((uint32_t)c->T + 2) % 3u);  // list slot of the last activate
   CK(cudaStreamWaitEvent(c->compute, c->ev_ready[m], 0));
-  if (c->last.nA == 0 || c->d.Kloc == 0) return TGS_OK;
+  if ((c->last_known && c->last.nA == 0) || c->d.Kloc == 0) return TGS_OK;
   Timer tf;
   prof_begin(c, c->compute, tf);
-  CK(launch_fine(dev_for(c, p, c->T - 1), c->last.nA, c->last_J, p, d_row_mask, c->compute));
+  CK(launch_fine(dev_for(c, p, c->T - 1), c->last_known ? c->last.nA : kFromHdr, c->last_J, p,
+                 d_row_mask, c->compute));
   prof_end(c, c->compute, tf, 8);
   c->tm.kernel_launches++;
   CK(cudaEventRecord(c->ev_lists[m], c->compute));  // k_fine reads this slot's K^(j)
@@ -1439,7 +1470,8 @@ uint32_t tgs_get_evicted_dirty(tgs_ctx* c, uint32_t* blocks, uint32_t cap) {
   if (check(c) != TGS_OK) return 0;
   if (sync_all(c) != TGS_OK) return 0;
   const int k = c->T > 0 ? (int)(((uint32_t)c->T - 1) % kRings) : 0;  // the last activate's slot
-  const uint32_t n = (c->T > 0 && c->last.nSm) ? c->ndirty[k] : 0;
+  // (after an asynchronous activate the write-back kernels always ran)
+  const uint32_t n = (c->T > 0 && (!c->last_known || c->last.nSm)) ? c->ndirty[k] : 0;
   for (uint32_t i = 0; i < n && i < cap; ++i)
     if (blocks) blocks[i] = c->dirty_map[k][2 * i] * c->cfg.world_size + c->cfg.rank;
   return n;

@@ -31,7 +31,7 @@ SYMBOLS = ("tgs_init_table", "tgs_destroy", "tgs_activate", "tgs_step_adam", "tg
            "tgs_pool_slots", "tgs_read_bound", "tgs_build_layout", "tgs_frustum_planes", "tgs_status_string", "tgs_last_error",
            "tgs_init_table_store", "tgs_get_store_stats", "tgs_store_index", "tgs_store_lru",
            "tgs_order_views", "tgs_store_compact", "tgs_set_comm", "tgs_get_global_stats",
-           "tgs_prefetch")
+           "tgs_prefetch", "tgs_activate_async")
 
 
 class Config(C.Structure):
@@ -64,7 +64,7 @@ class Activation(C.Structure):
                 ("d_grads", C.c_void_p), ("slot_stride", C.c_uint64),
                 ("grad_stride", C.c_uint64), ("ready", C.c_void_p),
                 ("d_global_active", C.c_void_p), ("global_stride", C.c_uint32),
-                ("global_ready", C.c_void_p)]
+                ("global_ready", C.c_void_p), ("d_n_active", C.c_void_p)]
 
 
 COMM_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -160,6 +160,7 @@ def lib():
         L.tgs_store_lru.argtypes = [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), u32]
         L.tgs_destroy.argtypes = [vp]
         L.tgs_activate.argtypes = [vp, C.c_void_p, u32, C.POINTER(Activation)]
+        L.tgs_activate_async.argtypes = [vp, C.c_void_p, u32, C.POINTER(Activation)]
         L.tgs_step_adam.argtypes = [vp, C.POINTER(Adam), vp]
         L.tgs_flush.argtypes = [vp]
         L.tgs_fine_filter.argtypes = [vp, vp]
@@ -374,6 +375,16 @@ class Table:
         p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)
         self._err(lib().tgs_prefetch(self.h, p.ctypes.data if p.shape[0] else None, p.shape[0],
                                      ahead), "tgs_prefetch")
+
+    def activate_async(self, planes: np.ndarray) -> Activation:
+        """tgs_activate_async: enqueue the activate, no plan readback; the host
+        counts come back unknown (0xFFFFFFFF), |A| is at act.d_n_active"""
+        p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)
+        out = Activation()
+        self._err(lib().tgs_activate_async(self.h, p.ctypes.data if p.shape[0] else None,
+                                           p.shape[0], C.byref(out)), "tgs_activate_async")
+        self.last = out
+        return out
 
     def activate(self, planes: np.ndarray, *, check=True) -> Activation:
         p = np.ascontiguousarray(planes, np.float32).reshape(-1, 6, 4)

@@ -373,7 +373,9 @@ def test_edge_configs(N, B, C, J, kw):
 
 @pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct",
                                   "plain_early_lists", "fine_early_lists", "fine_level2",
-                                  "fine_level2_masked_refresh", "plain_late_lists"])
+                                  "fine_level2_masked_refresh", "plain_late_lists",
+                                  "plain_async", "fine_async", "fine_refresh_cold_async",
+                                  "fine_level2_async"])
 def test_pipelined_run_matches_oracle(mode, monkeypatch):
     """The GPU runs ahead exactly as in bench.py -- no inspection call (hence no
     host sync) between batches -- so every cross-batch hazard (plan of t+1 vs
@@ -390,6 +392,9 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
     if mode.endswith("_late_lists"):  # plan of t+2 waits for all of Adam(t)
         monkeypatch.setenv("TGS_LISTS_AFTER_ADAM", "1")
         mode = mode[: -len("_late_lists")]
+    use_async = mode.endswith("_async")  # tgs_activate_async: no plan readback at all
+    if use_async:
+        mode = mode[: -len("_async")]
     kw = {"plain": {}, "fine": {}, "fine_refresh_cold": {"refresh_bounds": 1,
                                                           "moments": O.COLD_RESTART},
           "fine_level2": {"level2": 1}, "fine_level2_masked_refresh": {"level2": 1, "refresh_bounds": 1},
@@ -404,7 +409,7 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
     n = 40
     for t in range(n):  # GPU: back to back
         planes = tr.batch_planes(t, cfg.J)
-        act = pr.gpu.activate(planes)
+        act = pr.gpu.activate_async(planes) if use_async else pr.gpu.activate(planes)
         pr.grads_gpu_only(act, t)
         if fine:
             pr.gpu.fine_filter(dmask.data_ptr())
@@ -520,6 +525,32 @@ def test_transfer_grid_shapes_give_identical_results(ctas, monkeypatch):
         pr.t = n
         pr.compare_plan(cfg.J)
         pr.compare_stats()
+        pr.gpu.flush()
+        pr.orc.flush()
+        assert pr.compare_blocks(range(sc.K)) == 0
+        pr.close()
+
+
+@pytest.mark.parametrize("moments", [O.PERSIST, O.COLD_RESTART])
+def test_async_activate_step_by_step(moments):
+    """tgs_activate_async (no plan readback; every count from the device header):
+    after each batch the lists, slots, K^(j), dirty S- and counters equal the
+    oracle's, on the tiny orbit (C = 24 < K) and an edge config with random
+    cameras (ragged last block, J = 17)."""
+    for sc, tr, J, C in ((tiny()[1], tiny()[2], 2, 24),
+                         (W.Scene(20000, 36, side=60.0, lot=20.0, footprint=12.0, hmin=2.0,
+                                  hmax=12.0), _RandomCams(60.0), 17, 40)):
+        pr = _pair(sc, capacity=C, moments=moments)
+        for t in range(24):
+            planes = tr.batch_planes(t, J)
+            act = pr.gpu.activate_async(planes)
+            assert act.n_active_blocks == 0xFFFFFFFF
+            assert pr.orc.activate(planes) == O.OK
+            pr.t = t
+            pr.compare_plan(J)
+            pr.compare_evicted_dirty()
+            assert pr.step(act, t) == O.OK
+            pr.compare_stats()
         pr.gpu.flush()
         pr.orc.flush()
         assert pr.compare_blocks(range(sc.K)) == 0

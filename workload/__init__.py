@@ -325,6 +325,7 @@ def cuda_lib():
         L = C.CDLL(path)
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         L.wl_cuda_synth_grads.argtypes = [vp, u64, vp, vp, u32, u32, u64, u64, u64, vp]
+        L.wl_cuda_synth_grads_devn.argtypes = [vp, u64, vp, vp, vp, u32, u32, u64, u64, u64, vp]
         L.wl_cuda_synth_mask.argtypes = [vp, u32, vp, vp, u32, u32, u64, u64, u64, u32, vp]
         L.wl_cuda_poke.argtypes = [vp, C.c_float, vp]
         _cuda_lib = L
@@ -335,6 +336,13 @@ def synth_grads_cuda(act, B, N, seed, t, stream):
     """Write counter-hash gradients of the active blocks of a tgs_activation into
     its grad pool (on `stream`, after the activation's ready event)."""
     if act.n_active_blocks == 0:
+        return
+    if act.n_active_blocks == 0xFFFFFFFF:  # asynchronous activate: |A| on the device
+        rc = cuda_lib().wl_cuda_synth_grads_devn(act.d_grads, act.grad_stride, act.d_active_blocks,
+                                                 act.d_active_slots, act.d_n_active,
+                                                 act.global_stride, B, N, seed, t, stream)
+        if rc != 0:
+            raise RuntimeError(f"wl_cuda_synth_grads_devn: cuda error {rc}")
         return
     rc = cuda_lib().wl_cuda_synth_grads(act.d_grads, act.grad_stride, act.d_active_blocks,
                                         act.d_active_slots, act.n_active_blocks, B, N, seed, t,

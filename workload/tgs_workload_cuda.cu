@@ -24,12 +24,14 @@ __device__ __forceinline__ float grad_of(uint64_t seed, uint64_t gid, uint32_t a
   return __fmul_rn(__int2float_rn(q), 0x1p-33f);
 }
 
-// grid: (ceil(B*59/4 / 256), n_blocks); one float4 per thread
+// grid: (ceil(B*59/4 / 256), n_blocks); one float4 per thread.  d_n (may be
+// NULL): the block count on the device (an asynchronous activate's |A|)
 __global__ void wl_grad_kernel(float* __restrict__ grads, uint64_t slot_stride,
                                const uint32_t* __restrict__ blocks,
                                const uint32_t* __restrict__ slots, uint32_t B, uint64_t N,
-                               uint64_t seed, uint64_t t) {
+                               uint64_t seed, uint64_t t, const uint32_t* __restrict__ d_n) {
   const uint32_t i = blockIdx.y;
+  if (d_n && i >= *d_n) return;
   const uint64_t k = blocks[i];
   const uint64_t lo = k * B;
   const uint32_t rows = lo >= N ? 0u : (uint32_t)((N - lo) < B ? (N - lo) : B);
@@ -76,7 +78,20 @@ extern "C" int wl_cuda_synth_grads(float* d_grads, uint64_t slot_stride, const u
   uint32_t n4 = B * WL_DIM / 4;
   dim3 grid((n4 + 255) / 256, n);
   wl_grad_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_grads, slot_stride, d_blocks, d_slots,
-                                                         B, N, seed, t);
+                                                         B, N, seed, t, nullptr);
+  return (int)cudaGetLastError();
+}
+
+// the same with the block count on the device (n_max: an upper bound)
+extern "C" int wl_cuda_synth_grads_devn(float* d_grads, uint64_t slot_stride,
+                                        const uint32_t* d_blocks, const uint32_t* d_slots,
+                                        const uint32_t* d_n, uint32_t n_max, uint32_t B,
+                                        uint64_t N, uint64_t seed, uint64_t t, void* stream) {
+  if (n_max == 0) return 0;
+  uint32_t n4 = B * WL_DIM / 4;
+  dim3 grid((n4 + 255) / 256, n_max);
+  wl_grad_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_grads, slot_stride, d_blocks, d_slots,
+                                                         B, N, seed, t, d_n);
   return (int)cudaGetLastError();
 }
 
