@@ -92,6 +92,8 @@ struct tgs_ctx {
   // T % 3: the plan of T+3 reuses them once their consumers of T are done
   cudaEvent_t ev_ready[3] = {}, ev_lists[3] = {};
   cudaEvent_t ev_refresh[2] = {};  // R25: the refresh of the step of that parity done
+  cudaEvent_t ev_planes[3] = {};   // k_planes of the activate of that list slot done
+  bool rec_planes[3] = {};
   bool rec_refresh[2] = {};
   uint32_t *l3_percam[3] = {}, *l3_sp_blk[3] = {}, *l3_sp_slot[3] = {}, *l3_sm_blk[3] = {},
            *l3_sm_slot[3] = {};
@@ -129,12 +131,8 @@ struct tgs_ctx {
   std::string io_err;
   uint32_t last_ndirty = 0;
   std::mutex prof_mu;
-  // The plan of t+2 waits only for Adam(t)'s prologue (default; the A lists
-  // then come from the 3-deep ring), or with TGS_LISTS_AFTER_ADAM=1 for all of
-  // Adam(t).  With 256-thread plan CTAs the early release costs k_adam < 1% and
-  // takes the plan off the chain of the small configs (100m persist 0.96 ->
-  // 0.88 ms/step, 11m 0.199 -> 0.189; profiles/bench_r02.md).
-  bool lists_after_adam = false;
+  // (the list slot of activate T is released once Adam(T) -- and its refresh --
+  // is done: with three list slots the plan of T+3 is what waits for it)
   // Adam LUT (bias corrections, R9)
   std::vector<float> lut_bc1_h, lut_ibs_h;
   float* lut_pinned = nullptr;     // [2][lut_cap]
@@ -565,7 +563,8 @@ void destroy_impl(tgs_ctx* c) {
   for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_ready[2],
                         c->ev_evict[0], c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
                         c->ev_d2h[2], c->ev_lists[0], c->ev_lists[1], c->ev_lists[2],
-                        c->ev_refresh[0], c->ev_refresh[1], c->trace_base})
+                        c->ev_refresh[0], c->ev_refresh[1], c->ev_planes[0], c->ev_planes[1],
+                        c->ev_planes[2], c->trace_base})
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -679,6 +678,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
                          &c->ev_ready[2], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
                          &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_d2h[2], &c->ev_lists[0],
                          &c->ev_lists[1], &c->ev_lists[2], &c->ev_refresh[0], &c->ev_refresh[1],
+                         &c->ev_planes[0], &c->ev_planes[1], &c->ev_planes[2],
                          &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
                          &c->ev_job[3]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TGS_ECUDA);
@@ -881,7 +881,6 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (const char* m = getenv("TGS_SCATTER_CTAS")) c->scatter_ctas = std::max(1, atoi(m));
   if (const char* m = getenv("TGS_GATHER_BUFS")) c->gather_bufs = atoi(m);
   if (const char* m = getenv("TGS_SCATTER_BUFS")) c->scatter_bufs = atoi(m);
-  if (const char* m = getenv("TGS_LISTS_AFTER_ADAM")) c->lists_after_adam = atoi(m) != 0;
   if (c->store) c->io = std::thread(io_main, c);  // flat tier: no host work per write-back
   *out = c;
   return TGS_OK;
@@ -895,15 +894,9 @@ tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
   prof_begin(c, c->compute, t1);
   CK(launch_adam_prologue(dk, nA, p, d_row_mask, c->compute));
   prof_end(c, c->compute, t1, 1);
-  // After the prologue, Adam reads only its A lists (3-deep ring), the per-
-  // entry constants and slots the plan never hands out while R_{t+1} holds
-  // them: the plan of t+2 could overwrite this parity's other lists now
-  // (TGS_LISTS_AFTER_ADAM=0).  By default, and always with the bound refresh
-  // on (that plan merges the refreshed radii, R25), they stay in use until the
-  // end of this step's compute work.
-  const bool lists_late = c->d.refresh || c->lists_after_adam;
+  // Adam and the refresh read the A lists and header of list slot m: the plan
+  // of T+3, which rewrites them, waits for ev_lists[m] recorded after them
   const int m = (int)(((uint32_t)c->T + 2) % 3u);  // list slot of the last activate
-  if (!lists_late) CK(cudaEventRecord(c->ev_lists[m], c->compute));
   prof_begin(c, c->compute, t2);
   CK(launch_adam(dk, nA, p, d_row_mask, h, c->adam_grid, c->compute));
   prof_end(c, c->compute, t2, 0);
@@ -912,7 +905,7 @@ tgs_status adam_launches(tgs_ctx* c, int p, uint32_t nA, const AdamHyper& h,
     CK(launch_refresh(dk, nA, p, c->compute));
     c->tm.kernel_launches++;
   }
-  if (lists_late) CK(cudaEventRecord(c->ev_lists[m], c->compute));  // lists in use until here
+  CK(cudaEventRecord(c->ev_lists[m], c->compute));  // lists in use until here
   if (c->d.refresh) {  // the cull two batches later merges these radii (R25)
     CK(cudaEventRecord(c->ev_refresh[p], c->compute));
     c->rec_refresh[p] = true;
@@ -982,11 +975,16 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
   if (c->rec_ready[m]) CK(cudaStreamWaitEvent(c->plan, c->ev_ready[m], 0));
   if (d.refresh && c->rec_refresh[p]) CK(cudaStreamWaitEvent(c->plan, c->ev_refresh[p], 0));
   Timer tp;
-  // the batch of T-3 (same staging buffer) was consumed before that plan's readback
+  // the staging buffer of slot m held the batch of T-3: its k_planes must have
+  // copied it (free after a plan readback; with tgs_activate_async the host may
+  // be up to three plans ahead of the plan stream)
+  if (c->rec_planes[m]) CK(cudaEventSynchronize(c->ev_planes[m]));
   if (J) std::memcpy(c->planes_pinned + (size_t)m * kMaxCams * 24, cams, sizeof(float) * 24 * J);
   prof_begin(c, c->plan, tp);
   const Dev dk = dev_for(c, p, T);
   CK(launch_cull(dk, J, T, p, c->plan));
+  CK(cudaEventRecord(c->ev_planes[m], c->plan));
+  c->rec_planes[m] = true;
   CK(launch_quota(dk, J, T, p, c->plan));
   CK(launch_plan(dk, T, p, c->plan));
   prof_end(c, c->plan, tp, 2);

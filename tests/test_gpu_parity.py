@@ -372,8 +372,7 @@ def test_edge_configs(N, B, C, J, kw):
 
 
 @pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct",
-                                  "plain_early_lists", "fine_early_lists", "fine_level2",
-                                  "fine_level2_masked_refresh", "plain_late_lists",
+                                  "fine_level2", "fine_level2_masked_refresh",
                                   "plain_async", "fine_async", "fine_refresh_cold_async",
                                   "fine_level2_async"])
 def test_pipelined_run_matches_oracle(mode, monkeypatch):
@@ -386,12 +385,6 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
     import torch
     from gpu_harness import GRAD_SEED, Synth, _cfn
     cfg, sc, tr = tiny()
-    if mode.endswith("_early_lists"):  # plan of t+2 released after Adam(t)'s prologue (default)
-        monkeypatch.setenv("TGS_LISTS_AFTER_ADAM", "0")
-        mode = mode[: -len("_early_lists")]
-    if mode.endswith("_late_lists"):  # plan of t+2 waits for all of Adam(t)
-        monkeypatch.setenv("TGS_LISTS_AFTER_ADAM", "1")
-        mode = mode[: -len("_late_lists")]
     use_async = mode.endswith("_async")  # tgs_activate_async: no plan readback at all
     if use_async:
         mode = mode[: -len("_async")]
