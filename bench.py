@@ -86,6 +86,10 @@ def parse():
                     help="device slot pool P per GPU (0 -> 2 C_g, R13)")
     ap.add_argument("--sync-activate", action="store_true",
                     help="tgs_activate (plan readback every step) instead of tgs_activate_async")
+    ap.add_argument("--xfer", default="auto", choices=["auto", "kernel", "ce"],
+                    help="a4 transfers: TMA bulk-copy kernels (k_xfer) or copy-engine runs "
+                         "(TGS_XFER_COPY_ENGINE, plan readback); auto -> ce, except 11m (in-memory, "
+                         "latency-bound: the async activate needs the kernels)")
     ap.add_argument("--no-persist-detail", action="store_true",
                     help="skip the 100m persist measurement the default run adds (detail.persist)")
     ap.add_argument("--prefetch", type=int, default=-1, metavar="BLOCKS",
@@ -298,7 +302,11 @@ def _config_dict_base(args, wl, ws):
             "policy": "restage-all (w/o Tide)" if getattr(args, "no_tide", False) else "tide",
             "activate": ("tgs_activate (plan readback)" if (getattr(args, "sync_activate", False)
                          or getattr(args, "store", None) or getattr(args, "no_tide", False)
-                         or getattr(args, "pool_slots", 0)) else "tgs_activate_async"),
+                         or getattr(args, "pool_slots", 0) or xfer_mode(args) == 1)
+                         else "tgs_activate_async"),
+            "xfer": ("TMA bulk-copy kernels (k_xfer; store tier)" if getattr(args, "store", None)
+                     else "copy-engine runs of consecutive records + k_commit"
+                     if xfer_mode(args) == 1 else "TMA bulk-copy kernels (k_xfer)"),
             "overlap": not getattr(args, "no_overlap", False),
             "bound_refresh": bool(getattr(args, "refresh_bounds", False)),
             "world_size": ws,
@@ -445,6 +453,18 @@ def main():
         torch.distributed.destroy_process_group()
 
 
+def xfer_mode(args):
+    """tgs_xfer of the run: 1 = copy-engine runs (needs the plan readback), 0 = TMA kernels"""
+    if getattr(args, "store", None):
+        return 0
+    if getattr(args, "xfer", "auto") == "auto":
+        # copy-engine runs win wherever records move (profiles/ab_xfer_r02.md);
+        # 11m in-memory moves none after the fill and is bound by the host's
+        # per-step latency, which only the async activate (kernels) removes
+        return 0 if args.config == "11m" else 1
+    return 1 if args.xfer == "ce" else 0
+
+
 def persist_detail_wanted(args, ws):
     """the default invocation (300m cold, N = 1) also measures 100m persist"""
     return (ws == 1 and args.config == "300m" and args.moments == "cold" and not args.shard_of
@@ -477,7 +497,7 @@ def measure(args, ws, rank, local):
                         device=local, tide=0 if args.no_tide else 1,
                         serialize=1 if args.no_overlap else 0,
                         refresh_bounds=1 if args.refresh_bounds else 0,
-                        level2=1 if args.fine_filter else 0)
+                        level2=1 if args.fine_filter else 0, xfer=xfer_mode(args))
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)  # collectives and timing events on the compute stream
     build_ms = None
@@ -531,7 +551,8 @@ def measure(args, ws, rank, local):
                                       "active_blocks": st["n_active_blocks"], "B": sc.B}) + "\n")
             steplog.flush()
 
-    use_async = not (args.sync_activate or args.store or args.no_tide or args.pool_slots)
+    use_async = not (args.sync_activate or args.store or args.no_tide or args.pool_slots
+                     or xfer_mode(args) == 1)
 
     def _step(i, cams=None):
         pl = planes[i] if cams is None else cams

@@ -86,7 +86,21 @@ typedef struct {
                              tgs_fine_filter reads 16 B per row instead of theta;
                              implied by refresh_bounds (whose per-row radius k_adam
                              then computes in its epilogue)                      */
+  int32_t xfer;           /* a4 transfer mechanism (tgs_xfer; flat host tier only --
+                             the store tier always uses TGS_XFER_KERNEL)          */
 } tgs_config;
+
+/* a4 transfer mechanism.
+ * TGS_XFER_KERNEL: TMA bulk-copy kernels (k_xfer) read and write the pinned host
+ *   tier over PCIe; no host decision needs the plan, so tgs_activate_async works.
+ * TGS_XFER_COPY_ENGINE: the copy engines move runs of consecutive records (S+
+ *   runs host tier -> a device staging buffer, then k_commit places them in their
+ *   slots; dirty S- runs write-back ring -> host tier, issued by the library's I/O
+ *   thread once the dirty list is known).  Needs the plan on the host:
+ *   tgs_activate_async behaves as tgs_activate with it.  Why both: one copy per
+ *   run of records runs both PCIe directions near the link's rate, the kernels
+ *   do not need the plan readback (profiles/linkbench_dma_r02.txt). */
+typedef enum { TGS_XFER_KERNEL = 0, TGS_XFER_COPY_ENGINE = 1 } tgs_xfer;
 
 /* Optional device allocator hooks (PyTorch's caching allocator from Python).
  * NULL -> cudaMalloc / cudaFree. */
@@ -311,8 +325,8 @@ uint32_t tgs_store_lru(tgs_ctx* ctx, uint32_t* blocks, uint8_t* dirty, uint32_t 
 /* Activate the next camera batch (J = n_cams <= J_max; 0 is valid: K = {}).
  * Runs a1-a3 on the device, reads back the plan (one small host<->device
  * synchronisation that does NOT wait for the previous tgs_step_adam), issues
- * the H2D gather of S+ on a copy-engine stream (overlapping the previous
- * Adam), and the write-back of the dirty S- records after the previous Adam.
+ * the H2D gather of S+ on its own stream (overlapping the previous Adam), and
+ * the write-back of the dirty S- records after the previous Adam (tgs_xfer).
  * EINVAL: J > J_max, cams NULL with J > 0, non-finite plane.  Allowed after
  * init, after step_adam, after flush, and after another activate (R19). */
 tgs_status tgs_activate(tgs_ctx* ctx, const tgs_camera* cams, uint32_t n_cams,
@@ -322,7 +336,7 @@ tgs_status tgs_activate(tgs_ctx* ctx, const tgs_camera* cams, uint32_t n_cams,
  * returned at once, every count (|S+|, |S-|, |A|) read by the kernels from the
  * plan's device header -- the caller thread never waits for the GPU, so the
  * host runs ahead and small (latency-bound) steps are not bound by it.  Needs
- * the flat host tier, Tide on, pool_slots >= 2C (S+ never reuses an S- slot,
+ * the flat host tier, xfer = TGS_XFER_KERNEL, Tide on, pool_slots >= 2C (S+ never reuses an S- slot,
  * R13) and staging_blocks >= C (every S- fits the ring); otherwise it behaves as
  * tgs_activate.  out (may be NULL): the host counts are 0xFFFFFFFF (unknown),
  * the device pointers are valid, |A| is at d_n_active; tgs_get_stats /

@@ -88,6 +88,8 @@ struct Dev {
   int32_t* wb_tag;       // [Kloc] activate index at which the block was packed (-1 never)
   uint32_t* wb_idx;      // [Kloc] its staging-ring index then
   float* staging[3];     // [S_max][n_arr][B][59] write-back staging rings (ring slot)
+  float* stage_in;       // [C][n_arr][B][59] copy-engine gather staging: S+ record i at i
+                         // (xfer = TGS_XFER_COPY_ENGINE, else nullptr; read by k_commit)
   uint32_t S_max;        // staging capacity in records
   float4* last_planes[2];  // [kMaxCams*6] camera batch of the activate of that parity
   const float4* planes_map[2];  // mapped pinned host staging of the camera batch (parity)
@@ -135,6 +137,7 @@ cudaError_t launch_evict_tagged(const Dev& d, uint32_t nSm, int parity, int ring
 cudaError_t launch_xfer(const Dev& d, int mode, int parity, int ring, int32_t T,
                         const uint32_t* sel, uint32_t n_sel, uint32_t n_hint, int ctas, int bufs,
                         cudaStream_t s);
+cudaError_t launch_commit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s);
 cudaError_t launch_refresh(const Dev& d, uint32_t nA, int parity, cudaStream_t s);
 cudaError_t launch_probe(const Dev& d, const float4* planes, uint32_t J, uint32_t* out,
                          cudaStream_t s);

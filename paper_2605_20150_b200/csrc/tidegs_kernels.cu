@@ -524,6 +524,50 @@ __global__ void __launch_bounds__(256, 6) k_pack(Dev d, int ring) {
   }
 }
 
+// ------------------- a4 commit (xfer = TGS_XFER_COPY_ENGINE): staged S+ -> slots
+// The copy engines have put S+ record i (host tier) at stage_in[i]; entry i goes
+// to its slot, except a block packed by one of the last two activates (its host
+// write-back may still be in flight), whose newest copy is its ring record --
+// the same source rule as k_xfer's gather.  Cold restart resets the block's
+// step here (after the last Adam that updated it, as in the gather); with f1/f2
+// on, each theta row's centre and log-scales go to geo6 from the registers.
+// grid (chunks, min(nSp, 4096)), 256 threads, 128-bit streaming loads/stores.
+__global__ void __launch_bounds__(256, 6) k_commit(Dev d, int parity, int32_t T, uint32_t nSp) {
+  const size_t n4 = (size_t)d.n_arr * d.rec_floats / 4;
+  const size_t th4 = d.rec_floats / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.y; i < nSp; i += gridDim.y) {
+    const uint32_t l = d.sp_blk[parity][i], slot = d.sp_slot[parity][i];
+    const int32_t tg = d.wb_tag[l];
+    const bool ring = tg >= 0 && tg >= T - 2;
+    const float4* src = reinterpret_cast<const float4*>(
+        ring ? d.staging[tg % 3] + (size_t)d.wb_idx[l] * d.n_arr * d.rec_floats
+             : d.stage_in + (size_t)i * d.n_arr * d.rec_floats);
+    float4* dst = reinterpret_cast<float4*>(d.params + (size_t)slot * 3 * d.rec_floats);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (d.cold) d.step[l] = 0u;
+      if (ring) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
+    }
+    float* g6 = d.geo6 ? d.geo6 + (size_t)slot * d.B * 6 : nullptr;
+#pragma unroll 1
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += stride) {
+      const float4 v = __ldcs(src + e);
+      __stcs(dst + e, v);
+      if (g6 && e < th4) {  // theta floats 4e..4e+3: rows' attributes 0..2 and 52..54
+        const uint32_t f0 = (uint32_t)(4 * e);
+        uint32_t r = f0 / kDim, a = f0 - r * kDim;
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (a < 3u) g6[(size_t)r * 6 + a] = vv[q];
+          else if (a >= 52u && a < 55u) g6[(size_t)r * 6 + a - 49u] = vv[q];
+          if (++a == kDim) { a = 0; ++r; }
+        }
+      }
+    }
+  }
+}
+
 // R24 deterministic exp: k = rint(x log2 e) by the 1.5*2^23 trick, two-step
 // Cody-Waite reduction, degree-7 Taylor polynomial by fma Horner, exact 2^k.
 __device__ __forceinline__ float exp_det(float x) {
@@ -1440,6 +1484,13 @@ cudaError_t launch_pack(const Dev& d, uint32_t nSm, int ring, cudaStream_t s) {
   // grid-stride over the dirty records (count from the header: 64 rows of CTAs)
   dim3 grid(16, nSm == kFromHdr ? 64u : (nSm < 4096u ? nSm : 4096u));
   k_pack<<<grid, 256, 0, s>>>(d, ring);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_commit(const Dev& d, uint32_t nSp, int parity, int32_t T, cudaStream_t s) {
+  if (nSp == 0) return cudaSuccess;
+  dim3 grid(16, nSp < 4096u ? nSp : 4096u);
+  k_commit<<<grid, 256, 0, s>>>(d, parity, T, nSp);
   return cudaGetLastError();
 }
 

@@ -109,6 +109,9 @@ struct tgs_ctx {
   // a4 transfer kernels: CTAs of the gather (h2d) and the write-back (d2h)
   // (TGS_GATHER_CTAS / TGS_SCATTER_CTAS; defaults from profiles/linkbench2_r02.txt)
   int gather_ctas = 8, scatter_ctas = 4, gather_bufs = 4, scatter_bufs = 4;
+  // xfer = TGS_XFER_COPY_ENGINE (flat tier): runs of consecutive records move by
+  // copy-engine copies; the write-backs are issued by the I/O thread
+  bool ce = false;
   // store tier, per parity (the host fills them while the other parity's gather may still run):
   uint32_t* sel_map[2][2] = {};               // mapped host [C]: S+ subsets (hits, misses)
   uint32_t* sp_entry_map[2] = {};             // mapped host [C]: cache entry of S+ block i
@@ -231,7 +234,7 @@ int32_t prof_end(tgs_ctx* c, cudaStream_t s, Timer& t, int kind, uint64_t bytes 
 }
 void prof_collect(tgs_ctx* c) {
   std::lock_guard<std::mutex> g(c->prof_mu);
-  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "-", "-", "fine"};
+  static const char* names[] = {"adam", "prologue", "plan", "h2d", "d2h", "evict+pack", "commit", "-", "fine"};
   for (auto& p : c->pending) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.a, p.b) != cudaSuccess) ms = 0.f;
@@ -459,6 +462,32 @@ void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
   }
   const uint32_t nd = c->ndirty[p];
   const uint32_t* dl = c->dirty_map[p];
+  if (c->ce) {
+    // copy-engine write-back (flat tier): dirty record k sits at ring index k
+    // (ascending local id, k_evict / k_pack), so a run of consecutive ids is one
+    // contiguous copy on both sides; a direct write-back copies from the slots
+    const size_t w = (size_t)c->d.n_arr * c->rec_bytes;
+    CopyBatch b;
+    for (uint32_t k = 0; k < nd; ++k) {
+      const char* src = j.direct ? reinterpret_cast<const char*>(slot_rec(c, dl[2 * k + 1]))
+                                 : reinterpret_cast<const char*>(c->d.staging[p]) + (size_t)k * w;
+      b.add(host_rec(c, dl[2 * k]), src, w);
+    }
+    Timer td;
+    prof_begin(c, c->d2h, td);
+    for (size_t i = 0; i < b.dst.size() && e == cudaSuccess; ++i)
+      e = cudaMemcpyAsync(b.dst[i], b.src[i], b.size[i], cudaMemcpyDefault, c->d2h);
+    prof_end(c, c->d2h, td, 4, b.bytes);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_d2h[p], c->d2h);
+    std::lock_guard<std::mutex> g(c->mu);
+    c->tm.copy_calls += b.dst.size();
+    if (e != cudaSuccess) {
+      c->io_err = std::string("io: write-back copies: ") + cudaGetErrorString(e);
+      c->io_failed = true;
+    }
+    c->last_ndirty = nd;
+    return;
+  }
   for (uint32_t k = 0; k < nd; ++k) c->store->mark_dirty(dl[2 * k], j.T);  // R27 (a): inserted dirty
   std::lock_guard<std::mutex> g(c->mu);
   c->last_ndirty = nd;
@@ -612,6 +641,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (g.world_size < 1 || g.rank < 0 || g.rank >= g.world_size) return TGS_EINVAL;
   if (g.moments != TGS_MOMENTS_PERSIST && g.moments != TGS_MOMENTS_COLD_RESTART) return TGS_EINVAL;
   if (g.max_cameras < 1 || g.max_cameras > kMaxCams || g.max_age > kMaxAge) return TGS_EINVAL;
+  if (g.xfer != TGS_XFER_KERNEL && g.xfer != TGS_XFER_COPY_ENGINE) return TGS_EINVAL;
   const bool reopen = scfg && scfg->reopen;
   if (!reopen && (theta_rows == nullptr) == (fill == nullptr)) return TGS_EINVAL;
   if (reopen && theta_rows && fill) return TGS_EINVAL;
@@ -671,7 +701,10 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   const char* pp = getenv("TGS_PLAN_PRIO");
   const int plan_prio = (pp && atoi(pp) == 0) ? prio_lo : prio_hi;
   if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, plan_prio) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      // copy-engine transfers: k_commit on the h2d stream must get SMs while a
+      // many-wave Adam runs (it gates the next Adam): high priority
+      cudaStreamCreateWithPriority(&c->h2d, cudaStreamNonBlocking,
+                                   g.xfer == TGS_XFER_COPY_ENGINE ? prio_hi : prio_lo) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
   for (cudaEvent_t* e : {&c->ev_plan, &c->ev_probe, &c->ev_ready[0], &c->ev_ready[1],
@@ -823,6 +856,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C);
   for (int k = 0; k < kRings; ++k)
     d.staging[k] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
+  c->ce = g.xfer == TGS_XFER_COPY_ENGINE && !c->store;
+  d.stage_in = c->ce ? dalloc_t<float>(c, (size_t)Cc * d.n_arr * d.rec_floats, ok) : nullptr;
   std::vector<uint16_t> lut;
   uint32_t n_ranks = 0;
   build_rank_lut(g, lut, n_ranks);
@@ -881,7 +916,9 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (const char* m = getenv("TGS_SCATTER_CTAS")) c->scatter_ctas = std::max(1, atoi(m));
   if (const char* m = getenv("TGS_GATHER_BUFS")) c->gather_bufs = atoi(m);
   if (const char* m = getenv("TGS_SCATTER_BUFS")) c->scatter_bufs = atoi(m);
-  if (c->store) c->io = std::thread(io_main, c);  // flat tier: no host work per write-back
+  // store tier: CPU-cache dirty marks; copy-engine transfers: the write-back
+  // copies (the flat tier with the transfer kernels has no host work per write-back)
+  if (c->store || c->ce) c->io = std::thread(io_main, c);
   *out = c;
   return TGS_OK;
 }
@@ -1012,9 +1049,17 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     // every slot this gather may fill was freed by an earlier write-back, whose
     // k_evict / k_pack ran after the last Adam on it: wait for the newest one
     if (c->last_evict_ring >= 0) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[c->last_evict_ring], 0));
+    // (copy-engine write-backs: the I/O thread records ev_d2h -- join it first)
     for (int r : {k1, k2})  // a direct write-back (T-1, T-2) has no ring copy: wait for it
-      if (c->d2h_job[r] >= 0 && c->ring_direct[r]) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[r], 0));
-    if (c->d2h_job[k] >= 0 && c->d2h_job[k] <= T - 3) CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
+      if (c->d2h_job[r] >= 0 && c->ring_direct[r]) {
+        if (c->ce) io_join(c, c->d2h_job[r]);
+        CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[r], 0));
+      }
+    if (c->d2h_job[k] >= 0 && c->d2h_job[k] <= T - 3) {
+      if (c->ce) io_join(c, c->d2h_job[k]);
+      CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
+    }
+    if (c->io_failed) return check(c);
     return TGS_OK;
   };
   auto gather_flat = [&](uint32_t n_hint) -> tgs_status {
@@ -1022,14 +1067,31 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     if (gs != TGS_OK) return gs;
     Timer th;
     prof_begin(c, c->h2d, th);
-    CK(launch_xfer(dg, 0, p, k, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
-    c->h2d_prof = prof_end(c, c->h2d, th, 3);
+    if (c->ce) {
+      // copy engines (the plan is on the host): S+ record i from the host tier to
+      // stage_in[i] -- one copy per run of consecutive local ids -- then k_commit
+      // places each in its slot (or takes a ring re-admission from HBM)
+      const size_t w = (size_t)d.n_arr * c->rec_bytes;
+      CopyBatch b;
+      for (uint32_t i = 0; i < n_hint; ++i)
+        b.add(reinterpret_cast<char*>(d.stage_in) + (size_t)i * w, host_rec(c, c->sp_map[2 * i]), w);
+      tgs_status cs = submit(c, b, c->h2d);
+      if (cs != TGS_OK) return cs;
+      prof_end(c, c->h2d, th, 3, b.bytes);
+      Timer tc;
+      prof_begin(c, c->h2d, tc);
+      CK(launch_commit(dg, n_hint, p, T, c->h2d));
+      prof_end(c, c->h2d, tc, 6);
+    } else {
+      CK(launch_xfer(dg, 0, p, k, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
+      c->h2d_prof = prof_end(c, c->h2d, th, 3);
+    }
     c->tm.kernel_launches++;
     CK(cudaEventRecord(c->ev_ready[m], c->h2d));
     c->rec_ready[m] = true;
     return TGS_OK;
   };
-  const bool early = !c->store && d.tide && d.P >= 2u * d.C;
+  const bool early = !c->store && !c->ce && d.tide && d.P >= 2u * d.C;
   // asynchronous activate: no host decision needs the plan -- S+ never reuses an
   // S- slot (P >= 2C) and the ring holds any S- (S_max >= C), so every count is
   // read from the device header by the kernels themselves
@@ -1073,7 +1135,8 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     if (c->d2h_job[k] >= 0) {
       // the write-back of T-3 must be done with ring slot k (its ring, dirty
       // lists; store tier: the I/O job's read of dirty_map[k] / ndirty[k])
-      if (c->store) io_join(c, c->d2h_job[k]);
+      if (c->store || c->ce) io_join(c, c->d2h_job[k]);
+      if (c->io_failed) return check(c);
       CK(cudaStreamWaitEvent(c->compute, c->ev_d2h[k], 0));
     }
     prof_begin(c, c->compute, te);
@@ -1084,6 +1147,12 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     CK(cudaEventRecord(c->ev_evict[k], c->compute));
     c->rec_evict[k] = true;
     c->last_evict_ring = k;
+    if (c->ce) {  // the I/O thread copies the dirty runs once k_evict / k_pack are done
+      c->d2h_job[k] = T;
+      c->ring_direct[k] = direct;
+      io_submit(c, {T, k, direct});
+      return TGS_OK;
+    }
     CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[k], 0));
     prof_begin(c, c->d2h, td);
     CK(launch_xfer(dg, direct ? 2 : 1, p, k, T, nullptr, 0, async ? d.C : h.nSm, c->scatter_ctas,
@@ -1102,7 +1171,7 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
   if (reuse_now && h.nSm) {
     st = writeback();
     if (st != TGS_OK) return st;
-    if (c->store) io_join(c, T);
+    if (c->store || c->ce) io_join(c, T);
     if (c->io_failed) return check(c);
     CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
   }

@@ -43,7 +43,7 @@ class Config(C.Structure):
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32),
                 ("init_threads", C.c_int32), ("staging_blocks", C.c_uint32),
                 ("refresh_bounds", C.c_int32), ("serialize", C.c_int32),
-                ("level2", C.c_int32)]
+                ("level2", C.c_int32), ("xfer", C.c_int32)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -221,10 +221,10 @@ def _fp(a):
 def make_config(n_gaussians, block_size, capacity, *, pool_slots=0, max_cameras=256,
                 max_age=255, quota=(1, 2), lam=0.7, gamma=0.9, moments=PERSIST, tide=1,
                 world_size=1, rank=0, device=0, init_threads=0, staging_blocks=0,
-                refresh_bounds=0, serialize=0, level2=0) -> Config:
+                refresh_bounds=0, serialize=0, level2=0, xfer=0) -> Config:
     return Config(n_gaussians, DIM, block_size, capacity, pool_slots, max_cameras, max_age,
                   quota[0], quota[1], lam, gamma, moments, tide, world_size, rank, device,
-                  init_threads, staging_blocks, refresh_bounds, serialize, level2)
+                  init_threads, staging_blocks, refresh_bounds, serialize, level2, xfer)
 
 
 def torch_allocator(device=0):

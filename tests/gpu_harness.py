@@ -31,7 +31,7 @@ class Pair:
     def __init__(self, scene, *, capacity, pool_slots=0, max_cameras=256, max_age=255,
                  quota=(1, 2), lam=0.7, gamma=0.9, moments=O.PERSIST, tide=1, world_size=1,
                  rank=0, track_all=True, mask_p=None, staging_blocks=0, refresh_bounds=0,
-                 bounds=None, fill=None, store=None, level2=0):
+                 bounds=None, fill=None, store=None, level2=0, xfer=0):
         """store (NEXT f3): dict(gpu_dir, orc_dir, cache_blocks, segment_bytes=0,
         direct_io=0) -- the GPU table and the oracle each get their own store
         directory (orc_dir None: oracle metadata only)."""
@@ -53,7 +53,8 @@ class Pair:
                           direct_io=store.get("direct_io", 0), reopen=store.get("reopen", 0),
                           prefetch_blocks=store.get("prefetch_blocks", 0))
         self.gpu = T.Table(T.make_config(scene.N, scene.B, capacity, staging_blocks=staging_blocks,
-                                         refresh_bounds=refresh_bounds, level2=level2, **kw),
+                                         refresh_bounds=refresh_bounds, level2=level2, xfer=xfer,
+                                         **kw),
                            bounds,
                            fill=fill, store=gstore)
         self.orc = O.Oracle(O.make_config(scene.N, scene.B, capacity, refresh_bounds=refresh_bounds,

@@ -86,16 +86,18 @@ def _run(sc, tr, J, cap, n, *, world_size=1, rank=0, moments=O.PERSIST, expect_r
     return info, st, bound_batches
 
 
-def test_300m_bench_config_capacity_bound():
+@pytest.mark.parametrize("xfer", [0, 1])
+def test_300m_bench_config_capacity_bound(xfer):
     """The default bench workload (300m aerial smooth, J = 64, C = 6309, cold
     restart; K_loc = 73,243 blocks, W = 2289 words): 45 batches, selection binds
     from batch ~11 on, so k_quota's 512-thread and k_plan's 1024-thread
-    multi-pass carries decide R every batch from then on."""
+    multi-pass carries decide R every batch from then on.  Both a4 transfer
+    mechanisms (TMA kernels; copy-engine runs + k_commit)."""
     wl = W.CONFIGS["300m"]
     sc = wl.scene()
     tr = wl.trajectory(sc)
     info, st, bound = _run(sc, tr, wl.J, wl.capacity, 45, moments=O.COLD_RESTART,
-                           expect_readmit=False)
+                           expect_readmit=False, xfer=xfer)
     assert bound >= 20 and st["n_evict_dirty"] > 0, (info, st, bound)
 
 
@@ -109,7 +111,7 @@ def test_1b_shard8_rank0_capacity_bound_persist():
     tr = wl.trajectory(sc)
     cap = shard.shard_capacity(wl.capacity, 8)
     info, st, bound = _run(sc, tr, wl.J, cap, 40, world_size=8, rank=0, moments=O.PERSIST,
-                           expect_readmit=False)
+                           expect_readmit=False, xfer=1)
     assert bound >= 10, (info, bound)
 
 

@@ -51,14 +51,16 @@ def test_tiny_trajectory_parity(moments, lam, quota):
     pr.close()
 
 
+@pytest.mark.parametrize("xfer", [0, 1])
 @pytest.mark.parametrize("staging", [1, 64])
 @pytest.mark.parametrize("moments", [O.PERSIST, O.COLD_RESTART])
-def test_writeback_paths(staging, moments):
-    """Write-back through the staging ring (k_pack, I/O thread, re-admission
-    from the ring by k_readmit) and straight from the slots (ring too small):
-    same lists, bytes and contents as the oracle."""
+def test_writeback_paths(staging, moments, xfer):
+    """Write-back through the staging ring (k_pack, then the transfer: k_xfer, or
+    copy-engine runs issued by the I/O thread with xfer = 1; re-admission from
+    the ring by the gather / k_commit) and straight from the slots (ring too
+    small): same lists, bytes and contents as the oracle."""
     cfg, sc, tr = tiny()
-    pr = _pair(sc, capacity=cfg.capacity, moments=moments, staging_blocks=staging)
+    pr = _pair(sc, capacity=cfg.capacity, moments=moments, staging_blocks=staging, xfer=xfer)
     worst = _drive(pr, tr, cfg.J, 48, check_blocks_every=5)
     pr.gpu.flush()
     pr.orc.flush()
@@ -68,13 +70,14 @@ def test_writeback_paths(staging, moments):
     pr.close()
 
 
-def test_readmission_right_after_writeback():
+@pytest.mark.parametrize("xfer", [0, 1])
+def test_readmission_right_after_writeback(xfer):
     """Alternate two disjoint views with C = one view: every block is evicted
     dirty and re-admitted the next batch, so the gather must take the record
     from the staging ring (its host write-back may still be in flight)."""
     cfg, sc, tr = tiny()
     a, b = tr.batch_planes(0, 1), tr.batch_planes(8, 1)
-    pr = _pair(sc, capacity=14, staging_blocks=64, lam=1.0, quota=(0, 1))
+    pr = _pair(sc, capacity=14, staging_blocks=64, lam=1.0, quota=(0, 1), xfer=xfer)
     for t in range(16):
         act = pr.activate(a if t % 2 == 0 else b)
         pr.t = t
@@ -96,20 +99,22 @@ def test_tiny_batch_sizes_and_quota(J):
     pr.close()
 
 
-def test_tide_off_restage_all():
+@pytest.mark.parametrize("xfer", [0, 1])
+def test_tide_off_restage_all(xfer):
     """Ablation: every batch restages R_{t+1}, dirty R_t is
     written back first; bytes and contents still match the oracle."""
     cfg, sc, tr = tiny()
-    pr = _pair(sc, capacity=cfg.capacity, tide=0)
+    pr = _pair(sc, capacity=cfg.capacity, tide=0, xfer=xfer)
     worst = _drive(pr, tr, cfg.J, 20, check_blocks_every=5)
     assert worst == 0
     pr.close()
 
 
-def test_small_pool_uses_released_slots():
+@pytest.mark.parametrize("xfer", [0, 1])
+def test_small_pool_uses_released_slots(xfer):
     """P = C: S+ must reuse the slots S- releases (R13 fallback path)."""
     cfg, sc, tr = tiny()
-    pr = _pair(sc, capacity=cfg.capacity, pool_slots=cfg.capacity)
+    pr = _pair(sc, capacity=cfg.capacity, pool_slots=cfg.capacity, xfer=xfer)
     worst = _drive(pr, tr, cfg.J, 30, check_blocks_every=6)
     assert worst == 0
     pr.close()
@@ -374,7 +379,8 @@ def test_edge_configs(N, B, C, J, kw):
 @pytest.mark.parametrize("mode", ["plain", "fine", "fine_refresh_cold", "mask_direct",
                                   "fine_level2", "fine_level2_masked_refresh",
                                   "plain_async", "fine_async", "fine_refresh_cold_async",
-                                  "fine_level2_async"])
+                                  "fine_level2_async", "plain_ce", "fine_refresh_cold_ce",
+                                  "mask_direct_ce", "fine_level2_masked_refresh_ce"])
 def test_pipelined_run_matches_oracle(mode, monkeypatch):
     """The GPU runs ahead exactly as in bench.py -- no inspection call (hence no
     host sync) between batches -- so every cross-batch hazard (plan of t+1 vs
@@ -388,11 +394,14 @@ def test_pipelined_run_matches_oracle(mode, monkeypatch):
     use_async = mode.endswith("_async")  # tgs_activate_async: no plan readback at all
     if use_async:
         mode = mode[: -len("_async")]
+    xfer = 1 if mode.endswith("_ce") else 0  # copy-engine runs + k_commit
+    if xfer:
+        mode = mode[: -len("_ce")]
     kw = {"plain": {}, "fine": {}, "fine_refresh_cold": {"refresh_bounds": 1,
                                                           "moments": O.COLD_RESTART},
           "fine_level2": {"level2": 1}, "fine_level2_masked_refresh": {"level2": 1, "refresh_bounds": 1},
           "mask_direct": {"staging_blocks": 1, "mask_p": 0.5}}[mode]
-    pr = _pair(sc, capacity=cfg.capacity, **kw)
+    pr = _pair(sc, capacity=cfg.capacity, xfer=xfer, **kw)
     if "refresh" in mode:
         pr.lr[0:3] = 0.5
     fine = mode.startswith("fine")

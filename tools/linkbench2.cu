@@ -111,8 +111,11 @@ static float ms_between(cudaEvent_t a, cudaEvent_t b) { float m; cudaEventElapse
 
 int main(int argc, char** argv) {
   const bool tma_only = argc > 1 && !strcmp(argv[1], "tma");
+  const bool dma_only = argc > 1 && !strcmp(argv[1], "dma");
   const int nh = 382, nd = 228;
-  const size_t host_recs = 8192;
+  // LB_HOST_RECS: size of the pinned host tier in records (default 8192 = 7.9 GB;
+  // the 300m bench's is 73,243 = 70.8 GB)
+  const size_t host_recs = getenv("LB_HOST_RECS") ? (size_t)atoll(getenv("LB_HOST_RECS")) : 8192;
   char* h_tier;
   CK(cudaHostAlloc((void**)&h_tier, (size_t)kRec * host_recs, cudaHostAllocMapped));
   for (size_t i = 0; i < (size_t)kRec * host_recs; i += 4096) h_tier[i] = 1;
@@ -176,6 +179,36 @@ int main(int argc, char** argv) {
   auto d_runs = [&](int R) -> Fn {  // contiguous runs of R records (a log-structured append)
     return [=] { for (int i = 0; i < nd; i += R) cudaMemcpyAsync(h_tier + (size_t)(run0 + i) * kRec, d_ring + (size_t)i * kRec, (size_t)std::min(R, nd - i) * kRec, cudaMemcpyDeviceToHost, ds); };
   };
+  // copy-engine copies spread round-robin over S streams per direction, joined back
+  // into hs / ds by events (several copies in flight per direction)
+  cudaStream_t hsx[8], dsx[8];
+  cudaEvent_t ejh[8], ejd[8], efk;
+  for (int i = 0; i < 8; ++i) {
+    CK(cudaStreamCreateWithFlags(&hsx[i], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&dsx[i], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ejh[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ejd[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&efk, cudaEventDisableTiming));
+  auto h_dma_s = [&](int S) -> Fn {
+    return [=, &src_l] {
+      CK(cudaEventRecord(efk, hs));
+      for (int k = 0; k < S; ++k) CK(cudaStreamWaitEvent(hsx[k], efk, 0));
+      for (int i = 0; i < nh; ++i) cudaMemcpyAsync(d_slots + (size_t)i * kRec, h_tier + (size_t)src_l[i] * kRec, kRec, cudaMemcpyHostToDevice, hsx[i % S]);
+      for (int k = 0; k < S; ++k) { CK(cudaEventRecord(ejh[k], hsx[k])); CK(cudaStreamWaitEvent(hs, ejh[k], 0)); }
+    };
+  };
+  auto d_dma_s = [&](int S) -> Fn {
+    return [=, &dst_l] {
+      CK(cudaEventRecord(efk, ds));
+      for (int k = 0; k < S; ++k) CK(cudaStreamWaitEvent(dsx[k], efk, 0));
+      for (int i = 0; i < nd; ++i) cudaMemcpyAsync(h_tier + (size_t)dst_l[i] * kRec, d_ring + (size_t)i * kRec, kRec, cudaMemcpyDeviceToHost, dsx[i % S]);
+      for (int k = 0; k < S; ++k) { CK(cudaEventRecord(ejd[k], dsx[k])); CK(cudaStreamWaitEvent(ds, ejd[k], 0)); }
+    };
+  };
+  auto h_runs = [&](int R) -> Fn {  // h2d copies of contiguous host runs of R records
+    return [=] { for (int i = 0; i < nh; i += R) cudaMemcpyAsync(d_slots + (size_t)i * kRec, h_tier + (size_t)(run0 + i) * kRec, (size_t)std::min(R, nh - i) * kRec, cudaMemcpyHostToDevice, hs); };
+  };
   auto hbm = [&]() { hbm_pieces<<<(unsigned)(hbm_bytes / 262144), 256, 0, hb>>>((float4*)y, (const float4*)x); };
 
   auto run = [&](const char* name, Fn h, Fn d, bool with_hbm = false) {
@@ -201,6 +234,35 @@ int main(int argc, char** argv) {
     }
   };
   printf("# one step: %d records in (h2d), %d out (d2h), %u B each\n", nh, nd, kRec);
+  if (dma_only) {
+    run("h2d DMA runs of all (one copy)", h_runs(nh), nullptr);
+    run("d2h DMA runs of all (one copy)", nullptr, d_runs(nd));
+    run("h2d DMA runs of all || d2h DMA runs of all", h_runs(nh), d_runs(nd));
+    run("h2d DMA runs of 8 || d2h DMA runs of 8", h_runs(8), d_runs(8));
+    for (int S : {1, 2, 3, 4, 6, 8}) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "h2d DMA x%d streams", S);
+      run(nm, h_dma_s(S), nullptr);
+      snprintf(nm, sizeof nm, "d2h DMA x%d streams", S);
+      run(nm, nullptr, d_dma_s(S));
+      snprintf(nm, sizeof nm, "h2d DMA x%d || d2h DMA x%d", S, S);
+      run(nm, h_dma_s(S), d_dma_s(S));
+      snprintf(nm, sizeof nm, "h2d DMA x%d || d2h DMA x%d || HBM", S, S);
+      run(nm, h_dma_s(S), d_dma_s(S), true);
+    }
+    for (int S : {2, 4}) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "h2d TMA 8 || d2h DMA x%d", S);
+      run(nm, h_tma(8), d_dma_s(S));
+      snprintf(nm, sizeof nm, "h2d DMA x%d || d2h TMA 4", S);
+      run(nm, h_dma_s(S), d_tma(4));
+      snprintf(nm, sizeof nm, "h2d DMA x%d || d2h TMA 4 || HBM", S);
+      run(nm, h_dma_s(S), d_tma(4), true);
+    }
+    run("h2d TMA 8 || d2h TMA 4", h_tma(8), d_tma(4));
+    run("h2d TMA 8 || d2h TMA 4 || HBM", h_tma(8), d_tma(4), true);
+    return 0;
+  }
   if (tma_only) {
     for (int g : {1, 2, 4, 8, 16, 32}) {
       char nm[96];
