@@ -167,7 +167,28 @@ def link_peak(torch, dev):
             f()
             torch.cuda.synchronize()
             best[k] = max(best[k], n / (time.perf_counter() - t) / 1e9)
-    del x, d
+    # both directions at once (two streams, 1 GiB each): the ceiling of a step
+    # that gathers and writes back concurrently
+    y = torch.empty(n, dtype=torch.uint8).pin_memory()
+    e = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    best["bidir_h2d"] = best["bidir_d2h"] = 0.0
+    for _ in range(3):
+        a0, a1, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize()
+        a0.record()
+        s1.wait_event(a0)
+        s2.wait_event(a0)
+        with torch.cuda.stream(s1):
+            d.copy_(x, non_blocking=True)
+            a1.record(s1)
+        with torch.cuda.stream(s2):
+            y.copy_(e, non_blocking=True)
+            b1.record(s2)
+        torch.cuda.synchronize()
+        best["bidir_h2d"] = max(best["bidir_h2d"], n / (a0.elapsed_time(a1) * 1e6))
+        best["bidir_d2h"] = max(best["bidir_d2h"], n / (a0.elapsed_time(b1) * 1e6))
+    del x, d, y, e
     return best
 
 
@@ -630,7 +651,11 @@ def measure(args, ws, rank, local):
     # PCIe (not those re-admitted from the write-back ring in HBM) and dirty S-
     rec_b = sc.B * 59 * 4 * (3 if args.moments == "persist" else 1)
     ring_recs = tm["h2d_ring_records"] - tm0["h2d_ring_records"]
-    h2d_link, d2h_link = h2d - ring_recs * rec_b, d2h
+    # PCIe bytes: the transfer kernels skip ring re-admissions (read from HBM); the
+    # copy engines move whole runs, re-admitted records included (k_commit then
+    # takes the ring copy)
+    ce = xfer_mode(args) == 1
+    h2d_link, d2h_link = (h2d if ce else h2d - ring_recs * rec_b), d2h
     if ws > 1:  # whole job: counts summed over ranks, the slowest rank's clock
         t = torch.tensor([rows, ms, h2d, d2h, stage_in, visible, tm["adam_ms"], active_blocks],
                          dtype=torch.float64, device=dev)
@@ -692,9 +717,9 @@ def measure(args, ws, rank, local):
                                       "(m, v record written, not read)",
             "fresh_row_share": fresh_rows / max(1, rows_local),
             "avg_launch_ms": adam_ms,
-            "note": "k_adam is the dominant device-memory kernel; the longest-running kernel is "
-                    "k_xfer, the TMA transfer over PCIe, whose roofline is the host link "
-                    "(link_roofline)"}
+            "note": ("k_adam is the dominant device-memory kernel; the host link "
+                     "(link_roofline: copy-engine run copies, or the k_xfer TMA kernels) "
+                     "bounds the step when records move")}
     lp = link_peak(torch, dev) if rank == 0 else None
     if store and store_detail is not None:
         store_detail["ssd_read_peak_GBps"] = ssd_read_peak(os.path.join(store["dir"], "base.tdgs"))
@@ -706,9 +731,15 @@ def measure(args, ws, rank, local):
                 "h2d_peak": lp["h2d"], "d2h_peak": lp["d2h"], "unit": "GB/s",
                 "h2d_frac": (h2d_rate / lp["h2d"]) if h2d_rate else None,
                 "d2h_frac": (d2h_rate / lp["d2h"]) if d2h_rate else None,
-                "peak_kind": "measured in this run: pinned 1 GiB cudaMemcpy",
-                "how": "k_xfer gather / write-back kernel spans (CUDA events on the h2d / d2h "
-                       "streams) over the records they moved across PCIe",
+                "bidir_h2d_peak": lp["bidir_h2d"], "bidir_d2h_peak": lp["bidir_d2h"],
+                "bidir_h2d_frac": (h2d_rate / lp["bidir_h2d"]) if h2d_rate else None,
+                "bidir_d2h_frac": (d2h_rate / lp["bidir_d2h"]) if d2h_rate else None,
+                "peak_kind": "measured in this run: pinned 1 GiB cudaMemcpy, one direction "
+                             "alone (h2d/d2h_peak) and both at once on two streams (bidir_*)",
+                "how": ("copy-engine spans (CUDA events around each step's run copies on the "
+                        "h2d / d2h streams) over the bytes they moved" if ce else
+                        "k_xfer gather / write-back kernel spans (CUDA events on the h2d / d2h "
+                        "streams) over the records they moved across PCIe"),
                 "ring_readmissions_per_step": ring_recs / args.steps,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps}
     cpu = None

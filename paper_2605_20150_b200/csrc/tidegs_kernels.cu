@@ -1004,6 +1004,15 @@ __global__ void __launch_bounds__(kAdamNT, TGS_ADAM_MINB) k_adam(Dev d, uint32_t
   const bool dynamic = nA == kFromHdr;
   if (dynamic) nA = d.hdr_dev[parity]->nA;
   const uint64_t total = (uint64_t)nA * QB;
+  if (dynamic && qpw == 0) {
+    qpw = kAdamQPW;
+    // chunks small enough that every warp takes >= ~8 of them: with 16-quad
+    // chunks a small A (the in-memory configs) left a tail of one chunk per warp.
+    // (A static split -- warp w one contiguous range -- was slower still: the
+    // warps then stream from ~3.5k scattered places instead of neighbouring ones)
+    const uint64_t per = total / (8ull * gridDim.x * (kAdamNT / 32));
+    qpw = per < 1 ? 1u : per < (uint64_t)qpw ? (uint32_t)per : qpw;
+  }
   const uint64_t wid = (uint64_t)blockIdx.x * (kAdamNT / 32) + (threadIdx.x >> 5);
   uint64_t q0 = wid * qpw;
   uint64_t q1 = q0 + qpw < total ? q0 + qpw : total;
@@ -1505,12 +1514,16 @@ cudaError_t launch_adam_prologue(const Dev& d, uint32_t nA, int parity, const ui
 cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* mask,
                         const AdamHyper& hp, int grid_ctas, cudaStream_t s) {
   if (nA == 0) return cudaSuccess;
-  if (nA == kFromHdr) {  // count on the device: resident grid, dynamic chunks of 16 quads
+  if (nA == kFromHdr) {  // count on the device: resident grid, dynamic chunks (<= 16 quads)
     const unsigned grid = (unsigned)std::max(grid_ctas, 1);
+    static const uint32_t qd = [] {
+      const char* e = getenv("TGS_ADAM_DYNQPW");  // A/B: 0 -> fixed 16-quad chunks
+      return (e && atoi(e) == 0) ? kAdamQPW : 0u;
+    }();
     if (d.geo6)
-      k_adam<true><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, kAdamQPW);
+      k_adam<true><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qd);
     else
-      k_adam<false><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, kAdamQPW);
+      k_adam<false><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qd);
     return cudaGetLastError();
   }
   const uint64_t quads = (uint64_t)nA * (d.B / 4);
