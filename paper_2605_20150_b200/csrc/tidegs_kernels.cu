@@ -1516,9 +1516,11 @@ cudaError_t launch_adam(const Dev& d, uint32_t nA, int parity, const uint32_t* m
   if (nA == 0) return cudaSuccess;
   if (nA == kFromHdr) {  // count on the device: resident grid, dynamic chunks (<= 16 quads)
     const unsigned grid = (unsigned)std::max(grid_ctas, 1);
+    // TGS_ADAM_DYNQPW=1: chunks sized on the device (0); default fixed 16-quad
+    // chunks (same-box A/B at 11m: 0.177 vs 0.182 ms/step, profiles/ab_qpw_r02.md)
     static const uint32_t qd = [] {
-      const char* e = getenv("TGS_ADAM_DYNQPW");  // A/B: 0 -> fixed 16-quad chunks
-      return (e && atoi(e) == 0) ? kAdamQPW : 0u;
+      const char* e = getenv("TGS_ADAM_DYNQPW");
+      return (e && atoi(e) == 1) ? 0u : kAdamQPW;
     }();
     if (d.geo6)
       k_adam<true><<<grid, kAdamNT, 0, s>>>(d, nA, parity, mask, hp, qd);
