@@ -112,6 +112,9 @@ struct tgs_ctx {
   // xfer = TGS_XFER_COPY_ENGINE (flat tier): runs of consecutive records move by
   // copy-engine copies; the write-backs are issued by the I/O thread
   bool ce = false;
+  cudaStream_t cm = nullptr;            // k_commit (high priority)
+  cudaEvent_t ev_copies = nullptr, ev_commit[2] = {};  // stage_in buffer T & 1 copied / read
+  bool rec_commit[2] = {};
   // store tier, per parity (the host fills them while the other parity's gather may still run):
   uint32_t* sel_map[2][2] = {};               // mapped host [C]: S+ subsets (hits, misses)
   uint32_t* sp_entry_map[2] = {};             // mapped host [C]: cache entry of S+ block i
@@ -551,6 +554,7 @@ tgs_status sync_all(tgs_ctx* c) {
   CK(cudaStreamSynchronize(c->plan));
   CK(cudaStreamSynchronize(c->h2d));
   CK(cudaStreamSynchronize(c->compute));
+  if (c->cm) CK(cudaStreamSynchronize(c->cm));
   CK(cudaStreamSynchronize(c->d2h));
   prof_collect(c);
   return TGS_OK;
@@ -589,6 +593,8 @@ void destroy_impl(tgs_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_c1)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_copies, c->ev_commit[0], c->ev_commit[1]})
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_ready[2],
                         c->ev_evict[0], c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
                         c->ev_d2h[2], c->ev_lists[0], c->ev_lists[1], c->ev_lists[2],
@@ -597,7 +603,7 @@ void destroy_impl(tgs_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  for (cudaStream_t s : {c->plan, c->h2d, c->d2h}) if (s) cudaStreamDestroy(s);
+  for (cudaStream_t s : {c->plan, c->h2d, c->d2h, c->cm}) if (s) cudaStreamDestroy(s);
   cudaGetLastError();
   delete c;
 }
@@ -701,11 +707,14 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   const char* pp = getenv("TGS_PLAN_PRIO");
   const int plan_prio = (pp && atoi(pp) == 0) ? prio_lo : prio_hi;
   if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, plan_prio) != cudaSuccess ||
-      // copy-engine transfers: k_commit on the h2d stream must get SMs while a
-      // many-wave Adam runs (it gates the next Adam): high priority
-      cudaStreamCreateWithPriority(&c->h2d, cudaStreamNonBlocking,
-                                   g.xfer == TGS_XFER_COPY_ENGINE ? prio_hi : prio_lo) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(TGS_ECUDA);
+  if (g.xfer == TGS_XFER_COPY_ENGINE &&
+      (cudaStreamCreateWithPriority(&c->cm, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_copies, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_commit[0], cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_commit[1], cudaEventDisableTiming) != cudaSuccess))
     return fail(TGS_ECUDA);
   for (cudaEvent_t* e : {&c->ev_plan, &c->ev_probe, &c->ev_ready[0], &c->ev_ready[1],
                          &c->ev_ready[2], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
@@ -857,7 +866,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   for (int k = 0; k < kRings; ++k)
     d.staging[k] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
   c->ce = g.xfer == TGS_XFER_COPY_ENGINE && !c->store;
-  d.stage_in = c->ce ? dalloc_t<float>(c, (size_t)Cc * d.n_arr * d.rec_floats, ok) : nullptr;
+  d.stage_in = c->ce ? dalloc_t<float>(c, 2 * (size_t)Cc * d.n_arr * d.rec_floats, ok) : nullptr;
   std::vector<uint16_t> lut;
   uint32_t n_ranks = 0;
   build_rank_lut(g, lut, n_ranks);
@@ -1048,7 +1057,10 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
     // every slot this gather may fill was freed by an earlier write-back, whose
     // k_evict / k_pack ran after the last Adam on it: wait for the newest one
-    if (c->last_evict_ring >= 0) CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[c->last_evict_ring], 0));
+    // (copy engines: the copies only write stage_in -- k_commit, which fills the
+    // slots, waits for it on its own stream)
+    if (c->last_evict_ring >= 0 && !c->ce)
+      CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[c->last_evict_ring], 0));
     // (copy-engine write-backs: the I/O thread records ev_d2h -- join it first)
     for (int r : {k1, k2})  // a direct write-back (T-1, T-2) has no ring copy: wait for it
       if (c->d2h_job[r] >= 0 && c->ring_direct[r]) {
@@ -1071,17 +1083,35 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
       // copy engines (the plan is on the host): S+ record i from the host tier to
       // stage_in[i] -- one copy per run of consecutive local ids -- then k_commit
       // places each in its slot (or takes a ring re-admission from HBM)
+      // stage_in is double-buffered (buffer T & 1), k_commit runs on its own
+      // stream: the next gather's copies start as soon as these end, while
+      // k_commit waits for the newest evict / pack (the slots it fills)
+      const int sb = T & 1;
       const size_t w = (size_t)d.n_arr * c->rec_bytes;
+      char* const stage = reinterpret_cast<char*>(d.stage_in) + (size_t)sb * d.C * w;
+      if (c->rec_commit[sb]) CK(cudaStreamWaitEvent(c->h2d, c->ev_commit[sb], 0));
       CopyBatch b;
       for (uint32_t i = 0; i < n_hint; ++i)
-        b.add(reinterpret_cast<char*>(d.stage_in) + (size_t)i * w, host_rec(c, c->sp_map[2 * i]), w);
+        b.add(stage + (size_t)i * w, host_rec(c, c->sp_map[2 * i]), w);
       tgs_status cs = submit(c, b, c->h2d);
       if (cs != TGS_OK) return cs;
       prof_end(c, c->h2d, th, 3, b.bytes);
+      CK(cudaEventRecord(c->ev_copies, c->h2d));
+      CK(cudaStreamWaitEvent(c->cm, c->ev_copies, 0));
+      if (c->last_evict_ring >= 0)
+        CK(cudaStreamWaitEvent(c->cm, c->ev_evict[c->last_evict_ring], 0));
       Timer tc;
-      prof_begin(c, c->h2d, tc);
-      CK(launch_commit(dg, n_hint, p, T, c->h2d));
-      prof_end(c, c->h2d, tc, 6);
+      prof_begin(c, c->cm, tc);
+      Dev dc = dg;
+      dc.stage_in = reinterpret_cast<float*>(stage);
+      CK(launch_commit(dc, n_hint, p, T, c->cm));
+      prof_end(c, c->cm, tc, 6);
+      CK(cudaEventRecord(c->ev_commit[sb], c->cm));
+      c->rec_commit[sb] = true;
+      c->tm.kernel_launches++;
+      CK(cudaEventRecord(c->ev_ready[m], c->cm));
+      c->rec_ready[m] = true;
+      return TGS_OK;
     } else {
       CK(launch_xfer(dg, 0, p, k, T, nullptr, 0, n_hint, c->gather_ctas, c->gather_bufs, c->h2d));
       c->h2d_prof = prof_end(c, c->h2d, th, 3);
