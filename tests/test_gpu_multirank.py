@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir, iters, moments):
+def _worker(rank, world, port, out_dir, iters, moments, xfer):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -42,7 +42,7 @@ def _worker(rank, world, port, out_dir, iters, moments):
     torch.cuda.set_device(0)
     cfg, sc, tr = tiny()
     cap = shard.shard_capacity(cfg.capacity, world)
-    pr = Pair(sc, capacity=cap, world_size=world, rank=rank, moments=moments)
+    pr = Pair(sc, capacity=cap, world_size=world, rank=rank, moments=moments, xfer=xfer)
     pr.gpu.set_comm(T.torch_comm())
     log = {"batches": 0, "c1_rows": [], "errors": []}
     try:
@@ -82,12 +82,13 @@ def _worker(rank, world, port, out_dir, iters, moments):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("moments", [0, 1])
-def test_two_ranks_of_libtidegs_with_c1_c2(tmp_path, moments):
+@pytest.mark.parametrize("moments,xfer", [(0, 0), (1, 0), (0, 1)])
+def test_two_ranks_of_libtidegs_with_c1_c2(tmp_path, moments, xfer):
+    """xfer: 0 = TMA transfer kernels, 1 = copy-engine runs (the bench default)"""
     import torch.multiprocessing as mp
     world, iters = 2, 16
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), iters, moments), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), iters, moments, xfer),
+             nprocs=world, join=True)
     for r in range(world):
         log = json.load(open(tmp_path / f"rank{r}.json"))
         assert not log["errors"], log["errors"]
