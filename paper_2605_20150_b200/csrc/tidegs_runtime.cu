@@ -113,6 +113,11 @@ struct tgs_ctx {
   // copy-engine copies; the write-backs are issued by the I/O thread
   bool ce = false;
   cudaStream_t cm = nullptr;            // k_commit (high priority)
+  // TGS_CE_STREAMS=2: the run copies of each direction alternate between two
+  // streams (two copy engines), joined by an event (ev_fork / ev_join per direction)
+  int ce_streams = 1;
+  cudaStream_t h2d2 = nullptr, d2h2 = nullptr;
+  cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr, ev_dfork = nullptr, ev_djoin = nullptr;
   cudaEvent_t ev_copies = nullptr, ev_commit[2] = {};  // stage_in buffer T & 1 copied / read
   bool rec_commit[2] = {};
   // store tier, per parity (the host fills them while the other parity's gather may still run):
@@ -384,6 +389,26 @@ struct CopyBatch {
   }
 };
 
+// copies alternate between s and s2 (s2 forked from s and joined back into s)
+cudaError_t submit_split(tgs_ctx* c, CopyBatch& b, cudaStream_t s, cudaStream_t s2,
+                         cudaEvent_t fork, cudaEvent_t join) {
+  cudaError_t e = cudaSuccess;
+  const bool two = s2 && b.dst.size() > 1;
+  if (two) {
+    e = cudaEventRecord(fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, fork, 0);
+  }
+  for (size_t i = 0; i < b.dst.size() && e == cudaSuccess; ++i)
+    e = cudaMemcpyAsync(b.dst[i], b.src[i], b.size[i], cudaMemcpyDefault, (two && (i & 1)) ? s2 : s);
+  if (two && e == cudaSuccess) {
+    e = cudaEventRecord(join, s2);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, join, 0);
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  c->tm.copy_calls += b.dst.size();
+  return e;
+}
+
 tgs_status submit(tgs_ctx* c, CopyBatch& b, cudaStream_t s) {
   if (b.dst.empty()) return TGS_OK;
   for (size_t i = 0; i < b.dst.size(); ++i)
@@ -478,12 +503,10 @@ void io_process(tgs_ctx* c, const tgs_ctx::Job& j) {
     }
     Timer td;
     prof_begin(c, c->d2h, td);
-    for (size_t i = 0; i < b.dst.size() && e == cudaSuccess; ++i)
-      e = cudaMemcpyAsync(b.dst[i], b.src[i], b.size[i], cudaMemcpyDefault, c->d2h);
+    e = submit_split(c, b, c->d2h, c->d2h2, c->ev_dfork, c->ev_djoin);
     prof_end(c, c->d2h, td, 4, b.bytes);
     if (e == cudaSuccess) e = cudaEventRecord(c->ev_d2h[p], c->d2h);
     std::lock_guard<std::mutex> g(c->mu);
-    c->tm.copy_calls += b.dst.size();
     if (e != cudaSuccess) {
       c->io_err = std::string("io: write-back copies: ") + cudaGetErrorString(e);
       c->io_failed = true;
@@ -555,6 +578,8 @@ tgs_status sync_all(tgs_ctx* c) {
   CK(cudaStreamSynchronize(c->h2d));
   CK(cudaStreamSynchronize(c->compute));
   if (c->cm) CK(cudaStreamSynchronize(c->cm));
+  for (cudaStream_t s2 : {c->h2d2, c->d2h2})
+    if (s2) CK(cudaStreamSynchronize(s2));
   CK(cudaStreamSynchronize(c->d2h));
   prof_collect(c);
   return TGS_OK;
@@ -593,7 +618,8 @@ void destroy_impl(tgs_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_c1)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_copies, c->ev_commit[0], c->ev_commit[1]})
+  for (cudaEvent_t e : {c->ev_copies, c->ev_commit[0], c->ev_commit[1], c->ev_hfork, c->ev_hjoin,
+                        c->ev_dfork, c->ev_djoin})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_ready[2],
                         c->ev_evict[0], c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
@@ -603,7 +629,7 @@ void destroy_impl(tgs_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& p : c->pending) c->ev_pool.push_back(p.a), c->ev_pool.push_back(p.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  for (cudaStream_t s : {c->plan, c->h2d, c->d2h, c->cm}) if (s) cudaStreamDestroy(s);
+  for (cudaStream_t s : {c->plan, c->h2d, c->d2h, c->cm, c->h2d2, c->d2h2}) if (s) cudaStreamDestroy(s);
   cudaGetLastError();
   delete c;
 }
@@ -709,6 +735,15 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   if (cudaStreamCreateWithPriority(&c->plan, cudaStreamNonBlocking, plan_prio) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(TGS_ECUDA);
+  if (const char* cs = getenv("TGS_CE_STREAMS")) c->ce_streams = atoi(cs) == 2 ? 2 : 1;
+  if (g.xfer == TGS_XFER_COPY_ENGINE && c->ce_streams == 2 &&
+      (cudaStreamCreateWithFlags(&c->h2d2, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaStreamCreateWithFlags(&c->d2h2, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_hfork, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_hjoin, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_dfork, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_djoin, cudaEventDisableTiming) != cudaSuccess))
     return fail(TGS_ECUDA);
   if (g.xfer == TGS_XFER_COPY_ENGINE &&
       (cudaStreamCreateWithPriority(&c->cm, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
@@ -1093,8 +1128,7 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
       CopyBatch b;
       for (uint32_t i = 0; i < n_hint; ++i)
         b.add(stage + (size_t)i * w, host_rec(c, c->sp_map[2 * i]), w);
-      tgs_status cs = submit(c, b, c->h2d);
-      if (cs != TGS_OK) return cs;
+      CK(submit_split(c, b, c->h2d, c->h2d2, c->ev_hfork, c->ev_hjoin));
       prof_end(c, c->h2d, th, 3, b.bytes);
       CK(cudaEventRecord(c->ev_copies, c->h2d));
       CK(cudaStreamWaitEvent(c->cm, c->ev_copies, 0));
