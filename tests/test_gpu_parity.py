@@ -142,11 +142,12 @@ def test_empty_mask_leaves_everything_clean():
     pr.close()
 
 
-def test_static_batch_zero_traffic_and_empty_batch():
+@pytest.mark.parametrize("xfer", [0, 1])
+def test_static_batch_zero_traffic_and_empty_batch(xfer):
     """Static view with capacity: S+ = S- = {} after the first batch (SPEC.md:418);
-    J = 0 keeps R (R19)."""
+    J = 0 keeps R (R19).  Both transfer mechanisms (empty copy lists)."""
     cfg, sc, tr = tiny()
-    pr = _pair(sc, capacity=40)
+    pr = _pair(sc, capacity=40, xfer=xfer)
     pl = tr.batch_planes(3, cfg.J)
     for t in range(5):
         act = pr.activate(pl)
@@ -362,12 +363,14 @@ class _RandomCams:
     (30000, 100, 7, 5, {"tide": 0, "moments": O.COLD_RESTART}),  # restage-all, cold
     (30000, 100, 12, 4, {"quota": (1, 1), "lam": 1.0, "pool_slots": 13}),  # tight pool
 ])
-def test_edge_configs(N, B, C, J, kw):
+@pytest.mark.parametrize("xfer", [0, 1])
+def test_edge_configs(N, B, C, J, kw, xfer):
     """Degenerate and extreme shapes under random (high-churn) cameras:
-    bit-exact lists/slots/counters and 0-ULP rows against the oracle."""
+    bit-exact lists/slots/counters and 0-ULP rows against the oracle, with both
+    transfer mechanisms (copy-engine runs of tiny, odd-sized records)."""
     sc = W.Scene(N, B, side=60.0, lot=20.0, footprint=12.0, hmin=2.0, hmax=12.0)
     tr = _RandomCams(60.0)
-    pr = _pair(sc, capacity=C, **kw)
+    pr = _pair(sc, capacity=C, xfer=xfer, **kw)
     _drive(pr, tr, J, 12, check_blocks_every=3)
     pr.gpu.flush()
     pr.orc.flush()
