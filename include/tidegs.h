@@ -93,13 +93,15 @@ typedef struct {
 /* a4 transfer mechanism.
  * TGS_XFER_KERNEL: TMA bulk-copy kernels (k_xfer) read and write the pinned host
  *   tier over PCIe; no host decision needs the plan, so tgs_activate_async works.
- * TGS_XFER_COPY_ENGINE: the copy engines move runs of consecutive records (S+
- *   runs host tier -> a device staging buffer, then k_commit places them in their
- *   slots; dirty S- runs write-back ring -> host tier, issued by the library's I/O
- *   thread once the dirty list is known).  Needs the plan on the host:
- *   tgs_activate_async behaves as tgs_activate with it.  Why both: one copy per
- *   run of records runs both PCIe directions near the link's rate, the kernels
- *   do not need the plan readback (profiles/linkbench_dma_r02.txt). */
+ * TGS_XFER_COPY_ENGINE: the copy engines move the gather as runs of consecutive
+ *   records (S+ runs host tier -> a device staging buffer, then k_commit places
+ *   them in their slots); the dirty S- records go back from the write-back ring
+ *   by the TMA kernel with 2 CTAs (environment TGS_WB_KERNEL=0: copy-engine runs
+ *   issued by the library's I/O thread once the dirty list is known).  Needs the
+ *   plan on the host: tgs_activate_async behaves as tgs_activate with it.  Why
+ *   both mechanisms: copy-engine runs give the gather (which gates Adam) most of
+ *   the link, the kernels need no plan readback (profiles/ab_xfer_r02.md,
+ *   profiles/ab_wbk_r02.md). */
 typedef enum { TGS_XFER_KERNEL = 0, TGS_XFER_COPY_ENGINE = 1 } tgs_xfer;
 
 /* Optional device allocator hooks (PyTorch's caching allocator from Python).

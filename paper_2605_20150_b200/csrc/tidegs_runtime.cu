@@ -116,6 +116,12 @@ struct tgs_ctx {
   // TGS_CE_STREAMS=2: the run copies of each direction alternate between two
   // streams (two copy engines), joined by an event (ev_fork / ev_join per direction)
   int ce_streams = 1;
+  // TGS_WB_KERNEL (copy-engine mode): the write-back as the TMA kernel with N CTAs
+  // (default 2: the gather, which gates Adam, keeps more of the link;
+  // profiles/ab_wbk_r02.md), 0 = copy-engine runs from the I/O thread, -n = n CTAs
+  // while the write-backs keep up and scatter_ctas when the previous one is late
+  int wb_kernel = 2;
+  int last_d2h_ring = -1;    // ring slot of the newest kernel write-back
   cudaStream_t h2d2 = nullptr, d2h2 = nullptr;
   cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr, ev_dfork = nullptr, ev_djoin = nullptr;
   cudaEvent_t ev_copies = nullptr, ev_commit[2] = {};  // stage_in buffer T & 1 copied / read
@@ -737,6 +743,7 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TGS_ECUDA);
   if (const char* cs = getenv("TGS_CE_STREAMS")) c->ce_streams = atoi(cs) == 2 ? 2 : 1;
+  if (const char* wk = getenv("TGS_WB_KERNEL")) c->wb_kernel = atoi(wk);
   if (g.xfer == TGS_XFER_COPY_ENGINE && c->ce_streams == 2 &&
       (cudaStreamCreateWithFlags(&c->h2d2, cudaStreamNonBlocking) != cudaSuccess ||
        cudaStreamCreateWithFlags(&c->d2h2, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1211,7 +1218,20 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     CK(cudaEventRecord(c->ev_evict[k], c->compute));
     c->rec_evict[k] = true;
     c->last_evict_ring = k;
-    if (c->ce) {  // the I/O thread copies the dirty runs once k_evict / k_pack are done
+    // copy-engine mode: the write-back of a ring goes either as copy-engine runs
+    // (the I/O thread) or, with TGS_WB_KERNEL, as the TMA kernel: N CTAs, or -n =
+    // n CTAs while the write-backs keep up (the gather, on the critical path,
+    // then gets most of the link) and scatter_ctas when the previous one is late
+    int wb_ctas = c->scatter_ctas;
+    const bool ce_runs = c->ce && c->wb_kernel == 0;
+    if (c->ce && !ce_runs) {
+      wb_ctas = c->wb_kernel > 0 ? c->wb_kernel : -c->wb_kernel;
+      if (c->wb_kernel < 0 && c->last_d2h_ring >= 0 &&
+          cudaEventQuery(c->ev_d2h[c->last_d2h_ring]) == cudaErrorNotReady)
+        wb_ctas = c->scatter_ctas;
+      cudaGetLastError();
+    }
+    if (ce_runs) {  // the I/O thread copies the dirty runs once k_evict / k_pack are done
       c->d2h_job[k] = T;
       c->ring_direct[k] = direct;
       io_submit(c, {T, k, direct});
@@ -1219,11 +1239,12 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     }
     CK(cudaStreamWaitEvent(c->d2h, c->ev_evict[k], 0));
     prof_begin(c, c->d2h, td);
-    CK(launch_xfer(dg, direct ? 2 : 1, p, k, T, nullptr, 0, async ? d.C : h.nSm, c->scatter_ctas,
+    CK(launch_xfer(dg, direct ? 2 : 1, p, k, T, nullptr, 0, async ? d.C : h.nSm, wb_ctas,
                    c->scatter_bufs, c->d2h));
     prof_end(c, c->d2h, td, 4);
     c->tm.kernel_launches++;
     CK(cudaEventRecord(c->ev_d2h[k], c->d2h));
+    c->last_d2h_ring = k;
     if (c->store) {
       CK(cudaEventRecord(c->ev_job[T & 3], c->d2h));
       io_submit(c, {T, k, direct});

@@ -7,6 +7,7 @@
 // kernel (the Adam stand-in), whose rate is reported too.
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/linkbench2 tools/linkbench2.cu
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -112,6 +113,7 @@ static float ms_between(cudaEvent_t a, cudaEvent_t b) { float m; cudaEventElapse
 int main(int argc, char** argv) {
   const bool tma_only = argc > 1 && !strcmp(argv[1], "tma");
   const bool dma_only = argc > 1 && !strcmp(argv[1], "dma");
+  const bool graph_only = argc > 1 && !strcmp(argv[1], "graph");
   const int nh = 382, nd = 228;
   // LB_HOST_RECS: size of the pinned host tier in records (default 8192 = 7.9 GB;
   // the 300m bench's is 73,243 = 70.8 GB)
@@ -234,6 +236,63 @@ int main(int argc, char** argv) {
     }
   };
   printf("# one step: %d records in (h2d), %d out (d2h), %u B each\n", nh, nd, kRec);
+  // CUDA graphs of per-record memcpy nodes (independent, or chained), instantiated
+  // once and re-launched; plus the host cost of re-pointing every node
+  auto make_graph = [&](bool h2d, bool chain, cudaGraphExec_t& ge, std::vector<cudaGraphNode_t>& nodes) {
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    const int n = h2d ? nh : nd;
+    nodes.assign(n, nullptr);
+    for (int i = 0; i < n; ++i) {
+      void* dst = h2d ? (void*)(d_slots + (size_t)i * kRec) : (void*)(h_tier + (size_t)dst_l[i] * kRec);
+      const void* src = h2d ? (const void*)(h_tier + (size_t)src_l[i] * kRec) : (const void*)(d_ring + (size_t)i * kRec);
+      CK(cudaGraphAddMemcpyNode1D(&nodes[i], g, (chain && i) ? &nodes[i - 1] : nullptr, (chain && i) ? 1 : 0,
+                                  dst, src, kRec, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
+    }
+    CK(cudaGraphInstantiate(&ge, g, 0));
+  };
+  if (graph_only) {
+    for (int chain = 0; chain < 2; ++chain) {
+      cudaGraphExec_t gh, gd;
+      std::vector<cudaGraphNode_t> nhv, ndv;
+      auto t0 = std::chrono::steady_clock::now();
+      make_graph(true, chain, gh, nhv);
+      auto t1 = std::chrono::steady_clock::now();
+      make_graph(false, chain, gd, ndv);
+      printf("# graph build+instantiate (%s): h2d %.2f ms for %d nodes\n", chain ? "chained" : "independent",
+             std::chrono::duration<double, std::milli>(t1 - t0).count(), nh);
+      // re-point every node (what a per-step update costs on the host)
+      t0 = std::chrono::steady_clock::now();
+      for (int i = 0; i < nh; ++i)
+        CK(cudaGraphExecMemcpyNodeSetParams1D(gh, nhv[i], d_slots + (size_t)i * kRec, h_tier + (size_t)src_l[(i + 1) % nh] * kRec, kRec, cudaMemcpyHostToDevice));
+      t1 = std::chrono::steady_clock::now();
+      printf("# SetParams1D x %d: %.3f ms host\n", nh, std::chrono::duration<double, std::milli>(t1 - t0).count());
+      char nm[96];
+      snprintf(nm, sizeof nm, "h2d graph %s alone", chain ? "chained" : "indep");
+      run(nm, [=] { cudaGraphLaunch(gh, hs); }, nullptr);
+      snprintf(nm, sizeof nm, "d2h graph %s alone", chain ? "chained" : "indep");
+      run(nm, nullptr, [=] { cudaGraphLaunch(gd, ds); });
+      snprintf(nm, sizeof nm, "h2d graph %s || d2h graph", chain ? "chained" : "indep");
+      run(nm, [=] { cudaGraphLaunch(gh, hs); }, [=] { cudaGraphLaunch(gd, ds); });
+      snprintf(nm, sizeof nm, "h2d graph %s || d2h graph || HBM", chain ? "chained" : "indep");
+      run(nm, [=] { cudaGraphLaunch(gh, hs); }, [=] { cudaGraphLaunch(gd, ds); }, true);
+    }
+    run("h2d DMA x1 || d2h DMA x1 (per record, stream)", h_dma_s(1), d_dma_s(1));
+    run("h2d DMA runs of 8 || d2h DMA runs of 8", h_runs(8), d_runs(8));
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "mix")) {  // copy-engine runs in, TMA kernel out (and back)
+    for (int g : {1, 2, 4, 8}) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "h2d DMA runs of 6 || d2h TMA %d", g);
+      run(nm, h_runs(6), d_tma(g));
+      snprintf(nm, sizeof nm, "h2d DMA runs of 6 || d2h TMA %d || HBM", g);
+      run(nm, h_runs(6), d_tma(g), true);
+    }
+    run("h2d DMA runs of 6 || d2h DMA runs of 8", h_runs(6), d_runs(8));
+    run("h2d DMA runs of 6 || d2h DMA runs of 8 || HBM", h_runs(6), d_runs(8), true);
+    return 0;
+  }
   if (dma_only) {
     run("h2d DMA runs of all (one copy)", h_runs(nh), nullptr);
     run("d2h DMA runs of all (one copy)", nullptr, d_runs(nd));
