@@ -326,7 +326,8 @@ def _config_dict_base(args, wl, ws):
                          or getattr(args, "pool_slots", 0) or xfer_mode(args) == 1)
                          else "tgs_activate_async"),
             "xfer": ("TMA bulk-copy kernels (k_xfer; store tier)" if getattr(args, "store", None)
-                     else "copy-engine runs of consecutive records + k_commit"
+                     else "gather: copy-engine runs of consecutive records + k_commit; "
+                          "write-back: TMA kernel (k_xfer, 2 CTAs)"
                      if xfer_mode(args) == 1 else "TMA bulk-copy kernels (k_xfer)"),
             "overlap": not getattr(args, "no_overlap", False),
             "bound_refresh": bool(getattr(args, "refresh_bounds", False)),
@@ -736,8 +737,9 @@ def measure(args, ws, rank, local):
                 "bidir_d2h_frac": (d2h_rate / lp["bidir_d2h"]) if d2h_rate else None,
                 "peak_kind": "measured in this run: pinned 1 GiB cudaMemcpy, one direction "
                              "alone (h2d/d2h_peak) and both at once on two streams (bidir_*)",
-                "how": ("copy-engine spans (CUDA events around each step's run copies on the "
-                        "h2d / d2h streams) over the bytes they moved" if ce else
+                "how": ("h2d: copy-engine spans (CUDA events around each step's run copies "
+                        "on the h2d stream); d2h: the write-back kernel's spans (k_xfer, 2 CTAs, "
+                        "d2h stream); each over the bytes it moved" if ce else
                         "k_xfer gather / write-back kernel spans (CUDA events on the h2d / d2h "
                         "streams) over the records they moved across PCIe"),
                 "ring_readmissions_per_step": ring_recs / args.steps,
