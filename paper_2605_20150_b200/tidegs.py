@@ -20,6 +20,7 @@ DIM = 59
 
 OK, EINVAL, ESTATE, ENOMEM, ECUDA, ENCCL, ENONFINITE, EPOISONED, EIO = range(9)
 PERSIST, COLD_RESTART = 0, 1
+XFER_KERNEL, XFER_COPY_ENGINE = 0, 1  # tgs_xfer (include/tidegs.h)
 LISTS = {"K": 0, "R": 1, "S+": 2, "S-": 3, "Omega": 4, "A": 5}
 
 # every entry point include/tidegs.h declares (tests check the exports)

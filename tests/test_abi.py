@@ -26,6 +26,26 @@ def test_library_exports_every_symbol():
     assert L.tgs_status_string(T.EINVAL) == b"invalid argument"
 
 
+def test_config_struct_layout_matches_the_header(tmp_path):
+    """ctypes' tgs_config / tgs_activation / tgs_stats layouts equal the C header's
+    (a C program compiled against include/tidegs.h prints sizeof / offsetof)."""
+    src = tmp_path / "layout.c"
+    fields = [f[0] for f in T.Config._fields_]
+    body = "".join(f'printf("%zu ", offsetof(tgs_config, {("lambda" if f == "lambda_" else f)}));'
+                   for f in fields)
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "tidegs.h"\nint main(void){'
+                   + body + 'printf("%zu %zu %zu\\n", sizeof(tgs_config), sizeof(tgs_activation), '
+                   'sizeof(tgs_stats)); return 0;}\n')
+    import subprocess
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    out = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [getattr(T.Config, f).offset for f in fields]
+    assert out[:len(fields)] == want
+    assert out[len(fields):] == [C.sizeof(T.Config), C.sizeof(T.Activation), C.sizeof(T.Stats)]
+
+
 def test_elf_has_sm100a_code():
     """The product .so carries sm_100a SASS (no PTX-only JIT path)."""
     import subprocess
@@ -49,7 +69,8 @@ def _init(cfg, bounds, rows=None):
                                          ("gamma", 0.0), ("quota_den", 0), ("quota_num", 3),
                                          ("world_size", 0), ("rank", 2), ("moments", 7),
                                          ("max_cameras", 0), ("max_cameras", 300),
-                                         ("max_age", 5000), ("pool_slots", 3)])
+                                         ("max_age", 5000), ("pool_slots", 3), ("xfer", 2),
+                                         ("xfer", -1)])
 def test_invalid_config_is_einval(field, value):
     cfg = T.make_config(1000, 16, 4)
     setattr(cfg, field, value)
