@@ -148,3 +148,43 @@ def test_stress_small_capacity_many_blocks(J, C, moments):
     k_sizes = []
     info, st, bound = _run(sc, tr, J, C, 24, moments=moments)
     assert bound >= 20 and info["readmitted"] > 0, info
+
+
+@pytest.mark.parametrize("xfer", [1, 0])
+def test_300m_pipelined_no_sync(xfer):
+    """The default bench workload driven exactly as bench.py drives it -- 45 batches
+    back to back, no inspection (hence no host sync) between them, the copy-engine
+    gather (or the TMA kernels) running a batch ahead of Adam, write-backs draining
+    behind it -- then the last plan, the slot map, every counter and the tracked
+    blocks' theta/m/v (0 ULP, after the barrier) against the oracle.  Cross-batch
+    hazards at full size (staging-buffer reuse, ring reuse, write-back slack) show
+    up here and not in the step-by-step cases, which sync every batch."""
+    import ctypes as C
+
+    from gpu_harness import Pair, _cfn
+    wl = W.CONFIGS["300m"]
+    sc = wl.scene()
+    tr = wl.trajectory(sc)
+    n = 45
+    tracked, info = _pick_tracked(sc, tr, wl.J, wl.capacity, n, moments=O.COLD_RESTART)
+    assert info["S_minus"] > 0, info
+    pr = Pair(sc, capacity=wl.capacity, moments=O.COLD_RESTART, track_all=False, xfer=xfer)
+    for k in tracked:
+        assert pr.orc.track(k) == O.OK
+    planes = [tr.batch_planes(t, wl.J) for t in range(n)]
+    for t in range(n):  # GPU: back to back
+        act = pr.gpu.activate(planes[t])
+        pr.grads_gpu_only(act, t)
+        pr.gpu.step_adam(pr.lr)
+    g = (_cfn("wl_grad_cb"), C.addressof(pr.gsyn))
+    for t in range(n):  # oracle
+        assert pr.orc.activate(planes[t]) == O.OK
+        assert pr.orc.step_adam(pr.lr, grad=g) == O.OK
+    pr.t = n - 1
+    pr.compare_plan(wl.J)
+    pr.compare_stats()
+    pr.gpu.flush()
+    pr.orc.flush()
+    pr.compare_stats()
+    assert pr.compare_blocks(tracked) == 0
+    pr.close()
