@@ -8,7 +8,8 @@
 namespace tgs {
 
 constexpr uint32_t kDim = 59;
-constexpr int kRings = 3;                  // write-back ring slots (activate T uses T % 3)
+constexpr int kRings = 5;                  // write-back ring slots, at most (activate T uses
+                                           // T % nrings: 5 on the flat tier, 3 with the store)
 constexpr uint32_t kFromHdr = 0xFFFFFFFFu; // count argument: read it from the device plan header
 constexpr uint32_t kMaxCams = 256;
 constexpr uint32_t kMaxAge = 1023;
@@ -80,17 +81,19 @@ struct Dev {
   uint32_t* sm_map;      // mapped host [C] S- local ids (store mode only, else nullptr)
   // write-back state of activate T lives in ring slot T % kRings: the scatter of
   // T may still read it while the next two activates write theirs
-  uint32_t* dirty_map[3];  // mapped host [C][2] (local id, slot) of dirty S- (ring slot)
+  uint32_t* dirty_map[kRings];  // mapped host [C][2] (local id, slot) of dirty S- (ring slot)
   uint32_t* ndirty_map;    // mapped host [3] |dirty S-| (ring slot)
   uint32_t* ndirty_dev;    // [3] |dirty S-| (ring slot), read by k_pack and k_xfer
-  uint32_t* dl_slot[3];  // [C] dirty S- slots (pack / direct write-back source)
-  uint32_t* dl_blk[3];   // [C] dirty S- local ids (write-back destination)
+  uint32_t* dl_slot[kRings];  // [C] dirty S- slots (pack / direct write-back source)
+  uint32_t* dl_blk[kRings];   // [C] dirty S- local ids (write-back destination)
   int32_t* wb_tag;       // [Kloc] activate index at which the block was packed (-1 never)
   uint32_t* wb_idx;      // [Kloc] its staging-ring index then
-  float* staging[3];     // [S_max][n_arr][B][59] write-back staging rings (ring slot)
+  float* staging[kRings];     // [S_max][n_arr][B][59] write-back staging rings (ring slot)
   float* stage_in;       // [C][n_arr][B][59] copy-engine gather staging: S+ record i at i
                          // (xfer = TGS_XFER_COPY_ENGINE, else nullptr; read by k_commit)
   uint32_t S_max;        // staging capacity in records
+  int32_t nrings;        // ring slots in use: a block packed by one of the last nrings-1
+                         // activates is re-admitted from its ring record
   float4* last_planes[2];  // [kMaxCams*6] camera batch of the activate of that parity
   const float4* planes_map[2];  // mapped pinned host staging of the camera batch (parity)
   // selection

@@ -480,9 +480,11 @@ __global__ void __launch_bounds__(NT) k_evict(Dev d, uint32_t nSm, int parity, i
       d.dirty_map[ring][2 * o + 1] = s;
       d.dl_slot[ring][o] = s;
       d.dl_blk[ring][o] = l;
-      if (tag) {  // packed into staging[ring][o]: a re-admission within two batches reads it there
+      if (tag) {  // packed into staging[ring][o]: a re-admission within nrings-1 batches reads it there
         d.wb_tag[l] = T;
         d.wb_idx[l] = o;
+      } else {    // written back straight from its slot: an older ring record of l is stale
+        d.wb_tag[l] = -1;
       }
       atomicAnd(&d.dirty[s >> 5], ~(1u << (s & 31)));
     }
@@ -539,9 +541,9 @@ __global__ void __launch_bounds__(256, 6) k_commit(Dev d, int parity, int32_t T,
   for (uint32_t i = blockIdx.y; i < nSp; i += gridDim.y) {
     const uint32_t l = d.sp_blk[parity][i], slot = d.sp_slot[parity][i];
     const int32_t tg = d.wb_tag[l];
-    const bool ring = tg >= 0 && tg >= T - 2;
+    const bool ring = tg >= 0 && tg >= T - (d.nrings - 1);
     const float4* src = reinterpret_cast<const float4*>(
-        ring ? d.staging[tg % 3] + (size_t)d.wb_idx[l] * d.n_arr * d.rec_floats
+        ring ? d.staging[tg % d.nrings] + (size_t)d.wb_idx[l] * d.n_arr * d.rec_floats
              : d.stage_in + (size_t)i * d.n_arr * d.rec_floats);
     float4* dst = reinterpret_cast<float4*>(d.params + (size_t)slot * 3 * d.rec_floats);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -671,8 +673,8 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ri
       const uint32_t l = d.sp_blk[parity][i];
       slot = d.sp_slot[parity][i];
       const int32_t tg = d.wb_tag[l];
-      if (tg >= 0 && tg >= T - 2) {  // packed by one of the last two activates
-        src = reinterpret_cast<const unsigned char*>(d.staging[tg % kRings]) +
+      if (tg >= 0 && tg >= T - (d.nrings - 1)) {  // packed by one of the last nrings-1 activates
+        src = reinterpret_cast<const unsigned char*>(d.staging[tg % d.nrings]) +
               (uint64_t)d.wb_idx[l] * rec_bytes;
       } else {
         const uint64_t e = d.ent_of ? (uint64_t)d.sp_entry[i] : (uint64_t)l;
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__(32) k_xfer(Dev d, int mode, int parity, int ri
         // counts this block's last updates; the gather waits for that Adam
         if (d.cold) d.step[l] = 0u;
         if (d.ent_of) d.ent_of[l] = (int32_t)d.sp_entry[i];  // store tier: entry of a resident block
-        if (tg >= 0 && tg >= T - 2) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
+        if (tg >= 0 && tg >= T - (d.nrings - 1)) atomicAdd(&d.stats[ST_RING_READMIT], 1ull);
       }
     } else {
       const uint32_t l = d.dl_blk[ring][r];

@@ -80,7 +80,7 @@ struct tgs_ctx {
   // mapped pinned
   PlanHdr* hdr = nullptr;         // host view
   uint32_t* sp_map = nullptr;     // host view
-  uint32_t* dirty_map[kRings] = {};  // host views (ring slot T % 3)
+  uint32_t* dirty_map[kRings] = {};  // host views (ring slot T % nrings)
   uint32_t* ndirty = nullptr;     // host view [kRings]
   float* planes_pinned = nullptr; // [3][kMaxCams*24] mapped staging: camera batches (parity), prefetch
   uint32_t* probe_map = nullptr;  // mapped host [W] Level-1 union of an announced batch (prefetch)
@@ -100,10 +100,14 @@ struct tgs_ctx {
   PlanHdr* l3_hdr[3] = {};
   float4* l3_planes[3] = {};
   const float4* l3_planes_map[3] = {};
-  cudaEvent_t ev_evict[kRings] = {}, ev_d2h[kRings] = {};  // by ring slot T % 3
+  cudaEvent_t ev_evict[kRings] = {}, ev_d2h[kRings] = {};  // by ring slot T % nrings
+  // write-back ring slots in use: 5 on the flat tier (a churn burst's write-backs may
+  // lag four activates before a gather or a pack waits for them), 3 with the store tier
+  // (whose CPU-cache bookkeeping waits for write-backs of at most T-4)
+  int nrings = 3;
   cudaEvent_t ev_job[4] = {};      // write-back of activate J done: ev_job[J & 3] (store mode)
   bool rec_ready[3] = {}, rec_lists[3] = {}, rec_evict[kRings] = {};
-  int32_t d2h_job[kRings] = {-1, -1, -1};  // activate whose write-back last used ring slot k
+  int32_t d2h_job[kRings] = {-1, -1, -1, -1, -1};  // activate whose write-back last used ring slot k
   bool ring_direct[kRings] = {};   // ... and whether it wrote back straight from its slots
   int last_evict_ring = -1;        // ring slot of the most recent write-back kernels
   // a4 transfer kernels: CTAs of the gather (h2d) and the write-back (d2h)
@@ -616,8 +620,9 @@ void destroy_impl(tgs_ctx* c) {
   for (int q = 0; q < 2; ++q)
     for (void* h : {(void*)c->sel_map[q][0], (void*)c->sel_map[q][1], (void*)c->sp_entry_map[q]})
       if (h) cudaFreeHost(h);
-  for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->dirty_map[0], (void*)c->dirty_map[1],
-                  (void*)c->dirty_map[2], (void*)c->ndirty, (void*)c->planes_pinned,
+  for (void* h : c->dirty_map)
+    if (h) cudaFreeHost(h);
+  for (void* h : {(void*)c->hdr, (void*)c->sp_map, (void*)c->ndirty, (void*)c->planes_pinned,
                   (void*)c->lut_pinned, (void*)c->probe_map})
     if (h) cudaFreeHost(h);
   for (cudaEvent_t e : c->ev_job)
@@ -628,8 +633,9 @@ void destroy_impl(tgs_ctx* c) {
                         c->ev_dfork, c->ev_djoin})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_plan, c->ev_probe, c->ev_ready[0], c->ev_ready[1], c->ev_ready[2],
-                        c->ev_evict[0], c->ev_evict[1], c->ev_evict[2], c->ev_d2h[0], c->ev_d2h[1],
-                        c->ev_d2h[2], c->ev_lists[0], c->ev_lists[1], c->ev_lists[2],
+                        c->ev_evict[0], c->ev_evict[1], c->ev_evict[2], c->ev_evict[3],
+                        c->ev_evict[4], c->ev_d2h[0], c->ev_d2h[1], c->ev_d2h[2], c->ev_d2h[3],
+                        c->ev_d2h[4], c->ev_lists[0], c->ev_lists[1], c->ev_lists[2],
                         c->ev_refresh[0], c->ev_refresh[1], c->ev_planes[0], c->ev_planes[1],
                         c->ev_planes[2], c->trace_base})
     if (e) cudaEventDestroy(e);
@@ -760,7 +766,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
     return fail(TGS_ECUDA);
   for (cudaEvent_t* e : {&c->ev_plan, &c->ev_probe, &c->ev_ready[0], &c->ev_ready[1],
                          &c->ev_ready[2], &c->ev_evict[0], &c->ev_evict[1], &c->ev_evict[2],
-                         &c->ev_d2h[0], &c->ev_d2h[1], &c->ev_d2h[2], &c->ev_lists[0],
+                         &c->ev_evict[3], &c->ev_evict[4], &c->ev_d2h[0], &c->ev_d2h[1],
+                         &c->ev_d2h[2], &c->ev_d2h[3], &c->ev_d2h[4], &c->ev_lists[0],
                          &c->ev_lists[1], &c->ev_lists[2], &c->ev_refresh[0], &c->ev_refresh[1],
                          &c->ev_planes[0], &c->ev_planes[1], &c->ev_planes[2],
                          &c->ev_job[0], &c->ev_job[1], &c->ev_job[2],
@@ -812,6 +819,8 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
       cudaHostAlloc((void**)&c->dirty_map[0], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[1], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->dirty_map[2], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->dirty_map[3], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->dirty_map[4], list_bytes, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->ndirty, sizeof(uint32_t) * kRings, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void**)&c->planes_pinned, sizeof(float) * 4 * kMaxCams * 24,
                     cudaHostAllocMapped) != cudaSuccess ||
@@ -905,8 +914,11 @@ tgs_status init_impl(const tgs_config* cfg, const tgs_store_config* scfg, const 
   // default ring = C records: any S- fits, so no write-back ever has to come
   // straight from the slots (and tgs_activate_async needs no plan readback)
   d.S_max = g.staging_blocks ? g.staging_blocks : std::max(1u, d.C);
+  c->nrings = c->store ? 3 : kRings;
+  d.nrings = c->nrings;
   for (int k = 0; k < kRings; ++k)
-    d.staging[k] = dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok);
+    d.staging[k] = k < c->nrings ? dalloc_t<float>(c, (size_t)d.S_max * d.n_arr * d.rec_floats, ok)
+                                 : nullptr;
   c->ce = g.xfer == TGS_XFER_COPY_ENGINE && !c->store;
   d.stage_in = c->ce ? dalloc_t<float>(c, 2 * (size_t)Cc * d.n_arr * d.rec_floats, ok) : nullptr;
   std::vector<uint16_t> lut;
@@ -1089,12 +1101,12 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
   uint32_t* const* sel = c->sel_map[p];
   uint32_t* spe = c->sp_entry_map[p];
   if (c->store) CK(cudaHostGetDevicePointer((void**)&dg.sp_entry, spe, 0));
-  //      Write-back state: activate T uses ring slot T % 3.  A block packed by
-  //      T-1 or T-2 is re-admitted from its ring record (the host write-back may
-  //      still be in flight); one written back by T-3 or earlier from the host,
+  //      Write-back state: activate T uses ring slot T % nrings.  A block packed
+  //      by T-1 .. T-nrings+1 is re-admitted from its ring record (the host write-back
+  //      may still be in flight); one written back by T-nrings or earlier from the host,
   //      whose write-back (serial on the d2h stream) is waited for here.
-  const int k = (int)(((uint32_t)T) % kRings);
-  const int k1 = (int)(((uint32_t)T + 2) % kRings), k2 = (int)(((uint32_t)T + 1) % kRings);
+  const int NR = c->nrings;
+  const int k = (int)(((uint32_t)T) % (uint32_t)NR);
   auto gather_waits = [&]() -> tgs_status {
     CK(cudaStreamWaitEvent(c->h2d, c->ev_plan, 0));
     // every slot this gather may fill was freed by an earlier write-back, whose
@@ -1104,12 +1116,14 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
     if (c->last_evict_ring >= 0 && !c->ce)
       CK(cudaStreamWaitEvent(c->h2d, c->ev_evict[c->last_evict_ring], 0));
     // (copy-engine write-backs: the I/O thread records ev_d2h -- join it first)
-    for (int r : {k1, k2})  // a direct write-back (T-1, T-2) has no ring copy: wait for it
-      if (c->d2h_job[r] >= 0 && c->ring_direct[r]) {
+    for (int back = 1; back < NR; ++back) {  // a direct write-back (T-1 .. T-NR+1) has no
+      const int r = (int)(((uint32_t)(T - back)) % (uint32_t)NR);  // ring copy: wait for it
+      if (T - back >= 0 && c->d2h_job[r] >= 0 && c->ring_direct[r]) {
         if (c->ce) io_join(c, c->d2h_job[r]);
         CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[r], 0));
       }
-    if (c->d2h_job[k] >= 0 && c->d2h_job[k] <= T - 3) {
+    }
+    if (c->d2h_job[k] >= 0 && c->d2h_job[k] <= T - NR) {
       if (c->ce) io_join(c, c->d2h_job[k]);
       CK(cudaStreamWaitEvent(c->h2d, c->ev_d2h[k], 0));
     }
@@ -1200,11 +1214,11 @@ static tgs_status activate_impl(tgs_ctx* c, const tgs_camera* cams, uint32_t J,
   auto writeback = [&]() -> tgs_status {
     Timer te, td;
     CK(cudaStreamWaitEvent(c->compute, c->ev_plan, 0));
-    // ring slot k held T-3's records, which the previous activate's gather may
+    // ring slot k held T-nrings' records, which the previous activate's gather may
     // re-admit from: it must be done
     if (c->rec_ready[mq]) CK(cudaStreamWaitEvent(c->compute, c->ev_ready[mq], 0));
     if (c->d2h_job[k] >= 0) {
-      // the write-back of T-3 must be done with ring slot k (its ring, dirty
+      // the write-back of T-nrings must be done with ring slot k (its ring, dirty
       // lists; store tier: the I/O job's read of dirty_map[k] / ndirty[k])
       if (c->store || c->ce) io_join(c, c->d2h_job[k]);
       if (c->io_failed) return check(c);
@@ -1621,7 +1635,7 @@ uint32_t tgs_get_percam(tgs_ctx* c, uint32_t j, uint32_t* blocks, uint32_t cap) 
 uint32_t tgs_get_evicted_dirty(tgs_ctx* c, uint32_t* blocks, uint32_t cap) {
   if (check(c) != TGS_OK) return 0;
   if (sync_all(c) != TGS_OK) return 0;
-  const int k = c->T > 0 ? (int)(((uint32_t)c->T - 1) % kRings) : 0;  // the last activate's slot
+  const int k = c->T > 0 ? (int)(((uint32_t)c->T - 1) % (uint32_t)c->nrings) : 0;  // the last activate's slot
   // (after an asynchronous activate the write-back kernels always ran)
   const uint32_t n = (c->T > 0 && (!c->last_known || c->last.nSm)) ? c->ndirty[k] : 0;
   for (uint32_t i = 0; i < n && i < cap; ++i)
